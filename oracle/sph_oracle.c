@@ -1,0 +1,634 @@
+/*
+ * sph_oracle.c — CPU ORACLE for the arbitrary-positioned in/outlet buffer update
+ * of Zhang, Fan, Ren, Qian & Hu, "Generalized and high-efficiency arbitrary-
+ * positioned buffer for SPH" (arXiv 2406.16786).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load or call this file.  The product
+ * path (paper_2406_16786_b200/) never imports, links or executes it, and the two
+ * share no code, header, helper or constant generator.
+ *
+ * It is deliberately plain and slow: every particle is tested against every
+ * port by brute force, one loop per paper step, no blocking or
+ * fusion.  Citations: "P:n" = /root/reference/PAPER.md line n (the paper's LaTeX
+ * source); equations are named by their \label; "R<n>" = a reading of an
+ * ambiguous passage listed in DESIGN.md §3.
+ *
+ * Arithmetic.  The paper fixes no precision (R16).  State is fp32 (BASELINE
+ * configs).  Where floating point decides an integer (a crossing, an in-box
+ * test, a cell index) this oracle takes the decision in the kernel's precision
+ * with every operation a single IEEE-754 binary32 round-to-nearest operation in
+ * a fixed order ("pinned fp32", DESIGN.md §3 "Pinned arithmetic"):
+ *     d_j  = fl(x_j - o_j)
+ *     X'_r = fl( fl( fl(Q_r0*d_0) + fl(Q_r1*d_1) ) + fl(Q_r2*d_2) )   (3-D)
+ *     X'_r = fl( fl(Q_r0*d_0) + fl(Q_r1*d_1) )                          (2-D)
+ * This file must be compiled with -ffp-contract=off (no FMA contraction) on an
+ * SSE target (FLT_EVAL_METHOD == 0).  A second precision, prec=1, decides in
+ * f64 from the same fp32 inputs; it is used by the pins to show the pinned fp32
+ * decisions equal the exact-arithmetic decisions away from ties.
+ *
+ * parity pinned: see tests/test_oracle_pins.py (closed forms, hand cases
+ * H1-H6, lattice counts, invariants, brute force vs cell-restricted).
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#if defined(__FLT_EVAL_METHOD__) && __FLT_EVAL_METHOD__ != 0
+#error "oracle needs FLT_EVAL_METHOD == 0 (binary32 ops rounded per operation)"
+#endif
+
+/* ------------------------------------------------------------------ types */
+
+typedef struct {
+    int32_t dim;          /* 2 or 3 */
+    float lo[3];          /* grid lower corner (global) */
+    float cs;             /* cell size, >= 2h */
+    int32_t ncell[3];     /* global cell counts; ncell[2] == 1 in 2-D */
+    int32_t cx_begin;     /* owned x-slab of cells [cx_begin, cx_end) */
+    int32_t cx_end;
+} orc_grid;
+
+typedef struct {
+    float o[3];           /* origin O' in global coordinates */
+    float Q[9];           /* row-major; rows = local axes X',Y',Z' in global
+                             coordinates; X' = Q (x - o)  (Eq. 2D/3D_transformation) */
+    float he[3];          /* half extents a/2, b/2, c/2 */
+    int32_t kind;         /* 0 = inlet (Alg. 1), 1 = outlet (Alg. 2), 2 = bidirectional (Alg. 3) */
+} orc_port;
+
+typedef struct {
+    int64_t n;
+    float *x, *y, *z;     /* z == NULL in 2-D */
+    float *vx, *vy, *vz;  /* vz == NULL in 2-D */
+    int32_t n_extra;
+    float **extra;        /* n_extra fp32 columns copied on duplication ("same states") */
+    int64_t *id;
+    int32_t *label;       /* -1 = fluid, k = buffer particle of port k */
+} orc_state;
+
+enum { ORC_INLET = 0, ORC_OUTLET = 1, ORC_BIDIR = 2 };
+
+/* ------------------------------------------------------------ frames (§III.A) */
+
+/* Eq. 2D_transformation: rows [cos t, sin t], [-sin t, cos t];
+ * theta > 0 anticlockwise.  Embedded in 3x3 with Z' = Z. */
+void orc_frame_2d(double theta, double Q[9])
+{
+    double c = cos(theta), s = sin(theta);
+    Q[0] = c;  Q[1] = s; Q[2] = 0.0;
+    Q[3] = -s; Q[4] = c; Q[5] = 0.0;
+    Q[6] = 0.0; Q[7] = 0.0; Q[8] = 1.0;
+}
+
+/* 3-D frame from the in/outflow axis u (global, unit):
+ *   n = (OX x O'X') / |OX x O'X'|                 Eq. rotation_axis
+ *   S = [[0,-nz,ny],[nz,0,-nx],[-ny,nx,0]]        Eq. antisymmetric_matrix
+ *   R = I + S sin(theta) + S^2 (1 - cos(theta))   Eq. rotation_matrix
+ * with theta = arccos(X.u) in [0, pi] (R2: "the sign of theta is positive").
+ * As printed, R maps X-hat onto u (an active rotation), while the forward map
+ * r' = R (r - o) (Eq. 3D_transformation) and u = R^T e1
+ * (Eq. 3D_normal_transformation) need R u = e1.  Reading R1: the
+ * frame matrix is Q = R^T (row 0 of Q = u).  Degenerate axes (R2): u ~ +X -> Q = I;
+ * u ~ -X -> rotation by pi about Z, Q = diag(-1,-1,1).  Returns 0, or -1 if |u| == 0. */
+int orc_frame_3d(const double u_in[3], double Q[9])
+{
+    double nu = sqrt(u_in[0] * u_in[0] + u_in[1] * u_in[1] + u_in[2] * u_in[2]);
+    if (!(nu > 0.0)) return -1;
+    double u[3] = {u_in[0] / nu, u_in[1] / nu, u_in[2] / nu};
+    /* OX x O'X' with OX = (1,0,0), O'X' = u */
+    double cx = 0.0, cy = -u[2], cz = u[1];
+    double cn = sqrt(cx * cx + cy * cy + cz * cz);
+    if (cn < 1e-12) {
+        memset(Q, 0, 9 * sizeof(double));
+        if (u[0] > 0) { Q[0] = 1; Q[4] = 1; Q[8] = 1; }
+        else          { Q[0] = -1; Q[4] = -1; Q[8] = 1; }
+        return 0;
+    }
+    double n[3] = {cx / cn, cy / cn, cz / cn};
+    double cth = u[0];
+    if (cth > 1.0) cth = 1.0;
+    if (cth < -1.0) cth = -1.0;
+    double th = acos(cth);
+    double S[9] = {0.0, -n[2], n[1],
+                   n[2], 0.0, -n[0],
+                   -n[1], n[0], 0.0};
+    double S2[9];
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) {
+            double acc = 0.0;
+            for (int l = 0; l < 3; ++l) acc += S[3 * i + l] * S[3 * l + j];
+            S2[3 * i + j] = acc;
+        }
+    double R[9];
+    for (int i = 0; i < 9; ++i) {
+        double I = (i % 4 == 0) ? 1.0 : 0.0;
+        R[i] = I + S[i] * sin(th) + S2[i] * (1.0 - cos(th));
+    }
+    /* Q = R^T (reading R1) */
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) Q[3 * i + j] = R[3 * j + i];
+    return 0;
+}
+
+/* Forward transform r' = Q (r - o) in f64 from fp32 inputs
+ * (Eq. 2D_transformation; Eq. 3D_transformation). */
+void orc_to_local_f64(const orc_port *p, int32_t dim, float x, float y, float z, double out[3])
+{
+    double d[3] = {(double)x - (double)p->o[0], (double)y - (double)p->o[1],
+                   dim == 3 ? (double)z - (double)p->o[2] : 0.0};
+    for (int r = 0; r < 3; ++r) {
+        double acc = 0.0;
+        for (int j = 0; j < dim; ++j) acc += (double)p->Q[3 * r + j] * d[j];
+        out[r] = acc;
+    }
+    if (dim == 2) out[2] = 0.0;
+}
+
+/* Same transform, pinned fp32 (see file header). */
+void orc_to_local_f32(const orc_port *p, int32_t dim, float x, float y, float z, float out[3])
+{
+    float d0 = x - p->o[0];
+    float d1 = y - p->o[1];
+    if (dim == 3) {
+        float d2 = z - p->o[2];
+        for (int r = 0; r < 3; ++r) {
+            float a0 = p->Q[3 * r + 0] * d0;
+            float a1 = p->Q[3 * r + 1] * d1;
+            float s01 = a0 + a1;
+            float a2 = p->Q[3 * r + 2] * d2;
+            out[r] = s01 + a2;
+        }
+    } else {
+        for (int r = 0; r < 2; ++r) {
+            float a0 = p->Q[3 * r + 0] * d0;
+            float a1 = p->Q[3 * r + 1] * d1;
+            out[r] = a0 + a1;
+        }
+        out[2] = 0.0f;
+    }
+}
+
+/* The paper's recycle, literally: r = Q^T (r' - [a,0,0]^T) + o
+ * (Eq. 2D_Inverse_transformation, Eq. 3D_Inverse_transformation P:356-379,
+ * with a = 2 he_0).  f64; used by the pins to check reading R10. */
+void orc_inverse_recycle_f64(const orc_port *p, int32_t dim, const double xl[3], double out[3])
+{
+    double a = 2.0 * (double)p->he[0];
+    double v[3] = {xl[0] - a, xl[1], xl[2]};
+    for (int j = 0; j < 3; ++j) {
+        double acc = 0.0;
+        for (int r = 0; r < dim; ++r) acc += (double)p->Q[3 * r + j] * v[r];
+        out[j] = acc + (double)p->o[j];
+    }
+    if (dim == 2) out[2] = 0.0;
+}
+
+/* Recycle shift s = fl(a * u), u = row 0 of Q (Eq. 2D/3D_normal_transformation
+ * P:528-554), a = 2 he_0 (exact).  Reading R10: r - a u is the inverse
+ * transform above written in the global frame; pinned as one fp32 subtraction. */
+static void recycle_shift(const orc_port *p, float s[3])
+{
+    float a = 2.0f * p->he[0];
+    s[0] = a * p->Q[0];
+    s[1] = a * p->Q[1];
+    s[2] = a * p->Q[2];
+}
+
+/* ----------------------------------------------------------- predicates */
+
+/* Local-frame test of one particle against one port.  Returns:
+ *   bit0 = x in P_k   (|X'_r| < he_r + m, m = cs: reading R4, the paper's
+ *                      "approximately one layer of cells" P:413)
+ *   bit1 = InBox_k    (|X'| < a/2 & |Y'| < b/2 (& |Z'| < c/2), strict)
+ *   bit2 = X'_0 > a/2   (crossing the buffer-fluid interface / outlet boundary)
+ *   bit3 = X'_0 < -a/2  (bidirectional reverse crossing)
+ *   bit4 = X'_0 - a > a/2 (moved more than one buffer length; reading R12) */
+static int classify(const orc_port *p, int32_t dim, float cs, float x, float y, float z, int32_t prec)
+{
+    int bits = 0;
+    if (prec == 0) {
+        float X[3];
+        orc_to_local_f32(p, dim, x, y, z, X);
+        int inP = 1, inB = 1;
+        for (int r = 0; r < dim; ++r) {
+            float heP = p->he[r] + cs;
+            if (!(fabsf(X[r]) < heP)) inP = 0;
+            if (!(fabsf(X[r]) < p->he[r])) inB = 0;
+        }
+        if (inP) bits |= 1;
+        if (inB) bits |= 2;
+        if (X[0] > p->he[0]) bits |= 4;
+        if (X[0] < -p->he[0]) bits |= 8;
+        if (X[0] - 2.0f * p->he[0] > p->he[0]) bits |= 16;
+    } else {
+        double X[3];
+        orc_to_local_f64(p, dim, x, y, z, X);
+        int inP = 1, inB = 1;
+        for (int r = 0; r < dim; ++r) {
+            double heP = (double)p->he[r] + (double)cs;
+            if (!(fabs(X[r]) < heP)) inP = 0;
+            if (!(fabs(X[r]) < (double)p->he[r])) inB = 0;
+        }
+        if (inP) bits |= 1;
+        if (inB) bits |= 2;
+        if (X[0] > (double)p->he[0]) bits |= 4;
+        if (X[0] < -(double)p->he[0]) bits |= 8;
+        if (X[0] - 2.0 * (double)p->he[0] > (double)p->he[0]) bits |= 16;
+    }
+    return bits;
+}
+
+/* ------------------------------------------------------------ cell list */
+
+int64_t orc_ncells(const orc_grid *g)
+{
+    return (int64_t)(g->cx_end - g->cx_begin) * g->ncell[1] * (g->dim == 3 ? g->ncell[2] : 1);
+}
+
+static int32_t cell_axis(float x, float lo, float inv_cs, int32_t lo_c, int32_t hi_c, int32_t *oob)
+{
+    float t = (x - lo) * inv_cs;          /* pinned: fl(fl(x - lo) * inv_cs) */
+    float f = floorf(t);
+    if (f < (float)lo_c) { *oob = 1; return lo_c; }
+    if (f > (float)(hi_c - 1)) { *oob = 1; return hi_c - 1; }
+    return (int32_t)f;
+}
+
+/* Cell of a particle in the owned slab, linearised x-major (z fastest, y in 2-D):
+ * ((cx - cx_begin) * ny + cy) * nz + cz.  Out-of-slab coordinates are clamped to
+ * the boundary cell and flagged.  inv_cs = fl32(1/cs) formed in f64. */
+int64_t orc_cell_of(const orc_grid *g, float x, float y, float z, int32_t *oob)
+{
+    float inv_cs = (float)(1.0 / (double)g->cs);
+    int32_t o = 0;
+    int32_t cx = cell_axis(x, g->lo[0], inv_cs, g->cx_begin, g->cx_end, &o);
+    int32_t cy = cell_axis(y, g->lo[1], inv_cs, 0, g->ncell[1], &o);
+    int32_t cz = 0;
+    int32_t nz = 1;
+    if (g->dim == 3) { cz = cell_axis(z, g->lo[2], inv_cs, 0, g->ncell[2], &o); nz = g->ncell[2]; }
+    if (oob) *oob = o;
+    return ((int64_t)(cx - g->cx_begin) * g->ncell[1] + cy) * nz + cz;
+}
+
+/* Oracle's own enumeration of the cells intersecting P_k (inflated by 1e-3 cs to
+ * absorb fp32 rounding of X'): the cell-restricted candidate set of the paper's
+ * "local cell-linked lists".  Every cell of the slab's axis-aligned
+ * bounding box of P_k is tested by the separating-axis theorem between the cell
+ * box and the oriented box.  mask[c] = 1 for intersecting local cells. */
+static double dot3(const double *a, const double *b) { return a[0] * b[0] + a[1] * b[1] + a[2] * b[2]; }
+
+int64_t orc_port_cells(const orc_grid *g, const orc_port *p, uint8_t *mask)
+{
+    int dim = g->dim;
+    double cs = (double)g->cs;
+    double eps = 1e-3 * cs;
+    double o[3] = {p->o[0], p->o[1], dim == 3 ? p->o[2] : 0.0};
+    double ax[3][3];
+    double H[3];
+    for (int r = 0; r < 3; ++r) {
+        for (int j = 0; j < 3; ++j) ax[r][j] = p->Q[3 * r + j];
+        H[r] = (double)p->he[r] + cs + eps;
+    }
+    if (dim == 2) { ax[0][2] = 0; ax[1][2] = 0; ax[2][0] = 0; ax[2][1] = 0; ax[2][2] = 1; H[2] = 0.0; }
+    /* AABB of the oriented box */
+    double ext[3];
+    for (int j = 0; j < 3; ++j) {
+        ext[j] = 0.0;
+        for (int r = 0; r < 3; ++r) ext[j] += fabs(ax[r][j]) * H[r];
+    }
+    int64_t nmark = 0;
+    int32_t nc[3] = {g->ncell[0], g->ncell[1], dim == 3 ? g->ncell[2] : 1};
+    int32_t cmin[3], cmax[3];
+    for (int j = 0; j < 3; ++j) {
+        if (j == 2 && dim == 2) { cmin[2] = 0; cmax[2] = 0; continue; }
+        cmin[j] = (int32_t)floor((o[j] - ext[j] - (double)g->lo[j]) / cs) - 1;
+        cmax[j] = (int32_t)floor((o[j] + ext[j] - (double)g->lo[j]) / cs) + 1;
+        if (cmin[j] < 0) cmin[j] = 0;
+        if (cmax[j] > nc[j] - 1) cmax[j] = nc[j] - 1;
+    }
+    if (cmin[0] < g->cx_begin) cmin[0] = g->cx_begin;
+    if (cmax[0] > g->cx_end - 1) cmax[0] = g->cx_end - 1;
+    /* candidate separating axes: 3 world axes, 3 box axes, 9 cross products */
+    double axes[15][3];
+    int na = 0;
+    for (int j = 0; j < 3; ++j) { axes[na][0] = j == 0; axes[na][1] = j == 1; axes[na][2] = j == 2; ++na; }
+    for (int r = 0; r < 3; ++r) { axes[na][0] = ax[r][0]; axes[na][1] = ax[r][1]; axes[na][2] = ax[r][2]; ++na; }
+    if (dim == 3) {
+        for (int j = 0; j < 3; ++j)
+            for (int r = 0; r < 3; ++r) {
+                double e[3] = {j == 0, j == 1, j == 2};
+                double c[3] = {e[1] * ax[r][2] - e[2] * ax[r][1], e[2] * ax[r][0] - e[0] * ax[r][2],
+                               e[0] * ax[r][1] - e[1] * ax[r][0]};
+                if (dot3(c, c) > 1e-20) { axes[na][0] = c[0]; axes[na][1] = c[1]; axes[na][2] = c[2]; ++na; }
+            }
+    }
+    for (int32_t cx = cmin[0]; cx <= cmax[0]; ++cx)
+        for (int32_t cy = cmin[1]; cy <= cmax[1]; ++cy)
+            for (int32_t cz = cmin[2]; cz <= cmax[2]; ++cz) {
+                double half = 0.5 * cs;
+                double cc[3] = {(double)g->lo[0] + (cx + 0.5) * cs, (double)g->lo[1] + (cy + 0.5) * cs,
+                                dim == 3 ? (double)g->lo[2] + (cz + 0.5) * cs : 0.0};
+                double hc[3] = {half, half, dim == 3 ? half : 0.0};
+                double t[3] = {cc[0] - o[0], cc[1] - o[1], cc[2] - o[2]};
+                int separated = 0;
+                for (int a = 0; a < na && !separated; ++a) {
+                    double *L = axes[a];
+                    double rc = fabs(L[0]) * hc[0] + fabs(L[1]) * hc[1] + fabs(L[2]) * hc[2];
+                    double rb = 0.0;
+                    for (int r = 0; r < 3; ++r) rb += fabs(dot3(L, ax[r])) * H[r];
+                    if (fabs(dot3(L, t)) > rc + rb) separated = 1;
+                }
+                if (!separated) {
+                    int64_t lc = ((int64_t)(cx - g->cx_begin) * g->ncell[1] + cy) * nc[2] + cz;
+                    mask[lc] = 1;
+                    ++nmark;
+                }
+            }
+    return nmark;
+}
+
+/* --------------------------------------------------------- O1: advection */
+
+/* Driver step (not part of the method): x <- fl(x + fl(v dt)) per component. */
+void orc_advect(orc_state *s, int32_t dim, float dt)
+{
+    for (int64_t i = 0; i < s->n; ++i) {
+        float dx = s->vx[i] * dt;
+        s->x[i] = s->x[i] + dx;
+        float dy = s->vy[i] * dt;
+        s->y[i] = s->y[i] + dy;
+        if (dim == 3) {
+            float dz = s->vz[i] * dt;
+            s->z[i] = s->z[i] + dz;
+        }
+    }
+}
+
+/* ---------------------------------------------------- O0: registration */
+
+/* Alg. 1 "Buffer particle identification ... Execute only once":
+ * every fluid particle (label -1) with |X'|<a/2 & |Y'|<b/2 (& |Z'|<c/2) becomes a
+ * buffer particle of port k.  For outlet and bidirectional ports the same test is
+ * the initial relabel (Alg. 2/3 second procedure).
+ * Returns the number of particles labelled k afterwards. */
+int64_t orc_register(orc_state *s, const orc_grid *g, const orc_port *p, int32_t k, int32_t prec)
+{
+    int64_t members = 0;
+    for (int64_t i = 0; i < s->n; ++i) {
+        if (s->label[i] == -1) {
+            int b = classify(p, g->dim, g->cs, s->x[i], s->y[i], g->dim == 3 ? s->z[i] : 0.0f, prec);
+            if (b & 2) s->label[i] = k;
+        }
+        if (s->label[i] == k) ++members;
+    }
+    return members;
+}
+
+/* ------------------------------------------------------ O2 .. O5: update */
+
+typedef struct {
+    int64_t cell;
+    int64_t id;
+    int64_t idx;
+} key_t3;
+
+static int cmp_key(const void *a, const void *b)
+{
+    const key_t3 *u = (const key_t3 *)a, *v = (const key_t3 *)b;
+    if (u->cell != v->cell) return u->cell < v->cell ? -1 : 1;
+    if (u->id != v->id) return u->id < v->id ? -1 : 1;
+    return 0;
+}
+
+typedef struct {
+    /* O2 */
+    int64_t *order;        /* [n] sorted position -> input index */
+    int32_t *cell_start;   /* [ncells] first sorted position of cell c */
+    int32_t *cell_end;     /* [ncells] one past the last */
+    int64_t out_of_grid;
+    /* O3 (indexed by sorted position) */
+    int32_t *create_port;  /* [n] k or -1 */
+    int32_t *delete_port;  /* [n] k or -1 */
+    /* O4/O5: 'sorted' holds the input reordered by O2 with recycles and relabels applied */
+    orc_state sorted;
+    orc_state staged;      /* [cap_stage] bitwise copies (pre-recycle) in canonical order; id = source id */
+    int32_t *stage_port;   /* [cap_stage] */
+    int64_t *stage_src;    /* [cap_stage] sorted position of the source */
+    int64_t cap_stage;
+    int64_t n_stage;
+    int32_t *port_counts;  /* [2K]: created_k at [k], deleted_k at [K + k] */
+    int64_t checked;       /* particle-port tests performed */
+    int64_t multi_decision;/* particles with more than one decision (must be 0) */
+    int64_t motion_errors; /* members beyond 3a/2 (reading R12) */
+} orc_update_out;
+
+static void copy_row(const orc_state *src, int64_t i, orc_state *dst, int64_t j, int32_t dim)
+{
+    dst->x[j] = src->x[i];
+    dst->y[j] = src->y[i];
+    dst->vx[j] = src->vx[i];
+    dst->vy[j] = src->vy[i];
+    if (dim == 3) { dst->z[j] = src->z[i]; dst->vz[j] = src->vz[i]; }
+    for (int e = 0; e < src->n_extra; ++e) dst->extra[e][j] = src->extra[e][i];
+    dst->id[j] = src->id[i];
+    dst->label[j] = src->label[i];
+}
+
+/* One buffer update on one slab.  mode 0 = brute force over every particle and
+ * port in the global frame ("through the equation of the threshold line or
+ * surface"); mode 1 = only particles in the oracle's own P_k cell set (the
+ * paper's local cell-linked lists).  prec 0 = pinned fp32, 1 = f64.
+ * Returns 0, or -1 if staging overflows. */
+int orc_update(const orc_grid *g, const orc_port *ports, int32_t K, const orc_state *in,
+               int32_t mode, int32_t prec, orc_update_out *out)
+{
+    const int32_t dim = g->dim;
+    const int64_t n = in->n;
+    const int64_t nc = orc_ncells(g);
+
+    /* O2: cell-linked list -- cell of each particle, then order by (cell, id). */
+    key_t3 *keys = (key_t3 *)malloc(sizeof(key_t3) * (size_t)(n > 0 ? n : 1));
+    out->out_of_grid = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        int32_t oob = 0;
+        keys[i].cell = orc_cell_of(g, in->x[i], in->y[i], dim == 3 ? in->z[i] : 0.0f, &oob);
+        keys[i].id = in->id[i];
+        keys[i].idx = i;
+        out->out_of_grid += oob;
+    }
+    qsort(keys, (size_t)n, sizeof(key_t3), cmp_key);
+    for (int64_t c = 0; c < nc; ++c) { out->cell_start[c] = 0; out->cell_end[c] = 0; }
+    for (int64_t j = 0; j < n; ++j) out->cell_end[keys[j].cell] += 1;     /* counts */
+    int64_t run = 0;
+    for (int64_t c = 0; c < nc; ++c) {
+        int64_t cnt = out->cell_end[c];
+        out->cell_start[c] = (int32_t)run;
+        run += cnt;
+        out->cell_end[c] = (int32_t)run;
+    }
+    orc_state *S = &out->sorted;
+    S->n = n;
+    for (int64_t j = 0; j < n; ++j) {
+        out->order[j] = keys[j].idx;
+        copy_row(in, keys[j].idx, S, j, dim);
+    }
+    free(keys);
+
+    /* O3: decisions (Alg. 1, Alg. 2, Alg. 3). */
+    for (int64_t j = 0; j < n; ++j) { out->create_port[j] = -1; out->delete_port[j] = -1; }
+    int32_t *ndec = (int32_t *)calloc((size_t)(n > 0 ? n : 1), sizeof(int32_t));
+    uint8_t *mask = NULL;
+    out->checked = 0;
+    out->multi_decision = 0;
+    out->motion_errors = 0;
+    for (int32_t k = 0; k < K; ++k) {
+        const orc_port *p = &ports[k];
+        int64_t jb = 0, je = n;
+        if (mode == 1) {
+            mask = (uint8_t *)calloc((size_t)(nc > 0 ? nc : 1), 1);
+            orc_port_cells(g, p, mask);
+        }
+        for (int64_t c = 0; c < (mode == 1 ? nc : 1); ++c) {
+            if (mode == 1) {
+                if (!mask[c]) continue;
+                jb = out->cell_start[c];
+                je = out->cell_end[c];
+            }
+            for (int64_t j = jb; j < je; ++j) {
+                ++out->checked;
+                int b = classify(p, dim, g->cs, S->x[j], S->y[j], dim == 3 ? S->z[j] : 0.0f, prec);
+                if (!(b & 1)) continue;                               /* x not in P_k (R4) */
+                int create = 0, del = 0;
+                int member = (S->label[j] == k);
+                if (p->kind == ORC_INLET) {
+                    /* Alg. 1: buffer particles j with X'_j > a/2 (reading R5) */
+                    create = member && (b & 4);
+                } else if (p->kind == ORC_OUTLET) {
+                    /* Alg. 2: any checked particle with X'_i > a/2 (reading R6) */
+                    del = (b & 4) != 0;
+                } else {
+                    /* Alg. 3: buffer particles only */
+                    create = member && (b & 4);
+                    del = member && (b & 8);
+                }
+                if (member && (b & 16)) ++out->motion_errors;
+                if (create || del) {
+                    if (ndec[j]++ > 0) { ++out->multi_decision; continue; }
+                    if (create) out->create_port[j] = k;
+                    if (del) out->delete_port[j] = k;
+                }
+            }
+        }
+        free(mask);
+        mask = NULL;
+    }
+    free(ndec);
+
+    /* O4: apply.  CREATEs in canonical order (port k, source cell, source id) =
+     * port-major walk of the (cell, id)-sorted array (reading R14).  Duplicate =
+     * bitwise copy of the member's state before the recycle, label fluid
+     * ("the same states as the crossing ones"; R11).  Then recycle
+     * x <- fl(x - fl(a u)) (Eqs. 2D/3D_Inverse_transformation; R10). */
+    for (int32_t k = 0; k < 2 * K; ++k) out->port_counts[k] = 0;
+    out->n_stage = 0;
+    for (int32_t k = 0; k < K; ++k) {
+        float s[3];
+        recycle_shift(&ports[k], s);
+        for (int64_t j = 0; j < n; ++j) {
+            if (out->create_port[j] != k) continue;
+            if (out->n_stage >= out->cap_stage) return -1;
+            int64_t t = out->n_stage++;
+            copy_row(S, j, &out->staged, t, dim);
+            out->staged.label[t] = -1;
+            out->stage_port[t] = k;
+            out->stage_src[t] = j;
+            out->port_counts[k] += 1;
+            S->x[j] = S->x[j] - s[0];
+            S->y[j] = S->y[j] - s[1];
+            if (dim == 3) S->z[j] = S->z[j] - s[2];
+        }
+        for (int64_t j = 0; j < n; ++j)
+            if (out->delete_port[j] == k) out->port_counts[K + k] += 1;
+    }
+    out->staged.n = out->n_stage;
+
+    /* O5: relabel for outlet and bidirectional ports (Alg. 2/3 "Buffer particle
+     * identification (after the cell-linked lists have been rebuilt ...)",
+     * P:435-443; reading R9: on post-recycle positions, this update's
+     * cell list).  In-box -> label k; a former member outside -> fluid ("otherwise,
+     * they will not").  New (staged) and deleted particles are excluded;
+     * inlet members are fixed (Alg. 1 identifies them once). */
+    for (int32_t k = 0; k < K; ++k) {
+        const orc_port *p = &ports[k];
+        if (p->kind == ORC_INLET) continue;
+        int64_t jb = 0, je = n;
+        if (mode == 1) {
+            mask = (uint8_t *)calloc((size_t)(nc > 0 ? nc : 1), 1);
+            orc_port_cells(g, p, mask);
+        }
+        for (int64_t c = 0; c < (mode == 1 ? nc : 1); ++c) {
+            if (mode == 1) {
+                if (!mask[c]) continue;
+                jb = out->cell_start[c];
+                je = out->cell_end[c];
+            }
+            for (int64_t j = jb; j < je; ++j) {
+                if (out->delete_port[j] >= 0) continue;
+                int b = classify(p, dim, g->cs, S->x[j], S->y[j], dim == 3 ? S->z[j] : 0.0f, prec);
+                if (b & 2) S->label[j] = k;
+                else if (S->label[j] == k) S->label[j] = -1;
+            }
+        }
+        free(mask);
+        mask = NULL;
+    }
+    return 0;
+}
+
+/* ------------------------------------------------------- O6: compaction */
+
+/* Stable compaction + append + ID assignment (north star "scan-based stream
+ * compaction with an ID/permutation remap"; readings R14, R15).
+ * Survivors keep their (cell, id) order, staged particles are appended in
+ * canonical order.  New IDs follow the count matrix all_counts[r][2K]
+ * (created_k at [r*2K + k]):
+ *   off(k, r) = next_id + sum_{k'<k} sum_{r'} C[r'][k'] + sum_{r'<r} C[r'][k]
+ * and within (k, r) the canonical order.  perm[j] = new position of sorted
+ * position j, or -1 if deleted.  Returns the new count; *next_id_out receives
+ * next_id + sum of all C. */
+int64_t orc_compact(const orc_state *S, const int32_t *delete_port, const orc_state *staged,
+                    const int32_t *stage_port, int32_t dim, const int32_t *all_counts, int32_t nranks,
+                    int32_t rank, int32_t K, int64_t next_id, orc_state *out, int64_t *perm,
+                    int64_t *next_id_out)
+{
+    int64_t m = 0;
+    for (int64_t j = 0; j < S->n; ++j) {
+        if (delete_port[j] >= 0) { if (perm) perm[j] = -1; continue; }
+        copy_row(S, j, out, m, dim);
+        if (perm) perm[j] = m;
+        ++m;
+    }
+    int64_t total = 0;
+    for (int32_t r = 0; r < nranks; ++r)
+        for (int32_t k = 0; k < K; ++k) total += all_counts[(int64_t)r * 2 * K + k];
+    int64_t within = 0;
+    int32_t prev_k = -1;
+    for (int64_t t = 0; t < staged->n; ++t) {
+        int32_t k = stage_port[t];
+        if (k != prev_k) { within = 0; prev_k = k; }
+        int64_t off = next_id;
+        for (int32_t kk = 0; kk < k; ++kk)
+            for (int32_t r = 0; r < nranks; ++r) off += all_counts[(int64_t)r * 2 * K + kk];
+        for (int32_t r = 0; r < rank; ++r) off += all_counts[(int64_t)r * 2 * K + k];
+        copy_row(staged, t, out, m, dim);
+        out->id[m] = off + within;
+        out->label[m] = -1;
+        ++within;
+        ++m;
+    }
+    out->n = m;
+    if (next_id_out) *next_id_out = next_id + total;
+    return m;
+}

@@ -1,0 +1,480 @@
+"""Seeded synthetic inputs for the in/outlet buffer update (arXiv 2406.16786).
+
+This module is the ONLY code shared by the CUDA path and the CPU oracle
+(``oracle/``).  It builds particle lattices, velocity fields, port frames and
+grids shaped like the paper's workloads (DESIGN.md §4 "Input recipe"); it holds
+none of the method's arithmetic (no local-frame decisions, no cell lists, no
+generation/deletion).  Input shaping that needs geometry (pre-clearing an
+upstream column, projecting the lateral velocity near a port) is written here
+with its own plain torch expressions and is not the method: the method never
+pre-clears or projects.
+
+Configs (BASELINE.json ``configs``):
+
+* ``C1``  2-D orthogonal channel, 8,000 particles, 1 update at dt=0.002.
+* ``C1e`` C1 with dt=0.0095 (reading R18: C1 as written has no events).
+* ``C2``  2-D 30-degree channel with a 45-degree slanted end, ~200k particles,
+          two bidirectional ports (inflow normals at 30 and 255 degrees).
+* ``C3``  3-D square duct 1.0x0.2x0.2, 2.56M particles.
+* ``C4``  3-D 1.6x0.8x0.8 junction, 65.5M particles, 8 random ports.
+* ``C5``  3-D weak-scaling slabs, 128M particles per slab, 8 ports per slab.
+
+``scale`` < 1 shrinks C3/C4/C5 boxes (for CPU-sized parity cases).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+INLET, OUTLET, BIDIRECTIONAL = 0, 1, 2
+SEED_BASE = 240616786
+
+
+def f32(v: float) -> float:
+    """Round a python float to the nearest binary32 value."""
+    return float(np.float32(v))
+
+
+@dataclass
+class Port:
+    origin: tuple            # O' (global), binary32 values
+    Q: tuple                 # 9 values row-major; rows = local axes (row 0 = u, the in/outflow axis)
+    half_extents: tuple      # (a/2, b/2, c/2)
+    kind: int                # INLET / OUTLET / BIDIRECTIONAL
+    layers: int
+
+
+@dataclass
+class Grid:
+    dim: int
+    lo: tuple                # 3 binary32 values
+    cs: float                # binary32 cell size
+    ncell: tuple             # global cell counts (nz = 1 in 2-D)
+    cx_begin: int = 0
+    cx_end: int = -1         # -1 -> ncell[0]
+
+    def __post_init__(self):
+        if self.cx_end < 0:
+            self.cx_end = self.ncell[0]
+
+    def slab(self, cx_begin: int, cx_end: int) -> "Grid":
+        return Grid(self.dim, self.lo, self.cs, self.ncell, cx_begin, cx_end)
+
+    @property
+    def ncells_local(self) -> int:
+        return (self.cx_end - self.cx_begin) * self.ncell[1] * (self.ncell[2] if self.dim == 3 else 1)
+
+
+@dataclass
+class Workload:
+    name: str
+    dim: int
+    dp: float
+    h: float
+    grid: Grid
+    ports: list
+    state: dict              # x,y,(z),vx,vy,(vz): float32; id: int64; label: int32 (all -1)
+    dt: float
+    n_updates: int
+    next_id: int
+    notes: str = ""
+    slab_cells: list = field(default_factory=list)   # per-slab [cx_begin, cx_end) for C5
+
+    @property
+    def n(self) -> int:
+        return int(self.state["x"].numel())
+
+
+# ----------------------------------------------------------------- helpers
+
+def _gen(seed: int, device) -> torch.Generator:
+    g = torch.Generator(device=device)
+    g.manual_seed(int(seed))
+    return g
+
+
+def _noise(n, g, device, sigma=0.05):
+    """N(0, sigma^2) per component, clipped at +-4 sigma (reading R17)."""
+    z = torch.randn(n, generator=g, device=device, dtype=torch.float32) * sigma
+    return z.clamp_(-4 * sigma, 4 * sigma).double()
+
+
+def _jitter(n, g, device, dp):
+    return (torch.rand(n, generator=g, device=device, dtype=torch.float32).double() * 2.0 - 1.0) * (0.1 * dp)
+
+
+def frame_rows_2d(theta: float) -> tuple:
+    """Rows [cos t, sin t], [-sin t, cos t] as in the paper's 2-D frame; input data only."""
+    c, s = math.cos(theta), math.sin(theta)
+    return tuple(f32(v) for v in (c, s, 0.0, -s, c, 0.0, 0.0, 0.0, 1.0))
+
+
+def frame_rows_3d(u, psi: float) -> tuple:
+    """A random right-handed orthonormal frame with row 0 = u and roll psi about u
+    (Gram-Schmidt; C4/C5 draw the roll, reading R3)."""
+    u = np.asarray(u, dtype=np.float64)
+    u = u / np.linalg.norm(u)
+    e = np.zeros(3)
+    e[int(np.argmin(np.abs(u)))] = 1.0
+    t0 = e - np.dot(e, u) * u
+    t0 /= np.linalg.norm(t0)
+    b0 = np.cross(u, t0)
+    t = math.cos(psi) * t0 + math.sin(psi) * b0
+    w = np.cross(u, t)
+    return tuple(f32(v) for v in np.concatenate([u, t, w]))
+
+
+def _port(origin, Q, he, kind, layers) -> Port:
+    return Port(tuple(f32(v) for v in origin), tuple(Q), tuple(f32(v) for v in he), kind, layers)
+
+
+def _local(xyz: list, port: Port, dim: int):
+    """f64 local coordinates, used only for input shaping (pre-clear, projection)."""
+    Q = torch.tensor(port.Q, dtype=torch.float64, device=xyz[0].device).view(3, 3)
+    d = [xyz[j] - port.origin[j] for j in range(dim)]
+    return [sum(Q[r, j] * d[j] for j in range(dim)) for r in range(dim)]
+
+
+def _project_near_ports(xyz, v, ports, dim, radius_pad):
+    """Within each port's bounding sphere, keep only the axial velocity
+    (v <- (v.u)u) so buffer particles stay laterally inside their box
+    (reading R17; input shaping, the same projection as Eq. velocity_correction)."""
+    for p in ports:
+        r = math.sqrt(sum(h * h for h in p.half_extents[:dim])) + radius_pad
+        d2 = sum((xyz[j] - p.origin[j]) ** 2 for j in range(dim))
+        near = d2 < r * r
+        if not bool(near.any()):
+            continue
+        u = p.Q[0:3]
+        vu = sum(v[j] * u[j] for j in range(dim))
+        for j in range(dim):
+            v[j] = torch.where(near, vu * u[j], v[j])
+    return v
+
+
+def _pack_state(xyz, v, ids, dim):
+    st = {"x": xyz[0].float().contiguous(), "y": xyz[1].float().contiguous()}
+    st["vx"] = v[0].float().contiguous()
+    st["vy"] = v[1].float().contiguous()
+    if dim == 3:
+        st["z"] = xyz[2].float().contiguous()
+        st["vz"] = v[2].float().contiguous()
+    st["id"] = ids.to(torch.int64).contiguous()
+    st["label"] = torch.full_like(st["id"], -1, dtype=torch.int32)
+    return st
+
+
+def _lattice(counts, dp, device, origin=(0.0, 0.0, 0.0), index_offset=0):
+    """Cell-centred lattice ((i+1/2)dp), ids in lattice order with x slowest."""
+    n = 1
+    for c in counts:
+        n *= c
+    idx = torch.arange(n, device=device, dtype=torch.int64)
+    comps = []
+    rem = idx
+    strides = []
+    s = 1
+    for c in reversed(counts):
+        strides.append(s)
+        s *= c
+    strides = list(reversed(strides))
+    for a, c in enumerate(counts):
+        ia = (rem // strides[a]) % c
+        comps.append((ia.double() + 0.5) * dp + origin[a])
+    return comps, idx + index_offset
+
+
+# ----------------------------------------------------------------- configs
+
+def c1(device="cpu", dt=0.002, name="C1") -> Workload:
+    """2-D orthogonal channel 2.0x0.4 at dp=0.01 (BASELINE configs[0])."""
+    dim, dp = 2, 0.01
+    h = 1.3 * dp
+    cs = f32(2 * h)
+    g = _gen(SEED_BASE + 1, device)
+    xyz, ids = _lattice((200, 40), dp, device)
+    n = ids.numel()
+    for j in range(dim):
+        xyz[j] = xyz[j] + _jitter(n, g, device, dp)
+    v = [1.0 + _noise(n, g, device), _noise(n, g, device)]
+    I = (1.0, 0.0, 0.0, 0.0, 1.0, 0.0, 0.0, 0.0, 1.0)
+    ports = [_port((0.02, 0.2, 0.0), I, (0.02, 0.2, 0.0), INLET, 4),
+             _port((1.98, 0.2, 0.0), I, (0.02, 0.2, 0.0), OUTLET, 4)]
+    v = _project_near_ports(xyz, v, ports[:1], dim, 2 * dp)
+    lo = (f32(-2 * cs), f32(-2 * cs), 0.0)
+    ncell = (int(math.ceil(2.0 / cs)) + 4, int(math.ceil(0.4 / cs)) + 4, 1)
+    grid = Grid(dim, lo, cs, ncell)
+    return Workload(name, dim, dp, h, grid, ports, _pack_state(xyz, v, ids, dim), f32(dt), 1, n,
+                    notes="200x40 lattice; inlet x in (0,0.04), outlet x in (1.96,2.0)")
+
+
+def c1e(device="cpu") -> Workload:
+    """C1 with dt=0.0095: exactly the last lattice layer crosses at each end (R18)."""
+    return c1(device, dt=0.0095, name="C1e")
+
+
+def c2(device="cpu", n_updates=100) -> Workload:
+    """2-D channel rotated 30 degrees, end face slanted 45 degrees; both ports bidirectional."""
+    dim, dp = 2, 0.002
+    h = 1.3 * dp
+    cs = f32(2 * h)
+    g = _gen(SEED_BASE + 2, device)
+    (s, w), _ = _lattice((1100, 200), dp, device, origin=(0.0, -0.2))
+    c45 = math.cos(math.pi / 4)
+    keep = (s - 2.0) * c45 + w * c45 < 0
+    s, w = s[keep], w[keep]
+    n = s.numel()
+    ids = torch.arange(n, device=device, dtype=torch.int64)
+    th = math.radians(30.0)
+    X = math.cos(th) * s - math.sin(th) * w
+    Y = math.sin(th) * s + math.cos(th) * w
+    xyz = [X + _jitter(n, g, device, dp), Y + _jitter(n, g, device, dp)]
+    u0 = (math.cos(th), math.sin(th))
+    nrm = (math.cos(math.radians(75.0)), math.sin(math.radians(75.0)))
+    end = (2.0 * math.cos(th), 2.0 * math.sin(th))
+    p0 = _port((0.004 * u0[0], 0.004 * u0[1], 0.0), frame_rows_2d(th), (0.004, 0.2, 0.0), BIDIRECTIONAL, 4)
+    p1 = _port((end[0] - 0.004 * nrm[0], end[1] - 0.004 * nrm[1], 0.0), frame_rows_2d(math.radians(255.0)),
+               (0.004, 0.2 / c45, 0.0), BIDIRECTIONAL, 4)
+    ports = [p0, p1]
+    # velocity: nearest port k, sigma = +1 where Y'_k > 0 else -1 ("sign flipping per region")
+    d0 = (xyz[0] - p0.origin[0]) ** 2 + (xyz[1] - p0.origin[1]) ** 2
+    d1 = (xyz[0] - p1.origin[0]) ** 2 + (xyz[1] - p1.origin[1]) ** 2
+    near1 = d1 < d0
+    v = [torch.zeros(n, dtype=torch.float64, device=device) for _ in range(2)]
+    for k, p in enumerate(ports):
+        sel = near1 if k == 1 else ~near1
+        yl = _local(xyz, p, dim)[1]
+        sig = torch.where(yl > 0, 1.0, -1.0)
+        for j in range(2):
+            v[j] = torch.where(sel, sig * p.Q[j], v[j])
+    v = [v[0] + _noise(n, g, device), v[1] + _noise(n, g, device)]
+    v = _project_near_ports(xyz, v, ports, dim, 2 * dp)
+    xs, ys = xyz[0], xyz[1]
+    pad = 12
+    lo = (f32(float(xs.min()) - pad * cs), f32(float(ys.min()) - pad * cs), 0.0)
+    ncell = (int(math.ceil((float(xs.max()) - lo[0]) / cs)) + pad, int(math.ceil((float(ys.max()) - lo[1]) / cs)) + pad, 1)
+    grid = Grid(dim, lo, cs, ncell)
+    return Workload("C2", dim, dp, h, grid, ports, _pack_state(xyz, v, ids, dim), f32(0.0005), n_updates, n,
+                    notes="30-degree channel, 45-degree slanted end; bidirectional ports at 30 and 255 degrees")
+
+
+def c3(device="cpu", n_updates=100, scale=1.0) -> Workload:
+    """3-D square duct 1.0x0.2x0.2 at dp=0.0025 (2.56M particles at scale 1)."""
+    dim, dp = 3, 0.0025
+    h = 1.3 * dp
+    L = 1.0 * scale
+    nx = int(round(400 * scale))
+    cs = f32(1.0 / 153.0)
+    g = _gen(SEED_BASE + 3, device)
+    xyz, ids = _lattice((nx, 80, 80), dp, device)
+    n = ids.numel()
+    for j in range(3):
+        xyz[j] = xyz[j] + _jitter(n, g, device, dp)
+    v = [1.0 + _noise(n, g, device), _noise(n, g, device), _noise(n, g, device)]
+    I = (1.0, 0.0, 0.0, 0.0, 1.0, 0.0, 0.0, 0.0, 1.0)
+    ports = [_port((0.005, 0.1, 0.1), I, (0.005, 0.1, 0.1), INLET, 4),
+             _port((nx * dp - 0.005, 0.1, 0.1), I, (0.005, 0.1, 0.1), OUTLET, 4)]
+    v = _project_near_ports(xyz, v, ports[:1], dim, 2 * dp)
+    pad = 4
+    lo = (f32(-pad * cs),) * 3
+    ncell = (int(math.ceil(L / cs)) + 2 * pad, int(math.ceil(0.2 / cs)) + 2 * pad, int(math.ceil(0.2 / cs)) + 2 * pad)
+    grid = Grid(dim, lo, cs, ncell)
+    return Workload("C3" if scale == 1.0 else f"C3x{scale:g}", dim, dp, h, grid, ports,
+                    _pack_state(xyz, v, ids, dim), f32(0.0002), n_updates, n,
+                    notes=f"{nx}x80x80 lattice duct; inlet x in (0,0.01), outlet at x={nx * dp:g}")
+
+
+def _draw_ports(rng, nports, box_lo, box_hi, dp, cs, steps, dt, existing, x_margin_lo=True, x_margin_hi=True,
+                bc_range=(0.1, 0.2)):
+    """Random ports: u ~ normalise(N(0,I)), roll ~ U[0,2pi), b,c ~ U[bc_range],
+    he = (2dp, b/2, c/2), 4 layers; even index inlet, odd outlet.  Origins are
+    rejection-sampled so that bounding spheres (inflated by the inlet pre-clear
+    length) stay 2 cells apart and inside the box (margin only on the faces asked)."""
+    ports, radii = [], []
+    prior = list(existing)
+    Lpre = 1.25 * steps * dt + cs
+    for k in range(nports):
+        kind = INLET if k % 2 == 0 else OUTLET
+        for _ in range(10000):
+            u = rng.standard_normal(3)
+            u /= np.linalg.norm(u)
+            psi = rng.uniform(0.0, 2 * math.pi)
+            b, c = rng.uniform(*bc_range, size=2)
+            he = (2 * dp, b / 2, c / 2)
+            r = math.sqrt((he[0] + cs) ** 2 + (he[1] + cs) ** 2 + (he[2] + cs) ** 2)
+            if kind == INLET:
+                r = r + Lpre
+            lo = [box_lo[j] + r + 2 * cs for j in range(3)]
+            hi = [box_hi[j] - r - 2 * cs for j in range(3)]
+            if not x_margin_lo:
+                lo[0] = box_lo[0]
+            if not x_margin_hi:
+                hi[0] = box_hi[0]
+            if any(hi[j] <= lo[j] for j in range(3)):
+                continue
+            o = np.array([rng.uniform(lo[j], hi[j]) for j in range(3)])
+            if all(np.linalg.norm(o - q[0]) > r + q[1] + 2 * cs for q in prior):
+                ports.append(_port(tuple(o), frame_rows_3d(u, psi), he, kind, 4))
+                radii.append(r)
+                prior.append((o, r))
+                break
+        else:
+            raise RuntimeError("could not place port")
+    return ports, prior[len(existing):]
+
+
+def _preclear(xyz, ports, dp, cs, steps, dt):
+    """Remove each inlet's upstream column {-a/2-L < X' < -a/2, lateral in box}
+    and each outlet's downstream strip {a/2 < X' < a/2+m, lateral within he+m},
+    L = 1.25 steps dt + m, so step 1 has no deletion burst (input shaping)."""
+    keep = torch.ones_like(xyz[0], dtype=torch.bool)
+    Lpre = 1.25 * steps * dt + cs
+    for p in ports:
+        r = math.sqrt(sum((h + cs) ** 2 for h in p.half_extents)) + (Lpre if p.kind == INLET else 0.0)
+        d2 = sum((xyz[j] - p.origin[j]) ** 2 for j in range(3))
+        near = d2 < r * r
+        idx = torch.nonzero(near).squeeze(1)
+        if idx.numel() == 0:
+            continue
+        sub = [xyz[j][idx] for j in range(3)]
+        X = _local(sub, p, 3)
+        a2, b2, c2_ = p.half_extents
+        if p.kind == INLET:
+            rm = (X[0] < -a2) & (X[0] > -a2 - Lpre) & (X[1].abs() < b2) & (X[2].abs() < c2_)
+        else:
+            rm = (X[0] > a2) & (X[0] < a2 + cs) & (X[1].abs() < b2 + cs) & (X[2].abs() < c2_ + cs)
+        keep[idx[rm]] = False
+    return keep
+
+
+def _nearest_port_velocity(xyz, ports, n, g, device, dp):
+    best = torch.full((n,), float("inf"), dtype=torch.float64, device=device)
+    v = [torch.zeros(n, dtype=torch.float64, device=device) for _ in range(3)]
+    for p in ports:
+        d2 = sum((xyz[j] - p.origin[j]) ** 2 for j in range(3))
+        sel = d2 < best
+        best = torch.where(sel, d2, best)
+        for j in range(3):
+            v[j] = torch.where(sel, torch.full_like(v[j], p.Q[j]), v[j])
+    v = [v[j] + _noise(n, g, device) for j in range(3)]
+    return _project_near_ports(xyz, v, ports, 3, 2 * dp)
+
+
+def c4(device="cpu", n_updates=100, scale=1.0, nports=8) -> Workload:
+    """3-D 1.6x0.8x0.8 multi-branch junction at dp=0.0025 (reading R20): 640x320x320
+    = 65,536,000 lattice sites before pre-clearing; 8 random ports (4 in, 4 out)."""
+    dim, dp = 3, 0.0025
+    h = 1.3 * dp
+    box = (1.6 * scale, 0.8 * scale, 0.8 * scale)
+    counts = tuple(int(round(b / dp)) for b in box)
+    cs = f32(1.6 / 246.0)
+    dt = 0.0005
+    rng = np.random.default_rng(np.random.SeedSequence(SEED_BASE + 4).spawn(2)[0])
+    bc = (0.1 * scale, 0.2 * scale) if scale < 1 else (0.1, 0.2)
+    ports, _ = _draw_ports(rng, nports, (0, 0, 0), box, dp, cs, n_updates, dt, [], bc_range=bc)
+    g = _gen(SEED_BASE + 4, device)
+    xyz, ids = _lattice(counts, dp, device)
+    n0 = ids.numel()
+    for j in range(3):
+        xyz[j] = xyz[j] + _jitter(n0, g, device, dp)
+    keep = _preclear(xyz, ports, dp, cs, n_updates, dt)
+    xyz = [c[keep] for c in xyz]
+    ids = ids[keep]
+    n = ids.numel()
+    v = _nearest_port_velocity(xyz, ports, n, g, device, dp)
+    pad = 10
+    lo = (f32(-pad * cs),) * 3
+    ncell = tuple(int(math.ceil(b / cs)) + 2 * pad for b in box)
+    grid = Grid(dim, lo, cs, ncell)
+    return Workload("C4" if scale == 1.0 else f"C4x{scale:g}", dim, dp, h, grid, ports,
+                    _pack_state(xyz, v, ids, dim), f32(dt), n_updates, n0,
+                    notes=f"{counts} lattice junction, {nports} random ports, pre-cleared")
+
+
+C5_SLAB_LEN = 1.6
+C5_CELLS_PER_SLAB = 307
+C5_PAD_X = 34
+C5_PAD_YZ = 10
+C5_NEXT_ID = 1 << 40
+
+
+def c5_geometry(scale=1.0):
+    """dp, h, cs, slab length L, width W, lattice counts per slab, cells per slab.
+    cs = L / floor(L / 2h) >= 2h so slab faces lie on cell faces (307 cells at scale 1)."""
+    dp = 0.002
+    h = 1.3 * dp
+    L = C5_SLAB_LEN * scale
+    W = 0.8 * scale
+    cells = int(math.floor(L / (2 * h) + 1e-9))
+    cs = f32(L / cells)
+    counts = (int(round(L / dp)), int(round(W / dp)), int(round(W / dp)))
+    return dp, h, cs, L, W, counts, cells
+
+
+def c5_ports(nslabs: int, scale=1.0, n_updates=50):
+    """Ports of slabs 0..nslabs (one extra slab so every slab's velocity field is
+    P-independent).  Slab r's ports come from its own seeded stream, conditioned on
+    the ports of earlier slabs; x has no margin at interior faces (straddling)."""
+    dp, h, cs, L, W, counts, cells_per_slab = c5_geometry(scale)
+    dt = 0.0005
+    bc = (0.1 * scale, 0.2 * scale) if scale < 1 else (0.1, 0.2)
+    per_slab, prior = [], []
+    for r in range(nslabs + 1):
+        rng = np.random.default_rng(np.random.SeedSequence(SEED_BASE + 5 + 1000 * r))
+        pts, placed = _draw_ports(rng, 8, (L * r, 0.0, 0.0), (L * (r + 1), W, W), dp, cs, n_updates, dt, prior,
+                                  x_margin_lo=(r == 0), x_margin_hi=False, bc_range=bc)
+        per_slab.append(pts)
+        prior += placed
+    return per_slab
+
+
+def c5(device="cpu", slab=0, nslabs=1, scale=1.0, n_updates=50) -> Workload:
+    """3-D weak-scaling junction: slab r = [1.6r, 1.6(r+1)) x [0,0.8]^2 at dp=0.002
+    (800x400x400 = 128M lattice sites per slab at scale 1).  Returns slab ``slab``
+    of an ``nslabs``-slab problem; its content does not depend on nslabs."""
+    dim = 3
+    dp, h, cs, L, W, counts, cells_per_slab = c5_geometry(scale)
+    dt = 0.0005
+    per_slab = c5_ports(max(nslabs, slab + 1), scale, n_updates)
+    ports = [p for r in range(nslabs) for p in per_slab[r]]
+    shaping = [p for r in (slab - 1, slab, slab + 1) if 0 <= r < len(per_slab) for p in per_slab[r]]
+    g = _gen(SEED_BASE + 5 + 1000 * slab, device)
+    per = counts[0] * counts[1] * counts[2]
+    xyz, ids = _lattice(counts, dp, device, origin=(L * slab, 0.0, 0.0), index_offset=per * slab)
+    n0 = ids.numel()
+    for j in range(3):
+        xyz[j] = xyz[j] + _jitter(n0, g, device, dp)
+    keep = _preclear(xyz, shaping, dp, cs, n_updates, dt)
+    xyz = [c[keep] for c in xyz]
+    ids = ids[keep]
+    n = ids.numel()
+    v = _nearest_port_velocity(xyz, shaping, n, g, device, dp)
+    pad_x, pad_yz = C5_PAD_X, C5_PAD_YZ
+    lo = (f32(-pad_x * cs), f32(-pad_yz * cs), f32(-pad_yz * cs))
+    nyz = int(math.ceil(W / cs)) + 2 * pad_yz
+    ncell = (cells_per_slab * nslabs + 2 * pad_x, nyz, nyz)
+    slabs = []
+    for r in range(nslabs):
+        b = 0 if r == 0 else pad_x + cells_per_slab * r
+        e = ncell[0] if r == nslabs - 1 else pad_x + cells_per_slab * (r + 1)
+        slabs.append((b, e))
+    grid = Grid(dim, lo, cs, ncell, slabs[slab][0], slabs[slab][1])
+    name = "C5" if scale == 1.0 else f"C5x{scale:g}"
+    return Workload(name, dim, dp, h, grid, ports, _pack_state(xyz, v, ids, dim), f32(dt), n_updates, C5_NEXT_ID,
+                    notes=f"slab {slab}/{nslabs}, {counts} lattice per slab, 8 ports per slab",
+                    slab_cells=slabs)
+
+
+CONFIGS = {"C1": c1, "C1e": c1e, "C2": c2, "C3": c3, "C4": c4, "C5": c5}
+
+
+def make(name: str, device="cpu", **kw) -> Workload:
+    return CONFIGS[name](device=device, **kw)
+
+
+def capacity_for(w: Workload, headroom: float = 0.06) -> int:
+    """Array capacity with room for the ledger growth of the run."""
+    return int(w.n * (1.0 + headroom)) + 4096

@@ -1,0 +1,470 @@
+"""Pins of the CPU oracle (oracle/) to what the paper and mathematics fix.
+
+Each test cites the passage it checks ("P:n" = PAPER.md line n) and is chosen so
+that a plausible slip in the oracle (a dropped term, a transposed matrix, a wrong
+sign or index, a non-strict comparison, a wrong order) fails at least one of
+them.  None of these expected values is produced by the oracle itself.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2406_16786_b200 import inputs
+from paper_2406_16786_b200.inputs import BIDIRECTIONAL, INLET, OUTLET, Grid, Port, f32
+
+I9 = (1.0, 0.0, 0.0, 0.0, 1.0, 0.0, 0.0, 0.0, 1.0)
+
+
+def mkport(o, Q, he, kind):
+    return Port(tuple(f32(v) for v in o), tuple(f32(v) for v in np.asarray(Q).ravel()), tuple(f32(v) for v in he),
+                kind, 4)
+
+
+def mkstate(points, dim, ids=None, labels=None, vel=None):
+    pts = np.asarray(points, dtype=np.float32).reshape(-1, dim)
+    n = len(pts)
+    st = {"x": pts[:, 0].copy(), "y": pts[:, 1].copy(), "vx": np.zeros(n, np.float32), "vy": np.zeros(n, np.float32)}
+    if dim == 3:
+        st["z"] = pts[:, 2].copy()
+        st["vz"] = np.zeros(n, np.float32)
+    if vel is not None:
+        v = np.asarray(vel, np.float32).reshape(-1, dim)
+        st["vx"], st["vy"] = v[:, 0].copy(), v[:, 1].copy()
+        if dim == 3:
+            st["vz"] = v[:, 2].copy()
+    st["id"] = np.arange(n, dtype=np.int64) if ids is None else np.asarray(ids, np.int64)
+    st["label"] = np.full(n, -1, np.int32) if labels is None else np.asarray(labels, np.int32)
+    return st
+
+
+GRID2 = Grid(2, (f32(-0.052), f32(-0.052), 0.0), f32(0.026), (81, 20, 1))        # C1 grid
+GRID3 = Grid(3, (f32(-0.6), f32(-0.6), f32(-0.6)), f32(0.026), (47, 47, 47))
+
+
+# ------------------------------------------------------------- frames (§III.A)
+
+def test_frame_2d_closed_forms():
+    """Eq. 2D_transformation: origin (1,0), theta=pi/2 maps (1,1) to (1,0);
+    theta=0 is the identity; u = Rot^T e1 = (cos t, sin t) (Eq. 2D_normal_transformation)."""
+    Q = oracle.frame_2d(math.pi / 2)
+    p = mkport((1.0, 0.0, 0.0), Q, (0.02, 0.2, 0), INLET)
+    np.testing.assert_allclose(oracle.to_local(p, 2, (1.0, 1.0), prec=1)[:2], [1.0, 0.0], atol=1e-7)
+    np.testing.assert_allclose(oracle.frame_2d(0.0), np.eye(3), atol=0)
+    for th in (0.3, 1.2, -2.0, math.radians(255.0)):
+        Q = oracle.frame_2d(th)
+        np.testing.assert_allclose(Q.T @ [1, 0, 0], [math.cos(th), math.sin(th), 0], atol=1e-15)
+        # the local X' axis rotated back: local (1,0) -> global (cos t, sin t); theta=pi/2 gives (0,1)
+    np.testing.assert_allclose(oracle.frame_2d(math.pi / 2).T @ [1, 0, 0], [0, 1, 0], atol=1e-15)
+
+
+def test_frame_3d_rodrigues_reading_R1():
+    """Eqs. rotation_axis / antisymmetric_matrix / rotation_matrix with the
+    transpose reading R1: Q u = e1 (Eq. 3D_normal_transformation u = R^T e1).
+    u = (0,1,0): n = z, theta = pi/2, R_rod = [[0,-1,0],[1,0,0],[0,0,1]] by hand, so Q = R_rod^T."""
+    np.testing.assert_allclose(oracle.frame_3d([0, 1, 0]), [[0, 1, 0], [-1, 0, 0], [0, 0, 1]], atol=1e-15)
+    np.testing.assert_allclose(oracle.frame_3d([1, 0, 0]), np.eye(3), atol=0)
+    np.testing.assert_allclose(oracle.frame_3d([-1, 0, 0]), np.diag([-1.0, -1.0, 1.0]), atol=0)
+    rng = np.random.default_rng(7)
+    for _ in range(200):
+        u = rng.standard_normal(3)
+        u /= np.linalg.norm(u)
+        Q = oracle.frame_3d(u)
+        np.testing.assert_allclose(Q @ Q.T, np.eye(3), atol=1e-13)
+        assert abs(np.linalg.det(Q) - 1.0) < 1e-13
+        np.testing.assert_allclose(Q @ u, [1, 0, 0], atol=1e-13)
+        np.testing.assert_allclose(Q[0], u, atol=1e-13)
+        # Rodrigues rotates about n = X x u, so n is a fixed axis of Q
+        n = np.cross([1, 0, 0], u)
+        n /= np.linalg.norm(n)
+        np.testing.assert_allclose(Q @ n, n, atol=1e-13)
+
+
+def test_frame_3d_in_plane_equals_2d():
+    """For an axis in the xy-plane the 3-D construction must reduce to the paper's 2-D
+    matrix: this fails if Q were the literal R_rod instead of R_rod^T."""
+    for th in (0.1, 0.7, 1.5, 2.5, -0.4, -2.9):
+        np.testing.assert_allclose(oracle.frame_3d([math.cos(th), math.sin(th), 0.0]), oracle.frame_2d(th),
+                                   atol=1e-14)
+
+
+def test_recycle_equals_paper_inverse_transform_R10():
+    """Eqs. 2D/3D_Inverse_transformation: r = R^T(r' - [a,0,0]) + o equals
+    r - a u, and to_local(recycled) = r' - a e1."""
+    rng = np.random.default_rng(3)
+    for dim in (2, 3):
+        for _ in range(50):
+            if dim == 2:
+                Q = oracle.frame_2d(rng.uniform(-math.pi, math.pi))
+            else:
+                u = rng.standard_normal(3)
+                Q = oracle.frame_3d(u / np.linalg.norm(u))
+            o = rng.uniform(-1, 1, 3)
+            if dim == 2:
+                o[2] = 0
+            p = mkport(o, Q, (0.02, 0.1, 0.1), INLET)
+            Qf = np.asarray(p.Q, np.float64).reshape(3, 3)
+            x = rng.uniform(-1, 1, 3)
+            if dim == 2:
+                x[2] = 0
+            xl = oracle.to_local(p, dim, x.astype(np.float32), prec=1)
+            back = oracle.inverse_recycle(p, dim, xl)
+            a = 2 * p.half_extents[0]
+            expect = x.astype(np.float32).astype(np.float64) - a * Qf[0]
+            if dim == 2:
+                expect[2] = 0
+            # Q is rounded to binary32, so it is orthonormal only to ~1e-7 (|x| <= 2 here)
+            np.testing.assert_allclose(back, expect, atol=5e-7)
+            p2 = oracle.to_local(p, dim, back, prec=1)
+            np.testing.assert_allclose(p2[:dim], (xl - a * np.eye(3)[0])[:dim], atol=1e-6)
+
+
+# ------------------------------------------------- orthogonal reduction
+
+def test_orthogonal_port_reduces_to_single_axis_compare():
+    """With Q = I the crossing test X' > a/2 is the textbook x > o + a/2."""
+    rng = np.random.default_rng(11)
+    o = (0.3, 0.2, 0.0)
+    he = (0.02, 0.1, 0.0)
+    pts = np.stack([rng.uniform(0.2, 0.4, 4000), rng.uniform(0.05, 0.35, 4000)], 1).astype(np.float32)
+    st = mkstate(pts, 2)
+    out = mkport(o, np.eye(3), he, OUTLET)
+    res = oracle.update(GRID2, [out], st)
+    xs, ys = res.sorted["x"].astype(np.float64), res.sorted["y"].astype(np.float64)
+    m = float(GRID2.cs)
+    expect = (xs - np.float32(o[0]) > np.float32(he[0])) & (np.abs(xs - np.float32(o[0])) < np.float32(he[0]) + m) \
+        & (np.abs(ys - np.float32(o[1])) < np.float32(he[1]) + m)
+    np.testing.assert_array_equal(res.delete_port >= 0, expect)
+
+
+# ------------------------------------------------------------- hand cases H1-H6
+
+def run1(grid, ports, st, next_id=1000, mode=0):
+    res = oracle.update(grid, ports, st, mode=mode)
+    new, perm, nid = oracle.compact(res, grid.dim, len(ports), res.port_counts[None, :], 0, next_id)
+    return res, new, perm, nid
+
+
+def test_H1_inlet_orthogonal():
+    """Alg. 1 + Eq. 2D_Inverse_transformation: member at (0.0405, 0.1) has
+    X' = (0.0205, -0.1) > a/2 = 0.02 -> duplicate at (0.0405, 0.1), member recycled by a = 0.04."""
+    p = mkport((0.02, 0.2, 0), np.eye(3), (0.02, 0.2, 0), INLET)
+    st = mkstate([[0.0405, 0.1], [0.0395, 0.1]], 2, ids=[5, 6], labels=[0, 0], vel=[[1.0, 0.0], [1.0, 0.0]])
+    res, new, perm, nid = run1(GRID2, [p], st)
+    assert list(res.port_counts) == [1, 0]
+    assert len(new["x"]) == 3 and nid == 1001
+    dup = np.where(new["id"] == 1000)[0][0]
+    assert new["label"][dup] == -1 and new["x"][dup] == np.float32(0.0405) and new["vx"][dup] == 1.0
+    src = np.where(new["id"] == 5)[0][0]
+    assert abs(float(new["x"][src]) - 0.0005) < 1e-7 and new["y"][src] == np.float32(0.1)
+    assert new["label"][src] == 0
+    other = np.where(new["id"] == 6)[0][0]
+    assert new["x"][other] == np.float32(0.0395)
+
+
+def test_H2_inlet_30deg():
+    """H2: o = 0, theta = 30 deg, a = 0.04.  Local (0.021, 0.05) is global
+    (0.021 cos30 - 0.05 sin30, 0.021 sin30 + 0.05 cos30) = (-0.00681347, 0.05380127); it
+    crosses (0.021 > 0.02) and is recycled to (-0.04145448, 0.03380127) = local (-0.019, 0.05)."""
+    th = math.radians(30)
+    p = mkport((0, 0, 0), oracle.frame_2d(th), (0.02, 0.2, 0), INLET)
+    g = Grid(2, (f32(-0.52), f32(-0.52), 0.0), f32(0.026), (40, 40, 1))
+    st = mkstate([[-0.00681347, 0.05380127]], 2, ids=[1], labels=[0])
+    res, new, perm, nid = run1(g, [p], st)
+    assert list(res.port_counts) == [1, 0]
+    src = np.where(new["id"] == 1)[0][0]
+    np.testing.assert_allclose([new["x"][src], new["y"][src]], [-0.04145448, 0.03380127], atol=2e-7)
+    np.testing.assert_allclose(oracle.to_local(p, 2, (new["x"][src], new["y"][src]), prec=1)[:2], [-0.019, 0.05],
+                               atol=2e-7)
+    dup = np.where(new["id"] == 1000)[0][0]
+    np.testing.assert_allclose([new["x"][dup], new["y"][dup]], [-0.00681347, 0.05380127], atol=1e-8)
+
+
+def test_H3_outlet_deletion_region():
+    """Alg. 2 with the P_k gate (reading R4, m = cs = 0.026):
+    delete (2.0005, 0.1) and (2.01, 0.4205) (Y' = 0.2205 < 0.226); keep (1.9995, 0.1)
+    (X' = 0.0195), (2.0465, 0.1) (X' = 0.0665 > a/2 + m = 0.046) and (2.01, 0.43) (Y' = 0.23)."""
+    p = mkport((1.98, 0.2, 0), np.eye(3), (0.02, 0.2, 0), OUTLET)
+    pts = [[2.0005, 0.1], [2.01, 0.4205], [1.9995, 0.1], [2.0465, 0.1], [2.01, 0.43]]
+    st = mkstate(pts, 2, ids=[10, 11, 12, 13, 14])
+    res, new, perm, nid = run1(GRID2, [p], st)
+    assert sorted(set(range(10, 15)) - set(new["id"].tolist())) == [10, 11]
+    assert list(res.port_counts) == [0, 2]
+    # relabel: (1.9995, 0.1) is inside the box -> member; others fluid
+    lab = dict(zip(new["id"].tolist(), new["label"].tolist()))
+    assert lab == {12: 0, 13: -1, 14: -1}
+
+
+def test_H4_inlet_3d_rotated():
+    """u = (0,1,0), Q = [[0,1,0],[-1,0,0],[0,0,1]] (reading R1), o = 0, he = (0.02, 0.5, 0.5):
+    member (0.1, 0.0205, 0.3) has X' = (0.0205, -0.1, 0.3) -> duplicate, recycled to (0.1, -0.0195, 0.3)."""
+    Q = np.array([[0, 1, 0], [-1, 0, 0], [0, 0, 1]], float)
+    p = mkport((0, 0, 0), Q, (0.02, 0.5, 0.5), INLET)
+    np.testing.assert_allclose(oracle.to_local(p, 3, (0.1, 0.0205, 0.3), prec=1), [0.0205, -0.1, 0.3], atol=1e-8)
+    st = mkstate([[0.1, 0.0205, 0.3]], 3, ids=[3], labels=[0])
+    res, new, perm, nid = run1(GRID3, [p], st)
+    assert list(res.port_counts) == [1, 0]
+    src = np.where(new["id"] == 3)[0][0]
+    np.testing.assert_allclose([new["x"][src], new["y"][src], new["z"][src]], [0.1, -0.0195, 0.3], atol=1e-8)
+
+
+def test_H5_bidirectional():
+    """Alg. 3: member at X' = +0.0205 -> create + recycle; member at
+    -0.0205 -> delete; non-member at +0.0205 -> nothing; member inside stays; fluid inside
+    becomes a member (relabel)."""
+    p = mkport((1.0, 0.2, 0), np.eye(3), (0.02, 0.2, 0), BIDIRECTIONAL)
+    pts = [[1.0205, 0.1], [0.9795, 0.1], [1.0205, 0.3], [1.0, 0.2], [1.005, 0.25]]
+    st = mkstate(pts, 2, ids=[0, 1, 2, 3, 4], labels=[0, 0, -1, 0, -1])
+    res, new, perm, nid = run1(GRID2, [p], st)
+    assert list(res.port_counts) == [1, 1]
+    ids = new["id"].tolist()
+    assert 1 not in ids and 1000 in ids
+    lab = dict(zip(ids, new["label"].tolist()))
+    assert lab[0] == 0 and lab[2] == -1 and lab[3] == 0 and lab[4] == 0 and lab[1000] == -1
+    x0 = new["x"][ids.index(0)]
+    assert abs(float(x0) - 0.9805) < 1e-6
+
+
+def test_H6_new_id_order_is_port_cell_id():
+    """Reading R14: new IDs follow (port, source cell, source id).  ID 9 sits in a
+    lower cell than ID 7, so next_id goes to the copy of 9 and next_id+1 to the copy of 7;
+    a second port's crossing gets the later IDs even though its cell is lower."""
+    p0 = mkport((1.0, 0.2, 0), np.eye(3), (0.02, 0.2, 0), INLET)
+    p1 = mkport((0.3, 0.2, 0), np.eye(3), (0.02, 0.05, 0), INLET)
+    pts = [[1.0205, 0.3], [1.0205, 0.05], [0.3205, 0.2]]     # id 7 (cell y higher), id 9 (cell y lower), id 4
+    st = mkstate(pts, 2, ids=[7, 9, 4], labels=[0, 0, 1])
+    res, new, perm, nid = run1(GRID2, [p0, p1], st, next_id=500)
+    ids = new["id"].tolist()
+    pos = {i: (new["x"][j], new["y"][j]) for j, i in enumerate(ids)}
+    assert pos[500][1] == np.float32(0.05)      # copy of id 9
+    assert pos[501][1] == np.float32(0.3)       # copy of id 7
+    assert pos[502][0] == np.float32(0.3205)    # port 1
+    assert nid == 503
+
+
+def test_strict_inequalities_at_faces():
+    """Strict '<' and '>': a particle exactly on X' = a/2 is
+    neither in the box nor crossing."""
+    p = mkport((0.5, 0.25, 0), np.eye(3), (0.25, 0.125, 0), OUTLET)     # exact binary fractions
+    st = mkstate([[0.75, 0.25], [0.5, 0.375], [0.5, 0.25]], 2)
+    res, new, perm, nid = run1(GRID2, [p], st)
+    assert list(res.port_counts) == [0, 0]
+    lab = dict(zip(new["id"].tolist(), new["label"].tolist()))
+    assert lab == {0: -1, 1: -1, 2: 0}
+
+
+# ---------------------------------------------------- lattice counts
+
+def test_C1_member_counts_and_no_events():
+    """C1 (BASELINE configs[0]): a = 4dp, b = 40dp on a cell-centred lattice with
+    +-0.1dp jitter -> 4 x 40 = 160 members per port; one step of 0.2dp
+    moves nothing across a threshold (reading R18)."""
+    w = inputs.make("C1")
+    st = oracle.to_numpy_state(w.state)
+    assert w.n == 8000
+    assert [oracle.register(st, w.grid, p, k) for k, p in enumerate(w.ports)] == [160, 160]
+    new, res, perm, nid = oracle.step(st, w.grid, w.ports, w.next_id, w.dt)
+    assert list(res.port_counts) == [0, 0, 0, 0] and len(new["x"]) == 8000
+
+
+def test_C1e_exactly_last_layer_crosses():
+    """C1e (dt = 0.0095): the last inlet layer sits at x = 0.035 +- 0.001 and moves
+    0.0095 +- 0.0019 -> all 40 pass 0.04; the next layer (0.025) cannot.  Same at the
+    outlet boundary x = 2.0 (layer 1.995) -> exactly 40 created and 40 deleted."""
+    w = inputs.make("C1e")
+    st = oracle.to_numpy_state(w.state)
+    for k, p in enumerate(w.ports):
+        oracle.register(st, w.grid, p, k)
+    new, res, perm, nid = oracle.step(st, w.grid, w.ports, w.next_id, w.dt)
+    assert list(res.port_counts) == [40, 0, 0, 40]
+    assert len(new["x"]) == 8000 and nid == 8040
+    assert sorted(new["id"][new["id"] >= 8000].tolist()) == list(range(8000, 8040))
+
+
+def test_C3_inlet_members_lattice_count():
+    """C3 inlet a = 4dp, b = c = 80dp -> 4 x 80 x 80 = 25,600 members."""
+    w = inputs.c3(scale=0.25)
+    st = oracle.to_numpy_state(w.state)
+    assert oracle.register(st, w.grid, w.ports[0], 0) == 25600
+
+
+# ----------------------------------------------------------- invariants (§8(c) O7)
+
+def _check_step(grid, ports, st, next_id, dt):
+    """One update with every O7 self-check; returns (new_state, next_id)."""
+    dim = grid.dim
+    K = len(ports)
+    n0 = len(st["x"])
+    before = oracle.to_numpy_state(st)
+    oracle.advect(st, dim, dt)
+    res = oracle.update(grid, ports, st, mode=0)
+    res_r = oracle.update(grid, ports, st, mode=1)
+    # brute force == cell-restricted (the paper's local cell-linked lists)
+    np.testing.assert_array_equal(res.create_port, res_r.create_port)
+    np.testing.assert_array_equal(res.delete_port, res_r.delete_port)
+    for c in res.sorted:
+        if c != "extra":
+            np.testing.assert_array_equal(res.sorted[c], res_r.sorted[c])
+    assert res_r.checked < res.checked or n0 == 0
+    assert res.multi_decision == 0 and res.motion_errors == 0
+    # cell list: contiguous ranges, ascending ids within cells, counts match
+    # (sampled) the cell of the particle at sorted position j (positions at build time,
+    # i.e. before recycling) lies in [cell_start, cell_end); ids ascend within a cell
+    js = np.arange(0, n0, max(1, n0 // 500))
+    cells = np.array([oracle.cell_of(grid, [st[c][res.order[j]] for c in ("x", "y", "z")[:dim]])[0] for j in js])
+    for j, c in zip(js, cells):
+        ids_c = res.sorted["id"][res.cell_start[c]:res.cell_end[c]]
+        assert np.all(np.diff(ids_c) > 0)
+    assert np.all(res.cell_start[cells] <= js) and np.all(js < res.cell_end[cells])
+    assert res.cell_end[-1] == n0 if len(res.cell_end) else True
+    assert np.all(res.cell_start[1:] == res.cell_end[:-1])
+    # spawn fidelity: staged copy == source state before the recycle
+    src_ids = res.staged["id"]
+    id2pre = {int(i): j for j, i in enumerate(st["id"])}
+    for t in range(len(src_ids)):
+        j = id2pre[int(src_ids[t])]
+        for c in ("x", "y", "z", "vx", "vy", "vz"):
+            if c in st:
+                assert res.staged[c][t] == st[c][j]
+    # recycled members are back inside the box axially: |X'| < a/2, lateral unchanged
+    for t in range(len(src_ids)):
+        k = res.stage_port[t]
+        p = ports[k]
+        j = res.stage_src[t]
+        xl_old = oracle.to_local(p, dim, [st[c][id2pre[int(src_ids[t])]] for c in ("x", "y", "z")[:dim]], prec=1)
+        xl = oracle.to_local(p, dim, [res.sorted[c][j] for c in ("x", "y", "z")[:dim]], prec=1)
+        assert abs(xl[0]) < p.half_extents[0]
+        np.testing.assert_allclose(xl[1:dim], xl_old[1:dim], atol=2e-6)
+    # f64 decisions agree with pinned fp32 away from ties
+    res64 = oracle.update(grid, ports, st, mode=0, prec=1)
+    diff = np.nonzero((res64.create_port != res.create_port) | (res64.delete_port != res.delete_port))[0]
+    for j in diff:
+        near = False
+        for p in ports:
+            xl = oracle.to_local(p, dim, [res.sorted[c][j] for c in ("x", "y", "z")[:dim]], prec=1)
+            faces = [abs(abs(xl[r]) - p.half_extents[r]) for r in range(dim)]
+            faces += [abs(abs(xl[r]) - p.half_extents[r] - grid.cs) for r in range(dim)]
+            near |= min(faces) < 1e-6
+        assert near, "f64 and fp32 decisions differ away from a face"
+    # ledger
+    new, perm, nid = oracle.compact(res, dim, K, res.port_counts[None, :], 0, next_id)
+    C_ = int(res.port_counts[:K].sum())
+    D_ = int(res.port_counts[K:].sum())
+    assert len(new["x"]) == n0 + C_ - D_
+    assert nid == next_id + C_
+    assert len(np.unique(new["id"])) == len(new["id"])
+    assert np.sum(perm >= 0) == n0 - D_
+    assert np.all(np.diff(perm[perm >= 0]) == 1)            # stable
+    # inlet member count is constant
+    for k, p in enumerate(ports):
+        if p.kind == INLET:
+            assert np.sum(new["label"] == k) == np.sum(before["label"] == k)
+    # outlet / bidirectional membership == brute-force in-box scan, numpy f64,
+    # ignoring particles within 1e-6 of a face (there fp32 and f64 may differ)
+    old_mask = new["id"] < next_id
+    P = np.stack([new[c][old_mask].astype(np.float64) for c in ("x", "y", "z")[:dim]], 1)
+    for k, p in enumerate(ports):
+        if p.kind == INLET:
+            continue
+        Qm = np.asarray(p.Q, np.float64).reshape(3, 3)[:dim, :dim]
+        XL = (P - np.asarray(p.origin[:dim], np.float64)) @ Qm.T
+        he = np.asarray(p.half_extents[:dim], np.float64)
+        inb = np.all(np.abs(XL) < he, axis=1)
+        tie = np.any(np.abs(np.abs(XL) - he) < 1e-6, axis=1)
+        lab = new["label"][old_mask] == k
+        assert np.all((lab == inb) | tie)
+    return new, nid, res
+
+
+def test_invariants_C1e():
+    w = inputs.make("C1e")
+    st = oracle.to_numpy_state(w.state)
+    for k, p in enumerate(w.ports):
+        oracle.register(st, w.grid, p, k)
+    _check_step(w.grid, w.ports, st, w.next_id, w.dt)
+
+
+@pytest.mark.slow
+def test_invariants_C2_bidirectional_steps():
+    w = inputs.make("C2")
+    st = oracle.to_numpy_state(w.state)
+    for k, p in enumerate(w.ports):
+        oracle.register(st, w.grid, p, k)
+    nid = w.next_id
+    tot = np.zeros(4, int)
+    for _ in range(6):
+        st, nid, res = _check_step(w.grid, w.ports, st, nid, w.dt)
+        tot += res.port_counts
+    assert tot[:2].sum() > 0 and tot[2:].sum() > 0      # both generation and deletion happen
+
+
+def test_invariants_3d_junction_small():
+    w = inputs.c4(scale=0.25, nports=4, n_updates=10)
+    st = oracle.to_numpy_state(w.state)
+    for k, p in enumerate(w.ports):
+        oracle.register(st, w.grid, p, k)
+    nid = w.next_id
+    tot = np.zeros(8, int)
+    for _ in range(3):
+        st, nid, res = _check_step(w.grid, w.ports, st, nid, w.dt)
+        tot += res.port_counts
+    assert tot[:4].sum() > 0 and tot[4:].sum() > 0
+
+
+def test_C3_flux_sanity():
+    """Steady inflow: creations per update ~ members * |v.u| dt / a = 25,600 * 0.08/4 = 512
+    (SURVEY §8(c) flux sanity).  The lattice makes creation bursty (one layer every
+    12.5 updates), so the mean is taken over 100 updates (8 layers) within 10%."""
+    w = inputs.c3(scale=0.1, n_updates=100)
+    st = oracle.to_numpy_state(w.state)
+    for k, p in enumerate(w.ports):
+        oracle.register(st, w.grid, p, k)
+    nid = w.next_id
+    created = 0
+    for _ in range(100):
+        st, res, perm, nid = oracle.step(st, w.grid, w.ports, nid, w.dt)
+        created += int(res.port_counts[0])
+    assert abs(created / 100 - 512) < 0.1 * 512
+
+
+def test_ids_independent_of_slab_split():
+    """§8(e): per-slab updates with IDs from the allgathered count matrix reproduce the
+    single-slab IDs and states exactly (x-major cells, contiguous x-slabs)."""
+    w = inputs.c4(scale=0.25, nports=4, n_updates=10)
+    st = oracle.to_numpy_state(w.state)
+    for k, p in enumerate(w.ports):
+        oracle.register(st, w.grid, p, k)
+    oracle.advect(st, 3, w.dt)
+    K = len(w.ports)
+    one = oracle.update(w.grid, w.ports, st)
+    ref, _, nid_ref = oracle.compact(one, 3, K, one.port_counts[None, :], 0, w.next_id)
+    ncx = w.grid.ncell[0]
+    cuts = [0, ncx // 3, ncx // 2 + 3, ncx]
+    parts, counts = [], []
+    for r in range(3):
+        g = w.grid.slab(cuts[r], cuts[r + 1])
+        lo = w.grid.lo[0] + cuts[r] * w.grid.cs
+        hi = w.grid.lo[0] + cuts[r + 1] * w.grid.cs
+        # ownership by the pinned cell index
+        cx = np.floor((st["x"] - np.float32(w.grid.lo[0])) * np.float32(1.0 / w.grid.cs)).astype(np.int64)
+        cx = np.clip(cx, 0, ncx - 1)
+        sel = (cx >= cuts[r]) & (cx < cuts[r + 1])
+        sub = {k: v[sel] for k, v in st.items() if k != "extra"}
+        res = oracle.update(g, w.ports, sub)
+        parts.append((g, res))
+        counts.append(res.port_counts)
+        del lo, hi
+    allc = np.stack(counts)
+    outs = []
+    nids = set()
+    for r, (g, res) in enumerate(parts):
+        s, _, nid = oracle.compact(res, 3, K, allc, r, w.next_id)
+        outs.append(s)
+        nids.add(nid)
+    assert nids == {nid_ref}
+    cat = {k: np.concatenate([o[k] for o in outs]) for k in ref}
+    order_ref = np.argsort(ref["id"])
+    order_cat = np.argsort(cat["id"])
+    for k in ref:
+        np.testing.assert_array_equal(ref[k][order_ref], cat[k][order_cat])
