@@ -1,0 +1,403 @@
+#!/usr/bin/env python
+"""Benchmark of the in/outlet buffer update (arXiv 2406.16786) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C5|C4|C3|C2]
+
+A step is one update of the whole hot path on one
+batch of synthetic particles: advect (driver) -> [migrate, N>1] -> sph_cll_build
+-> sph_buffer_update -> [count allgather, N>1] -> sph_compact.  Default workload:
+C5 (BASELINE configs[4]): 128M particles per GPU in x-slabs, 8 ports per slab,
+weak scaling; inputs (4.6 GB per GPU) are far larger than L2, so no flush is
+needed between steps.  value = candidate particles checked per second summed
+over ranks (the metric's "buffer-update particles checked/sec").
+
+--impl reference times the CPU oracle (the "reference arm"; test
+infrastructure, oracle/) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from paper_2406_16786_b200 import inputs, sphbuf
+from paper_2406_16786_b200.dist import Comm, SlabUpdater
+
+PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM = 6650.0
+
+
+def hbm_peak():
+    try:
+        with open(PEAKS) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
+
+
+# ------------------------------------------------------------------ clocks
+
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ workload
+
+def make_workload(name, rank, world, device, scale=1.0):
+    if name == "C5":
+        return inputs.c5(device=device, slab=rank, nslabs=world, scale=scale)
+    if world != 1:
+        raise SystemExit(f"config {name} is single-GPU; use C5 for N>1")
+    if name == "C4":
+        return inputs.c4(device=device, scale=scale)
+    if name == "C3":
+        return inputs.c3(device=device, scale=scale)
+    return inputs.make(name, device=device)
+
+
+# algorithmic bytes per launch for the roofline of one kernel
+def algorithmic_bytes(kernel, dim, n, ncells, cand, created, deleted, moved):
+    S = 8 * dim + 12
+    return {
+        "advect": n * (2 * dim * 4 + dim * 4),
+        "cll_key": n * (4 * dim + 4),
+        "cell_scan": ncells * 12,
+        "cll_scatter": n * 8,
+        "cll_gather": n * 2 * S,
+        "upd_main": cand * (4 * dim + 4) + created * (2 * S + 4 * dim),
+        "compact": moved * S + (moved - deleted) * S,
+        "compact_append": created * S,
+    }.get(kernel)
+
+
+def run_ours(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        if world == 1 and args.gpus > 1:
+            raise SystemExit("--gpus N>1 must be launched with torch.distributed.run")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    tgen = time.time()
+    w = make_workload(args.config, rank, world, dev, args.scale)
+    torch.cuda.synchronize()
+    tgen = time.time() - tgen
+    cap = inputs.capacity_for(w, 0.05)
+    max_new = max(65536, w.n // 200)
+    su = SlabUpdater(w, rank, world, cap, max_migrate=1 << 18, max_new=max_new, comm=Comm(rank, world), device=dev)
+    su.load(w.state, w.next_id)
+    n0 = w.n
+    del w.state
+    torch.cuda.empty_cache()
+    bu = su.bu
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        su.step(w.dt)
+    s = bu.stats()
+    checked0 = s["checked_total"]
+    sphbuf.sph_profile(bu.ctx, True)
+    launches0 = bu.launches()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        su.step(w.dt)
+    e1.record(stream)
+    barrier()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    launches = bu.launches() - launches0
+    prof = sphbuf.sph_profile_read(bu.ctx)
+    sphbuf.sph_profile(bu.ctx, False)
+    s = bu.stats()
+    checked = s["checked_total"] - checked0
+    t = torch.tensor([ms, float(checked)], dtype=torch.float64, device=dev)
+    if world > 1:
+        tmax = t.clone()
+        dist.all_reduce(tmax[:1], op=dist.ReduceOp.MAX)
+        tsum = t.clone()
+        dist.all_reduce(tsum[1:], op=dist.ReduceOp.SUM)
+        ms_max, checked_all = float(tmax[0]), float(tsum[1])
+    else:
+        ms_max, checked_all = ms, float(checked)
+    value = checked_all / (ms_max / 1e3)
+
+    # roofline of the dominant kernel (live CUDA-event times of the timed region)
+    dim = bu.dim
+    n = s["n"]
+    ncells = w.grid.ncells_local
+    per_kernel = {k: v for k, v in prof.items() if v[1] > 0}
+    dom = max(per_kernel, key=lambda k: per_kernel[k][0])
+    dom_ms = per_kernel[dom][0] / per_kernel[dom][1]
+    cand = checked / max(1, args.steps)
+    created = s["created"]
+    deleted = s["deleted"]
+    moved = max(0, n + deleted - created - s["first_deleted"]) if deleted else 0
+    bytes_dom = algorithmic_bytes(dom, dim, n, ncells, cand, created, deleted, moved)
+    peak, peak_src = hbm_peak()
+    achieved = bytes_dom / (dom_ms / 1e3) / 1e9 if bytes_dom else None
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get(args.config, {}).get(dom)
+        except Exception:
+            traffic = None
+    step_ms = ms_max / args.steps
+    kernels = {k: {"ms_per_launch": round(v[0] / v[1], 4), "share": round(v[0] / sum(x[0] for x in per_kernel.values()), 4)}
+               for k, v in per_kernel.items()}
+
+    # e2e: same metric through the public API with host-resident particles
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(su, w, args, dev, world)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(args, dev)
+    if rank == 0:
+        line = {
+            "metric": "buffer-update particles checked/sec & us/step; % of B200 HBM peak; 1/2/4/8 GPU",
+            "value": value, "unit": "particles_checked/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": step_ms, "us_per_step": step_ms * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded lattice + jitter, BASELINE config shapes)",
+            "config": {"workload": f"{args.config}" + (f" scale {args.scale}" if args.scale != 1 else ""),
+                       "particles_per_gpu": n0, "ports": len(su.bu.ports), "candidates_per_step": cand,
+                       "created_last": created, "deleted_last": deleted, "dim": dim,
+                       "parallelism": f"x-slab dp{world}", "l2": "inputs (>=4.6 GB/GPU) larger than L2; no flush",
+                       "gen_s": round(tgen, 1)},
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak if achieved else None, "traffic": traffic,
+                         "peak_source": peak_src, "alg_bytes_per_launch": bytes_dom, "ms_per_launch": dom_ms},
+            "kernels": kernels,
+            "gpu_launches": launches,
+            "clocks": clk,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_e2e(su, w, args, dev, world):
+    """The same metric end to end: each step copies the rank's particle state from
+    pinned host memory to the device (H2D), runs the update through the public
+    API, and reads the updated state back (D2H).  Host-resident simulation loop."""
+    bu = su.bu
+    n = bu.A.count()
+    cols = list(bu.A.cols.items())
+    host_in = {c: torch.empty(bu.capacity, dtype=t.dtype, pin_memory=True) for c, t in cols}
+    host_in["id"] = torch.empty(bu.capacity, dtype=torch.int64, pin_memory=True)
+    host_in["label"] = torch.empty(bu.capacity, dtype=torch.int32, pin_memory=True)
+    host_out = {c: torch.empty_like(v).pin_memory() for c, v in host_in.items()}
+    for c, t in cols:
+        host_in[c][:n].copy_(t[:n])
+    host_in["id"][:n].copy_(bu.A.id[:n])
+    host_in["label"][:n].copy_(bu.A.label[:n])
+    steps = max(2, min(args.steps, args.e2e_steps))
+    stream = torch.cuda.current_stream()
+    checked0 = bu.stats()["checked_total"]
+    h2d = d2h = 0
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        for c, t in cols:
+            t[:n].copy_(host_in[c][:n], non_blocking=True)
+        bu.A.id[:n].copy_(host_in["id"][:n], non_blocking=True)
+        bu.A.label[:n].copy_(host_in["label"][:n], non_blocking=True)
+        bu.A.n.fill_(n)
+        h2d += n * (4 * len(cols) + 12)
+        su.step(w.dt)
+        n = int(bu.A.n.item())
+        for c, t in cols:
+            host_out[c][:n].copy_(t[:n], non_blocking=True)
+        host_out["id"][:n].copy_(bu.A.id[:n], non_blocking=True)
+        host_out["label"][:n].copy_(bu.A.label[:n], non_blocking=True)
+        d2h += n * (4 * len(cols) + 12) + 8
+        host_in, host_out = host_out, host_in
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    checked = bu.stats()["checked_total"] - checked0
+    t = torch.tensor([ms, float(checked)], dtype=torch.float64, device=dev)
+    if world > 1:
+        a = t.clone()
+        dist.all_reduce(a[:1], op=dist.ReduceOp.MAX)
+        b = t.clone()
+        dist.all_reduce(b[1:], op=dist.ReduceOp.SUM)
+        ms, checked = float(a[0]), float(b[1])
+    return {"value": checked / (ms / 1e3), "unit": "particles_checked/s", "ms_per_step": ms / steps,
+            "steps": steps, "h2d_bytes_per_step": h2d // steps, "d2h_bytes_per_step": d2h // steps,
+            "what": "pinned host state -> device, update via BufferUpdater/SlabUpdater, state -> pinned host"}
+
+
+# ------------------------------------------------------------------ CPU oracle (reference arm / cpu_baseline)
+
+def oracle_sample(args, dev):
+    """Bounded sample of the workload for the oracle: the same config at 1/8 of the
+    volume (scale 0.5: same dp, cell size, port shapes scaled)."""
+    import oracle
+    sc = args.cpu_scale
+    w = make_workload(args.config, 0, 1, dev, sc * args.scale) if args.config in ("C3", "C4", "C5") else \
+        make_workload(args.config, 0, 1, dev)
+    st = oracle.to_numpy_state(w.state)
+    for k, p in enumerate(w.ports):
+        oracle.register(st, w.grid, p, k)
+    return w, st
+
+
+def oracle_step_timed(w, st, nid):
+    import oracle
+    oracle.advect(st, w.dim, w.dt)
+    t0 = time.perf_counter()
+    res = oracle.update(w.grid, w.ports, st, mode=0)
+    new, perm, nid = oracle.compact(res, w.dim, len(w.ports), res.port_counts[None, :], 0, nid)
+    dt = time.perf_counter() - t0
+    # the method's candidates in this sample (cells intersecting P_k), the metric's unit of work
+    cand = 0
+    for p in w.ports:
+        m = oracle.port_cells(w.grid, p).astype(bool)
+        cand += int((res.cell_end - res.cell_start)[m].sum())
+    return new, nid, dt, cand
+
+
+def cpu_baseline(args, dev):
+    w, st = oracle_sample(args, dev)
+    new, nid, dt, cand = oracle_step_timed(w, st, w.next_id)
+    return {"value": cand / dt, "unit": "particles_checked/s", "cores": 1, "kind": "oracle",
+            "sample": f"one oracle update (brute force O2-O6, decide+apply+compact) of {args.config} at scale "
+                      f"{args.cpu_scale * args.scale} ({w.n} particles, {len(w.ports)} ports), {dt:.2f} s"}
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    dev = torch.device("cuda", 0) if torch.cuda.is_available() else torch.device("cpu")
+    w, st = oracle_sample(args, dev)
+    nid = w.next_id
+    for _ in range(args.warmup):
+        st, nid, _, _ = oracle_step_timed(w, st, nid)
+    tot, cand = 0.0, 0
+    for _ in range(args.steps):
+        st, nid, dt, c = oracle_step_timed(w, st, nid)
+        tot += dt
+        cand += c
+    v = cand / tot
+    line = {"impl": "reference", "metric": "buffer-update particles checked/sec & us/step; % of B200 HBM peak; "
+            "1/2/4/8 GPU", "value": v, "unit": "particles_checked/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": tot / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"{args.config} sample at scale {args.cpu_scale * args.scale}",
+                       "particles": w.n, "ports": len(w.ports)},
+            "cpu_baseline": {"value": v, "unit": "particles_checked/s", "cores": 1, "kind": "oracle",
+                             "sample": f"{args.steps} oracle updates of {args.config} at scale "
+                                       f"{args.cpu_scale * args.scale} ({w.n} particles)"},
+            "e2e": {"value": v, "unit": "particles_checked/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C5")
+    ap.add_argument("--scale", type=float, default=1.0)
+    ap.add_argument("--cpu-scale", type=float, default=0.5)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,223 @@
+/*
+ * sphbuf.h — C ABI of the B200-native in/outlet buffer update for SPH
+ * (Zhang, Fan, Ren, Qian & Hu, arXiv 2406.16786, §III "The rationale of
+ * arbitrary-positioned buffer").  Citations "P:n" are PAPER.md lines.
+ *
+ * Scope: cell-linked-list build (a1), per-port cell
+ * enumeration (a2), candidate transform + axial compare (a3), inflow generation
+ * (a4, Alg. 1 / Alg. 3), outflow deletion (a5, Alg. 2 / Alg. 3), relabel (a6)
+ * and ID assignment + stable compaction (a7), plus the slab-migration kernels of
+ * the multi-GPU decomposition (§8(e)).
+ *
+ * Conventions
+ *  - Every pointer inside sph_particles, every cell table, count array and the
+ *    workspace is DEVICE memory owned by the caller (torch tensors).  The library
+ *    owns only the host-side context.  Nothing is freed behind the caller's back.
+ *  - Calls that take `stream` (a cudaStream_t passed as void*) only enqueue work
+ *    on that stream and return; no call synchronises except sph_status_sync.
+ *    Live counts stay device-resident (`n_dev`), so a whole update can be
+ *    captured into a CUDA graph.
+ *  - Host-side argument errors are returned immediately with no work enqueued.
+ *    Device-side errors (capacity, staging overflow, excessive motion) are
+ *    recorded in a sticky device status word and reported by the next
+ *    sph_status_sync; after one the particle state is undefined.
+ *  - Arithmetic that decides an integer (cell index, crossing, in-box) or mutates
+ *    state (recycle, advection) is pinned: each op one binary32 round-to-nearest
+ *    operation in the order documented in DESIGN.md §3, never contracted to FMA.
+ *  - Layout: structure of arrays; cells linearised x-major
+ *    ((cx - cx_begin) * ny + cy) * nz + cz  (nz = 1 in 2-D); the particle array
+ *    after sph_cll_build is ordered by (cell, id).
+ */
+#ifndef SPHBUF_H
+#define SPHBUF_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SPH_MAX_PORTS 64      /* ports per context (C5 at 8 GPUs uses 64) */
+#define SPH_MAX_EXTRA 8       /* optional fp32 columns copied on duplication */
+
+typedef struct sph_ctx sph_ctx;
+
+typedef enum {
+    SPH_OK = 0,
+    SPH_ERR_ARG = -1,              /* bad argument (dim, extents, layers < 3, too many ports, NULL) */
+    SPH_ERR_NOT_ORTHONORMAL = -2,  /* |Q Q^T - I|max > 1e-5 or det Q <= 0 (or 2-D Q not planar) */
+    SPH_ERR_OVERLAP = -3,          /* decision region P_k intersects an existing port's P_j */
+    SPH_ERR_OUT_OF_GRID = -4,      /* P_k not strictly inside the grid */
+    SPH_ERR_CAPACITY = -5,         /* (device) N - D + C > capacity, or staging/migration buffer full */
+    SPH_ERR_MOTION = -6,           /* (device) a buffer particle moved more than a buffer length */
+    SPH_ERR_CUDA = -7,             /* a CUDA runtime call failed (see sph_last_error) */
+    SPH_ERR_STATE = -9             /* call order violated (e.g. no workspace) */
+} sph_status;
+
+/* Port kinds: unidirectional inlet (Alg. 1), unidirectional
+ * outlet (Alg. 2), bidirectional (Alg. 3; X' points along the inflow). */
+typedef enum { SPH_INLET = 0, SPH_OUTLET = 1, SPH_BIDIRECTIONAL = 2 } sph_kind;
+
+/* Uniform cell grid (cell size >= 2h).  The owning rank's x-slab is
+ * the cell range [cx_begin, cx_end); a single-GPU run uses [0, ncell[0]). */
+typedef struct {
+    int32_t dim;          /* 2 or 3 */
+    float lo[3];          /* lower corner (global coordinates) */
+    float cs;             /* cell size */
+    int32_t ncell[3];     /* global cell counts; ncell[2] = 1 in 2-D */
+    int32_t cx_begin;
+    int32_t cx_end;
+} sph_grid;
+
+/* Particle arrays (SoA, device).  z, vz = NULL in 2-D.  label: -1 = fluid,
+ * k >= 0 = buffer particle of port k (the paper's exclusive integer per buffer,
+ * P:416-417); values <= -2 are tombstones (deleted / migrated away) that the
+ * next sph_cll_build drops.  n_dev: device int64 live count.  capacity: length
+ * of every column. */
+typedef struct {
+    float *x, *y, *z;
+    float *vx, *vy, *vz;
+    float *extra[SPH_MAX_EXTRA];
+    int32_t n_extra;
+    int64_t *id;
+    int32_t *label;
+    int64_t *n_dev;
+    int64_t capacity;
+} sph_particles;
+
+/* Cumulative / last-update statistics returned by sph_status_sync. */
+typedef struct {
+    int64_t n;              /* live particles (read from n_dev of the particles passed) */
+    int64_t candidates;     /* candidates checked by the last sph_buffer_update */
+    int64_t created;        /* created by the last update (this rank) */
+    int64_t deleted;        /* deleted by the last update (this rank) */
+    int64_t checked_total;  /* candidates checked since context creation */
+    int64_t out_of_grid;    /* particles clamped into boundary cells, cumulative */
+    int64_t motion_errors;  /* buffer particles beyond 3a/2, cumulative */
+    int64_t migrated_out;   /* particles packed for neighbour slabs, cumulative */
+    int64_t first_deleted;  /* lowest deleted index of the last update (INT64_MAX if none) */
+    int32_t status_bits;    /* sticky device error bits: 1 capacity, 2 staging, 4 motion, 8 migration */
+    int32_t n_ports;
+} sph_stats;
+
+/* Create a context for one rank.  h: smoothing length (checks cs >= 2h,
+ * P:224-229).  capacity: particle array length.  max_ports <= SPH_MAX_PORTS.
+ * max_new: staging capacity for particles created per update.  max_migrate:
+ * per-direction migration buffer capacity (particles).  n_extra: extra columns.
+ * Host only; no CUDA call.  *out receives the context. */
+sph_status sph_ctx_create(const sph_grid *grid, float h, int64_t capacity, int32_t max_ports, int64_t max_new,
+                          int64_t max_migrate, int32_t n_extra, sph_ctx **out);
+void sph_ctx_destroy(sph_ctx *ctx);
+const char *sph_last_error(const sph_ctx *ctx);
+
+/* Device workspace: sph_workspace_bytes() bytes, 256-byte aligned, owned by the
+ * caller.  sph_set_workspace zero-initialises it (synchronous, once). */
+size_t sph_workspace_bytes(const sph_ctx *ctx);
+sph_status sph_set_workspace(sph_ctx *ctx, void *d_ws, size_t bytes);
+
+/* Host-only check of one port (what sph_buffer_register validates first):
+ * origin O', frame Q (row-major, rows = local axes; X' = Q (x - o),
+ * Eq. 2D_transformation P:252-269 / Eq. 3D_transformation),
+ * half extents (a/2, b/2, c/2), kind, layers (a = layers * dp,
+ * layers >= 3: P:226-229).  Returns SPH_OK or the error it would return. */
+sph_status sph_port_check(const sph_ctx *ctx, const float origin[3], const float Q[9], const float half_extents[3],
+                          int32_t kind, int32_t layers, float dp);
+
+/* Register port k = number of ports registered so far (*port_id_out).
+ * Enumerates on the host the cells of this slab intersecting the decision region
+ * P_k = {|X'_r| < he_r + cs} (the paper's local cell-linked lists, "a little larger
+ * than the size of outflow buffer, approximately one layer of cells"),
+ * uploads them, and runs Alg. 1's one-time identification over all particles
+ * ("Execute only once"): fluid particles in the box get label k; for
+ * outlets and bidirectional ports this is also the initial relabel.
+ * members_out_dev (device int64, may be NULL) receives the local member count. */
+sph_status sph_buffer_register(sph_ctx *ctx, sph_particles *p, const float origin[3], const float Q[9],
+                               const float half_extents[3], int32_t kind, int32_t layers, float dp,
+                               int32_t *port_id_out, int64_t *members_out_dev, void *stream);
+
+/* Driver step (not the method): x <- fl(x + fl(v dt)) per component. */
+sph_status sph_advect(sph_ctx *ctx, sph_particles *p, float dt, void *stream);
+
+/* Cell-linked-list build: cell = clamp(floor(fl(fl(x - lo) * inv_cs)))
+ * per axis, inv_cs = fl32(1/cs); counting sort by cell, ascending id within a
+ * cell; tombstones dropped; the SoA of `in` is gathered into `out` (distinct
+ * arrays) and out->n_dev receives the live count.  cell_start / cell_end
+ * [ncells of this slab]: first / one-past-last position of each cell in `out`.
+ * perm_or_null [in capacity]: new position of each input particle, -1 if dropped. */
+sph_status sph_cll_build(sph_ctx *ctx, const sph_particles *in, sph_particles *out, int32_t *cell_start,
+                         int32_t *cell_end, int32_t *perm_or_null, void *stream);
+
+/* One buffer update over the candidates of every port (cells from registration,
+ * particle ranges from the cell tables of the sph_cll_build just made on `p`):
+ * X' = Q_k (x - o_k) in pinned fp32; decisions gated by x in P_k:
+ *   inlet k         (Alg. 1): label k and X'_0 > a/2 -> CREATE
+ *   outlet k        (Alg. 2): X'_0 > a/2             -> DELETE
+ *   bidirectional k (Alg. 3): label k and X'_0 > a/2 -> CREATE,
+ *                                        label k and X'_0 < -a/2 -> DELETE
+ * CREATE stages a bitwise copy of the state in canonical order
+ * (port, cell, id) and recycles the particle x <- fl(x - fl(a u))
+ * (Eqs. 2D/3D_Inverse_transformation).  DELETE writes a tombstone.
+ * Outlet and bidirectional ports then relabel their non-deleted candidates on
+ * post-recycle positions.
+ * port_counts [2 * max_ports] (device int32): created_k at [k], deleted_k at
+ * [max_ports + k]; overwritten. */
+sph_status sph_buffer_update(sph_ctx *ctx, sph_particles *p, const int32_t *cell_start, const int32_t *cell_end,
+                             int32_t *port_counts, void *stream);
+
+/* Stable in-place compaction of the tombstones of the last update, then append
+ * of the staged particles with new IDs from the count matrix
+ * all_counts [nranks][2 * max_ports] (device; this rank's port_counts when
+ * nranks = 1):  off(k, r) = next_id + sum_{k'<k} sum_r' C[r'][k'] + sum_{r'<r} C[r'][k].
+ * *next_id_dev (device int64) += sum of all C; p->n_dev <- N - D + C.
+ * perm_or_null [capacity]: new position of each old position, -1 if deleted. */
+sph_status sph_compact(sph_ctx *ctx, sph_particles *p, const int32_t *all_counts, int32_t nranks, int32_t rank,
+                       int64_t *next_id_dev, int32_t *perm_or_null, void *stream);
+
+/* Multi-GPU slab migration (§8(e)).  pack: particles whose cell x-index left
+ * [cx_begin, cx_end) are copied into send_lo (cx < cx_begin) or send_hi
+ * (cx >= cx_end) and tombstoned.  A buffer holds a 4-word header (word 0 =
+ * particle count, int32 bits) followed by max_migrate records of
+ * sph_migrate_record_floats() = 2*dim + n_extra + 3 fp32 words
+ * (position, velocity, extras, id as two 32-bit words, label).
+ * unpack: appends the particles of a received buffer at the tail (n_dev += count).
+ * Neither synchronises; the exchange itself is the caller's (NCCL send/recv). */
+int32_t sph_migrate_record_floats(const sph_ctx *ctx);
+sph_status sph_migrate_pack(sph_ctx *ctx, sph_particles *p, float *send_lo, float *send_hi, void *stream);
+sph_status sph_migrate_unpack(sph_ctx *ctx, sph_particles *p, const float *recv, void *stream);
+
+/* The only synchronising call: waits for `stream`, returns the statistics and
+ * the first sticky device error (SPH_ERR_CAPACITY / SPH_ERR_MOTION) if any. */
+sph_status sph_status_sync(sph_ctx *ctx, const sph_particles *p, void *stream, sph_stats *out);
+
+/* Number of kernels this context has launched (for the bench's launch count). */
+int64_t sph_launch_count(const sph_ctx *ctx);
+
+/* Live per-kernel timing: when enabled, every kernel launch is bracketed by two
+ * CUDA events on its stream (no synchronisation).  sph_profile resets the
+ * totals; sph_profile_read waits for the last event and returns, per kernel id
+ * (0 .. SPH_NKERNELS-1, named by sph_kernel_name), the summed milliseconds and
+ * the number of launches.  ms, count: host arrays of SPH_NKERNELS. */
+#define SPH_NKERNELS 12
+sph_status sph_profile(sph_ctx *ctx, int32_t enable);
+sph_status sph_profile_read(sph_ctx *ctx, double *ms, int64_t *count);
+const char *sph_kernel_name(int32_t i);
+
+/* Host-only helpers ---------------------------------------------------------- */
+
+/* Cells of the slab intersecting P_k (separating-axis test, P_k inflated by
+ * 1e-3 cs), as x-major runs of consecutive local cell ids [c0, c1] (inclusive).
+ * runs_out: int32[2 * max_runs] or NULL to count only. */
+sph_status sph_port_cells(const sph_grid *grid, const float origin[3], const float Q[9], const float half_extents[3],
+                          int32_t *runs_out, int64_t max_runs, int64_t *n_runs, int64_t *n_cells);
+
+/* 3-D frame from the in/outflow axis u via Rodrigues (Eqs. rotation_axis,
+ * antisymmetric_matrix, rotation_matrix) with reading R1 (Q = R^T, so
+ * Q u = e1, Eq. 3D_normal_transformation), then a roll psi about u.
+ * Q_out: float[9] row-major. */
+sph_status sph_frame_from_axis(const double u[3], double psi, float Q_out[9]);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPHBUF_H */

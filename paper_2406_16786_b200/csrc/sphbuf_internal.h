@@ -1,0 +1,148 @@
+// sphbuf_internal.h — private types shared by the host side (sphbuf_host.cpp) and
+// the sm_100a kernels (sphbuf_kernels.cu).  Not part of the ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "sphbuf.h"
+
+namespace sphbuf {
+
+// ---------------------------------------------------------------- tiling
+constexpr int kThreads = 256;            // block size of the O(N) kernels
+constexpr int kCellItems = 8;            // cells per thread in the cell scan
+constexpr int kCellTile = kThreads * kCellItems;
+constexpr int kUpdItems = 2;             // candidates per thread in the update
+constexpr int kUpdTile = kThreads * kUpdItems;
+constexpr int kCmpItems = 4;             // particles per thread in the compaction
+constexpr int kCmpTile = kThreads * kCmpItems;
+constexpr int kGatherItems = 4;          // output slots per thread in the gather
+constexpr int kGatherTile = kThreads * kGatherItems;
+constexpr int64_t kMaxRuns = 1 << 20;    // port runs per context
+
+// ---------------------------------------------------------------- status bits
+constexpr int kStCapacity = 1;
+constexpr int kStStaging = 2;
+constexpr int kStMotion = 4;
+constexpr int kStMigrate = 8;
+
+// Port parameters as the kernels see them (passed by value in the kernel
+// parameter space, i.e. the constant bank: uniform broadcast reads).
+struct PortDev {
+    float o[3];      // origin O'
+    float Q[9];      // rows = local axes
+    float he[3];     // half extents (a/2, b/2, c/2)
+    float heP[3];    // fl(he + cs): decision region P_k (reading R4)
+    float s[3];      // recycle shift fl(a * u)
+    int kind;
+    int pad;
+};
+
+struct PortTable {
+    int n;
+    int max_ports;
+    PortDev p[SPH_MAX_PORTS];
+};
+
+struct GridDev {
+    int dim;
+    float lo[3];
+    float inv_cs;     // fl32(1/cs) formed in f64
+    int ncell[3];
+    int cx_begin, cx_end;
+    int ny, nz;
+    long long ncells;  // cells of the slab
+};
+
+struct PartDev {
+    float *x, *y, *z, *vx, *vy, *vz;
+    float *extra[SPH_MAX_EXTRA];
+    int n_extra;
+    long long *id;
+    int *label;
+    long long *n;
+    long long cap;
+};
+
+struct Counters {
+    unsigned int epoch_cll, epoch_upd, epoch_cmp, epoch_pad;
+    int ticket_cll, ticket_upd, ticket_cmp, ticket_pad;
+    long long n_in;        // cll: live+tombstone input length
+    long long n_cand;      // update: candidates this update
+    long long n_stage;     // update: created this update (may exceed staging capacity -> error)
+    long long n_del;       // update: deleted this update
+    long long i_first;     // update: lowest deleted index
+    long long out_of_grid; // cumulative
+    long long checked;     // cumulative candidates
+    long long motion;      // cumulative
+    long long cmp_n;       // compaction: N before
+    long long cmp_next_id; // compaction: next_id before
+    long long migrated;    // last pack
+    int status;            // sticky bits
+    int dummy;
+};
+
+struct Workspace {
+    Counters *ctr;
+    int *cell_count;                 // [ncells]
+    unsigned long long *tile_cells;  // [cell tiles]
+    int *key;                        // [capacity]
+    int *rank;                       // [capacity]
+    int *src;                        // [capacity]
+    unsigned long long *tile_upd;    // [upd tiles]
+    unsigned long long *tile_cmp;    // [cmp tiles]
+    int *runs;                       // [kMaxRuns * 3]: c0, c1, port
+    long long *run_off;              // [kMaxRuns + 1]
+    float *sx, *sy, *sz, *svx, *svy, *svz;
+    float *sextra[SPH_MAX_EXTRA];
+    long long *sid;                  // source id of each staged particle (diagnostic)
+    int *sport;                      // port of each staged particle
+    long long max_new;
+    long long upd_tiles;
+    long long cmp_tiles;
+};
+
+// ---------------------------------------------------------------- launch bookkeeping
+enum KernelId {
+    KID_ADVECT, KID_REGISTER, KID_CLL_KEY, KID_CELL_SCAN, KID_CLL_SCATTER, KID_CLL_GATHER, KID_UPD_PROLOGUE,
+    KID_UPD_MAIN, KID_COMPACT, KID_COMPACT_APPEND, KID_MIG_PACK, KID_MIG_UNPACK, KID_COUNT
+};
+
+// Counts launches; when profiling is on, brackets every launch with a pair of
+// CUDA events on the launching stream (sph_profile / sph_profile_read).
+struct Launch {
+    int64_t count = 0;
+    bool prof = false;
+    std::vector<cudaEvent_t> pool;
+    std::vector<int> kid;
+    size_t used = 0;
+    double ms[KID_COUNT] = {};
+    int64_t n[KID_COUNT] = {};
+    void before(cudaStream_t s);
+    void after(cudaStream_t s, int k);
+    cudaError_t flush();
+    ~Launch();
+};
+
+// ---------------------------------------------------------------- launchers (sphbuf_kernels.cu)
+cudaError_t launch_advect(const PartDev &p, int dim, float dt, cudaStream_t s, Launch *L);
+cudaError_t launch_register(const PartDev &p, const GridDev &g, const PortTable &pt, int k, long long *members,
+                            cudaStream_t s, Launch *L);
+cudaError_t launch_cll(const PartDev &in, const PartDev &out, const GridDev &g, const Workspace &ws,
+                       int *cell_start, int *cell_end, int *perm, cudaStream_t s, Launch *L);
+cudaError_t launch_update(const PartDev &p, const GridDev &g, const PortTable &pt, const Workspace &ws, int n_runs,
+                          const int *cell_start, const int *cell_end, int *port_counts, cudaStream_t s,
+                          Launch *L);
+cudaError_t launch_compact(const PartDev &p, const PortTable &pt, const Workspace &ws, const int *all_counts,
+                           int nranks, int rank, long long *next_id, int *perm, cudaStream_t s, Launch *L);
+cudaError_t launch_migrate_pack(const PartDev &p, const GridDev &g, const Workspace &ws, float *lo, float *hi,
+                                long long max_migrate, int rec, cudaStream_t s, Launch *L);
+cudaError_t launch_migrate_unpack(const PartDev &p, const GridDev &g, const Workspace &ws, const float *buf,
+                                  long long max_migrate, int rec, cudaStream_t s, Launch *L);
+int sm_count();
+
+}  // namespace sphbuf

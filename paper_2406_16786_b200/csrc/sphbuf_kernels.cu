@@ -1,0 +1,996 @@
+// sphbuf_kernels.cu — hand-written sm_100a kernels of the in/outlet buffer update
+// (arXiv 2406.16786 §III).  "P:n" = PAPER.md line n; readings R<n> are listed in
+// DESIGN.md §3.  All arithmetic that decides an integer or mutates particle state
+// uses __fadd_rn/__fsub_rn/__fmul_rn (one binary32 round-to-nearest op each, never
+// contracted), in the order fixed by DESIGN.md §3 "Pinned arithmetic".
+//
+// The path is HBM-bound (no dense contraction; tensor cores unused).  Design:
+//  * structure-of-arrays columns, striped (coalesced) 4-byte / 8-byte accesses;
+//  * single-pass decoupled look-back scans (tile status words tagged with a
+//    device-side epoch so nothing has to be zeroed between launches), tiles
+//    claimed in order through an atomic ticket (deadlock-free, persistent grids);
+//  * warp-aggregated atomics (__match_any_sync) for the cell histogram;
+//  * port parameters passed as a __grid_constant__ kernel parameter (constant
+//    bank) and staged in shared memory;
+//  * all counts device-resident: every kernel reads N from device memory, so an
+//    update is graph-capturable and needs no host synchronisation.
+#include <climits>
+#include <cstdint>
+
+#include "sphbuf_internal.h"
+
+namespace sphbuf {
+
+// ------------------------------------------------------------------ helpers
+
+__device__ __forceinline__ unsigned lanemask_lt()
+{
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+__device__ __forceinline__ void st_release(unsigned long long *p, unsigned long long v)
+{
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long *p)
+{
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// tile status word: [63:34] epoch (30 bits) | [33:32] flag (1 aggregate, 2 inclusive prefix) | [31:0] value
+__device__ __forceinline__ unsigned long long pack_status(unsigned epoch, unsigned flag, unsigned value)
+{
+    return ((unsigned long long)(epoch & 0x3fffffffu) << 34) | ((unsigned long long)flag << 32) | value;
+}
+
+__device__ __forceinline__ unsigned warp_sum(unsigned v)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__device__ __forceinline__ long long warp_sum_ll(long long v)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__device__ __forceinline__ long long warp_min_ll(long long v)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        long long w = __shfl_xor_sync(0xffffffffu, v, o);
+        v = w < v ? w : v;
+    }
+    return v;
+}
+
+// Decoupled look-back (single pass): called by all 32 lanes of warp 0 of a block
+// that owns `tile`.  Publishes the tile's aggregate, accumulates predecessors'
+// aggregates until an inclusive prefix is found, publishes its own inclusive
+// prefix and returns the exclusive prefix.  Publishing uses release stores and
+// reading acquire loads, so everything a predecessor did before publishing
+// happens-before what the caller does after this returns.
+__device__ unsigned tile_prefix(unsigned long long *status, long long tile, unsigned epoch, unsigned aggregate)
+{
+    const int lane = threadIdx.x & 31;
+    const unsigned ep = epoch & 0x3fffffffu;
+    if (tile == 0) {
+        if (lane == 0) st_release(&status[0], pack_status(epoch, 2, aggregate));
+        return 0;
+    }
+    if (lane == 0) st_release(&status[tile], pack_status(epoch, 1, aggregate));
+    unsigned excl = 0;
+    long long base = tile - 1;
+    while (true) {
+        long long t = base - lane;
+        unsigned long long s = 0;
+        unsigned flag;
+        if (t >= 0) {
+            do {
+                s = ld_acquire(&status[t]);
+                flag = ((unsigned)(s >> 34) == ep) ? (unsigned)((s >> 32) & 3u) : 0u;
+            } while (flag == 0);
+        } else {
+            flag = 2;
+            s = 0;
+        }
+        unsigned pmask = __ballot_sync(0xffffffffu, flag == 2);
+        int first = pmask ? __ffs(pmask) - 1 : 32;
+        unsigned v = (lane <= first) ? (unsigned)(s & 0xffffffffu) : 0u;
+        excl += warp_sum(v);
+        if (pmask) break;
+        base -= 32;
+    }
+    if (lane == 0) st_release(&status[tile], pack_status(epoch, 2, excl + aggregate));
+    return excl;
+}
+
+// Block-wide exclusive scan of one unsigned per thread (NT threads).
+template <int NT>
+__device__ __forceinline__ unsigned block_excl_scan(unsigned v, unsigned &total, unsigned *s_warp)
+{
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_warp[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        unsigned w = lane < NT / 32 ? s_warp[lane] : 0u;
+        unsigned wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            unsigned y = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= o) wi += y;
+        }
+        if (lane < NT / 32) s_warp[lane] = wi - w;
+        if (lane == NT / 32 - 1) s_warp[NT / 32] = wi;
+    }
+    __syncthreads();
+    unsigned res = s_warp[warp] + x - v;
+    total = s_warp[NT / 32];
+    __syncthreads();
+    return res;
+}
+
+// 64-bit variant (used for run offsets).
+template <int NT>
+__device__ __forceinline__ long long block_excl_scan_ll(long long v, long long &total, long long *s_warp)
+{
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    long long x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        long long y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_warp[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        long long w = lane < NT / 32 ? s_warp[lane] : 0;
+        long long wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            long long y = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= o) wi += y;
+        }
+        if (lane < NT / 32) s_warp[lane] = wi - w;
+        if (lane == NT / 32 - 1) s_warp[NT / 32] = wi;
+    }
+    __syncthreads();
+    long long res = s_warp[warp] + x - v;
+    total = s_warp[NT / 32];
+    __syncthreads();
+    return res;
+}
+
+// Pinned forward transform X' = Q (x - o) (Eq. 2D_transformation P:252-269,
+// Eq. 3D_transformation): d_j = fl(x_j - o_j);
+// X'_r = fl(fl(fl(Q_r0 d_0) + fl(Q_r1 d_1)) + fl(Q_r2 d_2)).
+__device__ __forceinline__ void to_local(const PortDev &P, int dim, float x, float y, float z, float X[3])
+{
+    const float d0 = __fsub_rn(x, P.o[0]);
+    const float d1 = __fsub_rn(y, P.o[1]);
+    if (dim == 3) {
+        const float d2 = __fsub_rn(z, P.o[2]);
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+            X[r] = __fadd_rn(__fadd_rn(__fmul_rn(P.Q[3 * r], d0), __fmul_rn(P.Q[3 * r + 1], d1)),
+                             __fmul_rn(P.Q[3 * r + 2], d2));
+    } else {
+#pragma unroll
+        for (int r = 0; r < 2; ++r) X[r] = __fadd_rn(__fmul_rn(P.Q[3 * r], d0), __fmul_rn(P.Q[3 * r + 1], d1));
+        X[2] = 0.0f;
+    }
+}
+
+__device__ __forceinline__ bool in_box(const float X[3], const float he[3], int dim)
+{
+    bool r = fabsf(X[0]) < he[0] && fabsf(X[1]) < he[1];
+    if (dim == 3) r = r && fabsf(X[2]) < he[2];
+    return r;
+}
+
+// Pinned cell index along one axis: floor(fl(fl(x - lo) * inv_cs)), clamped.
+__device__ __forceinline__ int cell_axis(float x, float lo, float inv, int lo_c, int hi_c, int &oob)
+{
+    const float t = __fmul_rn(__fsub_rn(x, lo), inv);
+    const float f = floorf(t);
+    if (f < (float)lo_c) { oob = 1; return lo_c; }
+    if (f > (float)(hi_c - 1)) { oob = 1; return hi_c - 1; }
+    return (int)f;
+}
+
+__device__ __forceinline__ int cell_of(const GridDev &g, float x, float y, float z, int &oob)
+{
+    const int cx = cell_axis(x, g.lo[0], g.inv_cs, g.cx_begin, g.cx_end, oob);
+    const int cy = cell_axis(y, g.lo[1], g.inv_cs, 0, g.ncell[1], oob);
+    int cz = 0;
+    if (g.dim == 3) cz = cell_axis(z, g.lo[2], g.inv_cs, 0, g.ncell[2], oob);
+    return ((cx - g.cx_begin) * g.ny + cy) * g.nz + cz;
+}
+
+// ------------------------------------------------------------------ driver: advection
+
+__global__ void __launch_bounds__(kThreads) k_advect(PartDev p, int dim, float dt)
+{
+    const long long n = *p.n;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        p.x[i] = __fadd_rn(p.x[i], __fmul_rn(p.vx[i], dt));
+        p.y[i] = __fadd_rn(p.y[i], __fmul_rn(p.vy[i], dt));
+        if (dim == 3) p.z[i] = __fadd_rn(p.z[i], __fmul_rn(p.vz[i], dt));
+    }
+}
+
+// ------------------------------------------------------------------ registration (Alg. 1 identification)
+
+// "Buffer particle identification ... Execute only once": every fluid
+// particle in the box of port k becomes a buffer particle of k; the same test is
+// the initial relabel of outlet / bidirectional ports.
+__global__ void __launch_bounds__(kThreads) k_register(PartDev p, int dim, PortDev P, int k, long long *members)
+{
+    const long long n = *p.n;
+    long long cnt = 0;
+    const int lane = threadIdx.x & 31;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i - lane < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        if (i < n) {
+            int lab = p.label[i];
+            if (lab == -1) {
+                float X[3];
+                to_local(P, dim, p.x[i], p.y[i], dim == 3 ? p.z[i] : 0.0f, X);
+                if (in_box(X, P.he, dim)) {
+                    lab = k;
+                    p.label[i] = k;
+                }
+            }
+            cnt += (lab == k);
+        }
+    }
+    cnt = warp_sum_ll(cnt);
+    if (lane == 0 && cnt && members) atomicAdd((unsigned long long *)members, (unsigned long long)cnt);
+}
+
+// ------------------------------------------------------------------ a1: cell-linked-list build
+
+// K1: pinned cell key of every live particle (tombstones get no cell) and its
+// rank inside the cell from a warp-aggregated histogram atomic.
+__global__ void __launch_bounds__(kThreads) k_cll_key(PartDev in, GridDev g, Workspace ws)
+{
+    Counters *ctr = ws.ctr;
+    const long long n = *in.n;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        ctr->epoch_cll += 1;
+        ctr->ticket_cll = 0;
+        ctr->n_in = n;
+    }
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = lanemask_lt();
+    int oob_acc = 0;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i - lane < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        int key = -1;
+        if (i < n && in.label[i] > -2) {
+            int oob = 0;
+            key = cell_of(g, in.x[i], in.y[i], g.dim == 3 ? in.z[i] : 0.0f, oob);
+            oob_acc += oob;
+        }
+        const unsigned grp = __match_any_sync(0xffffffffu, key);
+        const int leader = __ffs(grp) - 1;
+        int base = 0;
+        if (key >= 0 && lane == leader) base = atomicAdd(&ws.cell_count[key], __popc(grp));
+        base = __shfl_sync(0xffffffffu, base, leader);
+        if (i < n) {
+            ws.key[i] = key;
+            ws.rank[i] = base + __popc(grp & lt);
+        }
+    }
+    const unsigned o = warp_sum((unsigned)oob_acc);
+    if (lane == 0 && o) atomicAdd((unsigned long long *)&ctr->out_of_grid, (unsigned long long)o);
+}
+
+// K2: exclusive scan of the cell histogram -> cell_start / cell_end (single pass,
+// decoupled look-back); re-zeroes the histogram for the next build; the last tile
+// writes the live count.
+__global__ void __launch_bounds__(kThreads) k_cell_scan(GridDev g, Workspace ws, int *cell_start, int *cell_end,
+                                                        long long *n_out, long long ntiles)
+{
+    __shared__ unsigned s_warp[kThreads / 32 + 1];
+    __shared__ long long s_tile;
+    __shared__ unsigned s_prefix;
+    Counters *ctr = ws.ctr;
+    if (threadIdx.x == 0) s_tile = atomicAdd(&ctr->ticket_cll, 1);
+    __syncthreads();
+    const long long tile = s_tile;
+    const unsigned epoch = ctr->epoch_cll;
+    const long long nc = g.ncells;
+    const long long base = tile * kCellTile + (long long)threadIdx.x * kCellItems;
+    int c[kCellItems];
+    if (base + kCellItems <= nc) {
+        int4 *pc = reinterpret_cast<int4 *>(ws.cell_count + base);
+        int4 a = pc[0], b = pc[1];
+        c[0] = a.x; c[1] = a.y; c[2] = a.z; c[3] = a.w; c[4] = b.x; c[5] = b.y; c[6] = b.z; c[7] = b.w;
+        pc[0] = make_int4(0, 0, 0, 0);
+        pc[1] = make_int4(0, 0, 0, 0);
+    } else {
+#pragma unroll
+        for (int j = 0; j < kCellItems; ++j) {
+            c[j] = (base + j < nc) ? ws.cell_count[base + j] : 0;
+            if (base + j < nc) ws.cell_count[base + j] = 0;
+        }
+    }
+    unsigned sum = 0;
+#pragma unroll
+    for (int j = 0; j < kCellItems; ++j) sum += (unsigned)c[j];
+    unsigned total;
+    const unsigned excl = block_excl_scan<kThreads>(sum, total, s_warp);
+    if (threadIdx.x < 32) {
+        unsigned pre = tile_prefix(ws.tile_cells, tile, epoch, total);
+        if (threadIdx.x == 0) s_prefix = pre;
+    }
+    __syncthreads();
+    const unsigned prefix = s_prefix;
+    int run = (int)(prefix + excl);
+    int st[kCellItems], en[kCellItems];
+#pragma unroll
+    for (int j = 0; j < kCellItems; ++j) {
+        st[j] = run;
+        run += c[j];
+        en[j] = run;
+    }
+    if (base + kCellItems <= nc) {
+        int4 *ps = reinterpret_cast<int4 *>(cell_start + base);
+        int4 *pe = reinterpret_cast<int4 *>(cell_end + base);
+        ps[0] = make_int4(st[0], st[1], st[2], st[3]);
+        ps[1] = make_int4(st[4], st[5], st[6], st[7]);
+        pe[0] = make_int4(en[0], en[1], en[2], en[3]);
+        pe[1] = make_int4(en[4], en[5], en[6], en[7]);
+    } else {
+#pragma unroll
+        for (int j = 0; j < kCellItems; ++j)
+            if (base + j < nc) {
+                cell_start[base + j] = st[j];
+                cell_end[base + j] = en[j];
+            }
+    }
+    if (tile == ntiles - 1 && threadIdx.x == 0) *n_out = (long long)(prefix + total);
+}
+
+// K3: scatter each live particle's index into its slot (cell start + rank).
+__global__ void __launch_bounds__(kThreads) k_cll_scatter(Workspace ws, const int *cell_start, int *perm)
+{
+    const long long n = ws.ctr->n_in;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const int key = ws.key[i];
+        if (key >= 0) ws.src[cell_start[key] + ws.rank[i]] = (int)i;
+        else if (perm) perm[i] = -1;
+    }
+}
+
+// K4: order inside each cell by ascending id (rank by counting against the ids of
+// the cell's other slots, staged in shared memory) and gather the SoA into `out`.
+template <bool HasExtra>
+__global__ void __launch_bounds__(kThreads) k_cll_gather(PartDev in, PartDev out, int dim, Workspace ws,
+                                                         const int *cell_start, const int *cell_end, int *perm)
+{
+    __shared__ long long s_id[kGatherTile];
+    const long long n = *out.n;
+    for (long long j0 = (long long)blockIdx.x * kGatherTile; j0 < n; j0 += (long long)gridDim.x * kGatherTile) {
+        int srcs[kGatherItems];
+        long long ids[kGatherItems];
+#pragma unroll
+        for (int it = 0; it < kGatherItems; ++it) {
+            const long long j = j0 + it * kThreads + threadIdx.x;
+            srcs[it] = -1;
+            ids[it] = 0;
+            if (j < n) {
+                srcs[it] = ws.src[j];
+                ids[it] = in.id[srcs[it]];
+                s_id[it * kThreads + threadIdx.x] = ids[it];
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int it = 0; it < kGatherItems; ++it) {
+            const long long j = j0 + it * kThreads + threadIdx.x;
+            if (j < n) {
+                const int s = srcs[it];
+                const int c = ws.key[s];
+                const int cb = cell_start[c], ce = cell_end[c];
+                int r = 0;
+                for (int q = cb; q < ce; ++q) {
+                    const long long idq = (q >= j0 && q < j0 + kGatherTile) ? s_id[q - j0] : in.id[ws.src[q]];
+                    r += (idq < ids[it]);
+                }
+                const int d = cb + r;
+                out.x[d] = in.x[s];
+                out.y[d] = in.y[s];
+                out.vx[d] = in.vx[s];
+                out.vy[d] = in.vy[s];
+                if (dim == 3) {
+                    out.z[d] = in.z[s];
+                    out.vz[d] = in.vz[s];
+                }
+                if (HasExtra)
+                    for (int e = 0; e < in.n_extra; ++e) out.extra[e][d] = in.extra[e][s];
+                out.id[d] = ids[it];
+                out.label[d] = in.label[s];
+                if (perm) perm[s] = d;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// ------------------------------------------------------------------ a3-a6: buffer update
+
+// K5: candidate count per port run (cell ranges from the current cell list) and
+// their exclusive scan; resets the per-update counters.  One block.
+__global__ void __launch_bounds__(1024) k_upd_prologue(Workspace ws, int n_runs, const int *cell_start,
+                                                       const int *cell_end, int *port_counts, int max_ports)
+{
+    __shared__ long long s_warp[1024 / 32 + 1];
+    Counters *ctr = ws.ctr;
+    if (threadIdx.x == 0) {
+        ctr->epoch_upd += 1;
+        ctr->ticket_upd = 0;
+        ctr->n_stage = 0;
+        ctr->n_del = 0;
+        ctr->i_first = LLONG_MAX;
+    }
+    for (int i = threadIdx.x; i < 2 * max_ports; i += blockDim.x) port_counts[i] = 0;
+    long long carry = 0;
+    for (int r0 = 0; r0 < n_runs; r0 += 1024) {
+        const int r = r0 + threadIdx.x;
+        long long len = 0;
+        if (r < n_runs) len = (long long)cell_end[ws.runs[3 * r + 1]] - (long long)cell_start[ws.runs[3 * r]];
+        long long total;
+        const long long ex = block_excl_scan_ll<1024>(len, total, s_warp);
+        if (r < n_runs) ws.run_off[r] = carry + ex;
+        carry += total;
+    }
+    if (threadIdx.x == 0) {
+        ws.run_off[n_runs] = carry;
+        ctr->n_cand = carry;
+        ctr->checked += carry;
+        if ((carry + kUpdTile - 1) / kUpdTile > ws.upd_tiles) ctr->status |= kStCapacity;
+    }
+}
+
+// K6: the candidate check (a3) with generation (a4), deletion (a5) and relabel
+// (a6) fused; CREATEs are appended to the staging area in canonical order
+// (port, cell, id) by a ballot/block scan + decoupled look-back over ordered tiles.
+__global__ void __launch_bounds__(kThreads) k_upd_main(PartDev p, int dim, const __grid_constant__ PortTable pt,
+                                                       Workspace ws, int n_runs, const int *cell_start,
+                                                       int *port_counts)
+{
+    __shared__ PortDev s_ports[SPH_MAX_PORTS];
+    __shared__ unsigned s_warp[kThreads / 32 + 1];
+    __shared__ long long s_tile;
+    __shared__ unsigned s_prefix;
+    {
+        const int words = pt.n * (int)(sizeof(PortDev) / 4);
+        const unsigned *src = reinterpret_cast<const unsigned *>(pt.p);
+        unsigned *dst = reinterpret_cast<unsigned *>(s_ports);
+        for (int w = threadIdx.x; w < words; w += blockDim.x) dst[w] = src[w];
+    }
+    Counters *ctr = ws.ctr;
+    const long long n_cand = ctr->n_cand;
+    const unsigned epoch = ctr->epoch_upd;
+    const long long ntiles = (n_cand + kUpdTile - 1) / kUpdTile;
+    const int max_ports = pt.max_ports;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        ctr->epoch_cmp += 1;  // consumed by the compaction that follows
+        ctr->ticket_cmp = 0;
+    }
+    long long del_cnt = 0, del_min = LLONG_MAX, motion = 0;
+    __syncthreads();
+    while (true) {
+        if (threadIdx.x == 0) s_tile = atomicAdd(&ctr->ticket_upd, 1);
+        __syncthreads();
+        const long long tile = s_tile;
+        if (tile >= ntiles || tile >= ws.upd_tiles) break;
+        bool cr[kUpdItems];
+        int pidx[kUpdItems], kk[kUpdItems];
+        float ox[kUpdItems], oy[kUpdItems], oz[kUpdItems];
+#pragma unroll
+        for (int it = 0; it < kUpdItems; ++it) {
+            cr[it] = false;
+            pidx[it] = -1;
+            kk[it] = 0;
+            ox[it] = oy[it] = oz[it] = 0.0f;
+            const long long g = tile * kUpdTile + it * kThreads + threadIdx.x;
+            if (g >= n_cand) continue;
+            // run containing g: largest r with run_off[r] <= g
+            int lo = 0, hi = n_runs - 1;
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (ws.run_off[mid] <= g) lo = mid;
+                else hi = mid - 1;
+            }
+            const int r = lo;
+            const int k = ws.runs[3 * r + 2];
+            const int pi = cell_start[ws.runs[3 * r]] + (int)(g - ws.run_off[r]);
+            const PortDev &P = s_ports[k];
+            const float x = p.x[pi], y = p.y[pi], z = dim == 3 ? p.z[pi] : 0.0f;
+            const int lab = p.label[pi];
+            float X[3];
+            to_local(P, dim, x, y, z, X);
+            const bool inP = in_box(X, P.heP, dim);              // x in P_k (reading R4)
+            const bool member = (lab == k);
+            const bool beyond = X[0] > P.he[0];                  // X'_0 > a/2
+            bool create = false, del = false;
+            if (inP) {
+                if (P.kind == SPH_INLET) {
+                    create = member && beyond;                   // Alg. 1 (R5)
+                } else if (P.kind == SPH_OUTLET) {
+                    del = beyond;                                // Alg. 2 (R6)
+                } else {
+                    create = member && beyond;                   // Alg. 3
+                    del = member && (X[0] < -P.he[0]);           // Alg. 3
+                }
+            }
+            // R12: a buffer particle more than one buffer length beyond the interface
+            if (member && __fsub_rn(X[0], __fmul_rn(2.0f, P.he[0])) > P.he[0]) ++motion;
+            float px = x, py = y, pz = z;
+            if (create) {
+                // recycle: x <- fl(x - fl(a u)) (Eqs. 2D/3D_Inverse_transformation, R10)
+                px = __fsub_rn(x, P.s[0]);
+                py = __fsub_rn(y, P.s[1]);
+                p.x[pi] = px;
+                p.y[pi] = py;
+                if (dim == 3) {
+                    pz = __fsub_rn(z, P.s[2]);
+                    p.z[pi] = pz;
+                }
+                cr[it] = true;
+                pidx[it] = pi;
+                kk[it] = k;
+                ox[it] = x;
+                oy[it] = y;
+                oz[it] = z;
+                atomicAdd(&port_counts[k], 1);
+            }
+            if (del) {
+                p.label[pi] = -2;                                // tombstone, removed by sph_compact
+                atomicAdd(&port_counts[max_ports + k], 1);
+                ++del_cnt;
+                del_min = pi < del_min ? pi : del_min;
+            } else if (P.kind != SPH_INLET) {
+                // relabel on post-recycle positions (R9)
+                float Xp[3] = {X[0], X[1], X[2]};
+                if (create) to_local(P, dim, px, py, pz, Xp);
+                if (in_box(Xp, P.he, dim)) {
+                    if (lab != k) p.label[pi] = k;
+                } else if (lab == k) {
+                    p.label[pi] = -1;
+                }
+            }
+        }
+        unsigned mine = 0;
+#pragma unroll
+        for (int it = 0; it < kUpdItems; ++it) mine += cr[it];
+        unsigned total;
+        const unsigned excl = block_excl_scan<kThreads>(mine, total, s_warp);
+        if (threadIdx.x < 32) {
+            const unsigned pre = tile_prefix(ws.tile_upd, tile, epoch, total);
+            if (threadIdx.x == 0) s_prefix = pre;
+        }
+        __syncthreads();
+        long long slot = (long long)s_prefix + excl;
+#pragma unroll
+        for (int it = 0; it < kUpdItems; ++it) {
+            if (!cr[it]) continue;
+            if (slot < ws.max_new) {
+                const int pi = pidx[it];
+                // duplicate = bitwise copy of the pre-recycle state, label fluid (R11)
+                ws.sx[slot] = ox[it];
+                ws.sy[slot] = oy[it];
+                ws.svx[slot] = p.vx[pi];
+                ws.svy[slot] = p.vy[pi];
+                if (dim == 3) {
+                    ws.sz[slot] = oz[it];
+                    ws.svz[slot] = p.vz[pi];
+                }
+                for (int e = 0; e < p.n_extra; ++e) ws.sextra[e][slot] = p.extra[e][pi];
+                ws.sid[slot] = p.id[pi];
+                ws.sport[slot] = kk[it];
+            } else {
+                atomicOr(&ctr->status, kStStaging);
+            }
+            ++slot;
+        }
+        if (tile == ntiles - 1 && threadIdx.x == 0) ctr->n_stage = (long long)s_prefix + total;
+        __syncthreads();
+    }
+    const int lane = threadIdx.x & 31;
+    del_cnt = warp_sum_ll(del_cnt);
+    del_min = warp_min_ll(del_min);
+    motion = warp_sum_ll(motion);
+    if (lane == 0) {
+        if (del_cnt) {
+            atomicAdd((unsigned long long *)&ctr->n_del, (unsigned long long)del_cnt);
+            atomicMin(&ctr->i_first, del_min);
+        }
+        if (motion) {
+            atomicAdd((unsigned long long *)&ctr->motion, (unsigned long long)motion);
+            atomicOr(&ctr->status, kStMotion);
+        }
+    }
+}
+
+// ------------------------------------------------------------------ a7: compaction
+
+// K7: stable in-place compaction of [i_first, N): each ordered tile loads all of
+// its columns into registers before publishing its aggregate, so a later tile
+// (which only writes below its own start) never overwrites unread data.
+template <bool HasExtra>
+__global__ void __launch_bounds__(kThreads) k_compact(PartDev p, int dim, Workspace ws, int *perm,
+                                                      const long long *next_id)
+{
+    __shared__ unsigned s_warp[kThreads / 32 + 1];
+    __shared__ long long s_tile;
+    __shared__ unsigned s_prefix;
+    Counters *ctr = ws.ctr;
+    const long long N = *p.n;
+    const long long D = ctr->n_del;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        ctr->cmp_n = N;
+        ctr->cmp_next_id = *next_id;
+    }
+    if (D == 0) return;
+    const long long ibeg = ctr->i_first;
+    const unsigned epoch = ctr->epoch_cmp;
+    const long long ntiles = (N - ibeg + kCmpTile - 1) / kCmpTile;
+    int dep = 0;
+    while (true) {
+        if (threadIdx.x == 0) s_tile = atomicAdd(&ctr->ticket_cmp, 1);
+        __syncthreads();
+        const long long tile = s_tile;
+        if (tile >= ntiles) break;
+        bool alive[kCmpItems];
+        float x[kCmpItems], y[kCmpItems], z[kCmpItems], vx[kCmpItems], vy[kCmpItems], vz[kCmpItems];
+        float ex[kCmpItems][SPH_MAX_EXTRA];
+        long long id[kCmpItems];
+        int lab[kCmpItems];
+        unsigned mine = 0;
+#pragma unroll
+        for (int it = 0; it < kCmpItems; ++it) {
+            const long long i = ibeg + tile * kCmpTile + it * kThreads + threadIdx.x;
+            alive[it] = false;
+            if (i < N) {
+                lab[it] = p.label[i];
+                x[it] = p.x[i];
+                y[it] = p.y[i];
+                vx[it] = p.vx[i];
+                vy[it] = p.vy[i];
+                if (dim == 3) {
+                    z[it] = p.z[i];
+                    vz[it] = p.vz[i];
+                } else {
+                    z[it] = vz[it] = 0.0f;
+                }
+                if (HasExtra) {
+#pragma unroll
+                    for (int e = 0; e < SPH_MAX_EXTRA; ++e)
+                        ex[it][e] = (e < p.n_extra) ? p.extra[e][i] : 0.0f;
+                }
+                id[it] = p.id[i];
+                alive[it] = lab[it] > -2;
+                mine += alive[it];
+                // consume every loaded word so the loads are complete before the barrier below
+                dep ^= __float_as_int(x[it]) ^ __float_as_int(y[it]) ^ __float_as_int(z[it]) ^
+                       __float_as_int(vx[it]) ^ __float_as_int(vy[it]) ^ __float_as_int(vz[it]) ^ (int)id[it] ^
+                       (int)(id[it] >> 32);
+                if (HasExtra) {
+#pragma unroll
+                    for (int e = 0; e < SPH_MAX_EXTRA; ++e) dep ^= __float_as_int(ex[it][e]);
+                }
+            }
+        }
+        if (dep == 0x7f3a5c11 && mine == 77u) ctr->dummy = dep;   // never true in practice; keeps the dependency
+        unsigned total;
+        const unsigned excl = block_excl_scan<kThreads>(mine, total, s_warp);
+        if (threadIdx.x < 32) {
+            const unsigned pre = tile_prefix(ws.tile_cmp, tile, epoch, total);
+            if (threadIdx.x == 0) s_prefix = pre;
+        }
+        __syncthreads();
+        long long o = ibeg + (long long)s_prefix + excl;
+#pragma unroll
+        for (int it = 0; it < kCmpItems; ++it) {
+            const long long i = ibeg + tile * kCmpTile + it * kThreads + threadIdx.x;
+            if (i >= N) continue;
+            if (!alive[it]) {
+                if (perm) perm[i] = -1;
+                continue;
+            }
+            p.x[o] = x[it];
+            p.y[o] = y[it];
+            p.vx[o] = vx[it];
+            p.vy[o] = vy[it];
+            if (dim == 3) {
+                p.z[o] = z[it];
+                p.vz[o] = vz[it];
+            }
+            if (HasExtra)
+                for (int e = 0; e < p.n_extra; ++e) p.extra[e][o] = ex[it][e];
+            p.id[o] = id[it];
+            p.label[o] = lab[it];
+            if (perm) perm[i] = (int)o;
+            ++o;
+        }
+        __syncthreads();
+    }
+}
+
+// K7b: append the staged particles after the survivors with IDs from the count
+// matrix (reading R14, §8(e)), identity perm below i_first, then N and next_id.
+__global__ void __launch_bounds__(kThreads) k_compact_append(PartDev p, int dim, int n_ports, int max_ports,
+                                                             Workspace ws, const int *all_counts, int nranks,
+                                                             int rank, long long *next_id, int *perm)
+{
+    __shared__ long long s_off[SPH_MAX_PORTS];
+    __shared__ long long s_beg[SPH_MAX_PORTS];
+    __shared__ long long s_total;
+    Counters *ctr = ws.ctr;
+    const long long nid0 = ctr->cmp_next_id;
+    if (threadIdx.x == 0) {
+        long long acc = nid0, beg = 0;
+        for (int k = 0; k < n_ports; ++k) {
+            long long before = 0, all = 0;
+            for (int r = 0; r < nranks; ++r) {
+                const long long c = all_counts[(long long)r * 2 * max_ports + k];
+                all += c;
+                if (r < rank) before += c;
+            }
+            s_off[k] = acc + before;
+            s_beg[k] = beg;
+            beg += all_counts[(long long)rank * 2 * max_ports + k];
+            acc += all;
+        }
+        s_total = acc - nid0;
+    }
+    __syncthreads();
+    const long long N = ctr->cmp_n;
+    const long long D = ctr->n_del;
+    long long C = ctr->n_stage;
+    if (C > ws.max_new) C = ws.max_new;
+    const long long dst0 = N - D;
+    if (dst0 + C > p.cap) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(&ctr->status, kStCapacity);
+        C = p.cap - dst0 > 0 ? p.cap - dst0 : 0;
+    }
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long s = (long long)blockIdx.x * blockDim.x + threadIdx.x; s < C; s += stride) {
+        const int k = ws.sport[s];
+        const long long d = dst0 + s;
+        p.x[d] = ws.sx[s];
+        p.y[d] = ws.sy[s];
+        p.vx[d] = ws.svx[s];
+        p.vy[d] = ws.svy[s];
+        if (dim == 3) {
+            p.z[d] = ws.sz[s];
+            p.vz[d] = ws.svz[s];
+        }
+        for (int e = 0; e < p.n_extra; ++e) p.extra[e][d] = ws.sextra[e][s];
+        p.id[d] = s_off[k] + (s - s_beg[k]);
+        p.label[d] = -1;
+    }
+    if (perm) {
+        const long long ibeg = D ? ctr->i_first : N;
+        for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < ibeg; i += stride) perm[i] = (int)i;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        *p.n = dst0 + C;
+        *next_id = nid0 + s_total;
+    }
+}
+
+// ------------------------------------------------------------------ multi-GPU slab migration
+
+__global__ void __launch_bounds__(kThreads) k_mig_pack(PartDev p, GridDev g, Workspace ws, float *blo, float *bhi,
+                                                       long long maxm, int rec)
+{
+    const long long n = *p.n;
+    long long moved = 0;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        if (p.label[i] <= -2) continue;
+        int oob = 0;
+        const int cx = cell_axis(p.x[i], g.lo[0], g.inv_cs, 0, g.ncell[0], oob);
+        float *buf = cx < g.cx_begin ? blo : (cx >= g.cx_end ? bhi : nullptr);
+        if (!buf) continue;
+        const int slot = atomicAdd(reinterpret_cast<int *>(buf), 1);
+        if (slot >= maxm) {
+            atomicOr(&ws.ctr->status, kStMigrate);
+            continue;
+        }
+        float *r = buf + 4 + (long long)slot * rec;
+        int w = 0;
+        r[w++] = p.x[i];
+        r[w++] = p.y[i];
+        if (g.dim == 3) r[w++] = p.z[i];
+        r[w++] = p.vx[i];
+        r[w++] = p.vy[i];
+        if (g.dim == 3) r[w++] = p.vz[i];
+        for (int e = 0; e < p.n_extra; ++e) r[w++] = p.extra[e][i];
+        const long long id = p.id[i];
+        r[w++] = __int_as_float((int)(id & 0xffffffffll));
+        r[w++] = __int_as_float((int)(id >> 32));
+        r[w++] = __int_as_float(p.label[i]);
+        p.label[i] = -3;  // migrated away: dropped by the next cell-list build
+        ++moved;
+    }
+    moved = warp_sum_ll(moved);
+    if ((threadIdx.x & 31) == 0 && moved) atomicAdd((unsigned long long *)&ws.ctr->migrated, (unsigned long long)moved);
+}
+
+// one block: append a received buffer at the tail
+__global__ void __launch_bounds__(1024) k_mig_unpack(PartDev p, int dim, Workspace ws, const float *buf,
+                                                     long long maxm, int rec)
+{
+    const long long n = *p.n;
+    long long cnt = __float_as_int(buf[0]);
+    if (cnt > maxm) cnt = maxm;
+    if (n + cnt > p.cap) {
+        if (threadIdx.x == 0) atomicOr(&ws.ctr->status, kStCapacity);
+        cnt = p.cap - n;
+    }
+    for (long long s = threadIdx.x; s < cnt; s += blockDim.x) {
+        const float *r = buf + 4 + s * rec;
+        const long long d = n + s;
+        int w = 0;
+        p.x[d] = r[w++];
+        p.y[d] = r[w++];
+        if (dim == 3) p.z[d] = r[w++];
+        p.vx[d] = r[w++];
+        p.vy[d] = r[w++];
+        if (dim == 3) p.vz[d] = r[w++];
+        for (int e = 0; e < p.n_extra; ++e) p.extra[e][d] = r[w++];
+        const long long lo = (unsigned)__float_as_int(r[w++]);
+        const long long hi = __float_as_int(r[w++]);
+        p.id[d] = (hi << 32) | lo;
+        p.label[d] = __float_as_int(r[w++]);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) *p.n = n + cnt;
+}
+
+// ------------------------------------------------------------------ launchers
+
+static int g_sms = 0;
+
+int sm_count()
+{
+    if (!g_sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+        if (g_sms <= 0) g_sms = 148;
+    }
+    return g_sms;
+}
+
+template <typename K>
+static int occ_grid(K kernel, int threads, size_t smem = 0)
+{
+    int per = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, threads, smem);
+    if (per <= 0) per = 1;
+    return per * sm_count();
+}
+
+cudaError_t launch_advect(const PartDev &p, int dim, float dt, cudaStream_t s, Launch *L)
+{
+    L->before(s);
+    k_advect<<<sm_count() * 8, kThreads, 0, s>>>(p, dim, dt);
+    L->after(s, KID_ADVECT);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_register(const PartDev &p, const GridDev &g, const PortTable &pt, int k, long long *members,
+                            cudaStream_t s, Launch *L)
+{
+    L->before(s);
+    k_register<<<sm_count() * 8, kThreads, 0, s>>>(p, g.dim, pt.p[k], k, members);
+    L->after(s, KID_REGISTER);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_cll(const PartDev &in, const PartDev &out, const GridDev &g, const Workspace &ws,
+                       int *cell_start, int *cell_end, int *perm, cudaStream_t s, Launch *L)
+{
+    const long long ntiles = (g.ncells + kCellTile - 1) / kCellTile;
+    L->before(s);
+    k_cll_key<<<sm_count() * 8, kThreads, 0, s>>>(in, g, ws);
+    L->after(s, KID_CLL_KEY);
+    L->before(s);
+    k_cell_scan<<<(unsigned)(ntiles > 0 ? ntiles : 1), kThreads, 0, s>>>(g, ws, cell_start, cell_end, out.n, ntiles);
+    L->after(s, KID_CELL_SCAN);
+    L->before(s);
+    k_cll_scatter<<<sm_count() * 8, kThreads, 0, s>>>(ws, cell_start, perm);
+    L->after(s, KID_CLL_SCATTER);
+    L->before(s);
+    if (in.n_extra > 0) {
+        static int grid = 0;
+        if (!grid) grid = occ_grid(k_cll_gather<true>, kThreads);
+        k_cll_gather<true><<<grid, kThreads, 0, s>>>(in, out, g.dim, ws, cell_start, cell_end, perm);
+    } else {
+        static int grid = 0;
+        if (!grid) grid = occ_grid(k_cll_gather<false>, kThreads);
+        k_cll_gather<false><<<grid, kThreads, 0, s>>>(in, out, g.dim, ws, cell_start, cell_end, perm);
+    }
+    L->after(s, KID_CLL_GATHER);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_update(const PartDev &p, const GridDev &g, const PortTable &pt, const Workspace &ws, int n_runs,
+                          const int *cell_start, const int *cell_end, int *port_counts, cudaStream_t s,
+                          Launch *L)
+{
+    L->before(s);
+    k_upd_prologue<<<1, 1024, 0, s>>>(ws, n_runs, cell_start, cell_end, port_counts, pt.max_ports);
+    L->after(s, KID_UPD_PROLOGUE);
+    static int grid = 0;
+    if (!grid) grid = occ_grid(k_upd_main, kThreads);
+    L->before(s);
+    k_upd_main<<<grid, kThreads, 0, s>>>(p, g.dim, pt, ws, n_runs, cell_start, port_counts);
+    L->after(s, KID_UPD_MAIN);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_compact(const PartDev &p, const PortTable &pt, const Workspace &ws, const int *all_counts,
+                           int nranks, int rank, long long *next_id, int *perm, cudaStream_t s, Launch *L)
+{
+    const int dim = p.z ? 3 : 2;
+    L->before(s);
+    if (p.n_extra > 0) {
+        static int grid = 0;
+        if (!grid) grid = occ_grid(k_compact<true>, kThreads);
+        k_compact<true><<<grid, kThreads, 0, s>>>(p, dim, ws, perm, next_id);
+    } else {
+        static int grid = 0;
+        if (!grid) grid = occ_grid(k_compact<false>, kThreads);
+        k_compact<false><<<grid, kThreads, 0, s>>>(p, dim, ws, perm, next_id);
+    }
+    L->after(s, KID_COMPACT);
+    L->before(s);
+    k_compact_append<<<sm_count() * 4, kThreads, 0, s>>>(p, dim, pt.n, pt.max_ports, ws, all_counts, nranks, rank,
+                                                          next_id, perm);
+    L->after(s, KID_COMPACT_APPEND);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_migrate_pack(const PartDev &p, const GridDev &g, const Workspace &ws, float *lo, float *hi,
+                                long long max_migrate, int rec, cudaStream_t s, Launch *L)
+{
+    cudaError_t e = cudaMemsetAsync(lo, 0, 16, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(hi, 0, 16, s);
+    if (e != cudaSuccess) return e;
+    L->before(s);
+    k_mig_pack<<<sm_count() * 8, kThreads, 0, s>>>(p, g, ws, lo, hi, max_migrate, rec);
+    L->after(s, KID_MIG_PACK);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_migrate_unpack(const PartDev &p, const GridDev &g, const Workspace &ws, const float *buf,
+                                  long long max_migrate, int rec, cudaStream_t s, Launch *L)
+{
+    L->before(s);
+    k_mig_unpack<<<1, 1024, 0, s>>>(p, g.dim, ws, buf, max_migrate, rec);
+    L->after(s, KID_MIG_UNPACK);
+    return cudaGetLastError();
+}
+
+}  // namespace sphbuf
