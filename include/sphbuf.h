@@ -50,7 +50,8 @@ typedef enum {
     SPH_ERR_OVERLAP = -3,          /* decision region P_k intersects an existing port's P_j */
     SPH_ERR_OUT_OF_GRID = -4,      /* P_k not strictly inside the grid */
     SPH_ERR_CAPACITY = -5,         /* (device) N - D + C > capacity, or staging/migration buffer full */
-    SPH_ERR_MOTION = -6,           /* (device) a buffer particle moved more than a buffer length */
+    SPH_ERR_MOTION = -6,           /* (device) a buffer particle found outside its decision region P_k
+                                      (it moved more than the one-cell margin in one step; reading R12) */
     SPH_ERR_CUDA = -7,             /* a CUDA runtime call failed (see sph_last_error) */
     SPH_ERR_STATE = -9             /* call order violated (e.g. no workspace) */
 } sph_status;

@@ -421,7 +421,7 @@ typedef struct {
     int32_t *port_counts;  /* [2K]: created_k at [k], deleted_k at [K + k] */
     int64_t checked;       /* particle-port tests performed */
     int64_t multi_decision;/* particles with more than one decision (must be 0) */
-    int64_t motion_errors; /* members of k with X'_0 > 3a/2 (reading R12; diagnostic) */
+    int64_t motion_errors; /* members of k outside P_k (reading R12; diagnostic) */
 } orc_update_out;
 
 static void copy_row(const orc_state *src, int64_t i, orc_state *dst, int64_t j, int32_t dim)
@@ -500,7 +500,7 @@ int orc_update(const orc_grid *g, const orc_port *ports, int32_t K, const orc_st
                 ++out->checked;
                 int b = classify(p, dim, g->cs, S->x[j], S->y[j], dim == 3 ? S->z[j] : 0.0f, prec);
                 int member = (S->label[j] == k);
-                if (member && (b & 16)) ++out->motion_errors;          /* reading R12 (diagnostic) */
+                if (member && !(b & 1)) ++out->motion_errors;          /* reading R12 (diagnostic) */
                 if (!(b & 1)) continue;                               /* x not in P_k (R4) */
                 int create = 0, del = 0;
                 if (p->kind == ORC_INLET) {

@@ -144,6 +144,37 @@ __device__ __forceinline__ unsigned block_excl_scan(unsigned v, unsigned &total,
     return res;
 }
 
+// Exclusive ranks of flagged items in STRIPED order: item `it` of thread t is
+// element it * NT + t of the tile, so the order is (item, warp, lane).  One
+// ballot per item and warp, one barrier.  s_cnt: ITEMS * NT/32 words.
+template <int NT, int ITEMS>
+__device__ __forceinline__ void striped_scan(const bool (&flag)[ITEMS], unsigned (&excl)[ITEMS], unsigned &total,
+                                             unsigned *s_cnt)
+{
+    constexpr int NW = NT / 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned lt = lanemask_lt();
+    unsigned b[ITEMS];
+#pragma unroll
+    for (int it = 0; it < ITEMS; ++it) {
+        b[it] = __ballot_sync(0xffffffffu, flag[it]);
+        if (lane == 0) s_cnt[it * NW + warp] = __popc(b[it]);
+    }
+    __syncthreads();
+    unsigned run = 0;
+#pragma unroll
+    for (int it = 0; it < ITEMS; ++it) {
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+            const unsigned c = s_cnt[it * NW + w];
+            if (w == warp) excl[it] = run + __popc(b[it] & lt);
+            run += c;
+        }
+    }
+    total = run;
+    __syncthreads();
+}
+
 // 64-bit variant (used for run offsets).
 template <int NT>
 __device__ __forceinline__ long long block_excl_scan_ll(long long v, long long &total, long long *s_warp)
@@ -476,7 +507,7 @@ __global__ void __launch_bounds__(kThreads) k_upd_main(PartDev p, int dim, const
                                                        int *port_counts)
 {
     __shared__ PortDev s_ports[SPH_MAX_PORTS];
-    __shared__ unsigned s_warp[kThreads / 32 + 1];
+    __shared__ unsigned s_warp[kUpdItems * kThreads / 32 + 1];
     __shared__ long long s_tile;
     __shared__ unsigned s_prefix;
     {
@@ -541,8 +572,9 @@ __global__ void __launch_bounds__(kThreads) k_upd_main(PartDev p, int dim, const
                     del = member && (X[0] < -P.he[0]);           // Alg. 3
                 }
             }
-            // R12: a buffer particle more than one buffer length beyond the interface
-            if (member && __fsub_rn(X[0], __fmul_rn(2.0f, P.he[0])) > P.he[0]) ++motion;
+            // R12: a buffer particle outside its decision region moved more than the
+            // one-cell margin in one step; it can no longer be generated/deleted.
+            if (member && !inP) ++motion;
             float px = x, py = y, pz = z;
             if (create) {
                 // recycle: x <- fl(x - fl(a u)) (Eqs. 2D/3D_Inverse_transformation, R10)
@@ -578,20 +610,17 @@ __global__ void __launch_bounds__(kThreads) k_upd_main(PartDev p, int dim, const
                 }
             }
         }
-        unsigned mine = 0;
-#pragma unroll
-        for (int it = 0; it < kUpdItems; ++it) mine += cr[it];
-        unsigned total;
-        const unsigned excl = block_excl_scan<kThreads>(mine, total, s_warp);
+        unsigned excl[kUpdItems], total;
+        striped_scan<kThreads, kUpdItems>(cr, excl, total, s_warp);
         if (threadIdx.x < 32) {
             const unsigned pre = tile_prefix(ws.tile_upd, tile, epoch, total);
             if (threadIdx.x == 0) s_prefix = pre;
         }
         __syncthreads();
-        long long slot = (long long)s_prefix + excl;
 #pragma unroll
         for (int it = 0; it < kUpdItems; ++it) {
             if (!cr[it]) continue;
+            const long long slot = (long long)s_prefix + excl[it];
             if (slot < ws.max_new) {
                 const int pi = pidx[it];
                 // duplicate = bitwise copy of the pre-recycle state, label fluid (R11)
@@ -609,7 +638,6 @@ __global__ void __launch_bounds__(kThreads) k_upd_main(PartDev p, int dim, const
             } else {
                 atomicOr(&ctr->status, kStStaging);
             }
-            ++slot;
         }
         if (tile == ntiles - 1 && threadIdx.x == 0) ctr->n_stage = (long long)s_prefix + total;
         __syncthreads();
@@ -639,7 +667,7 @@ template <bool HasExtra>
 __global__ void __launch_bounds__(kThreads) k_compact(PartDev p, int dim, Workspace ws, int *perm,
                                                       const long long *next_id)
 {
-    __shared__ unsigned s_warp[kThreads / 32 + 1];
+    __shared__ unsigned s_warp[kCmpItems * kThreads / 32 + 1];
     __shared__ long long s_tile;
     __shared__ unsigned s_prefix;
     Counters *ctr = ws.ctr;
@@ -700,14 +728,13 @@ __global__ void __launch_bounds__(kThreads) k_compact(PartDev p, int dim, Worksp
             }
         }
         if (dep == 0x7f3a5c11 && mine == 77u) ctr->dummy = dep;   // never true in practice; keeps the dependency
-        unsigned total;
-        const unsigned excl = block_excl_scan<kThreads>(mine, total, s_warp);
+        unsigned excl[kCmpItems], total;
+        striped_scan<kThreads, kCmpItems>(alive, excl, total, s_warp);
         if (threadIdx.x < 32) {
             const unsigned pre = tile_prefix(ws.tile_cmp, tile, epoch, total);
             if (threadIdx.x == 0) s_prefix = pre;
         }
         __syncthreads();
-        long long o = ibeg + (long long)s_prefix + excl;
 #pragma unroll
         for (int it = 0; it < kCmpItems; ++it) {
             const long long i = ibeg + tile * kCmpTile + it * kThreads + threadIdx.x;
@@ -716,6 +743,7 @@ __global__ void __launch_bounds__(kThreads) k_compact(PartDev p, int dim, Worksp
                 if (perm) perm[i] = -1;
                 continue;
             }
+            const long long o = ibeg + (long long)s_prefix + excl[it];
             p.x[o] = x[it];
             p.y[o] = y[it];
             p.vx[o] = vx[it];
@@ -729,7 +757,6 @@ __global__ void __launch_bounds__(kThreads) k_compact(PartDev p, int dim, Worksp
             p.id[o] = id[it];
             p.label[o] = lab[it];
             if (perm) perm[i] = (int)o;
-            ++o;
         }
         __syncthreads();
     }

@@ -49,14 +49,14 @@ def test_C3_duct_scaled_full_run():
 
 
 def test_C4_junction_scaled():
-    w = inputs.c4(scale=0.3, nports=8, n_updates=30)
-    tot, bu = lockstep(w, 30, check_every=3)
+    w = inputs.c4(scale=0.5, nports=8, n_updates=12)
+    tot, bu = lockstep(w, 12, check_every=3)
     assert tot[0] > 0 and tot[1] > 0
 
 
 def test_C5_slab_scaled():
-    w = inputs.c5(scale=0.25, slab=0, nslabs=1, n_updates=10)
-    tot, bu = lockstep(w, 10, check_every=2)
+    w = inputs.c5(scale=0.5, slab=0, nslabs=1, n_updates=6)
+    tot, bu = lockstep(w, 6, check_every=2)
     assert tot[0] > 0
 
 
