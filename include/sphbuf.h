@@ -149,6 +149,12 @@ sph_status sph_advect(sph_ctx *ctx, sph_particles *p, float dt, void *stream);
 sph_status sph_cll_build(sph_ctx *ctx, const sph_particles *in, sph_particles *out, int32_t *cell_start,
                          int32_t *cell_end, int32_t *perm_or_null, void *stream);
 
+/* sph_advect (the driver's step) fused into the key pass of sph_cll_build: the
+ * advected positions are written back to `in` and the build proceeds as above.
+ * Identical results to sph_advect followed by sph_cll_build, one pass less. */
+sph_status sph_advect_cll_build(sph_ctx *ctx, sph_particles *in, sph_particles *out, float dt, int32_t *cell_start,
+                                int32_t *cell_end, int32_t *perm_or_null, void *stream);
+
 /* One buffer update over the candidates of every port (cells from registration,
  * particle ranges from the cell tables of the sph_cll_build just made on `p`):
  * X' = Q_k (x - o_k) in pinned fp32; decisions gated by x in P_k:
@@ -199,7 +205,7 @@ int64_t sph_launch_count(const sph_ctx *ctx);
  * totals; sph_profile_read waits for the last event and returns, per kernel id
  * (0 .. SPH_NKERNELS-1, named by sph_kernel_name), the summed milliseconds and
  * the number of launches.  ms, count: host arrays of SPH_NKERNELS. */
-#define SPH_NKERNELS 12
+#define SPH_NKERNELS 13
 sph_status sph_profile(sph_ctx *ctx, int32_t enable);
 sph_status sph_profile_read(sph_ctx *ctx, double *ms, int64_t *count);
 const char *sph_kernel_name(int32_t i);

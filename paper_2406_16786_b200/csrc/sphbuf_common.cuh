@@ -1,0 +1,271 @@
+// sphbuf_common.cuh — device helpers shared by the sm_100a kernels of the
+// in/outlet buffer update (arXiv 2406.16786 §III): warp/block scans, the
+// decoupled look-back, and the pinned fp32 local-frame transform and cell index.
+// "P:n" = PAPER.md line n; readings R<n> are listed in DESIGN.md §3.
+//
+// All arithmetic that decides an integer or mutates particle state uses
+// __fadd_rn/__fsub_rn/__fmul_rn (one binary32 round-to-nearest op each, never
+// contracted), in the order fixed by DESIGN.md §3 "Pinned arithmetic".
+#pragma once
+#include <climits>
+#include <cstdint>
+
+#include "sphbuf_internal.h"
+
+namespace sphbuf {
+
+// ------------------------------------------------------------------ helpers
+
+__device__ __forceinline__ unsigned lanemask_lt()
+{
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+__device__ __forceinline__ void st_release(unsigned long long *p, unsigned long long v)
+{
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long *p)
+{
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// tile status word: [63:34] epoch (30 bits) | [33:32] flag (1 aggregate, 2 inclusive prefix) | [31:0] value
+__device__ __forceinline__ unsigned long long pack_status(unsigned epoch, unsigned flag, unsigned value)
+{
+    return ((unsigned long long)(epoch & 0x3fffffffu) << 34) | ((unsigned long long)flag << 32) | value;
+}
+
+__device__ __forceinline__ unsigned warp_sum(unsigned v)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__device__ __forceinline__ long long warp_sum_ll(long long v)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__device__ __forceinline__ long long warp_min_ll(long long v)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        long long w = __shfl_xor_sync(0xffffffffu, v, o);
+        v = w < v ? w : v;
+    }
+    return v;
+}
+
+// Decoupled look-back (single pass): called by all 32 lanes of warp 0 of a block
+// that owns `tile`.  Publishes the tile's aggregate, accumulates predecessors'
+// aggregates until an inclusive prefix is found, publishes its own inclusive
+// prefix and returns the exclusive prefix.  Publishing uses release stores and
+// reading acquire loads, so everything a predecessor did before publishing
+// happens-before what the caller does after this returns.
+static __device__ unsigned tile_prefix(unsigned long long *status, long long tile, unsigned epoch, unsigned aggregate)
+{
+    const int lane = threadIdx.x & 31;
+    const unsigned ep = epoch & 0x3fffffffu;
+    if (tile == 0) {
+        if (lane == 0) st_release(&status[0], pack_status(epoch, 2, aggregate));
+        return 0;
+    }
+    if (lane == 0) st_release(&status[tile], pack_status(epoch, 1, aggregate));
+    unsigned excl = 0;
+    long long base = tile - 1;
+    while (true) {
+        long long t = base - lane;
+        unsigned long long s = 0;
+        unsigned flag;
+        if (t >= 0) {
+            do {
+                s = ld_acquire(&status[t]);
+                flag = ((unsigned)(s >> 34) == ep) ? (unsigned)((s >> 32) & 3u) : 0u;
+            } while (flag == 0);
+        } else {
+            flag = 2;
+            s = 0;
+        }
+        unsigned pmask = __ballot_sync(0xffffffffu, flag == 2);
+        int first = pmask ? __ffs(pmask) - 1 : 32;
+        unsigned v = (lane <= first) ? (unsigned)(s & 0xffffffffu) : 0u;
+        excl += warp_sum(v);
+        if (pmask) break;
+        base -= 32;
+    }
+    if (lane == 0) st_release(&status[tile], pack_status(epoch, 2, excl + aggregate));
+    return excl;
+}
+
+// Block-wide exclusive scan of one unsigned per thread (NT threads).
+template <int NT>
+__device__ __forceinline__ unsigned block_excl_scan(unsigned v, unsigned &total, unsigned *s_warp)
+{
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_warp[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        unsigned w = lane < NT / 32 ? s_warp[lane] : 0u;
+        unsigned wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            unsigned y = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= o) wi += y;
+        }
+        if (lane < NT / 32) s_warp[lane] = wi - w;
+        if (lane == NT / 32 - 1) s_warp[NT / 32] = wi;
+    }
+    __syncthreads();
+    unsigned res = s_warp[warp] + x - v;
+    total = s_warp[NT / 32];
+    __syncthreads();
+    return res;
+}
+
+// Exclusive ranks of flagged items in STRIPED order: item `it` of thread t is
+// element it * NT + t of the tile, so the order is (item, warp, lane).  One
+// ballot per item and warp, one barrier.  s_cnt: ITEMS * NT/32 words.
+template <int NT, int ITEMS>
+__device__ __forceinline__ void striped_scan(const bool (&flag)[ITEMS], unsigned (&excl)[ITEMS], unsigned &total,
+                                             unsigned *s_cnt)
+{
+    constexpr int NW = NT / 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned lt = lanemask_lt();
+    unsigned b[ITEMS];
+#pragma unroll
+    for (int it = 0; it < ITEMS; ++it) {
+        b[it] = __ballot_sync(0xffffffffu, flag[it]);
+        if (lane == 0) s_cnt[it * NW + warp] = __popc(b[it]);
+    }
+    __syncthreads();
+    unsigned run = 0;
+#pragma unroll
+    for (int it = 0; it < ITEMS; ++it) {
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+            const unsigned c = s_cnt[it * NW + w];
+            if (w == warp) excl[it] = run + __popc(b[it] & lt);
+            run += c;
+        }
+    }
+    total = run;
+    __syncthreads();
+}
+
+// 64-bit variant (used for run offsets).
+template <int NT>
+__device__ __forceinline__ long long block_excl_scan_ll(long long v, long long &total, long long *s_warp)
+{
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    long long x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        long long y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_warp[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        long long w = lane < NT / 32 ? s_warp[lane] : 0;
+        long long wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            long long y = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= o) wi += y;
+        }
+        if (lane < NT / 32) s_warp[lane] = wi - w;
+        if (lane == NT / 32 - 1) s_warp[NT / 32] = wi;
+    }
+    __syncthreads();
+    long long res = s_warp[warp] + x - v;
+    total = s_warp[NT / 32];
+    __syncthreads();
+    return res;
+}
+
+// Pinned forward transform X' = Q (x - o) (Eq. 2D_transformation P:252-269,
+// Eq. 3D_transformation): d_j = fl(x_j - o_j);
+// X'_r = fl(fl(fl(Q_r0 d_0) + fl(Q_r1 d_1)) + fl(Q_r2 d_2)).
+__device__ __forceinline__ void to_local(const PortDev &P, int dim, float x, float y, float z, float X[3])
+{
+    const float d0 = __fsub_rn(x, P.o[0]);
+    const float d1 = __fsub_rn(y, P.o[1]);
+    if (dim == 3) {
+        const float d2 = __fsub_rn(z, P.o[2]);
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+            X[r] = __fadd_rn(__fadd_rn(__fmul_rn(P.Q[3 * r], d0), __fmul_rn(P.Q[3 * r + 1], d1)),
+                             __fmul_rn(P.Q[3 * r + 2], d2));
+    } else {
+#pragma unroll
+        for (int r = 0; r < 2; ++r) X[r] = __fadd_rn(__fmul_rn(P.Q[3 * r], d0), __fmul_rn(P.Q[3 * r + 1], d1));
+        X[2] = 0.0f;
+    }
+}
+
+__device__ __forceinline__ bool in_box(const float X[3], const float he[3], int dim)
+{
+    bool r = fabsf(X[0]) < he[0] && fabsf(X[1]) < he[1];
+    if (dim == 3) r = r && fabsf(X[2]) < he[2];
+    return r;
+}
+
+// Pinned cell index along one axis: floor(fl(fl(x - lo) * inv_cs)), clamped.
+__device__ __forceinline__ int cell_axis(float x, float lo, float inv, int lo_c, int hi_c, int &oob)
+{
+    const float t = __fmul_rn(__fsub_rn(x, lo), inv);
+    const float f = floorf(t);
+    if (f < (float)lo_c) { oob = 1; return lo_c; }
+    if (f > (float)(hi_c - 1)) { oob = 1; return hi_c - 1; }
+    return (int)f;
+}
+
+__device__ __forceinline__ int cell_of(const GridDev &g, float x, float y, float z, int &oob)
+{
+    const int cx = cell_axis(x, g.lo[0], g.inv_cs, g.cx_begin, g.cx_end, oob);
+    const int cy = cell_axis(y, g.lo[1], g.inv_cs, 0, g.ncell[1], oob);
+    int cz = 0;
+    if (g.dim == 3) cz = cell_axis(z, g.lo[2], g.inv_cs, 0, g.ncell[2], oob);
+    return ((cx - g.cx_begin) * g.ny + cy) * g.nz + cz;
+}
+
+// ------------------------------------------------------------------ launch helpers (host)
+
+inline int sm_count_cached()
+{
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    return sms;
+}
+
+template <typename K>
+inline int occ_grid(K kernel, int threads, size_t smem = 0)
+{
+    int per = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, threads, smem);
+    if (per <= 0) per = 1;
+    return per * sm_count_cached();
+}
+
+}  // namespace sphbuf

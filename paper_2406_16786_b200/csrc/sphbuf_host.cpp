@@ -120,19 +120,22 @@ size_t layout(const sph_ctx *c, char *base, Workspace *W)
     const long long cap = c->capacity;
     const long long cell_tiles = (ncells + kCellTile - 1) / kCellTile + 1;
     const long long upd_tiles = (2 * cap + kUpdTile - 1) / kUpdTile + 64;
-    const long long cmp_tiles = (cap + kCmpTile - 1) / kCmpTile + 1;
+    const long long cmp_tiles = (cap + kCntTile - 1) / kCntTile + 1;
+    const long long cmp_subs = cmp_tiles * (kCntTile / kCmpTile);
     Workspace w{};
     w.ctr = (Counters *)take(sizeof(Counters));
     w.cell_count = (int *)take(sizeof(int) * ncells);
     w.tile_cells = (unsigned long long *)take(8 * cell_tiles);
     w.tile_upd = (unsigned long long *)take(8 * upd_tiles);
     w.tile_cmp = (unsigned long long *)take(8 * cmp_tiles);
+    w.rd = (unsigned *)take(4 * cmp_subs);
     w.runs = (int *)take(sizeof(int) * 3 * kMaxRuns);
     w.run_off = (long long *)take(sizeof(long long) * (kMaxRuns + 1));
     const size_t zero_end = off;   // everything above must start zeroed
+    w.sub_off = (unsigned *)take(4 * cmp_subs);
     w.key = (int *)take(sizeof(int) * cap);
     w.rank = (int *)take(sizeof(int) * cap);
-    w.src = (int *)take(sizeof(int) * cap);
+    w.pair = (int2 *)take(sizeof(int2) * cap);
     const long long mn = c->max_new;
     w.sx = (float *)take(4 * mn);
     w.sy = (float *)take(4 * mn);
@@ -159,7 +162,7 @@ size_t zero_bytes(const sph_ctx *c)
     Workspace w{};
     char *fake = reinterpret_cast<char *>(size_t(1) << 40);
     layout(c, fake, &w);
-    return (size_t)(reinterpret_cast<char *>(w.key) - fake);
+    return (size_t)(reinterpret_cast<char *>(w.sub_off) - fake);
 }
 
 PartDev part_dev(const sph_particles *p)
@@ -539,8 +542,8 @@ sph_status sph_advect(sph_ctx *c, sph_particles *p, float dt, void *stream)
     return e == cudaSuccess ? SPH_OK : cuda_fail(c, e, "advect");
 }
 
-sph_status sph_cll_build(sph_ctx *c, const sph_particles *in, sph_particles *out, int32_t *cell_start,
-                         int32_t *cell_end, int32_t *perm, void *stream)
+static sph_status cll_build(sph_ctx *c, const sph_particles *in, sph_particles *out, int32_t *cell_start,
+                            int32_t *cell_end, int32_t *perm, float dt, bool advect, void *stream)
 {
     if (!c) return SPH_ERR_ARG;
     sph_status st = check_particles(c, in);
@@ -551,9 +554,21 @@ sph_status sph_cll_build(sph_ctx *c, const sph_particles *in, sph_particles *out
         return fail(c, SPH_ERR_ARG, "cll_build needs distinct input and output arrays");
     if ((reinterpret_cast<size_t>(cell_start) | reinterpret_cast<size_t>(cell_end)) % 16)
         return fail(c, SPH_ERR_ARG, "cell tables must be 16-byte aligned");
-    cudaError_t e = launch_cll(part_dev(in), part_dev(out), c->gd, c->W, cell_start, cell_end, perm,
+    cudaError_t e = launch_cll(part_dev(in), part_dev(out), c->gd, c->W, cell_start, cell_end, perm, dt, advect,
                                static_cast<cudaStream_t>(stream), &c->L);
     return e == cudaSuccess ? SPH_OK : cuda_fail(c, e, "cll_build");
+}
+
+sph_status sph_cll_build(sph_ctx *c, const sph_particles *in, sph_particles *out, int32_t *cell_start,
+                         int32_t *cell_end, int32_t *perm, void *stream)
+{
+    return cll_build(c, in, out, cell_start, cell_end, perm, 0.0f, false, stream);
+}
+
+sph_status sph_advect_cll_build(sph_ctx *c, sph_particles *in, sph_particles *out, float dt, int32_t *cell_start,
+                                int32_t *cell_end, int32_t *perm, void *stream)
+{
+    return cll_build(c, in, out, cell_start, cell_end, perm, dt, true, stream);
 }
 
 sph_status sph_buffer_update(sph_ctx *c, sph_particles *p, const int32_t *cell_start, const int32_t *cell_end,
@@ -641,7 +656,7 @@ int64_t sph_launch_count(const sph_ctx *c) { return c ? c->L.count : 0; }
 
 static const char *kKernelNames[KID_COUNT] = {
     "advect", "register", "cll_key", "cell_scan", "cll_scatter", "cll_gather", "upd_prologue",
-    "upd_main", "compact", "compact_append", "mig_pack", "mig_unpack"};
+    "upd_main", "compact", "compact_append", "mig_pack", "mig_unpack", "compact_count"};
 
 const char *sph_kernel_name(int32_t i) { return (i >= 0 && i < KID_COUNT) ? kKernelNames[i] : ""; }
 

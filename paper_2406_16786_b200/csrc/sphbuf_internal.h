@@ -20,6 +20,7 @@ constexpr int kUpdItems = 2;             // candidates per thread in the update
 constexpr int kUpdTile = kThreads * kUpdItems;
 constexpr int kCmpItems = 4;             // particles per thread in the compaction
 constexpr int kCmpTile = kThreads * kCmpItems;
+constexpr int kCntTile = 8192;           // labels per tile in the compaction count
 constexpr int kGatherItems = 4;          // output slots per thread in the gather
 constexpr int kGatherTile = kThreads * kGatherItems;
 constexpr int64_t kMaxRuns = 1 << 20;    // port runs per context
@@ -70,7 +71,7 @@ struct PartDev {
 
 struct Counters {
     unsigned int epoch_cll, epoch_upd, epoch_cmp, epoch_pad;
-    int ticket_cll, ticket_upd, ticket_cmp, ticket_pad;
+    int ticket_cll, ticket_upd, ticket_cmp, ticket_cmp2;
     long long n_in;        // cll: live+tombstone input length
     long long n_cand;      // update: candidates this update
     long long n_stage;     // update: created this update (may exceed staging capacity -> error)
@@ -92,9 +93,11 @@ struct Workspace {
     unsigned long long *tile_cells;  // [cell tiles]
     int *key;                        // [capacity]
     int *rank;                       // [capacity]
-    int *src;                        // [capacity]
+    int2 *pair;                      // [capacity]: (source index, cell) per sorted slot
     unsigned long long *tile_upd;    // [upd tiles]
-    unsigned long long *tile_cmp;    // [cmp tiles]
+    unsigned long long *tile_cmp;    // [cmp count tiles]
+    unsigned *sub_off;               // [cmp sub-tiles]: tombstones before each sub-tile
+    unsigned *rd;                    // [cmp sub-tiles]: "read done" epoch flags
     int *runs;                       // [kMaxRuns * 3]: c0, c1, port
     long long *run_off;              // [kMaxRuns + 1]
     float *sx, *sy, *sz, *svx, *svy, *svz;
@@ -109,7 +112,7 @@ struct Workspace {
 // ---------------------------------------------------------------- launch bookkeeping
 enum KernelId {
     KID_ADVECT, KID_REGISTER, KID_CLL_KEY, KID_CELL_SCAN, KID_CLL_SCATTER, KID_CLL_GATHER, KID_UPD_PROLOGUE,
-    KID_UPD_MAIN, KID_COMPACT, KID_COMPACT_APPEND, KID_MIG_PACK, KID_MIG_UNPACK, KID_COUNT
+    KID_UPD_MAIN, KID_COMPACT, KID_COMPACT_APPEND, KID_MIG_PACK, KID_MIG_UNPACK, KID_COMPACT_COUNT, KID_COUNT
 };
 
 // Counts launches; when profiling is on, brackets every launch with a pair of
@@ -133,7 +136,7 @@ cudaError_t launch_advect(const PartDev &p, int dim, float dt, cudaStream_t s, L
 cudaError_t launch_register(const PartDev &p, const GridDev &g, const PortTable &pt, int k, long long *members,
                             cudaStream_t s, Launch *L);
 cudaError_t launch_cll(const PartDev &in, const PartDev &out, const GridDev &g, const Workspace &ws,
-                       int *cell_start, int *cell_end, int *perm, cudaStream_t s, Launch *L);
+                       int *cell_start, int *cell_end, int *perm, float dt, bool advect, cudaStream_t s, Launch *L);
 cudaError_t launch_update(const PartDev &p, const GridDev &g, const PortTable &pt, const Workspace &ws, int n_runs,
                           const int *cell_start, const int *cell_end, int *port_counts, cudaStream_t s,
                           Launch *L);

@@ -1,0 +1,282 @@
+// sphbuf_update.cu — registration (Alg. 1 identification), the driver's advection,
+// and the buffer update: candidate transform + axial compare (a3), inflow
+// generation (a4), outflow deletion (a5) and relabel (a6), fused in one pass over
+// the candidates of the port cell runs (arXiv 2406.16786 §III).
+#include <climits>
+#include <cstdint>
+
+#include "sphbuf_common.cuh"
+
+namespace sphbuf {
+
+// ------------------------------------------------------------------ driver: advection
+
+__global__ void __launch_bounds__(kThreads) k_advect(PartDev p, int dim, float dt)
+{
+    const long long n = *p.n;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        p.x[i] = __fadd_rn(p.x[i], __fmul_rn(p.vx[i], dt));
+        p.y[i] = __fadd_rn(p.y[i], __fmul_rn(p.vy[i], dt));
+        if (dim == 3) p.z[i] = __fadd_rn(p.z[i], __fmul_rn(p.vz[i], dt));
+    }
+}
+
+// ------------------------------------------------------------------ registration (Alg. 1 identification)
+
+// "Buffer particle identification ... Execute only once": every fluid
+// particle in the box of port k becomes a buffer particle of k; the same test is
+// the initial relabel of outlet / bidirectional ports.
+__global__ void __launch_bounds__(kThreads) k_register(PartDev p, int dim, PortDev P, int k, long long *members)
+{
+    const long long n = *p.n;
+    long long cnt = 0;
+    const int lane = threadIdx.x & 31;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i - lane < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        if (i < n) {
+            int lab = p.label[i];
+            if (lab == -1) {
+                float X[3];
+                to_local(P, dim, p.x[i], p.y[i], dim == 3 ? p.z[i] : 0.0f, X);
+                if (in_box(X, P.he, dim)) {
+                    lab = k;
+                    p.label[i] = k;
+                }
+            }
+            cnt += (lab == k);
+        }
+    }
+    cnt = warp_sum_ll(cnt);
+    if (lane == 0 && cnt && members) atomicAdd((unsigned long long *)members, (unsigned long long)cnt);
+}
+
+// ------------------------------------------------------------------ a3-a6: buffer update
+
+// K5: candidate count per port run (cell ranges from the current cell list) and
+// their exclusive scan; resets the per-update counters.  One block.
+__global__ void __launch_bounds__(1024) k_upd_prologue(Workspace ws, int n_runs, const int *cell_start,
+                                                       const int *cell_end, int *port_counts, int max_ports)
+{
+    __shared__ long long s_warp[1024 / 32 + 1];
+    Counters *ctr = ws.ctr;
+    if (threadIdx.x == 0) {
+        ctr->epoch_upd += 1;
+        ctr->ticket_upd = 0;
+        ctr->n_stage = 0;
+        ctr->n_del = 0;
+        ctr->i_first = LLONG_MAX;
+    }
+    for (int i = threadIdx.x; i < 2 * max_ports; i += blockDim.x) port_counts[i] = 0;
+    long long carry = 0;
+    for (int r0 = 0; r0 < n_runs; r0 += 1024) {
+        const int r = r0 + threadIdx.x;
+        long long len = 0;
+        if (r < n_runs) len = (long long)cell_end[ws.runs[3 * r + 1]] - (long long)cell_start[ws.runs[3 * r]];
+        long long total;
+        const long long ex = block_excl_scan_ll<1024>(len, total, s_warp);
+        if (r < n_runs) ws.run_off[r] = carry + ex;
+        carry += total;
+    }
+    if (threadIdx.x == 0) {
+        ws.run_off[n_runs] = carry;
+        ctr->n_cand = carry;
+        ctr->checked += carry;
+        if ((carry + kUpdTile - 1) / kUpdTile > ws.upd_tiles) ctr->status |= kStCapacity;
+    }
+}
+
+// K6: the candidate check (a3) with generation (a4), deletion (a5) and relabel
+// (a6) fused; CREATEs are appended to the staging area in canonical order
+// (port, cell, id) by a ballot/block scan + decoupled look-back over ordered tiles.
+__global__ void __launch_bounds__(kThreads) k_upd_main(PartDev p, int dim, const __grid_constant__ PortTable pt,
+                                                       Workspace ws, int n_runs, const int *cell_start,
+                                                       int *port_counts)
+{
+    __shared__ PortDev s_ports[SPH_MAX_PORTS];
+    __shared__ unsigned s_warp[kUpdItems * kThreads / 32 + 1];
+    __shared__ long long s_tile;
+    __shared__ unsigned s_prefix;
+    {
+        const int words = pt.n * (int)(sizeof(PortDev) / 4);
+        const unsigned *src = reinterpret_cast<const unsigned *>(pt.p);
+        unsigned *dst = reinterpret_cast<unsigned *>(s_ports);
+        for (int w = threadIdx.x; w < words; w += blockDim.x) dst[w] = src[w];
+    }
+    Counters *ctr = ws.ctr;
+    const long long n_cand = ctr->n_cand;
+    const unsigned epoch = ctr->epoch_upd;
+    const long long ntiles = (n_cand + kUpdTile - 1) / kUpdTile;
+    const int max_ports = pt.max_ports;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        ctr->epoch_cmp += 1;  // consumed by the compaction that follows
+        ctr->ticket_cmp = 0;
+        ctr->ticket_cmp2 = 0;
+    }
+    long long del_cnt = 0, del_min = LLONG_MAX, motion = 0;
+    __syncthreads();
+    while (true) {
+        if (threadIdx.x == 0) s_tile = atomicAdd(&ctr->ticket_upd, 1);
+        __syncthreads();
+        const long long tile = s_tile;
+        if (tile >= ntiles || tile >= ws.upd_tiles) break;
+        bool cr[kUpdItems];
+        int pidx[kUpdItems], kk[kUpdItems];
+        float ox[kUpdItems], oy[kUpdItems], oz[kUpdItems];
+#pragma unroll
+        for (int it = 0; it < kUpdItems; ++it) {
+            cr[it] = false;
+            pidx[it] = -1;
+            kk[it] = 0;
+            ox[it] = oy[it] = oz[it] = 0.0f;
+            const long long g = tile * kUpdTile + it * kThreads + threadIdx.x;
+            if (g >= n_cand) continue;
+            // run containing g: largest r with run_off[r] <= g
+            int lo = 0, hi = n_runs - 1;
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (ws.run_off[mid] <= g) lo = mid;
+                else hi = mid - 1;
+            }
+            const int r = lo;
+            const int k = ws.runs[3 * r + 2];
+            const int pi = cell_start[ws.runs[3 * r]] + (int)(g - ws.run_off[r]);
+            const PortDev &P = s_ports[k];
+            const float x = p.x[pi], y = p.y[pi], z = dim == 3 ? p.z[pi] : 0.0f;
+            const int lab = p.label[pi];
+            float X[3];
+            to_local(P, dim, x, y, z, X);
+            const bool inP = in_box(X, P.heP, dim);              // x in P_k (reading R4)
+            const bool member = (lab == k);
+            const bool beyond = X[0] > P.he[0];                  // X'_0 > a/2
+            bool create = false, del = false;
+            if (inP) {
+                if (P.kind == SPH_INLET) {
+                    create = member && beyond;                   // Alg. 1 (R5)
+                } else if (P.kind == SPH_OUTLET) {
+                    del = beyond;                                // Alg. 2 (R6)
+                } else {
+                    create = member && beyond;                   // Alg. 3
+                    del = member && (X[0] < -P.he[0]);           // Alg. 3
+                }
+            }
+            // R12: a buffer particle outside its decision region moved more than the
+            // one-cell margin in one step; it can no longer be generated/deleted.
+            if (member && !inP) ++motion;
+            float px = x, py = y, pz = z;
+            if (create) {
+                // recycle: x <- fl(x - fl(a u)) (Eqs. 2D/3D_Inverse_transformation, R10)
+                px = __fsub_rn(x, P.s[0]);
+                py = __fsub_rn(y, P.s[1]);
+                p.x[pi] = px;
+                p.y[pi] = py;
+                if (dim == 3) {
+                    pz = __fsub_rn(z, P.s[2]);
+                    p.z[pi] = pz;
+                }
+                cr[it] = true;
+                pidx[it] = pi;
+                kk[it] = k;
+                ox[it] = x;
+                oy[it] = y;
+                oz[it] = z;
+                atomicAdd(&port_counts[k], 1);
+            }
+            if (del) {
+                p.label[pi] = -2;                                // tombstone, removed by sph_compact
+                atomicAdd(&port_counts[max_ports + k], 1);
+                ++del_cnt;
+                del_min = pi < del_min ? pi : del_min;
+            } else if (P.kind != SPH_INLET) {
+                // relabel on post-recycle positions (R9)
+                float Xp[3] = {X[0], X[1], X[2]};
+                if (create) to_local(P, dim, px, py, pz, Xp);
+                if (in_box(Xp, P.he, dim)) {
+                    if (lab != k) p.label[pi] = k;
+                } else if (lab == k) {
+                    p.label[pi] = -1;
+                }
+            }
+        }
+        unsigned excl[kUpdItems], total;
+        striped_scan<kThreads, kUpdItems>(cr, excl, total, s_warp);
+        if (threadIdx.x < 32) {
+            const unsigned pre = tile_prefix(ws.tile_upd, tile, epoch, total);
+            if (threadIdx.x == 0) s_prefix = pre;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int it = 0; it < kUpdItems; ++it) {
+            if (!cr[it]) continue;
+            const long long slot = (long long)s_prefix + excl[it];
+            if (slot < ws.max_new) {
+                const int pi = pidx[it];
+                // duplicate = bitwise copy of the pre-recycle state, label fluid (R11)
+                ws.sx[slot] = ox[it];
+                ws.sy[slot] = oy[it];
+                ws.svx[slot] = p.vx[pi];
+                ws.svy[slot] = p.vy[pi];
+                if (dim == 3) {
+                    ws.sz[slot] = oz[it];
+                    ws.svz[slot] = p.vz[pi];
+                }
+                for (int e = 0; e < p.n_extra; ++e) ws.sextra[e][slot] = p.extra[e][pi];
+                ws.sid[slot] = p.id[pi];
+                ws.sport[slot] = kk[it];
+            } else {
+                atomicOr(&ctr->status, kStStaging);
+            }
+        }
+        if (tile == ntiles - 1 && threadIdx.x == 0) ctr->n_stage = (long long)s_prefix + total;
+        __syncthreads();
+    }
+    const int lane = threadIdx.x & 31;
+    del_cnt = warp_sum_ll(del_cnt);
+    del_min = warp_min_ll(del_min);
+    motion = warp_sum_ll(motion);
+    if (lane == 0) {
+        if (del_cnt) {
+            atomicAdd((unsigned long long *)&ctr->n_del, (unsigned long long)del_cnt);
+            atomicMin(&ctr->i_first, del_min);
+        }
+        if (motion) {
+            atomicAdd((unsigned long long *)&ctr->motion, (unsigned long long)motion);
+            atomicOr(&ctr->status, kStMotion);
+        }
+    }
+}
+
+
+// ------------------------------------------------------------------ launchers
+
+cudaError_t launch_advect(const PartDev &p, int dim, float dt, cudaStream_t s, Launch *L)
+{
+    L->before(s);
+    k_advect<<<sm_count_cached() * 8, kThreads, 0, s>>>(p, dim, dt);
+    L->after(s, KID_ADVECT);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_register(const PartDev &p, const GridDev &g, const PortTable &pt, int k, long long *members,
+                            cudaStream_t s, Launch *L)
+{
+    L->before(s);
+    k_register<<<sm_count_cached() * 8, kThreads, 0, s>>>(p, g.dim, pt.p[k], k, members);
+    L->after(s, KID_REGISTER);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_update(const PartDev &p, const GridDev &g, const PortTable &pt, const Workspace &ws, int n_runs,
+                          const int *cell_start, const int *cell_end, int *port_counts, cudaStream_t s, Launch *L)
+{
+    L->before(s);
+    k_upd_prologue<<<1, 1024, 0, s>>>(ws, n_runs, cell_start, cell_end, port_counts, pt.max_ports);
+    L->after(s, KID_UPD_PROLOGUE);
+    static int grid = 0;
+    if (!grid) grid = occ_grid(k_upd_main, kThreads);
+    L->before(s);
+    k_upd_main<<<grid, kThreads, 0, s>>>(p, g.dim, pt, ws, n_runs, cell_start, port_counts);
+    L->after(s, KID_UPD_MAIN);
+    return cudaGetLastError();
+}
+
+}  // namespace sphbuf

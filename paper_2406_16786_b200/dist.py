@@ -86,10 +86,13 @@ class SlabUpdater:
 
     # phases (LoopbackGroup interleaves them across slabs)
     def phase_advect_pack(self, dt):
-        if dt is not None:
-            self.bu.advect(dt)
+        self._dt = None
         if self.world > 1:
+            if dt is not None:
+                self.bu.advect(dt)
             sphbuf.sph_migrate_pack(self.bu.ctx, self.bu.A, self.send_lo, self.send_hi)
+        else:
+            self._dt = dt       # single slab: advection fused into the cell-list build
 
     def phase_unpack_update(self):
         if self.world > 1:
@@ -97,7 +100,7 @@ class SlabUpdater:
                 sphbuf.sph_migrate_unpack(self.bu.ctx, self.bu.A, self.recv_lo)
             if self.rank < self.world - 1:
                 sphbuf.sph_migrate_unpack(self.bu.ctx, self.bu.A, self.recv_hi)
-        self.bu.cll_build()
+        self.bu.cll_build(dt=self._dt)
         self.bu.update()
 
     def phase_compact(self):

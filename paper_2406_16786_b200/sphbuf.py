@@ -55,8 +55,8 @@ EXPORTS = ["sph_ctx_create", "sph_ctx_destroy", "sph_last_error", "sph_workspace
            "sph_port_check", "sph_buffer_register", "sph_advect", "sph_cll_build", "sph_buffer_update",
            "sph_compact", "sph_migrate_record_floats", "sph_migrate_pack", "sph_migrate_unpack", "sph_status_sync",
            "sph_launch_count", "sph_port_cells", "sph_frame_from_axis", "sph_profile", "sph_profile_read",
-           "sph_kernel_name"]
-NKERNELS = 12
+           "sph_kernel_name", "sph_advect_cll_build"]
+NKERNELS = 13
 
 
 def lib():
@@ -82,6 +82,8 @@ def lib():
     L.sph_buffer_register.argtypes = [vp, P(sph_particles), vp, vp, vp, i32, i32, f32, P(i32), vp, vp]
     L.sph_advect.argtypes = [vp, P(sph_particles), f32, vp]
     L.sph_cll_build.argtypes = [vp, P(sph_particles), P(sph_particles), vp, vp, vp, vp]
+    L.sph_advect_cll_build.argtypes = [vp, P(sph_particles), P(sph_particles), f32, vp, vp, vp, vp]
+    L.sph_advect_cll_build.restype = C.c_int
     L.sph_buffer_update.argtypes = [vp, P(sph_particles), vp, vp, vp, vp]
     L.sph_compact.argtypes = [vp, P(sph_particles), vp, i32, i32, vp, vp, vp]
     L.sph_migrate_record_floats.argtypes = [vp]
@@ -193,6 +195,11 @@ def sph_advect(ctx, parts, dt, stream=None):
 def sph_cll_build(ctx, pin, pout, cell_start, cell_end, perm=None, stream=None):
     _check(lib().sph_cll_build(ctx.h, C.byref(pin.abi), C.byref(pout.abi), _ptr(cell_start), _ptr(cell_end),
                                _ptr(perm), _stream(stream)), ctx.h)
+
+
+def sph_advect_cll_build(ctx, pin, pout, dt, cell_start, cell_end, perm=None, stream=None):
+    _check(lib().sph_advect_cll_build(ctx.h, C.byref(pin.abi), C.byref(pout.abi), float(dt), _ptr(cell_start),
+                                      _ptr(cell_end), _ptr(perm), _stream(stream)), ctx.h)
 
 
 def sph_buffer_update(ctx, parts, cell_start, cell_end, port_counts, stream=None):
@@ -361,8 +368,12 @@ class BufferUpdater:
     def advect(self, dt, stream=None):
         sph_advect(self.ctx, self.A, dt, stream)
 
-    def cll_build(self, perm=None, stream=None):
-        sph_cll_build(self.ctx, self.A, self.B, self.cell_start, self.cell_end, perm, stream)
+    def cll_build(self, perm=None, stream=None, dt=None):
+        """Cell-list build A -> B (then swap); with dt, the advection is fused into its key pass."""
+        if dt is None:
+            sph_cll_build(self.ctx, self.A, self.B, self.cell_start, self.cell_end, perm, stream)
+        else:
+            sph_advect_cll_build(self.ctx, self.A, self.B, dt, self.cell_start, self.cell_end, perm, stream)
         self.A, self.B = self.B, self.A
 
     def update(self, stream=None):
@@ -372,10 +383,13 @@ class BufferUpdater:
         ac = self.port_counts if all_counts is None else all_counts
         sph_compact(self.ctx, self.A, ac, nranks, rank, self.next_id, perm, stream)
 
-    def step(self, dt, stream=None):
-        if dt is not None:
+    def step(self, dt, stream=None, fused=True):
+        """advect -> cell-list build -> buffer update -> compaction.  fused: the
+        advection runs inside the build's key pass (sph_advect_cll_build)."""
+        if dt is not None and not fused:
             self.advect(dt, stream)
-        self.cll_build(stream=stream)
+            dt = None
+        self.cll_build(stream=stream, dt=dt)
         self.update(stream)
         self.compact(stream=stream)
 

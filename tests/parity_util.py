@@ -44,7 +44,7 @@ def make_updater(w, capacity=None, max_new=None, n_extra=0):
 
 
 def lockstep(w, n_updates, check_cll=True, state=None, next_id=None, capacity=None, max_new=None,
-             check_every=1):
+             check_every=1, fused=False):
     """Run n_updates on GPU and oracle from the same state; compare registration,
     cell lists, counts and the full post-compaction state bit-exactly.
     Returns totals of (created, deleted) and the GPU updater."""
@@ -67,8 +67,11 @@ def lockstep(w, n_updates, check_cll=True, state=None, next_id=None, capacity=No
         res = oracle.update(w.grid, w.ports, st)
         assert res.multi_decision == 0
         new, perm, nid = oracle.compact(res, dim, K, res.port_counts[None, :], 0, nid)
-        bu.advect(w.dt)
-        bu.cll_build()
+        if fused:
+            bu.cll_build(dt=w.dt)          # sph_advect_cll_build
+        else:
+            bu.advect(w.dt)
+            bu.cll_build()
         cmp_now = (step % check_every == 0) or step == n_updates - 1
         if check_cll and cmp_now:
             torch.cuda.synchronize()

@@ -42,6 +42,12 @@ def test_C2_bidirectional_100_updates():
     assert tot[0] > 0 and tot[1] > 0
 
 
+def test_C2_fused_advect_cll_build():
+    w = inputs.make("C2")
+    tot, bu = lockstep(w, 30, check_every=3, fused=True)
+    assert tot[0] > 0 and tot[1] > 0
+
+
 def test_C3_duct_scaled_full_run():
     w = inputs.c3(scale=0.25, n_updates=100)
     tot, bu = lockstep(w, 100, check_every=10)
