@@ -125,6 +125,8 @@ def algorithmic_bytes(kernel, dim, n, ncells, cand, created, deleted, moved):
         "cell_scan": ncells * 12,
         "cll_scatter": n * 8,
         "cll_gather": n * 2 * S,
+        "cll_rank": n * (8 + 8),
+        "compact_count": moved * 4,
         "upd_main": cand * (4 * dim + 4) + created * (2 * S + 4 * dim),
         "compact": moved * S + (moved - deleted) * S,
         "compact_append": created * S,

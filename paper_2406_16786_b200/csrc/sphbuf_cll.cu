@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(kThreads) k_cell_scan(GridDev g, Workspace ws,
 
 constexpr int kScatterItems = 4;
 
-__global__ void __launch_bounds__(kThreads) k_cll_scatter(Workspace ws, const int *cell_start, int *perm)
+__global__ void __launch_bounds__(kThreads) k_cll_scatter(Workspace ws, const int *cell_start, int *dst)
 {
     const long long n = ws.ctr->n_in;
     const long long stride = (long long)gridDim.x * kThreads * kScatterItems;
@@ -173,23 +173,23 @@ __global__ void __launch_bounds__(kThreads) k_cll_scatter(Workspace ws, const in
             const long long i = base + it * kThreads + threadIdx.x;
             if (i >= n) continue;
             if (key[it] >= 0) ws.pair[cell_start[key[it]] + rk[it]] = make_int2((int)i, key[it]);
-            else if (perm) perm[i] = -1;
+            else dst[i] = -1;                                     // tombstone: dropped
         }
     }
 }
 
-template <bool HasExtra>
-__global__ void __launch_bounds__(kThreads) k_cll_gather(PartDev in, PartDev out, int dim, Workspace ws,
-                                                         const int *cell_start, const int *cell_end, int *perm)
+// K4a: destination of every source particle: its cell's start plus its rank by id
+// among the cell's slots (ids staged in shared memory; slots of a cell that
+// straddle the tile edge are read from global memory).
+__global__ void __launch_bounds__(kThreads) k_cll_rank(PartDev in, Workspace ws, const int *cell_start,
+                                                       const int *cell_end, int *dst, const long long *n_out)
 {
     __shared__ long long s_id[kGatherTile];
-    const long long n = *out.n;
+    const long long n = *n_out;
     for (long long j0 = (long long)blockIdx.x * kGatherTile; j0 < n; j0 += (long long)gridDim.x * kGatherTile) {
-        int src[kGatherItems], cb[kGatherItems], ce[kGatherItems], lab[kGatherItems];
-        float x[kGatherItems], y[kGatherItems], z[kGatherItems], vx[kGatherItems], vy[kGatherItems],
-            vz[kGatherItems];
-        long long id[kGatherItems];
         int2 pr[kGatherItems];
+        long long id[kGatherItems];
+        int cb[kGatherItems], ce[kGatherItems];
 #pragma unroll
         for (int it = 0; it < kGatherItems; ++it) {
             const long long j = j0 + it * kThreads + threadIdx.x;
@@ -197,48 +197,79 @@ __global__ void __launch_bounds__(kThreads) k_cll_gather(PartDev in, PartDev out
         }
 #pragma unroll
         for (int it = 0; it < kGatherItems; ++it) {
-            src[it] = pr[it].x;
-            if (src[it] < 0) continue;
-            const int s = src[it];
+            if (pr[it].x < 0) continue;
+            id[it] = in.id[pr[it].x];
             cb[it] = cell_start[pr[it].y];
             ce[it] = cell_end[pr[it].y];
-            x[it] = in.x[s];
-            y[it] = in.y[s];
-            vx[it] = in.vx[s];
-            vy[it] = in.vy[s];
-            if (dim == 3) {
-                z[it] = in.z[s];
-                vz[it] = in.vz[s];
-            }
-            id[it] = in.id[s];
-            lab[it] = in.label[s];
             s_id[it * kThreads + threadIdx.x] = id[it];
         }
         __syncthreads();
 #pragma unroll
         for (int it = 0; it < kGatherItems; ++it) {
-            if (src[it] < 0) continue;
+            if (pr[it].x < 0) continue;
             int r = 0;
-            for (int q = cb[it]; q < ce[it]; ++q) {
-                const long long idq = (q >= j0 && q < j0 + kGatherTile) ? s_id[q - j0] : in.id[ws.pair[q].x];
-                r += (idq < id[it]);
-            }
-            const int d = cb[it] + r;
-            out.x[d] = x[it];
-            out.y[d] = y[it];
-            out.vx[d] = vx[it];
-            out.vy[d] = vy[it];
-            if (dim == 3) {
-                out.z[d] = z[it];
-                out.vz[d] = vz[it];
-            }
-            if (HasExtra)
-                for (int e = 0; e < in.n_extra; ++e) out.extra[e][d] = in.extra[e][src[it]];
-            out.id[d] = id[it];
-            out.label[d] = lab[it];
-            if (perm) perm[src[it]] = d;
+            const long long lo = cb[it] > j0 ? cb[it] : j0;
+            const long long hi = ce[it] < j0 + kGatherTile ? ce[it] : j0 + kGatherTile;
+            for (long long q = lo; q < hi; ++q) r += (s_id[q - j0] < id[it]);
+            for (long long q = cb[it]; q < lo; ++q) r += (in.id[ws.pair[q].x] < id[it]);
+            for (long long q = hi; q < ce[it]; ++q) r += (in.id[ws.pair[q].x] < id[it]);
+            dst[pr[it].x] = cb[it] + r;
         }
         __syncthreads();
+    }
+}
+
+// K4b: streaming copy in input order (coalesced loads) to the destinations
+// (nearly sequential, since the input is nearly sorted already).
+constexpr int kCopyItems = 4;
+
+template <bool HasExtra>
+__global__ void __launch_bounds__(kThreads) k_cll_copy(PartDev in, PartDev out, int dim, Workspace ws, const int *dst)
+{
+    const long long n = ws.ctr->n_in;
+    const long long stride = (long long)gridDim.x * kThreads * kCopyItems;
+    for (long long base = (long long)blockIdx.x * kThreads * kCopyItems; base < n; base += stride) {
+        int d[kCopyItems];
+        float x[kCopyItems], y[kCopyItems], z[kCopyItems], vx[kCopyItems], vy[kCopyItems], vz[kCopyItems];
+        long long id[kCopyItems];
+        int lab[kCopyItems];
+#pragma unroll
+        for (int it = 0; it < kCopyItems; ++it) {
+            const long long i = base + it * kThreads + threadIdx.x;
+            d[it] = -1;
+            if (i < n) {
+                d[it] = dst[i];
+                x[it] = in.x[i];
+                y[it] = in.y[i];
+                vx[it] = in.vx[i];
+                vy[it] = in.vy[i];
+                if (dim == 3) {
+                    z[it] = in.z[i];
+                    vz[it] = in.vz[i];
+                }
+                id[it] = in.id[i];
+                lab[it] = in.label[i];
+            }
+        }
+#pragma unroll
+        for (int it = 0; it < kCopyItems; ++it) {
+            const int o = d[it];
+            if (o < 0) continue;
+            out.x[o] = x[it];
+            out.y[o] = y[it];
+            out.vx[o] = vx[it];
+            out.vy[o] = vy[it];
+            if (dim == 3) {
+                out.z[o] = z[it];
+                out.vz[o] = vz[it];
+            }
+            out.id[o] = id[it];
+            out.label[o] = lab[it];
+            if (HasExtra) {
+                const long long i = base + it * kThreads + threadIdx.x;
+                for (int e = 0; e < in.n_extra; ++e) out.extra[e][o] = in.extra[e][i];
+            }
+        }
     }
 }
 
@@ -264,22 +295,30 @@ cudaError_t launch_cll(const PartDev &in, const PartDev &out, const GridDev &g, 
     L->before(s);
     k_cell_scan<<<(unsigned)(ntiles > 0 ? ntiles : 1), kThreads, 0, s>>>(g, ws, cell_start, cell_end, out.n, ntiles);
     L->after(s, KID_CELL_SCAN);
+    int *dst = perm ? perm : ws.dst;   // destination of each input particle (the optional perm output)
     {
         static int grid = 0;
         if (!grid) grid = occ_grid(k_cll_scatter, kThreads);
         L->before(s);
-        k_cll_scatter<<<grid, kThreads, 0, s>>>(ws, cell_start, perm);
+        k_cll_scatter<<<grid, kThreads, 0, s>>>(ws, cell_start, dst);
         L->after(s, KID_CLL_SCATTER);
+    }
+    {
+        static int grid = 0;
+        if (!grid) grid = occ_grid(k_cll_rank, kThreads);
+        L->before(s);
+        k_cll_rank<<<grid, kThreads, 0, s>>>(in, ws, cell_start, cell_end, dst, out.n);
+        L->after(s, KID_CLL_RANK);
     }
     L->before(s);
     if (in.n_extra > 0) {
         static int grid = 0;
-        if (!grid) grid = occ_grid(k_cll_gather<true>, kThreads);
-        k_cll_gather<true><<<grid, kThreads, 0, s>>>(in, out, g.dim, ws, cell_start, cell_end, perm);
+        if (!grid) grid = occ_grid(k_cll_copy<true>, kThreads);
+        k_cll_copy<true><<<grid, kThreads, 0, s>>>(in, out, g.dim, ws, dst);
     } else {
         static int grid = 0;
-        if (!grid) grid = occ_grid(k_cll_gather<false>, kThreads);
-        k_cll_gather<false><<<grid, kThreads, 0, s>>>(in, out, g.dim, ws, cell_start, cell_end, perm);
+        if (!grid) grid = occ_grid(k_cll_copy<false>, kThreads);
+        k_cll_copy<false><<<grid, kThreads, 0, s>>>(in, out, g.dim, ws, dst);
     }
     L->after(s, KID_CLL_GATHER);
     return cudaGetLastError();

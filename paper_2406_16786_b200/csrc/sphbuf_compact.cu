@@ -23,6 +23,12 @@ namespace sphbuf {
 
 constexpr int kCntSub = kCntTile / kCmpTile;        // sub-tiles per count tile (8)
 constexpr int kCntItems = kCntTile / kThreads;      // labels per thread (32)
+static_assert(kCntSub == kThreads / 32, "one warp per compaction sub-tile");
+
+// First element the compaction touches: i_first rounded down to a count tile,
+// so label loads are 16-byte aligned (elements in [begin, i_first) are alive and
+// are rewritten onto themselves).
+__device__ __forceinline__ long long cmp_begin(long long i_first) { return (i_first / kCntTile) * kCntTile; }
 
 __global__ void __launch_bounds__(kThreads) k_compact_count(PartDev p, Workspace ws, const long long *next_id)
 {
@@ -38,7 +44,7 @@ __global__ void __launch_bounds__(kThreads) k_compact_count(PartDev p, Workspace
         ctr->cmp_next_id = *next_id;
     }
     if (D == 0) return;
-    const long long ibeg = ctr->i_first;
+    const long long ibeg = cmp_begin(ctr->i_first);
     const unsigned epoch = ctr->epoch_cmp;
     const long long ntiles = (N - ibeg + kCntTile - 1) / kCntTile;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -47,25 +53,29 @@ __global__ void __launch_bounds__(kThreads) k_compact_count(PartDev p, Workspace
         __syncthreads();
         const long long tile = s_tile;
         if (tile >= ntiles) break;
-        int lab[kCntItems];
+        // blocked: thread t counts labels [t*32, t*32+32) of the tile, so warp w
+        // covers exactly sub-tile w (1024 labels) of the compaction move
+        const long long base = ibeg + tile * kCntTile + (long long)threadIdx.x * kCntItems;
+        unsigned c = 0;
+        if (base + kCntItems <= N) {
+            const int4 *q = reinterpret_cast<const int4 *>(p.label + base);
 #pragma unroll
-        for (int it = 0; it < kCntItems; ++it) {
-            const long long i = ibeg + tile * kCntTile + it * kThreads + threadIdx.x;
-            lab[it] = i < N ? p.label[i] : 0;
+            for (int v = 0; v < kCntItems / 4; ++v) {
+                const int4 a = q[v];
+                c += (a.x <= -2) + (a.y <= -2) + (a.z <= -2) + (a.w <= -2);
+            }
+        } else {
+            for (int j = 0; j < kCntItems; ++j)
+                if (base + j < N) c += (p.label[base + j] <= -2);
         }
-#pragma unroll
-        for (int sub = 0; sub < kCntSub; ++sub) {
-            unsigned c = 0;
-#pragma unroll
-            for (int k = 0; k < kCmpItems; ++k) c += __popc(__ballot_sync(0xffffffffu, lab[sub * kCmpItems + k] <= -2));
-            if (lane == 0) s_sub[sub][warp] = c;
-        }
+        c = warp_sum(c);
+        if (lane == 0) s_sub[0][warp] = c;
         __syncthreads();
         if (threadIdx.x == 0) {
             unsigned run = 0;
             for (int sub = 0; sub < kCntSub; ++sub) {
                 s_tot[sub] = run;
-                for (int w = 0; w < kThreads / 32; ++w) run += s_sub[sub][w];
+                run += s_sub[0][sub];
             }
             s_tot[kCntSub] = run;
         }
@@ -89,7 +99,7 @@ __global__ void __launch_bounds__(kThreads) k_compact_move(PartDev p, int dim, W
     const long long D = ctr->n_del;
     if (D == 0) return;
     const long long N = ctr->cmp_n;
-    const long long ibeg = ctr->i_first;
+    const long long ibeg = cmp_begin(ctr->i_first);
     const unsigned epoch = ctr->epoch_cmp;
     const long long nsub = (N - ibeg + kCmpTile - 1) / kCmpTile;
     int dep = 0;
@@ -238,7 +248,7 @@ __global__ void __launch_bounds__(kThreads) k_compact_append(PartDev p, int dim,
         p.label[d] = -1;
     }
     if (perm) {
-        const long long ibeg = D ? ctr->i_first : N;
+        const long long ibeg = D ? cmp_begin(ctr->i_first) : N;
         for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < ibeg; i += stride) perm[i] = (int)i;
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {

@@ -136,6 +136,7 @@ size_t layout(const sph_ctx *c, char *base, Workspace *W)
     w.key = (int *)take(sizeof(int) * cap);
     w.rank = (int *)take(sizeof(int) * cap);
     w.pair = (int2 *)take(sizeof(int2) * cap);
+    w.dst = (int *)take(sizeof(int) * cap);
     const long long mn = c->max_new;
     w.sx = (float *)take(4 * mn);
     w.sy = (float *)take(4 * mn);
@@ -656,7 +657,7 @@ int64_t sph_launch_count(const sph_ctx *c) { return c ? c->L.count : 0; }
 
 static const char *kKernelNames[KID_COUNT] = {
     "advect", "register", "cll_key", "cell_scan", "cll_scatter", "cll_gather", "upd_prologue",
-    "upd_main", "compact", "compact_append", "mig_pack", "mig_unpack", "compact_count"};
+    "upd_main", "compact", "compact_append", "mig_pack", "mig_unpack", "compact_count", "cll_rank"};
 
 const char *sph_kernel_name(int32_t i) { return (i >= 0 && i < KID_COUNT) ? kKernelNames[i] : ""; }
 

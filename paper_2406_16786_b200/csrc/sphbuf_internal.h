@@ -94,6 +94,7 @@ struct Workspace {
     int *key;                        // [capacity]
     int *rank;                       // [capacity]
     int2 *pair;                      // [capacity]: (source index, cell) per sorted slot
+    int *dst;                        // [capacity]: sorted position of each input particle (-1 dropped)
     unsigned long long *tile_upd;    // [upd tiles]
     unsigned long long *tile_cmp;    // [cmp count tiles]
     unsigned *sub_off;               // [cmp sub-tiles]: tombstones before each sub-tile
@@ -112,7 +113,8 @@ struct Workspace {
 // ---------------------------------------------------------------- launch bookkeeping
 enum KernelId {
     KID_ADVECT, KID_REGISTER, KID_CLL_KEY, KID_CELL_SCAN, KID_CLL_SCATTER, KID_CLL_GATHER, KID_UPD_PROLOGUE,
-    KID_UPD_MAIN, KID_COMPACT, KID_COMPACT_APPEND, KID_MIG_PACK, KID_MIG_UNPACK, KID_COMPACT_COUNT, KID_COUNT
+    KID_UPD_MAIN, KID_COMPACT, KID_COMPACT_APPEND, KID_MIG_PACK, KID_MIG_UNPACK, KID_COMPACT_COUNT, KID_CLL_RANK,
+    KID_COUNT
 };
 
 // Counts launches; when profiling is on, brackets every launch with a pair of

@@ -56,7 +56,7 @@ EXPORTS = ["sph_ctx_create", "sph_ctx_destroy", "sph_last_error", "sph_workspace
            "sph_compact", "sph_migrate_record_floats", "sph_migrate_pack", "sph_migrate_unpack", "sph_status_sync",
            "sph_launch_count", "sph_port_cells", "sph_frame_from_axis", "sph_profile", "sph_profile_read",
            "sph_kernel_name", "sph_advect_cll_build"]
-NKERNELS = 13
+NKERNELS = 14
 
 
 def lib():
