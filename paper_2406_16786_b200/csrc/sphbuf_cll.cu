@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(kThreads) k_cell_scan(GridDev g, Workspace ws,
 
 constexpr int kScatterItems = 4;
 
-__global__ void __launch_bounds__(kThreads) k_cll_scatter(Workspace ws, const int *cell_start, int *dst)
+__global__ void __launch_bounds__(kThreads) k_cll_scatter(Workspace ws, const int *cell_start, int *perm)
 {
     const long long n = ws.ctr->n_in;
     const long long stride = (long long)gridDim.x * kThreads * kScatterItems;
@@ -173,16 +173,17 @@ __global__ void __launch_bounds__(kThreads) k_cll_scatter(Workspace ws, const in
             const long long i = base + it * kThreads + threadIdx.x;
             if (i >= n) continue;
             if (key[it] >= 0) ws.pair[cell_start[key[it]] + rk[it]] = make_int2((int)i, key[it]);
-            else dst[i] = -1;                                     // tombstone: dropped
+            else if (perm) perm[i] = -1;                          // tombstone: dropped
         }
     }
 }
 
-// K4a: destination of every source particle: its cell's start plus its rank by id
-// among the cell's slots (ids staged in shared memory; slots of a cell that
-// straddle the tile edge are read from global memory).
+// K4a: final order inside each cell: slot cb + (rank by id among the cell's
+// slots) receives its source index in ws.dst (ids staged in shared memory; slots
+// of a cell that straddles the tile edge are read from global memory).  The
+// writes stay inside the cell, so they are nearly sequential.
 __global__ void __launch_bounds__(kThreads) k_cll_rank(PartDev in, Workspace ws, const int *cell_start,
-                                                       const int *cell_end, int *dst, const long long *n_out)
+                                                       const int *cell_end, int *perm, const long long *n_out)
 {
     __shared__ long long s_id[kGatherTile];
     const long long n = *n_out;
@@ -213,48 +214,52 @@ __global__ void __launch_bounds__(kThreads) k_cll_rank(PartDev in, Workspace ws,
             for (long long q = lo; q < hi; ++q) r += (s_id[q - j0] < id[it]);
             for (long long q = cb[it]; q < lo; ++q) r += (in.id[ws.pair[q].x] < id[it]);
             for (long long q = hi; q < ce[it]; ++q) r += (in.id[ws.pair[q].x] < id[it]);
-            dst[pr[it].x] = cb[it] + r;
+            ws.dst[cb[it] + r] = pr[it].x;
+            if (perm) perm[pr[it].x] = cb[it] + r;
         }
         __syncthreads();
     }
 }
 
-// K4b: streaming copy in input order (coalesced loads) to the destinations
-// (nearly sequential, since the input is nearly sorted already).
+// K4b: gather in output order: slot j <- source ws.dst[j].  Stores are perfectly
+// sequential; loads are nearly sequential (the input is nearly sorted already:
+// only particles that changed cell come from far away).
 constexpr int kCopyItems = 4;
 
 template <bool HasExtra>
-__global__ void __launch_bounds__(kThreads) k_cll_copy(PartDev in, PartDev out, int dim, Workspace ws, const int *dst)
+__global__ void __launch_bounds__(kThreads) k_cll_copy(PartDev in, PartDev out, int dim, Workspace ws)
 {
-    const long long n = ws.ctr->n_in;
+    const long long n = *out.n;
     const long long stride = (long long)gridDim.x * kThreads * kCopyItems;
     for (long long base = (long long)blockIdx.x * kThreads * kCopyItems; base < n; base += stride) {
-        int d[kCopyItems];
+        int s[kCopyItems];
+#pragma unroll
+        for (int it = 0; it < kCopyItems; ++it) {
+            const long long j = base + it * kThreads + threadIdx.x;
+            s[it] = j < n ? ws.dst[j] : -1;
+        }
         float x[kCopyItems], y[kCopyItems], z[kCopyItems], vx[kCopyItems], vy[kCopyItems], vz[kCopyItems];
         long long id[kCopyItems];
         int lab[kCopyItems];
 #pragma unroll
         for (int it = 0; it < kCopyItems; ++it) {
-            const long long i = base + it * kThreads + threadIdx.x;
-            d[it] = -1;
-            if (i < n) {
-                d[it] = dst[i];
-                x[it] = in.x[i];
-                y[it] = in.y[i];
-                vx[it] = in.vx[i];
-                vy[it] = in.vy[i];
-                if (dim == 3) {
-                    z[it] = in.z[i];
-                    vz[it] = in.vz[i];
-                }
-                id[it] = in.id[i];
-                lab[it] = in.label[i];
+            if (s[it] < 0) continue;
+            const int i = s[it];
+            x[it] = in.x[i];
+            y[it] = in.y[i];
+            vx[it] = in.vx[i];
+            vy[it] = in.vy[i];
+            if (dim == 3) {
+                z[it] = in.z[i];
+                vz[it] = in.vz[i];
             }
+            id[it] = in.id[i];
+            lab[it] = in.label[i];
         }
 #pragma unroll
         for (int it = 0; it < kCopyItems; ++it) {
-            const int o = d[it];
-            if (o < 0) continue;
+            if (s[it] < 0) continue;
+            const long long o = base + it * kThreads + threadIdx.x;
             out.x[o] = x[it];
             out.y[o] = y[it];
             out.vx[o] = vx[it];
@@ -265,10 +270,8 @@ __global__ void __launch_bounds__(kThreads) k_cll_copy(PartDev in, PartDev out, 
             }
             out.id[o] = id[it];
             out.label[o] = lab[it];
-            if (HasExtra) {
-                const long long i = base + it * kThreads + threadIdx.x;
-                for (int e = 0; e < in.n_extra; ++e) out.extra[e][o] = in.extra[e][i];
-            }
+            if (HasExtra)
+                for (int e = 0; e < in.n_extra; ++e) out.extra[e][o] = in.extra[e][s[it]];
         }
     }
 }
@@ -295,30 +298,29 @@ cudaError_t launch_cll(const PartDev &in, const PartDev &out, const GridDev &g, 
     L->before(s);
     k_cell_scan<<<(unsigned)(ntiles > 0 ? ntiles : 1), kThreads, 0, s>>>(g, ws, cell_start, cell_end, out.n, ntiles);
     L->after(s, KID_CELL_SCAN);
-    int *dst = perm ? perm : ws.dst;   // destination of each input particle (the optional perm output)
     {
         static int grid = 0;
         if (!grid) grid = occ_grid(k_cll_scatter, kThreads);
         L->before(s);
-        k_cll_scatter<<<grid, kThreads, 0, s>>>(ws, cell_start, dst);
+        k_cll_scatter<<<grid, kThreads, 0, s>>>(ws, cell_start, perm);
         L->after(s, KID_CLL_SCATTER);
     }
     {
         static int grid = 0;
         if (!grid) grid = occ_grid(k_cll_rank, kThreads);
         L->before(s);
-        k_cll_rank<<<grid, kThreads, 0, s>>>(in, ws, cell_start, cell_end, dst, out.n);
+        k_cll_rank<<<grid, kThreads, 0, s>>>(in, ws, cell_start, cell_end, perm, out.n);
         L->after(s, KID_CLL_RANK);
     }
     L->before(s);
     if (in.n_extra > 0) {
         static int grid = 0;
         if (!grid) grid = occ_grid(k_cll_copy<true>, kThreads);
-        k_cll_copy<true><<<grid, kThreads, 0, s>>>(in, out, g.dim, ws, dst);
+        k_cll_copy<true><<<grid, kThreads, 0, s>>>(in, out, g.dim, ws);
     } else {
         static int grid = 0;
         if (!grid) grid = occ_grid(k_cll_copy<false>, kThreads);
-        k_cll_copy<false><<<grid, kThreads, 0, s>>>(in, out, g.dim, ws, dst);
+        k_cll_copy<false><<<grid, kThreads, 0, s>>>(in, out, g.dim, ws);
     }
     L->after(s, KID_CLL_GATHER);
     return cudaGetLastError();
