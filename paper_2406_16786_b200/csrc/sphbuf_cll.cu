@@ -36,28 +36,44 @@ __global__ void __launch_bounds__(kThreads) k_cll_key(PartDev in, GridDev g, Wor
     int oob_acc = 0;
     const long long stride = (long long)gridDim.x * kThreads * kKeyItems;
     for (long long base = (long long)blockIdx.x * kThreads * kKeyItems; base < n; base += stride) {
-        int key[kKeyItems];
+        int key[kKeyItems], lab[kKeyItems];
+        float x[kKeyItems], y[kKeyItems], z[kKeyItems], vx[kKeyItems], vy[kKeyItems], vz[kKeyItems];
+        // all loads of the tile first (memory-level parallelism), then the arithmetic
+#pragma unroll
+        for (int it = 0; it < kKeyItems; ++it) {
+            const long long i = base + it * kThreads + threadIdx.x;
+            lab[it] = -9;
+            if (i < n) {
+                lab[it] = in.label[i];
+                x[it] = in.x[i];
+                y[it] = in.y[i];
+                z[it] = g.dim == 3 ? in.z[i] : 0.0f;
+                if (Advect) {
+                    vx[it] = in.vx[i];
+                    vy[it] = in.vy[i];
+                    vz[it] = g.dim == 3 ? in.vz[i] : 0.0f;
+                }
+            }
+        }
 #pragma unroll
         for (int it = 0; it < kKeyItems; ++it) {
             const long long i = base + it * kThreads + threadIdx.x;
             key[it] = -1;
             if (i < n) {
-                const int lab = in.label[i];
-                float x = in.x[i], y = in.y[i], z = g.dim == 3 ? in.z[i] : 0.0f;
                 if (Advect) {
                     // driver step fused in: x <- fl(x + fl(v dt))
-                    x = __fadd_rn(x, __fmul_rn(in.vx[i], dt));
-                    y = __fadd_rn(y, __fmul_rn(in.vy[i], dt));
-                    in.x[i] = x;
-                    in.y[i] = y;
+                    x[it] = __fadd_rn(x[it], __fmul_rn(vx[it], dt));
+                    y[it] = __fadd_rn(y[it], __fmul_rn(vy[it], dt));
+                    in.x[i] = x[it];
+                    in.y[i] = y[it];
                     if (g.dim == 3) {
-                        z = __fadd_rn(z, __fmul_rn(in.vz[i], dt));
-                        in.z[i] = z;
+                        z[it] = __fadd_rn(z[it], __fmul_rn(vz[it], dt));
+                        in.z[i] = z[it];
                     }
                 }
-                if (lab > -2) {
+                if (lab[it] > -2) {
                     int oob = 0;
-                    key[it] = cell_of(g, x, y, z, oob);
+                    key[it] = cell_of(g, x[it], y[it], z[it], oob);
                     oob_acc += oob;
                 }
             }
@@ -178,19 +194,24 @@ __global__ void __launch_bounds__(kThreads) k_cll_scatter(Workspace ws, const in
     }
 }
 
-// K4a: final order inside each cell: slot cb + (rank by id among the cell's
-// slots) receives its source index in ws.dst (ids staged in shared memory; slots
-// of a cell that straddles the tile edge are read from global memory).  The
-// writes stay inside the cell, so they are nearly sequential.
-__global__ void __launch_bounds__(kThreads) k_cll_rank(PartDev in, Workspace ws, const int *cell_start,
-                                                       const int *cell_end, int *perm, const long long *n_out)
+// K4: one round of loads per output slot (the source's columns and its cell's
+// range, all independent), the rank by id among the cell's slots from ids staged
+// in shared memory (slots of a cell that straddles the tile edge are read from
+// global memory), and the store into the sorted position.  Loads are nearly
+// sequential (only particles that changed cell come from far away); stores stay
+// inside the cell.
+template <bool HasExtra>
+__global__ void __launch_bounds__(kThreads) k_cll_gather(PartDev in, PartDev out, int dim, Workspace ws,
+                                                         const int *cell_start, const int *cell_end, int *perm)
 {
     __shared__ long long s_id[kGatherTile];
-    const long long n = *n_out;
+    const long long n = *out.n;
     for (long long j0 = (long long)blockIdx.x * kGatherTile; j0 < n; j0 += (long long)gridDim.x * kGatherTile) {
-        int2 pr[kGatherItems];
+        int src[kGatherItems], cb[kGatherItems], ce[kGatherItems], lab[kGatherItems];
+        float x[kGatherItems], y[kGatherItems], z[kGatherItems], vx[kGatherItems], vy[kGatherItems],
+            vz[kGatherItems];
         long long id[kGatherItems];
-        int cb[kGatherItems], ce[kGatherItems];
+        int2 pr[kGatherItems];
 #pragma unroll
         for (int it = 0; it < kGatherItems; ++it) {
             const long long j = j0 + it * kThreads + threadIdx.x;
@@ -198,81 +219,49 @@ __global__ void __launch_bounds__(kThreads) k_cll_rank(PartDev in, Workspace ws,
         }
 #pragma unroll
         for (int it = 0; it < kGatherItems; ++it) {
-            if (pr[it].x < 0) continue;
-            id[it] = in.id[pr[it].x];
+            src[it] = pr[it].x;
+            if (src[it] < 0) continue;
+            const int s = src[it];
             cb[it] = cell_start[pr[it].y];
             ce[it] = cell_end[pr[it].y];
+            x[it] = in.x[s];
+            y[it] = in.y[s];
+            vx[it] = in.vx[s];
+            vy[it] = in.vy[s];
+            if (dim == 3) {
+                z[it] = in.z[s];
+                vz[it] = in.vz[s];
+            }
+            id[it] = in.id[s];
+            lab[it] = in.label[s];
             s_id[it * kThreads + threadIdx.x] = id[it];
         }
         __syncthreads();
 #pragma unroll
         for (int it = 0; it < kGatherItems; ++it) {
-            if (pr[it].x < 0) continue;
+            if (src[it] < 0) continue;
             int r = 0;
             const long long lo = cb[it] > j0 ? cb[it] : j0;
             const long long hi = ce[it] < j0 + kGatherTile ? ce[it] : j0 + kGatherTile;
             for (long long q = lo; q < hi; ++q) r += (s_id[q - j0] < id[it]);
             for (long long q = cb[it]; q < lo; ++q) r += (in.id[ws.pair[q].x] < id[it]);
             for (long long q = hi; q < ce[it]; ++q) r += (in.id[ws.pair[q].x] < id[it]);
-            ws.dst[cb[it] + r] = pr[it].x;
-            if (perm) perm[pr[it].x] = cb[it] + r;
+            const int d = cb[it] + r;
+            out.x[d] = x[it];
+            out.y[d] = y[it];
+            out.vx[d] = vx[it];
+            out.vy[d] = vy[it];
+            if (dim == 3) {
+                out.z[d] = z[it];
+                out.vz[d] = vz[it];
+            }
+            if (HasExtra)
+                for (int e = 0; e < in.n_extra; ++e) out.extra[e][d] = in.extra[e][src[it]];
+            out.id[d] = id[it];
+            out.label[d] = lab[it];
+            if (perm) perm[src[it]] = d;
         }
         __syncthreads();
-    }
-}
-
-// K4b: gather in output order: slot j <- source ws.dst[j].  Stores are perfectly
-// sequential; loads are nearly sequential (the input is nearly sorted already:
-// only particles that changed cell come from far away).
-constexpr int kCopyItems = 4;
-
-template <bool HasExtra>
-__global__ void __launch_bounds__(kThreads) k_cll_copy(PartDev in, PartDev out, int dim, Workspace ws)
-{
-    const long long n = *out.n;
-    const long long stride = (long long)gridDim.x * kThreads * kCopyItems;
-    for (long long base = (long long)blockIdx.x * kThreads * kCopyItems; base < n; base += stride) {
-        int s[kCopyItems];
-#pragma unroll
-        for (int it = 0; it < kCopyItems; ++it) {
-            const long long j = base + it * kThreads + threadIdx.x;
-            s[it] = j < n ? ws.dst[j] : -1;
-        }
-        float x[kCopyItems], y[kCopyItems], z[kCopyItems], vx[kCopyItems], vy[kCopyItems], vz[kCopyItems];
-        long long id[kCopyItems];
-        int lab[kCopyItems];
-#pragma unroll
-        for (int it = 0; it < kCopyItems; ++it) {
-            if (s[it] < 0) continue;
-            const int i = s[it];
-            x[it] = in.x[i];
-            y[it] = in.y[i];
-            vx[it] = in.vx[i];
-            vy[it] = in.vy[i];
-            if (dim == 3) {
-                z[it] = in.z[i];
-                vz[it] = in.vz[i];
-            }
-            id[it] = in.id[i];
-            lab[it] = in.label[i];
-        }
-#pragma unroll
-        for (int it = 0; it < kCopyItems; ++it) {
-            if (s[it] < 0) continue;
-            const long long o = base + it * kThreads + threadIdx.x;
-            out.x[o] = x[it];
-            out.y[o] = y[it];
-            out.vx[o] = vx[it];
-            out.vy[o] = vy[it];
-            if (dim == 3) {
-                out.z[o] = z[it];
-                out.vz[o] = vz[it];
-            }
-            out.id[o] = id[it];
-            out.label[o] = lab[it];
-            if (HasExtra)
-                for (int e = 0; e < in.n_extra; ++e) out.extra[e][o] = in.extra[e][s[it]];
-        }
     }
 }
 
@@ -305,22 +294,15 @@ cudaError_t launch_cll(const PartDev &in, const PartDev &out, const GridDev &g, 
         k_cll_scatter<<<grid, kThreads, 0, s>>>(ws, cell_start, perm);
         L->after(s, KID_CLL_SCATTER);
     }
-    {
-        static int grid = 0;
-        if (!grid) grid = occ_grid(k_cll_rank, kThreads);
-        L->before(s);
-        k_cll_rank<<<grid, kThreads, 0, s>>>(in, ws, cell_start, cell_end, perm, out.n);
-        L->after(s, KID_CLL_RANK);
-    }
     L->before(s);
     if (in.n_extra > 0) {
         static int grid = 0;
-        if (!grid) grid = occ_grid(k_cll_copy<true>, kThreads);
-        k_cll_copy<true><<<grid, kThreads, 0, s>>>(in, out, g.dim, ws);
+        if (!grid) grid = occ_grid(k_cll_gather<true>, kThreads);
+        k_cll_gather<true><<<grid, kThreads, 0, s>>>(in, out, g.dim, ws, cell_start, cell_end, perm);
     } else {
         static int grid = 0;
-        if (!grid) grid = occ_grid(k_cll_copy<false>, kThreads);
-        k_cll_copy<false><<<grid, kThreads, 0, s>>>(in, out, g.dim, ws);
+        if (!grid) grid = occ_grid(k_cll_gather<false>, kThreads);
+        k_cll_gather<false><<<grid, kThreads, 0, s>>>(in, out, g.dim, ws, cell_start, cell_end, perm);
     }
     L->after(s, KID_CLL_GATHER);
     return cudaGetLastError();

@@ -35,6 +35,13 @@ __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long lon
     return v;
 }
 
+__device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long *p)
+{
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
 // tile status word: [63:34] epoch (30 bits) | [33:32] flag (1 aggregate, 2 inclusive prefix) | [31:0] value
 __device__ __forceinline__ unsigned long long pack_status(unsigned epoch, unsigned flag, unsigned value)
 {
@@ -88,7 +95,7 @@ static __device__ unsigned tile_prefix(unsigned long long *status, long long til
         unsigned flag;
         if (t >= 0) {
             do {
-                s = ld_acquire(&status[t]);
+                s = ld_relaxed(&status[t]);   // polled relaxed; one acquire fence below
                 flag = ((unsigned)(s >> 34) == ep) ? (unsigned)((s >> 32) & 3u) : 0u;
             } while (flag == 0);
         } else {
@@ -102,6 +109,7 @@ static __device__ unsigned tile_prefix(unsigned long long *status, long long til
         if (pmask) break;
         base -= 32;
     }
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
     if (lane == 0) st_release(&status[tile], pack_status(epoch, 2, excl + aggregate));
     return excl;
 }

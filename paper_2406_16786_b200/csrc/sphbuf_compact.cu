@@ -157,12 +157,14 @@ __global__ void __launch_bounds__(kThreads) k_compact_move(PartDev p, int dim, W
                 asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(ws.rd + u), "r"(epoch) : "memory");
             // wait for the sub-tiles whose input overlaps [dst0, start)
             const long long vlo = (dst0 - ibeg) / kCmpTile;
+            // relaxed polling (no L1 invalidation per probe), one acquire fence after
             for (long long v = vlo + threadIdx.x; v < u; v += 32) {
                 unsigned f;
                 do {
-                    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(ws.rd + v) : "memory");
+                    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(ws.rd + v) : "memory");
                 } while (f != epoch);
             }
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");
             __syncwarp();
         }
         __syncthreads();
