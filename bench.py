@@ -150,7 +150,8 @@ def run_ours(args):
     tgen = time.time() - tgen
     cap = inputs.capacity_for(w, 0.05)
     max_new = max(65536, w.n // 200)
-    su = SlabUpdater(w, rank, world, cap, max_migrate=1 << 18, max_new=max_new, comm=Comm(rank, world), device=dev)
+    su = SlabUpdater(w, rank, world, cap, max_migrate=1 << 18, max_new=max_new, comm=Comm(rank, world), device=dev,
+                     deferred=(args.compaction == "deferred"))
     su.load(w.state, w.next_id)
     n0 = w.n
     del w.state
@@ -241,6 +242,8 @@ def run_ours(args):
                        "particles_per_gpu": n0, "ports": len(su.bu.ports), "candidates_per_step": cand,
                        "created_last": created, "deleted_last": deleted, "dim": dim,
                        "parallelism": f"x-slab dp{world}", "l2": "inputs (>=4.6 GB/GPU) larger than L2; no flush",
+                       "compaction": args.compaction, "advection": "fused into the cell-list key pass" if world == 1
+                       else "separate (before migration)",
                        "gen_s": round(tgen, 1)},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak if achieved else None, "traffic": traffic,
@@ -392,6 +395,9 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--compaction", default="inplace", choices=["inplace", "deferred"],
+                    help="sph_compact (in-place stable compaction each update) or sph_compact_deferred "
+                         "(removal fused into the next cell-list build)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

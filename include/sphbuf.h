@@ -181,6 +181,14 @@ sph_status sph_buffer_update(sph_ctx *ctx, sph_particles *p, const int32_t *cell
 sph_status sph_compact(sph_ctx *ctx, sph_particles *p, const int32_t *all_counts, int32_t nranks, int32_t rank,
                        int64_t *next_id_dev, int32_t *perm_or_null, void *stream);
 
+/* Compaction fused into the next cell-list build: assigns
+ * the new IDs exactly as sph_compact and appends the staged particles at
+ * [N, N + C) after the tombstones (p->n_dev <- N + C); the tombstones are
+ * removed by the next sph_cll_build, whose result is identical to that of
+ * sph_compact followed by sph_cll_build.  Saves one pass over the suffix. */
+sph_status sph_compact_deferred(sph_ctx *ctx, sph_particles *p, const int32_t *all_counts, int32_t nranks,
+                                int32_t rank, int64_t *next_id_dev, void *stream);
+
 /* Multi-GPU slab migration (§8(e)).  pack: particles whose cell x-index left
  * [cx_begin, cx_end) are copied into send_lo (cx < cx_begin) or send_hi
  * (cx >= cx_end) and tombstoned.  A buffer holds a 4-word header (word 0 =

@@ -198,14 +198,22 @@ __global__ void __launch_bounds__(kThreads) k_compact_move(PartDev p, int dim, W
 // Staged particles after the survivors with IDs from the count matrix (reading
 // R14, §8(e)): off(k, r) = next_id + sum_{k'<k} sum_r' C[r'][k'] + sum_{r'<r} C[r'][k];
 // identity perm below i_first; then N and next_id.
+// defer: the tombstones stay in place (the next sph_cll_build drops them) and the
+// staged particles go to [N, N + C); launched with one block, so N and next_id
+// can be read directly.
 __global__ void __launch_bounds__(kThreads) k_compact_append(PartDev p, int dim, int n_ports, int max_ports,
                                                              Workspace ws, const int *all_counts, int nranks,
-                                                             int rank, long long *next_id, int *perm)
+                                                             int rank, long long *next_id, int *perm, bool defer)
 {
     __shared__ long long s_off[SPH_MAX_PORTS];
     __shared__ long long s_beg[SPH_MAX_PORTS];
     __shared__ long long s_total;
     Counters *ctr = ws.ctr;
+    if (defer && threadIdx.x == 0) {
+        ctr->cmp_n = *p.n;
+        ctr->cmp_next_id = *next_id;
+    }
+    __syncthreads();
     const long long nid0 = ctr->cmp_next_id;
     if (threadIdx.x == 0) {
         long long acc = nid0, beg = 0;
@@ -225,7 +233,7 @@ __global__ void __launch_bounds__(kThreads) k_compact_append(PartDev p, int dim,
     }
     __syncthreads();
     const long long N = ctr->cmp_n;
-    const long long D = ctr->n_del;
+    const long long D = defer ? 0 : ctr->n_del;
     long long C = ctr->n_stage;
     if (C > ws.max_new) C = ws.max_new;
     const long long dst0 = N - D;
@@ -262,9 +270,17 @@ __global__ void __launch_bounds__(kThreads) k_compact_append(PartDev p, int dim,
 // ------------------------------------------------------------------ launcher
 
 cudaError_t launch_compact(const PartDev &p, const PortTable &pt, const Workspace &ws, const int *all_counts,
-                           int nranks, int rank, long long *next_id, int *perm, cudaStream_t s, Launch *L)
+                           int nranks, int rank, long long *next_id, int *perm, bool defer, cudaStream_t s,
+                           Launch *L)
 {
     const int dim = p.z ? 3 : 2;
+    if (defer) {
+        L->before(s);
+        k_compact_append<<<1, kThreads, 0, s>>>(p, dim, pt.n, pt.max_ports, ws, all_counts, nranks, rank, next_id,
+                                                nullptr, true);
+        L->after(s, KID_COMPACT_APPEND);
+        return cudaGetLastError();
+    }
     {
         static int grid = 0;
         if (!grid) grid = occ_grid(k_compact_count, kThreads);
@@ -285,7 +301,7 @@ cudaError_t launch_compact(const PartDev &p, const PortTable &pt, const Workspac
     L->after(s, KID_COMPACT);
     L->before(s);
     k_compact_append<<<sm_count_cached() * 4, kThreads, 0, s>>>(p, dim, pt.n, pt.max_ports, ws, all_counts, nranks,
-                                                                 rank, next_id, perm);
+                                                                 rank, next_id, perm, false);
     L->after(s, KID_COMPACT_APPEND);
     return cudaGetLastError();
 }

@@ -585,8 +585,8 @@ sph_status sph_buffer_update(sph_ctx *c, sph_particles *p, const int32_t *cell_s
     return e == cudaSuccess ? SPH_OK : cuda_fail(c, e, "buffer_update");
 }
 
-sph_status sph_compact(sph_ctx *c, sph_particles *p, const int32_t *all_counts, int32_t nranks, int32_t rank,
-                       int64_t *next_id_dev, int32_t *perm, void *stream)
+static sph_status compact(sph_ctx *c, sph_particles *p, const int32_t *all_counts, int32_t nranks, int32_t rank,
+                          int64_t *next_id_dev, int32_t *perm, bool defer, void *stream)
 {
     if (!c) return SPH_ERR_ARG;
     sph_status st = check_particles(c, p);
@@ -594,9 +594,21 @@ sph_status sph_compact(sph_ctx *c, sph_particles *p, const int32_t *all_counts, 
     if (!all_counts || !next_id_dev || nranks <= 0 || rank < 0 || rank >= nranks)
         return fail(c, SPH_ERR_ARG, "bad count matrix / rank");
     cudaError_t e = launch_compact(part_dev(p), c->pt, c->W, all_counts, nranks, rank,
-                                   reinterpret_cast<long long *>(next_id_dev), perm, static_cast<cudaStream_t>(stream),
-                                   &c->L);
+                                   reinterpret_cast<long long *>(next_id_dev), perm, defer,
+                                   static_cast<cudaStream_t>(stream), &c->L);
     return e == cudaSuccess ? SPH_OK : cuda_fail(c, e, "compact");
+}
+
+sph_status sph_compact(sph_ctx *c, sph_particles *p, const int32_t *all_counts, int32_t nranks, int32_t rank,
+                       int64_t *next_id_dev, int32_t *perm, void *stream)
+{
+    return compact(c, p, all_counts, nranks, rank, next_id_dev, perm, false, stream);
+}
+
+sph_status sph_compact_deferred(sph_ctx *c, sph_particles *p, const int32_t *all_counts, int32_t nranks,
+                                int32_t rank, int64_t *next_id_dev, void *stream)
+{
+    return compact(c, p, all_counts, nranks, rank, next_id_dev, nullptr, true, stream);
 }
 
 int32_t sph_migrate_record_floats(const sph_ctx *c) { return c ? 2 * c->grid.dim + c->n_extra + 3 : 0; }

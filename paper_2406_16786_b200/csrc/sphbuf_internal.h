@@ -143,7 +143,8 @@ cudaError_t launch_update(const PartDev &p, const GridDev &g, const PortTable &p
                           const int *cell_start, const int *cell_end, int *port_counts, cudaStream_t s,
                           Launch *L);
 cudaError_t launch_compact(const PartDev &p, const PortTable &pt, const Workspace &ws, const int *all_counts,
-                           int nranks, int rank, long long *next_id, int *perm, cudaStream_t s, Launch *L);
+                           int nranks, int rank, long long *next_id, int *perm, bool defer, cudaStream_t s,
+                           Launch *L);
 cudaError_t launch_migrate_pack(const PartDev &p, const GridDev &g, const Workspace &ws, float *lo, float *hi,
                                 long long max_migrate, int rec, cudaStream_t s, Launch *L);
 cudaError_t launch_migrate_unpack(const PartDev &p, const GridDev &g, const Workspace &ws, const float *buf,

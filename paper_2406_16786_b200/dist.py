@@ -69,8 +69,9 @@ class SlabUpdater:
     """One rank: BufferUpdater + migration buffers + count matrix."""
 
     def __init__(self, w, rank: int, world: int, capacity: int, max_migrate: int, max_new=None, comm=None,
-                 device="cuda"):
+                 device="cuda", deferred=False):
         self.rank, self.world = rank, world
+        self.deferred = deferred
         self.bu = sphbuf.BufferUpdater(w.grid, w.h, w.dp, w.ports, capacity, max_new=max_new,
                                        max_migrate=max_migrate, device=device)
         rec = sphbuf.sph_migrate_record_floats(self.bu.ctx)
@@ -105,9 +106,9 @@ class SlabUpdater:
 
     def phase_compact(self):
         if self.world > 1:
-            self.bu.compact(self.all_counts, self.world, self.rank)
+            self.bu.compact(self.all_counts, self.world, self.rank, deferred=self.deferred)
         else:
-            self.bu.compact()
+            self.bu.compact(deferred=self.deferred)
 
     def step(self, dt):
         self.phase_advect_pack(dt)

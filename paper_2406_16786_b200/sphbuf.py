@@ -55,7 +55,7 @@ EXPORTS = ["sph_ctx_create", "sph_ctx_destroy", "sph_last_error", "sph_workspace
            "sph_port_check", "sph_buffer_register", "sph_advect", "sph_cll_build", "sph_buffer_update",
            "sph_compact", "sph_migrate_record_floats", "sph_migrate_pack", "sph_migrate_unpack", "sph_status_sync",
            "sph_launch_count", "sph_port_cells", "sph_frame_from_axis", "sph_profile", "sph_profile_read",
-           "sph_kernel_name", "sph_advect_cll_build"]
+           "sph_kernel_name", "sph_advect_cll_build", "sph_compact_deferred"]
 NKERNELS = 14
 
 
@@ -86,6 +86,8 @@ def lib():
     L.sph_advect_cll_build.restype = C.c_int
     L.sph_buffer_update.argtypes = [vp, P(sph_particles), vp, vp, vp, vp]
     L.sph_compact.argtypes = [vp, P(sph_particles), vp, i32, i32, vp, vp, vp]
+    L.sph_compact_deferred.argtypes = [vp, P(sph_particles), vp, i32, i32, vp, vp]
+    L.sph_compact_deferred.restype = C.c_int
     L.sph_migrate_record_floats.argtypes = [vp]
     L.sph_migrate_record_floats.restype = i32
     L.sph_migrate_pack.argtypes = [vp, P(sph_particles), vp, vp, vp]
@@ -210,6 +212,11 @@ def sph_buffer_update(ctx, parts, cell_start, cell_end, port_counts, stream=None
 def sph_compact(ctx, parts, all_counts, nranks, rank, next_id, perm=None, stream=None):
     _check(lib().sph_compact(ctx.h, C.byref(parts.abi), _ptr(all_counts), int(nranks), int(rank), _ptr(next_id),
                              _ptr(perm), _stream(stream)), ctx.h)
+
+
+def sph_compact_deferred(ctx, parts, all_counts, nranks, rank, next_id, stream=None):
+    _check(lib().sph_compact_deferred(ctx.h, C.byref(parts.abi), _ptr(all_counts), int(nranks), int(rank),
+                                      _ptr(next_id), _stream(stream)), ctx.h)
 
 
 def sph_migrate_record_floats(ctx) -> int:
@@ -379,19 +386,25 @@ class BufferUpdater:
     def update(self, stream=None):
         sph_buffer_update(self.ctx, self.A, self.cell_start, self.cell_end, self.port_counts, stream)
 
-    def compact(self, all_counts=None, nranks=1, rank=0, perm=None, stream=None):
+    def compact(self, all_counts=None, nranks=1, rank=0, perm=None, stream=None, deferred=False):
+        """IDs + compaction (sph_compact), or IDs + append with the removal left to
+        the next cell-list build (sph_compact_deferred)."""
         ac = self.port_counts if all_counts is None else all_counts
-        sph_compact(self.ctx, self.A, ac, nranks, rank, self.next_id, perm, stream)
+        if deferred:
+            sph_compact_deferred(self.ctx, self.A, ac, nranks, rank, self.next_id, stream)
+        else:
+            sph_compact(self.ctx, self.A, ac, nranks, rank, self.next_id, perm, stream)
 
-    def step(self, dt, stream=None, fused=True):
+    def step(self, dt, stream=None, fused=True, deferred=False):
         """advect -> cell-list build -> buffer update -> compaction.  fused: the
-        advection runs inside the build's key pass (sph_advect_cll_build)."""
+        advection runs inside the build's key pass (sph_advect_cll_build);
+        deferred: the compaction's removal runs inside the next build."""
         if dt is not None and not fused:
             self.advect(dt, stream)
             dt = None
         self.cll_build(stream=stream, dt=dt)
         self.update(stream)
-        self.compact(stream=stream)
+        self.compact(stream=stream, deferred=deferred)
 
     # --- inspection (synchronising)
     def stats(self, check=True) -> dict:

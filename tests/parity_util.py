@@ -44,7 +44,10 @@ def make_updater(w, capacity=None, max_new=None, n_extra=0):
 
 
 def lockstep(w, n_updates, check_cll=True, state=None, next_id=None, capacity=None, max_new=None,
-             check_every=1, fused=False):
+             check_every=1, fused=False, deferred=False):
+    """deferred: the GPU runs sph_compact_deferred; the tombstones then vanish in the
+    next cell-list build, so states are compared in cell-list order (every checked
+    step and once more after the last update) instead of post-compaction order."""
     """Run n_updates on GPU and oracle from the same state; compare registration,
     cell lists, counts and the full post-compaction state bit-exactly.
     Returns totals of (created, deleted) and the GPU updater."""
@@ -81,14 +84,23 @@ def lockstep(w, n_updates, check_cll=True, state=None, next_id=None, capacity=No
             pre = {c: v[res.order] for c, v in st.items() if c != "extra"}
             assert_state_equal(bu.state(), pre, f"cell-list order step {step}")
         bu.update()
-        bu.compact()
+        bu.compact(deferred=deferred)
         if cmp_now:
             s = bu.stats()
             assert (gpu_counts_to_oracle(bu.port_counts, K) == res.port_counts).all(), (
                 step, gpu_counts_to_oracle(bu.port_counts, K), res.port_counts)
             assert s["candidates"] >= 0
-            assert_state_equal(bu.state(), new, f"post-compaction step {step}")
+            if deferred:
+                C_, D_ = int(res.port_counts[:K].sum()), int(res.port_counts[K:].sum())
+                assert s["n"] == len(new["x"]) + D_, "deferred: N counts the tombstones"
+            else:
+                assert_state_equal(bu.state(), new, f"post-compaction step {step}")
             assert int(bu.next_id.item()) == nid
         tot += [res.port_counts[:K].sum(), res.port_counts[K:].sum()]
         st = new
+    if deferred:
+        # one more build removes the tombstones: compare with the oracle's final state in cell-list order
+        bu.cll_build()
+        fin = oracle.update(w.grid, [], st)
+        assert_state_equal(bu.state(), {c: v[fin.order] for c, v in st.items() if c != "extra"}, "deferred final")
     return tot, bu

@@ -48,6 +48,19 @@ def test_C2_fused_advect_cll_build():
     assert tot[0] > 0 and tot[1] > 0
 
 
+@pytest.mark.parametrize("name", ["C1e", "C2"])
+def test_deferred_compaction(name):
+    w = inputs.make(name)
+    tot, bu = lockstep(w, 20 if name == "C2" else 5, check_every=1, fused=True, deferred=True)
+    assert tot[0] > 0 and tot[1] > 0
+
+
+def test_C4_junction_deferred():
+    w = inputs.c4(scale=0.5, nports=8, n_updates=8)
+    tot, bu = lockstep(w, 8, check_every=2, fused=True, deferred=True)
+    assert tot[0] > 0 and tot[1] > 0
+
+
 def test_C3_duct_scaled_full_run():
     w = inputs.c3(scale=0.25, n_updates=100)
     tot, bu = lockstep(w, 100, check_every=10)
