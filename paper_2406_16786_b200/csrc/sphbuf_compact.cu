@@ -155,16 +155,21 @@ __global__ void __launch_bounds__(kThreads) k_compact_move(PartDev p, int dim, W
         if (threadIdx.x < 32) {
             if (threadIdx.x == 0)
                 asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(ws.rd + u), "r"(epoch) : "memory");
-            // wait for the sub-tiles whose input overlaps [dst0, start)
-            const long long vlo = (dst0 - ibeg) / kCmpTile;
-            // relaxed polling (no L1 invalidation per probe), one acquire fence after
-            for (long long v = vlo + threadIdx.x; v < u; v += 32) {
-                unsigned f;
-                do {
-                    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(ws.rd + v) : "memory");
-                } while (f != epoch);
+            // wait only for the earlier sub-tiles whose input overlaps the output range
+            // [dst0, dst0 + alive) (when the shift exceeds a sub-tile these are a few
+            // tiles back, claimed long ago); relaxed polling, one acquire fence after
+            if (total > 0 && dst0 < start) {
+                const long long vlo = (dst0 - ibeg) / kCmpTile;
+                long long vhi = (dst0 + total - 1 - ibeg) / kCmpTile;
+                if (vhi > u - 1) vhi = u - 1;
+                for (long long v = vlo + threadIdx.x; v <= vhi; v += 32) {
+                    unsigned f;
+                    do {
+                        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(ws.rd + v) : "memory");
+                    } while (f != epoch);
+                }
+                asm volatile("fence.acq_rel.gpu;" ::: "memory");
             }
-            asm volatile("fence.acq_rel.gpu;" ::: "memory");
             __syncwarp();
         }
         __syncthreads();
