@@ -206,16 +206,7 @@ __global__ void __launch_bounds__(kThreads) k_cll_gather(PartDev in, PartDev out
 {
     __shared__ long long s_id[kGatherTile];
     const long long n = *out.n;
-    const long long tstride = (long long)gridDim.x * kGatherTile;
-    // software pipeline: the (source, cell) pairs of the next tile are loaded while
-    // the current tile's columns are gathered, so the dependent loads never wait on them
-    int2 nxt[kGatherItems];
-#pragma unroll
-    for (int it = 0; it < kGatherItems; ++it) {
-        const long long j = (long long)blockIdx.x * kGatherTile + it * kThreads + threadIdx.x;
-        nxt[it] = j < n ? ws.pair[j] : make_int2(-1, -1);
-    }
-    for (long long j0 = (long long)blockIdx.x * kGatherTile; j0 < n; j0 += tstride) {
+    for (long long j0 = (long long)blockIdx.x * kGatherTile; j0 < n; j0 += (long long)gridDim.x * kGatherTile) {
         int src[kGatherItems], cb[kGatherItems], ce[kGatherItems], lab[kGatherItems];
         float x[kGatherItems], y[kGatherItems], z[kGatherItems], vx[kGatherItems], vy[kGatherItems],
             vz[kGatherItems];
@@ -223,9 +214,8 @@ __global__ void __launch_bounds__(kThreads) k_cll_gather(PartDev in, PartDev out
         int2 pr[kGatherItems];
 #pragma unroll
         for (int it = 0; it < kGatherItems; ++it) {
-            pr[it] = nxt[it];
-            const long long j = j0 + tstride + it * kThreads + threadIdx.x;
-            nxt[it] = j < n ? ws.pair[j] : make_int2(-1, -1);
+            const long long j = j0 + it * kThreads + threadIdx.x;
+            pr[it] = j < n ? ws.pair[j] : make_int2(-1, -1);
         }
 #pragma unroll
         for (int it = 0; it < kGatherItems; ++it) {
