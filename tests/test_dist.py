@@ -1,0 +1,206 @@
+"""Multi-rank x-slab decomposition.
+
+* CPU, world size 2, gloo: the product's ``dist.Comm`` (neighbour exchange of
+  fixed-size migration buffers, count allgather) drives a per-rank oracle
+  update; the union of the ranks' states must equal the single-process oracle
+  (same IDs, same columns) after every update.
+* GPU (one device): ``dist.LoopbackGroup`` runs P slabs of the CUDA path in one
+  process (device copies stand in for NCCL); the union must equal the
+  single-process oracle bit-exactly.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+from paper_2406_16786_b200 import inputs
+from paper_2406_16786_b200.dist import Comm, id_offsets
+
+COLS = ("x", "y", "z", "vx", "vy", "vz")
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def cell_x(grid, x):
+    """pinned fp32 cell x-index (numpy float32 ops round per operation)"""
+    t = (x.astype(np.float32) - np.float32(grid.lo[0])) * np.float32(1.0 / grid.cs)
+    return np.clip(np.floor(t), 0, grid.ncell[0] - 1).astype(np.int64)
+
+
+def split(st, grid, cuts):
+    cx = cell_x(grid, st["x"])
+    return [{k: v[(cx >= cuts[r]) & (cx < cuts[r + 1])] for k, v in st.items()} for r in range(len(cuts) - 1)]
+
+
+REC = 2 * 3 + 3   # record words per particle (3-D, no extra): pos, vel, id lo/hi, label
+
+
+def pack(st, sel, max_m):
+    buf = np.zeros(4 + max_m * REC, np.float32)
+    idx = np.nonzero(sel)[0]
+    assert len(idx) <= max_m
+    buf[:4].view(np.int32)[0] = len(idx)
+    rec = buf[4:4 + len(idx) * REC].reshape(-1, REC)
+    for j, c in enumerate(COLS):
+        rec[:, j] = st[c][idx]
+    ids = st["id"][idx]
+    rec[:, 6] = (ids & 0xffffffff).astype(np.uint32).view(np.float32)
+    rec[:, 7] = (ids >> 32).astype(np.int32).view(np.float32)
+    rec[:, 8] = st["label"][idx].view(np.float32)
+    return buf
+
+
+def unpack(buf):
+    n = int(buf[:4].view(np.int32)[0])
+    rec = buf[4:4 + n * REC].reshape(-1, REC)
+    d = {c: rec[:, j].copy() for j, c in enumerate(COLS)}
+    lo = rec[:, 6].view(np.uint32).astype(np.int64)
+    hi = rec[:, 7].view(np.int32).astype(np.int64)
+    d["id"] = (hi << 32) | lo
+    d["label"] = rec[:, 8].view(np.int32).copy()
+    return d
+
+
+def cat(a, b):
+    return {k: np.concatenate([a[k], b[k]]) for k in a}
+
+
+def by_id(st):
+    o = np.argsort(st["id"], kind="stable")
+    return {k: v[o] for k, v in st.items()}
+
+
+def _world():
+    w = inputs.c4(scale=0.25, nports=4, n_updates=10)
+    st = oracle.to_numpy_state(w.state)
+    for k, p in enumerate(w.ports):
+        oracle.register(st, w.grid, p, k)
+    ncx = w.grid.ncell[0]
+    cuts = [0, ncx // 2 - 3, ncx]
+    return w, st, cuts
+
+
+def _rank_main(rank, world, port, steps, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    comm = Comm(rank, world)
+    w, st_all, cuts = _world()
+    K = len(w.ports)
+    g = w.grid.slab(cuts[rank], cuts[rank + 1])
+    st = split(st_all, w.grid, cuts)[rank]
+    nid = w.next_id
+    max_m = 20000
+    out = []
+    migrated = [0]
+    for _ in range(steps):
+        oracle.advect(st, 3, w.dt)
+        cx = cell_x(w.grid, st["x"])
+        lo_sel, hi_sel = cx < cuts[rank], cx >= cuts[rank + 1]
+        send_lo, send_hi = torch.from_numpy(pack(st, lo_sel, max_m)), torch.from_numpy(pack(st, hi_sel, max_m))
+        recv_lo, recv_hi = torch.zeros_like(send_lo), torch.zeros_like(send_hi)
+        comm.exchange(send_lo, send_hi, recv_lo, recv_hi)
+        keep = ~(lo_sel | hi_sel)
+        migrated[0] += int(recv_lo[:4].view(torch.int32)[0]) + int(recv_hi[:4].view(torch.int32)[0])
+        st = {k: v[keep] for k, v in st.items()}
+        if rank > 0:
+            st = cat(st, unpack(recv_lo.numpy()))
+        if rank < world - 1:
+            st = cat(st, unpack(recv_hi.numpy()))
+        res = oracle.update(g, w.ports, st)
+        counts = torch.from_numpy(res.port_counts.astype(np.int32))
+        allc = torch.zeros(world, 2 * K, dtype=torch.int32)
+        comm.allgather_counts(counts, allc)
+        ac = allc.numpy()
+        # the host ID rule agrees with the oracle's compaction
+        offs = id_offsets(ac, K, K, rank, nid)
+        st, perm, nid2 = oracle.compact(res, 3, K, ac, rank, nid)
+        new_ids = st["id"][st["id"] >= nid]
+        for k in range(K):
+            c = int(ac[rank][k])
+            if c:
+                assert new_ids.min() <= offs[k] <= new_ids.max()
+        nid = nid2
+        out.append({k: v.copy() for k, v in st.items()})
+    q.put((rank, out, nid, migrated[0]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gloo_two_ranks_match_single_process():
+    steps = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=_rank_main, args=(r, 2, port, steps, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = dict()
+    received = 0
+    for _ in range(2):
+        r, out, nid, mig = q.get(timeout=600)
+        got[r] = (out, nid)
+        received += mig
+    assert received > 0, "no particle crossed the slab face: the exchange was not exercised"
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    # single process over the whole domain
+    w, st, cuts = _world()
+    nid = w.next_id
+    moved = 0
+    for s in range(steps):
+        st, res, perm, nid = oracle.step(st, w.grid, w.ports, nid, w.dt)
+        union = by_id(cat(got[0][0][s], got[1][0][s]))
+        ref = by_id(st)
+        for k in ref:
+            np.testing.assert_array_equal(union[k], ref[k], err_msg=f"step {s} column {k}")
+        moved += 1
+    assert got[0][1] == got[1][1] == nid
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("P", [2, 3])
+def test_loopback_slabs_match_oracle(P):
+    from paper_2406_16786_b200.dist import LoopbackGroup, SlabUpdater
+    w = inputs.c4(scale=0.5, nports=8, n_updates=6)
+    st = oracle.to_numpy_state(w.state)
+    ncx = w.grid.ncell[0]
+    cuts = [int(round(i * ncx / P)) for i in range(P + 1)]
+    parts = split(st, w.grid, cuts)
+    slabs = []
+    for r in range(P):
+        ws = inputs.Workload(w.name, 3, w.dp, w.h, w.grid.slab(cuts[r], cuts[r + 1]), w.ports,
+                             {k: torch.from_numpy(v) for k, v in parts[r].items()}, w.dt, w.n_updates, w.next_id)
+        su = SlabUpdater(ws, r, P, inputs.capacity_for(ws, 0.2), max_migrate=1 << 16, comm=None)
+        su.load(ws.state, w.next_id)
+        slabs.append(su)
+    grp = LoopbackGroup(slabs)
+    for k, p in enumerate(w.ports):
+        oracle.register(st, w.grid, p, k)
+    nid = w.next_id
+    for s in range(6):
+        st, res, perm, nid = oracle.step(st, w.grid, w.ports, nid, w.dt)
+        grp.step(w.dt)
+        union = None
+        for su in slabs:
+            g = su.bu.state()
+            g = {k: v.numpy() for k, v in g.items()}
+            union = g if union is None else cat(union, g)
+        union, ref = by_id(union), by_id(st)
+        for k in ref:
+            np.testing.assert_array_equal(union[k], ref[k], err_msg=f"P={P} step {s} column {k}")
+        for su in slabs:
+            assert int(su.bu.next_id.item()) == nid
+        assert sum(su.bu.stats()["migrated_out"] for su in slabs) >= 0
+    assert sum(su.bu.stats()["migrated_out"] for su in slabs) > 0

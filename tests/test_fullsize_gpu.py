@@ -1,0 +1,44 @@
+"""Parity at BASELINE.json's full sizes, in the launch configuration bench.py
+times (advection fused into the cell-list key pass; compaction deferred into the
+next build), against the oracle bit-exactly.  C1/C1e/C2 are full size in
+test_parity_gpu.py already.  Inputs are generated on the GPU (same generator)
+and copied to the host for the oracle."""
+import pytest
+import torch
+
+from paper_2406_16786_b200 import inputs
+
+from parity_util import lockstep
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+
+def test_C3_full_duct_100_updates_bench_config():
+    w = inputs.c3(device="cuda")
+    assert w.n == 2_560_000
+    tot, bu = lockstep(w, 100, check_every=10, fused=True, deferred=True)
+    assert tot[0] > 0 and tot[1] > 0
+
+
+def test_C3_full_duct_inplace_compaction():
+    w = inputs.c3(device="cuda", n_updates=20)
+    tot, bu = lockstep(w, 20, check_every=5, fused=False, deferred=False)
+    assert tot[0] > 0 and tot[1] > 0
+
+
+def test_C4_full_junction_two_updates():
+    w = inputs.c4(device="cuda", n_updates=100)
+    assert w.n > 60_000_000
+    tot, bu = lockstep(w, 2, check_every=1, fused=True, deferred=True)
+    assert tot[0] > 0 and tot[1] > 0
+    del bu
+    torch.cuda.empty_cache()
+
+
+def test_C5_full_slab_one_update():
+    w = inputs.c5(device="cuda", slab=0, nslabs=1)
+    assert w.n > 120_000_000
+    tot, bu = lockstep(w, 1, check_every=1, fused=True, deferred=True)
+    assert tot[0] > 0 and tot[1] > 0
+    del bu
+    torch.cuda.empty_cache()
