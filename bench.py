@@ -164,39 +164,55 @@ def run_ours(args):
             dist.barrier()
         torch.cuda.synchronize()
 
+    def timed(steps, sample_clocks):
+        """Exactly `steps` steps between barrier + synchronize on both sides, CUDA
+        events on the launching stream, max over ranks; per-kernel event times."""
+        s0 = bu.stats()
+        sphbuf.sph_profile(bu.ctx, True)
+        l0 = bu.launches()
+        clocks = ClockSampler(local) if sample_clocks else None
+        if clocks:
+            clocks.start()
+            time.sleep(0.3)
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            su.step(w.dt)
+        e1.record(stream)
+        barrier()
+        clk = clocks.stop() if clocks else None
+        ms = e0.elapsed_time(e1)
+        prof = sphbuf.sph_profile_read(bu.ctx)
+        sphbuf.sph_profile(bu.ctx, False)
+        s1 = bu.stats()
+        checked = s1["checked_total"] - s0["checked_total"]
+        t = torch.tensor([ms, float(checked)], dtype=torch.float64, device=dev)
+        if world > 1:
+            tmax = t.clone()
+            dist.all_reduce(tmax[:1], op=dist.ReduceOp.MAX)
+            tsum = t.clone()
+            dist.all_reduce(tsum[1:], op=dist.ReduceOp.SUM)
+            ms, checked_all = float(tmax[0]), float(tsum[1])
+        else:
+            checked_all = float(checked)
+        return ms, checked_all, checked, bu.launches() - l0, prof, clk, s1
+
     for _ in range(args.warmup):
         su.step(w.dt)
-    s = bu.stats()
-    checked0 = s["checked_total"]
-    sphbuf.sph_profile(bu.ctx, True)
-    launches0 = bu.launches()
-    clocks = ClockSampler(local)
-    clocks.start()
-    time.sleep(0.3)
-    barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.steps):
-        su.step(w.dt)
-    e1.record(stream)
-    barrier()
-    clk = clocks.stop()
-    ms = e0.elapsed_time(e1)
-    launches = bu.launches() - launches0
-    prof = sphbuf.sph_profile_read(bu.ctx)
-    sphbuf.sph_profile(bu.ctx, False)
-    s = bu.stats()
-    checked = s["checked_total"] - checked0
-    t = torch.tensor([ms, float(checked)], dtype=torch.float64, device=dev)
-    if world > 1:
-        tmax = t.clone()
-        dist.all_reduce(tmax[:1], op=dist.ReduceOp.MAX)
-        tsum = t.clone()
-        dist.all_reduce(tsum[1:], op=dist.ReduceOp.SUM)
-        ms_max, checked_all = float(tmax[0]), float(tsum[1])
-    else:
-        ms_max, checked_all = ms, float(checked)
+    ms_max, checked_all, checked, launches, prof, clk, s = timed(args.steps, True)
     value = checked_all / (ms_max / 1e3)
+    # the other compaction mode, same state and harness (reported beside the headline)
+    su.deferred = not su.deferred
+    for _ in range(2):
+        su.step(w.dt)
+    ams, achk, _, _, aprof, _, _ = timed(args.steps, False)
+    su.deferred = not su.deferred
+    alt = {"compaction": "inplace" if args.compaction == "deferred" else "deferred",
+           "ms_per_step": ams / args.steps, "value": achk / (ams / 1e3),
+           "kernels_ms": {k: round(v[0] / v[1], 4) for k, v in aprof.items() if v[1] > 0}}
+    for _ in range(2):
+        su.step(w.dt)
 
     # roofline of the dominant kernel (live CUDA-event times of the timed region)
     dim = bu.dim
@@ -222,6 +238,21 @@ def run_ours(args):
     step_ms = ms_max / args.steps
     kernels = {k: {"ms_per_launch": round(v[0] / v[1], 4), "share": round(v[0] / sum(x[0] for x in per_kernel.values()), 4)}
                for k, v in per_kernel.items()}
+    # SURVEY §8(d) phase budgets: update+compaction bytes vs their time, and the cell-list
+    # build at 2S + 32 B per particle (plain counting sort), each against the HBM peak
+    S = 8 * dim + 12
+    kms = {k: v[0] / v[1] for k, v in per_kernel.items()}
+    t_upd = kms.get("upd_prologue", 0) + kms.get("upd_main", 0)
+    t_cmp = kms.get("compact_count", 0) + kms.get("compact", 0) + kms.get("compact_append", 0)
+    t_cll = sum(kms.get(k, 0) for k in ("cll_key", "cell_scan", "cll_scatter", "cll_gather", "advect"))
+    b_upd = cand * (4 * dim + 4) + created * (2 * S + 4 * dim)
+    b_cmp = (2 * S * moved - S * deleted + S * created) if args.compaction == "inplace" else S * created
+    b_cll = n * (2 * S + 32)
+    phases = {"update_compact_ms": t_upd + t_cmp, "update_compact_alg_bytes": b_upd + b_cmp,
+              "update_compact_frac": (b_upd + b_cmp) / ((t_upd + t_cmp) / 1e3) / 1e9 / peak if t_upd + t_cmp else None,
+              "cll_ms": t_cll, "cll_alg_bytes": b_cll,
+              "cll_frac": b_cll / (t_cll / 1e3) / 1e9 / peak if t_cll else None,
+              "note": "update+compact is latency-bound at C5 size (~12 MB of candidate work); see DESIGN.md §6"}
 
     # e2e: same metric through the public API with host-resident particles
     e2e = None
@@ -249,6 +280,8 @@ def run_ours(args):
                          "frac": achieved / peak if achieved else None, "traffic": traffic,
                          "peak_source": peak_src, "alg_bytes_per_launch": bytes_dom, "ms_per_launch": dom_ms},
             "kernels": kernels,
+            "phases": phases,
+            "other_compaction_mode": alt,
             "gpu_launches": launches,
             "clocks": clk,
             "e2e": e2e,
@@ -395,7 +428,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--compaction", default="inplace", choices=["inplace", "deferred"],
+    ap.add_argument("--compaction", default="deferred", choices=["inplace", "deferred"],
                     help="sph_compact (in-place stable compaction each update) or sph_compact_deferred "
                          "(removal fused into the next cell-list build)")
     args = ap.parse_args()
