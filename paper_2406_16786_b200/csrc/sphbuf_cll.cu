@@ -200,25 +200,25 @@ __global__ void __launch_bounds__(kThreads) k_cll_scatter(Workspace ws, const in
 // global memory), and the store into the sorted position.  Loads are nearly
 // sequential (only particles that changed cell come from far away); stores stay
 // inside the cell.
-template <bool HasExtra>
-__global__ void __launch_bounds__(kThreads) k_cll_gather(PartDev in, PartDev out, int dim, Workspace ws,
+template <bool HasExtra, int ITEMS, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) k_cll_gather(PartDev in, PartDev out, int dim, Workspace ws,
                                                          const int *cell_start, const int *cell_end, int *perm)
 {
-    __shared__ long long s_id[kGatherTile];
+    __shared__ long long s_id[(kThreads * ITEMS)];
     const long long n = *out.n;
-    for (long long j0 = (long long)blockIdx.x * kGatherTile; j0 < n; j0 += (long long)gridDim.x * kGatherTile) {
-        int src[kGatherItems], cb[kGatherItems], ce[kGatherItems], lab[kGatherItems];
-        float x[kGatherItems], y[kGatherItems], z[kGatherItems], vx[kGatherItems], vy[kGatherItems],
-            vz[kGatherItems];
-        long long id[kGatherItems];
-        int2 pr[kGatherItems];
+    for (long long j0 = (long long)blockIdx.x * (kThreads * ITEMS); j0 < n; j0 += (long long)gridDim.x * (kThreads * ITEMS)) {
+        int src[ITEMS], cb[ITEMS], ce[ITEMS], lab[ITEMS];
+        float x[ITEMS], y[ITEMS], z[ITEMS], vx[ITEMS], vy[ITEMS],
+            vz[ITEMS];
+        long long id[ITEMS];
+        int2 pr[ITEMS];
 #pragma unroll
-        for (int it = 0; it < kGatherItems; ++it) {
+        for (int it = 0; it < ITEMS; ++it) {
             const long long j = j0 + it * kThreads + threadIdx.x;
             pr[it] = j < n ? ws.pair[j] : make_int2(-1, -1);
         }
 #pragma unroll
-        for (int it = 0; it < kGatherItems; ++it) {
+        for (int it = 0; it < ITEMS; ++it) {
             src[it] = pr[it].x;
             if (src[it] < 0) continue;
             const int s = src[it];
@@ -238,11 +238,11 @@ __global__ void __launch_bounds__(kThreads) k_cll_gather(PartDev in, PartDev out
         }
         __syncthreads();
 #pragma unroll
-        for (int it = 0; it < kGatherItems; ++it) {
+        for (int it = 0; it < ITEMS; ++it) {
             if (src[it] < 0) continue;
             int r = 0;
             const long long lo = cb[it] > j0 ? cb[it] : j0;
-            const long long hi = ce[it] < j0 + kGatherTile ? ce[it] : j0 + kGatherTile;
+            const long long hi = ce[it] < j0 + (kThreads * ITEMS) ? ce[it] : j0 + (kThreads * ITEMS);
             for (long long q = lo; q < hi; ++q) r += (s_id[q - j0] < id[it]);
             for (long long q = cb[it]; q < lo; ++q) r += (in.id[ws.pair[q].x] < id[it]);
             for (long long q = hi; q < ce[it]; ++q) r += (in.id[ws.pair[q].x] < id[it]);
@@ -295,14 +295,16 @@ cudaError_t launch_cll(const PartDev &in, const PartDev &out, const GridDev &g, 
         L->after(s, KID_CLL_SCATTER);
     }
     L->before(s);
+    // 3 slots per thread at <= 64 registers (4 blocks/SM): measured best on C5
+    // among 1-4 slots x 1-8 min blocks (profiles/r1_summary.md)
     if (in.n_extra > 0) {
         static int grid = 0;
-        if (!grid) grid = occ_grid(k_cll_gather<true>, kThreads);
-        k_cll_gather<true><<<grid, kThreads, 0, s>>>(in, out, g.dim, ws, cell_start, cell_end, perm);
+        if (!grid) grid = occ_grid(k_cll_gather<true, 3, 4>, kThreads);
+        k_cll_gather<true, 3, 4><<<grid, kThreads, 0, s>>>(in, out, g.dim, ws, cell_start, cell_end, perm);
     } else {
         static int grid = 0;
-        if (!grid) grid = occ_grid(k_cll_gather<false>, kThreads);
-        k_cll_gather<false><<<grid, kThreads, 0, s>>>(in, out, g.dim, ws, cell_start, cell_end, perm);
+        if (!grid) grid = occ_grid(k_cll_gather<false, 3, 4>, kThreads);
+        k_cll_gather<false, 3, 4><<<grid, kThreads, 0, s>>>(in, out, g.dim, ws, cell_start, cell_end, perm);
     }
     L->after(s, KID_CLL_GATHER);
     return cudaGetLastError();
