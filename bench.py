@@ -262,6 +262,12 @@ def run_ours(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline(args, dev)
+    n_ports = len(su.bu.ports)
+    sweep = None
+    if rank == 0 and world == 1 and not args.no_sweep:
+        del su, bu
+        torch.cuda.empty_cache()
+        sweep = sweep_configs(dev)
     if rank == 0:
         line = {
             "metric": "buffer-update particles checked/sec & us/step; % of B200 HBM peak; 1/2/4/8 GPU",
@@ -270,7 +276,7 @@ def run_ours(args):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded lattice + jitter, BASELINE config shapes)",
             "config": {"workload": f"{args.config}" + (f" scale {args.scale}" if args.scale != 1 else ""),
-                       "particles_per_gpu": n0, "ports": len(su.bu.ports), "candidates_per_step": cand,
+                       "particles_per_gpu": n0, "ports": n_ports, "candidates_per_step": cand,
                        "created_last": created, "deleted_last": deleted, "dim": dim,
                        "parallelism": f"x-slab dp{world}", "l2": "inputs (>=4.6 GB/GPU) larger than L2; no flush",
                        "compaction": args.compaction, "advection": "fused into the cell-list key pass" if world == 1
@@ -286,6 +292,7 @@ def run_ours(args):
             "clocks": clk,
             "e2e": e2e,
             "cpu_baseline": cpu,
+            "configs_us_per_update": sweep,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -350,6 +357,50 @@ def run_e2e(su, w, args, dev, world):
 
 
 # ------------------------------------------------------------------ CPU oracle (reference arm / cpu_baseline)
+
+def sweep_configs(dev, names=("C1", "C1e", "C2", "C3", "C4"), replays=50):
+    """µs per buffer update of each BASELINE config on one GPU (the
+    small configs are latency-bound, so they replay a CUDA graph of two captured
+    updates; the stream-launched time is reported beside it)."""
+    out = {}
+    for name in names:
+        w = make_workload(name, 0, 1, dev)
+        bu = sphbuf.BufferUpdater(w.grid, w.h, w.dp, w.ports, inputs.capacity_for(w, 0.3), device=dev)
+        bu.load(w.state, w.next_id)
+        bu.register_ports()
+        n0 = w.n
+        del w
+        stream = torch.cuda.current_stream()
+        g = bu.capture(dt_of(name))
+        for _ in range(3):
+            g.replay()
+        c0 = bu.stats()["checked_total"]
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(replays):
+            g.replay()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        us_graph = e0.elapsed_time(e1) * 1e3 / (2 * replays)
+        cand = (bu.stats()["checked_total"] - c0) / (2 * replays)
+        e0.record(stream)
+        for _ in range(replays):
+            bu.step(dt_of(name), deferred=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        us_stream = e0.elapsed_time(e1) * 1e3 / replays
+        out[name] = {"particles": n0, "us_per_update_graph": round(us_graph, 2),
+                     "us_per_update_stream": round(us_stream, 2), "candidates_per_update": round(cand, 1),
+                     "particles_checked_per_s": cand / (us_graph * 1e-6) if us_graph else None}
+        del bu, g
+        torch.cuda.empty_cache()
+    return out
+
+
+def dt_of(name):
+    return {"C1": 0.002, "C1e": 0.0095, "C2": 0.0005, "C3": 0.0002, "C4": 0.0005, "C5": 0.0005}[name]
+
 
 def oracle_sample(args, dev):
     """Bounded sample of the workload for the oracle: the same config at 1/8 of the
@@ -428,6 +479,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the per-config us/update sweep (C1-C4)")
     ap.add_argument("--compaction", default="deferred", choices=["inplace", "deferred"],
                     help="sph_compact (in-place stable compaction each update) or sph_compact_deferred "
                          "(removal fused into the next cell-list build)")

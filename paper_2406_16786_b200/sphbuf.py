@@ -415,3 +415,19 @@ class BufferUpdater:
 
     def launches(self) -> int:
         return sph_launch_count(self.ctx)
+
+    def capture(self, dt, deferred=True):
+        """Capture two updates (A -> B -> A, so replays are composable) into one CUDA
+        graph.  Every count the kernels need is device-resident, so a replay needs no
+        host work: the launch-bound small configurations run at kernel speed."""
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):          # warm-up: occupancy queries, lazy init
+            self.step(dt, deferred=deferred)
+            self.step(dt, deferred=deferred)
+        torch.cuda.current_stream().wait_stream(side)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.step(dt, deferred=deferred)
+            self.step(dt, deferred=deferred)
+        return g

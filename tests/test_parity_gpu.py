@@ -55,6 +55,27 @@ def test_deferred_compaction(name):
     assert tot[0] > 0 and tot[1] > 0
 
 
+def test_cuda_graph_replay_matches_oracle():
+    """Two captured updates replayed 5 times (+2 warm-up updates) = 12 oracle updates."""
+    w = inputs.make("C2")
+    bu = make_updater(w)
+    bu.load(w.state, w.next_id)
+    bu.register_ports()
+    g = bu.capture(w.dt)
+    for _ in range(5):
+        g.replay()
+    bu.cll_build()           # drops the last deferred tombstones
+    st = oracle.to_numpy_state(w.state)
+    for k, p in enumerate(w.ports):
+        oracle.register(st, w.grid, p, k)
+    nid = w.next_id
+    for _ in range(12):
+        st, res, perm, nid = oracle.step(st, w.grid, w.ports, nid, w.dt)
+    fin = oracle.update(w.grid, [], st)
+    assert_state_equal(bu.state(), {c: v[fin.order] for c, v in st.items()}, "graph replay")
+    assert int(bu.next_id.item()) == nid
+
+
 def test_C4_junction_deferred():
     w = inputs.c4(scale=0.5, nports=8, n_updates=8)
     tot, bu = lockstep(w, 8, check_every=2, fused=True, deferred=True)
