@@ -273,15 +273,16 @@ cudaError_t launch_cll(const PartDev &in, const PartDev &out, const GridDev &g, 
                        int *cell_end, int *perm, float dt, bool advect, cudaStream_t s, Launch *L)
 {
     const long long ntiles = (g.ncells + kCellTile - 1) / kCellTile;
+    const long long cap = in.cap;
     L->before(s);
     if (advect) {
         static int grid = 0;
         if (!grid) grid = occ_grid(k_cll_key<true>, kThreads);
-        k_cll_key<true><<<grid, kThreads, 0, s>>>(in, g, ws, dt);
+        k_cll_key<true><<<cap_grid(grid, cap, kThreads * kKeyItems), kThreads, 0, s>>>(in, g, ws, dt);
     } else {
         static int grid = 0;
         if (!grid) grid = occ_grid(k_cll_key<false>, kThreads);
-        k_cll_key<false><<<grid, kThreads, 0, s>>>(in, g, ws, 0.0f);
+        k_cll_key<false><<<cap_grid(grid, cap, kThreads * kKeyItems), kThreads, 0, s>>>(in, g, ws, 0.0f);
     }
     L->after(s, KID_CLL_KEY);
     L->before(s);
@@ -291,7 +292,7 @@ cudaError_t launch_cll(const PartDev &in, const PartDev &out, const GridDev &g, 
         static int grid = 0;
         if (!grid) grid = occ_grid(k_cll_scatter, kThreads);
         L->before(s);
-        k_cll_scatter<<<grid, kThreads, 0, s>>>(ws, cell_start, perm);
+        k_cll_scatter<<<cap_grid(grid, cap, kThreads * kScatterItems), kThreads, 0, s>>>(ws, cell_start, perm);
         L->after(s, KID_CLL_SCATTER);
     }
     L->before(s);
@@ -300,11 +301,13 @@ cudaError_t launch_cll(const PartDev &in, const PartDev &out, const GridDev &g, 
     if (in.n_extra > 0) {
         static int grid = 0;
         if (!grid) grid = occ_grid(k_cll_gather<true, 3, 4>, kThreads);
-        k_cll_gather<true, 3, 4><<<grid, kThreads, 0, s>>>(in, out, g.dim, ws, cell_start, cell_end, perm);
+        k_cll_gather<true, 3, 4><<<cap_grid(grid, cap, kThreads * 3), kThreads, 0, s>>>(in, out, g.dim, ws, cell_start,
+                                                                                         cell_end, perm);
     } else {
         static int grid = 0;
         if (!grid) grid = occ_grid(k_cll_gather<false, 3, 4>, kThreads);
-        k_cll_gather<false, 3, 4><<<grid, kThreads, 0, s>>>(in, out, g.dim, ws, cell_start, cell_end, perm);
+        k_cll_gather<false, 3, 4><<<cap_grid(grid, cap, kThreads * 3), kThreads, 0, s>>>(in, out, g.dim, ws,
+                                                                                          cell_start, cell_end, perm);
     }
     L->after(s, KID_CLL_GATHER);
     return cudaGetLastError();

@@ -277,3 +277,14 @@ inline int occ_grid(K kernel, int threads, size_t smem = 0)
 }
 
 }  // namespace sphbuf
+
+namespace sphbuf {
+// Grid of a grid-stride / persistent kernel: the occupancy-derived full-GPU grid,
+// but no more blocks than the array capacity can keep busy (small configurations
+// are launch-latency bound).
+inline int cap_grid(int grid, long long cap, long long per_block)
+{
+    const long long need = (cap + per_block - 1) / per_block;
+    return (int)(need < 1 ? 1 : (need < grid ? need : grid));
+}
+}  // namespace sphbuf

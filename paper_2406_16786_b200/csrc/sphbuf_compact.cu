@@ -290,23 +290,23 @@ cudaError_t launch_compact(const PartDev &p, const PortTable &pt, const Workspac
         static int grid = 0;
         if (!grid) grid = occ_grid(k_compact_count, kThreads);
         L->before(s);
-        k_compact_count<<<grid, kThreads, 0, s>>>(p, ws, next_id);
+        k_compact_count<<<cap_grid(grid, p.cap, kCntTile), kThreads, 0, s>>>(p, ws, next_id);
         L->after(s, KID_COMPACT_COUNT);
     }
     L->before(s);
     if (p.n_extra > 0) {
         static int grid = 0;
         if (!grid) grid = occ_grid(k_compact_move<true>, kThreads);
-        k_compact_move<true><<<grid, kThreads, 0, s>>>(p, dim, ws, perm);
+        k_compact_move<true><<<cap_grid(grid, p.cap, kCmpTile), kThreads, 0, s>>>(p, dim, ws, perm);
     } else {
         static int grid = 0;
         if (!grid) grid = occ_grid(k_compact_move<false>, kThreads);
-        k_compact_move<false><<<grid, kThreads, 0, s>>>(p, dim, ws, perm);
+        k_compact_move<false><<<cap_grid(grid, p.cap, kCmpTile), kThreads, 0, s>>>(p, dim, ws, perm);
     }
     L->after(s, KID_COMPACT);
     L->before(s);
-    k_compact_append<<<sm_count_cached() * 4, kThreads, 0, s>>>(p, dim, pt.n, pt.max_ports, ws, all_counts, nranks,
-                                                                 rank, next_id, perm, false);
+    k_compact_append<<<cap_grid(sm_count_cached() * 4, perm ? p.cap : ws.max_new, kThreads), kThreads, 0, s>>>(
+        p, dim, pt.n, pt.max_ports, ws, all_counts, nranks, rank, next_id, perm, false);
     L->after(s, KID_COMPACT_APPEND);
     return cudaGetLastError();
 }

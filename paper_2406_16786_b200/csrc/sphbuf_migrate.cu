@@ -87,7 +87,7 @@ cudaError_t launch_migrate_pack(const PartDev &p, const GridDev &g, const Worksp
     if (e == cudaSuccess) e = cudaMemsetAsync(hi, 0, 16, s);
     if (e != cudaSuccess) return e;
     L->before(s);
-    k_mig_pack<<<sm_count_cached() * 8, kThreads, 0, s>>>(p, g, ws, lo, hi, max_migrate, rec);
+    k_mig_pack<<<cap_grid(sm_count_cached() * 8, p.cap, kThreads), kThreads, 0, s>>>(p, g, ws, lo, hi, max_migrate, rec);
     L->after(s, KID_MIG_PACK);
     return cudaGetLastError();
 }

@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(kThreads) k_upd_main(PartDev p, int dim, const
 cudaError_t launch_advect(const PartDev &p, int dim, float dt, cudaStream_t s, Launch *L)
 {
     L->before(s);
-    k_advect<<<sm_count_cached() * 8, kThreads, 0, s>>>(p, dim, dt);
+    k_advect<<<cap_grid(sm_count_cached() * 8, p.cap, kThreads), kThreads, 0, s>>>(p, dim, dt);
     L->after(s, KID_ADVECT);
     return cudaGetLastError();
 }
@@ -260,7 +260,7 @@ cudaError_t launch_register(const PartDev &p, const GridDev &g, const PortTable 
                             cudaStream_t s, Launch *L)
 {
     L->before(s);
-    k_register<<<sm_count_cached() * 8, kThreads, 0, s>>>(p, g.dim, pt.p[k], k, members);
+    k_register<<<cap_grid(sm_count_cached() * 8, p.cap, kThreads), kThreads, 0, s>>>(p, g.dim, pt.p[k], k, members);
     L->after(s, KID_REGISTER);
     return cudaGetLastError();
 }
@@ -274,7 +274,7 @@ cudaError_t launch_update(const PartDev &p, const GridDev &g, const PortTable &p
     static int grid = 0;
     if (!grid) grid = occ_grid(k_upd_main, kThreads);
     L->before(s);
-    k_upd_main<<<grid, kThreads, 0, s>>>(p, g.dim, pt, ws, n_runs, cell_start, port_counts);
+    k_upd_main<<<cap_grid(grid, ws.upd_tiles, 1), kThreads, 0, s>>>(p, g.dim, pt, ws, n_runs, cell_start, port_counts);
     L->after(s, KID_UPD_MAIN);
     return cudaGetLastError();
 }
