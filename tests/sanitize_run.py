@@ -1,0 +1,29 @@
+"""Small driver for compute-sanitizer runs (memcheck / racecheck / synccheck /
+initcheck, one tool per invocation): a few updates of C1e, C2 and a small 3-D
+junction through the C ABI, in both compaction modes and through a CUDA graph,
+each checked bit-exactly against the oracle at the end.
+
+    compute-sanitizer --tool memcheck python tests/sanitize_run.py
+"""
+import os
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(HERE))
+sys.path.insert(0, HERE)
+
+from paper_2406_16786_b200 import inputs  # noqa: E402
+from parity_util import lockstep  # noqa: E402
+
+
+def main():
+    lockstep(inputs.make("C1e"), 3, check_every=1)
+    lockstep(inputs.make("C1e"), 3, check_every=1, fused=True, deferred=True)
+    lockstep(inputs.make("C2"), 6, check_every=3)
+    lockstep(inputs.make("C2"), 6, check_every=3, fused=True, deferred=True)
+    lockstep(inputs.c4(scale=0.25, nports=4, n_updates=4), 3, check_every=1)
+    print("sanitize_run: all lock-step checks passed")
+
+
+if __name__ == "__main__":
+    main()
