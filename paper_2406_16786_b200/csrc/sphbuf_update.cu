@@ -52,59 +52,48 @@ __global__ void __launch_bounds__(kThreads) k_register(PartDev p, int dim, PortD
 
 // ------------------------------------------------------------------ a3-a6: buffer update
 
-// Update tiles are static groups of kRunGroup consecutive port runs (runs are in
-// canonical order: port-major, then cell), so no global scan of candidate
-// offsets is needed: a block sizes its group from the cell tables itself.
-constexpr int kRunGroup = 16;
-
-// K5: resets the per-update counters and the caller's per-port counts.
-__global__ void __launch_bounds__(128) k_upd_prologue(Workspace ws, int *port_counts, int max_ports)
+// K5: candidate count per port run (cell ranges from the current cell list) and
+// their exclusive scan; resets the per-update counters.  One block.
+__global__ void __launch_bounds__(1024) k_upd_prologue(Workspace ws, int n_runs, const int *cell_start,
+                                                       const int *cell_end, int *port_counts, int max_ports)
 {
+    __shared__ long long s_warp[1024 / 32 + 1];
     Counters *ctr = ws.ctr;
     if (threadIdx.x == 0) {
         ctr->epoch_upd += 1;
         ctr->ticket_upd = 0;
         ctr->n_stage = 0;
         ctr->n_del = 0;
-        ctr->n_cand = 0;
         ctr->i_first = LLONG_MAX;
     }
     for (int i = threadIdx.x; i < 2 * max_ports; i += blockDim.x) port_counts[i] = 0;
-}
-
-// The decision of Alg. 1-3 for one candidate of port k (pure; pinned transform).
-__device__ __forceinline__ void decide(const PortDev &P, int k, int dim, float x, float y, float z, int lab,
-                                       float X[3], bool &inP, bool &create, bool &del)
-{
-    to_local(P, dim, x, y, z, X);
-    inP = in_box(X, P.heP, dim);                         // x in P_k (reading R4)
-    const bool member = (lab == k);
-    const bool beyond = X[0] > P.he[0];                  // X'_0 > a/2
-    create = false;
-    del = false;
-    if (!inP) return;
-    if (P.kind == SPH_INLET) {
-        create = member && beyond;                       // Alg. 1 (R5)
-    } else if (P.kind == SPH_OUTLET) {
-        del = beyond;                                    // Alg. 2 (R6)
-    } else {
-        create = member && beyond;                       // Alg. 3
-        del = member && (X[0] < -P.he[0]);               // Alg. 3
+    long long carry = 0;
+    for (int r0 = 0; r0 < n_runs; r0 += 1024) {
+        const int r = r0 + threadIdx.x;
+        long long len = 0;
+        if (r < n_runs) len = (long long)cell_end[ws.runs[3 * r + 1]] - (long long)cell_start[ws.runs[3 * r]];
+        long long total;
+        const long long ex = block_excl_scan_ll<1024>(len, total, s_warp);
+        if (r < n_runs) ws.run_off[r] = carry + ex;
+        carry += total;
+    }
+    if (threadIdx.x == 0) {
+        ws.run_off[n_runs] = carry;
+        ctr->n_cand = carry;
+        ctr->checked += carry;
+        if ((carry + kUpdTile - 1) / kUpdTile > ws.upd_tiles) ctr->status |= kStCapacity;
     }
 }
 
 // K6: the candidate check (a3) with generation (a4), deletion (a5) and relabel
-// (a6) fused.  Per group: pass 1 counts the CREATEs (read only), a decoupled
-// look-back over the ordered groups gives the group's first staging slot, pass 2
-// decides again and applies; CREATE slots inside the group follow the candidate
-// order (port, cell, id) through a ballot scan per chunk.
+// (a6) fused; CREATEs are appended to the staging area in canonical order
+// (port, cell, id) by a ballot/block scan + decoupled look-back over ordered tiles.
 __global__ void __launch_bounds__(kThreads) k_upd_main(PartDev p, int dim, const __grid_constant__ PortTable pt,
                                                        Workspace ws, int n_runs, const int *cell_start,
-                                                       const int *cell_end, int *port_counts)
+                                                       int *port_counts)
 {
     __shared__ PortDev s_ports[SPH_MAX_PORTS];
-    __shared__ unsigned s_cnt[kThreads / 32 + 1];
-    __shared__ int s_beg[kRunGroup], s_port[kRunGroup], s_off[kRunGroup + 1];
+    __shared__ unsigned s_warp[kUpdItems * kThreads / 32 + 1];
     __shared__ long long s_tile;
     __shared__ unsigned s_prefix;
     {
@@ -114,150 +103,133 @@ __global__ void __launch_bounds__(kThreads) k_upd_main(PartDev p, int dim, const
         for (int w = threadIdx.x; w < words; w += blockDim.x) dst[w] = src[w];
     }
     Counters *ctr = ws.ctr;
+    const long long n_cand = ctr->n_cand;
     const unsigned epoch = ctr->epoch_upd;
-    const long long ngroups = (n_runs + kRunGroup - 1) / kRunGroup;
+    const long long ntiles = (n_cand + kUpdTile - 1) / kUpdTile;
     const int max_ports = pt.max_ports;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         ctr->epoch_cmp += 1;  // consumed by the compaction that follows
         ctr->ticket_cmp = 0;
         ctr->ticket_cmp2 = 0;
-        if (ngroups > ws.upd_tiles) ctr->status |= kStCapacity;
     }
     long long del_cnt = 0, del_min = LLONG_MAX, motion = 0;
     __syncthreads();
     while (true) {
         if (threadIdx.x == 0) s_tile = atomicAdd(&ctr->ticket_upd, 1);
         __syncthreads();
-        const long long grp = s_tile;
-        if (grp >= ngroups || grp >= ws.upd_tiles) break;
-        if (warp == 0) {
-            const long long r = grp * kRunGroup + lane;
-            int len = 0;
-            if (lane < kRunGroup && r < n_runs) {
-                const int beg = cell_start[ws.runs[3 * r]];
-                len = cell_end[ws.runs[3 * r + 1]] - beg;
-                s_beg[lane] = beg;
-                s_port[lane] = ws.runs[3 * r + 2];
-            }
-            int inc = len;
+        const long long tile = s_tile;
+        if (tile >= ntiles || tile >= ws.upd_tiles) break;
+        bool cr[kUpdItems];
+        int pidx[kUpdItems], kk[kUpdItems];
+        float ox[kUpdItems], oy[kUpdItems], oz[kUpdItems];
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int y = __shfl_up_sync(0xffffffffu, inc, o);
-                if (lane >= o) inc += y;
+        for (int it = 0; it < kUpdItems; ++it) {
+            cr[it] = false;
+            pidx[it] = -1;
+            kk[it] = 0;
+            ox[it] = oy[it] = oz[it] = 0.0f;
+            const long long g = tile * kUpdTile + it * kThreads + threadIdx.x;
+            if (g >= n_cand) continue;
+            // run containing g: largest r with run_off[r] <= g
+            int lo = 0, hi = n_runs - 1;
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (ws.run_off[mid] <= g) lo = mid;
+                else hi = mid - 1;
             }
-            if (lane < kRunGroup) s_off[lane] = inc - len;
-            if (lane == kRunGroup - 1) s_off[kRunGroup] = inc;
-        }
-        __syncthreads();
-        const int total = s_off[kRunGroup];
-        // pass 1: CREATEs of the group (no writes)
-        unsigned mine = 0;
-        for (int q0 = 0; q0 < total; q0 += kThreads) {
-            const int q = q0 + threadIdx.x;
-            if (q >= total) continue;
-            int r = 0;
-            while (r + 1 < kRunGroup && s_off[r + 1] <= q) ++r;
-            const int k = s_port[r];
-            const int pi = s_beg[r] + (q - s_off[r]);
+            const int r = lo;
+            const int k = ws.runs[3 * r + 2];
+            const int pi = cell_start[ws.runs[3 * r]] + (int)(g - ws.run_off[r]);
+            const PortDev &P = s_ports[k];
+            const float x = p.x[pi], y = p.y[pi], z = dim == 3 ? p.z[pi] : 0.0f;
+            const int lab = p.label[pi];
             float X[3];
-            bool inP, cr, dl;
-            decide(s_ports[k], k, dim, p.x[pi], p.y[pi], dim == 3 ? p.z[pi] : 0.0f, p.label[pi], X, inP, cr, dl);
-            mine += cr;
-        }
-        mine = warp_sum(mine);
-        if (lane == 0) s_cnt[warp] = mine;
-        __syncthreads();
-        if (warp == 0) {
-            unsigned c = lane < kThreads / 32 ? s_cnt[lane] : 0u;
-            c = warp_sum(c);
-            const unsigned pre = tile_prefix(ws.tile_upd, grp, epoch, c);
-            if (lane == 0) {
-                s_prefix = pre;
-                atomicAdd((unsigned long long *)&ctr->n_cand, (unsigned long long)total);
-                atomicAdd((unsigned long long *)&ctr->checked, (unsigned long long)total);
-                if (grp == ngroups - 1) ctr->n_stage = (long long)pre + c;
-            }
-        }
-        __syncthreads();
-        // pass 2: decide and apply
-        long long run = s_prefix;
-        for (int q0 = 0; q0 < total; q0 += kThreads) {
-            const int q = q0 + threadIdx.x;
-            bool cr[1] = {false};
-            int pi = 0, k = 0;
-            float x = 0.f, y = 0.f, z = 0.f;
-            if (q < total) {
-                int r = 0;
-                while (r + 1 < kRunGroup && s_off[r + 1] <= q) ++r;
-                k = s_port[r];
-                pi = s_beg[r] + (q - s_off[r]);
-                const PortDev &P = s_ports[k];
-                x = p.x[pi];
-                y = p.y[pi];
-                z = dim == 3 ? p.z[pi] : 0.0f;
-                const int lab = p.label[pi];
-                float X[3];
-                bool inP, create, del;
-                decide(P, k, dim, x, y, z, lab, X, inP, create, del);
-                // R12: a buffer particle outside its decision region moved more than
-                // the one-cell margin in one step; it can no longer be generated/deleted
-                if (lab == k && !inP) ++motion;
-                float px = x, py = y, pz = z;
-                if (create) {
-                    // recycle: x <- fl(x - fl(a u)) (Eqs. 2D/3D_Inverse_transformation, R10)
-                    px = __fsub_rn(x, P.s[0]);
-                    py = __fsub_rn(y, P.s[1]);
-                    p.x[pi] = px;
-                    p.y[pi] = py;
-                    if (dim == 3) {
-                        pz = __fsub_rn(z, P.s[2]);
-                        p.z[pi] = pz;
-                    }
-                    cr[0] = true;
-                    atomicAdd(&port_counts[k], 1);
-                }
-                if (del) {
-                    p.label[pi] = -2;                    // tombstone, removed by sph_compact
-                    atomicAdd(&port_counts[max_ports + k], 1);
-                    ++del_cnt;
-                    del_min = pi < del_min ? pi : del_min;
-                } else if (P.kind != SPH_INLET) {
-                    // relabel on post-recycle positions (R9)
-                    float Xp[3] = {X[0], X[1], X[2]};
-                    if (create) to_local(P, dim, px, py, pz, Xp);
-                    if (in_box(Xp, P.he, dim)) {
-                        if (lab != k) p.label[pi] = k;
-                    } else if (lab == k) {
-                        p.label[pi] = -1;
-                    }
-                }
-            }
-            unsigned excl[1], tot;
-            striped_scan<kThreads, 1>(cr, excl, tot, s_cnt);
-            if (cr[0]) {
-                const long long slot = run + excl[0];
-                if (slot < ws.max_new) {
-                    // duplicate = bitwise copy of the pre-recycle state, label fluid (R11)
-                    ws.sx[slot] = x;
-                    ws.sy[slot] = y;
-                    ws.svx[slot] = p.vx[pi];
-                    ws.svy[slot] = p.vy[pi];
-                    if (dim == 3) {
-                        ws.sz[slot] = z;
-                        ws.svz[slot] = p.vz[pi];
-                    }
-                    for (int e = 0; e < p.n_extra; ++e) ws.sextra[e][slot] = p.extra[e][pi];
-                    ws.sid[slot] = p.id[pi];
-                    ws.sport[slot] = k;
+            to_local(P, dim, x, y, z, X);
+            const bool inP = in_box(X, P.heP, dim);              // x in P_k (reading R4)
+            const bool member = (lab == k);
+            const bool beyond = X[0] > P.he[0];                  // X'_0 > a/2
+            bool create = false, del = false;
+            if (inP) {
+                if (P.kind == SPH_INLET) {
+                    create = member && beyond;                   // Alg. 1 (R5)
+                } else if (P.kind == SPH_OUTLET) {
+                    del = beyond;                                // Alg. 2 (R6)
                 } else {
-                    atomicOr(&ctr->status, kStStaging);
+                    create = member && beyond;                   // Alg. 3
+                    del = member && (X[0] < -P.he[0]);           // Alg. 3
                 }
             }
-            run += tot;
+            // R12: a buffer particle outside its decision region moved more than the
+            // one-cell margin in one step; it can no longer be generated/deleted.
+            if (member && !inP) ++motion;
+            float px = x, py = y, pz = z;
+            if (create) {
+                // recycle: x <- fl(x - fl(a u)) (Eqs. 2D/3D_Inverse_transformation, R10)
+                px = __fsub_rn(x, P.s[0]);
+                py = __fsub_rn(y, P.s[1]);
+                p.x[pi] = px;
+                p.y[pi] = py;
+                if (dim == 3) {
+                    pz = __fsub_rn(z, P.s[2]);
+                    p.z[pi] = pz;
+                }
+                cr[it] = true;
+                pidx[it] = pi;
+                kk[it] = k;
+                ox[it] = x;
+                oy[it] = y;
+                oz[it] = z;
+                atomicAdd(&port_counts[k], 1);
+            }
+            if (del) {
+                p.label[pi] = -2;                                // tombstone, removed by sph_compact
+                atomicAdd(&port_counts[max_ports + k], 1);
+                ++del_cnt;
+                del_min = pi < del_min ? pi : del_min;
+            } else if (P.kind != SPH_INLET) {
+                // relabel on post-recycle positions (R9)
+                float Xp[3] = {X[0], X[1], X[2]};
+                if (create) to_local(P, dim, px, py, pz, Xp);
+                if (in_box(Xp, P.he, dim)) {
+                    if (lab != k) p.label[pi] = k;
+                } else if (lab == k) {
+                    p.label[pi] = -1;
+                }
+            }
         }
+        unsigned excl[kUpdItems], total;
+        striped_scan<kThreads, kUpdItems>(cr, excl, total, s_warp);
+        if (threadIdx.x < 32) {
+            const unsigned pre = tile_prefix(ws.tile_upd, tile, epoch, total);
+            if (threadIdx.x == 0) s_prefix = pre;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int it = 0; it < kUpdItems; ++it) {
+            if (!cr[it]) continue;
+            const long long slot = (long long)s_prefix + excl[it];
+            if (slot < ws.max_new) {
+                const int pi = pidx[it];
+                // duplicate = bitwise copy of the pre-recycle state, label fluid (R11)
+                ws.sx[slot] = ox[it];
+                ws.sy[slot] = oy[it];
+                ws.svx[slot] = p.vx[pi];
+                ws.svy[slot] = p.vy[pi];
+                if (dim == 3) {
+                    ws.sz[slot] = oz[it];
+                    ws.svz[slot] = p.vz[pi];
+                }
+                for (int e = 0; e < p.n_extra; ++e) ws.sextra[e][slot] = p.extra[e][pi];
+                ws.sid[slot] = p.id[pi];
+                ws.sport[slot] = kk[it];
+            } else {
+                atomicOr(&ctr->status, kStStaging);
+            }
+        }
+        if (tile == ntiles - 1 && threadIdx.x == 0) ctr->n_stage = (long long)s_prefix + total;
         __syncthreads();
     }
+    const int lane = threadIdx.x & 31;
     del_cnt = warp_sum_ll(del_cnt);
     del_min = warp_min_ll(del_min);
     motion = warp_sum_ll(motion);
@@ -272,6 +244,7 @@ __global__ void __launch_bounds__(kThreads) k_upd_main(PartDev p, int dim, const
         }
     }
 }
+
 
 // ------------------------------------------------------------------ launchers
 
@@ -296,14 +269,12 @@ cudaError_t launch_update(const PartDev &p, const GridDev &g, const PortTable &p
                           const int *cell_start, const int *cell_end, int *port_counts, cudaStream_t s, Launch *L)
 {
     L->before(s);
-    k_upd_prologue<<<1, 128, 0, s>>>(ws, port_counts, pt.max_ports);
+    k_upd_prologue<<<1, 1024, 0, s>>>(ws, n_runs, cell_start, cell_end, port_counts, pt.max_ports);
     L->after(s, KID_UPD_PROLOGUE);
     static int grid = 0;
     if (!grid) grid = occ_grid(k_upd_main, kThreads);
-    const long long ngroups = (n_runs + kRunGroup - 1) / kRunGroup;
     L->before(s);
-    k_upd_main<<<cap_grid(grid, ngroups, 1), kThreads, 0, s>>>(p, g.dim, pt, ws, n_runs, cell_start, cell_end,
-                                                               port_counts);
+    k_upd_main<<<cap_grid(grid, ws.upd_tiles, 1), kThreads, 0, s>>>(p, g.dim, pt, ws, n_runs, cell_start, port_counts);
     L->after(s, KID_UPD_MAIN);
     return cudaGetLastError();
 }
