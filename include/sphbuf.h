@@ -155,6 +155,23 @@ sph_status sph_cll_build(sph_ctx *ctx, const sph_particles *in, sph_particles *o
 sph_status sph_advect_cll_build(sph_ctx *ctx, sph_particles *in, sph_particles *out, float dt, int32_t *cell_start,
                                 int32_t *cell_end, int32_t *perm_or_null, void *stream);
 
+/* The same build in two halves around the multi-GPU neighbour exchange (§8(e)),
+ * so migration costs no extra pass over the particles:
+ *   sph_cll_key    (optional advection when advect != 0) pinned cell keys; with
+ *                  send buffers (layout as sph_migrate_pack) every particle whose
+ *                  cell x-index left [cx_begin, cx_end) is packed for rank r-1 /
+ *                  r+1 instead of being keyed;
+ *   -- the caller exchanges the buffers (NCCL send/recv) --
+ *   sph_cll_finish appends the received particles (recv_lo / recv_hi, may be
+ *                  NULL) after the local ones with their keys, then scan,
+ *                  scatter and gather exactly as sph_cll_build.
+ * Without buffers the pair equals sph_cll_build / sph_advect_cll_build. */
+sph_status sph_cll_key(sph_ctx *ctx, sph_particles *in, float dt, int32_t advect, float *send_lo, float *send_hi,
+                       void *stream);
+sph_status sph_cll_finish(sph_ctx *ctx, sph_particles *in, sph_particles *out, const float *recv_lo,
+                          const float *recv_hi, int32_t *cell_start, int32_t *cell_end, int32_t *perm_or_null,
+                          void *stream);
+
 /* One buffer update over the candidates of every port (cells from registration,
  * particle ranges from the cell tables of the sph_cll_build just made on `p`):
  * X' = Q_k (x - o_k) in pinned fp32; decisions gated by x in P_k:

@@ -20,8 +20,37 @@ namespace sphbuf {
 
 constexpr int kKeyItems = 4;
 
-template <bool Advect>
-__global__ void __launch_bounds__(kThreads) k_cll_key(PartDev in, GridDev g, Workspace ws, float dt)
+// Migration record of particle i (multi-GPU x-slabs): position,
+// velocity, extras, id (two 32-bit words), label; slot from the header count.
+__device__ __forceinline__ void pack_record(const PartDev &in, int dim, long long i, float x, float y, float z,
+                                            int lab, float *buf, long long maxm, int rec, Counters *ctr)
+{
+    const int slot = atomicAdd(reinterpret_cast<int *>(buf), 1);
+    if (slot >= maxm) {
+        atomicOr(&ctr->status, kStMigrate);
+        return;
+    }
+    float *r = buf + 4 + (long long)slot * rec;
+    int w = 0;
+    r[w++] = x;
+    r[w++] = y;
+    if (dim == 3) r[w++] = z;
+    r[w++] = in.vx[i];
+    r[w++] = in.vy[i];
+    if (dim == 3) r[w++] = in.vz[i];
+    for (int e = 0; e < in.n_extra; ++e) r[w++] = in.extra[e][i];
+    const long long id = in.id[i];
+    r[w++] = __int_as_float((int)(id & 0xffffffffll));
+    r[w++] = __int_as_float((int)(id >> 32));
+    r[w++] = __int_as_float(lab);
+}
+
+// K1.  Migrate (multi-GPU): a particle whose (advected) cell x-index left the
+// slab is packed for the neighbour rank and gets no key (dropped from this
+// slab's build) — the migration costs no extra pass over the array.
+template <bool Advect, bool Migrate>
+__global__ void __launch_bounds__(kThreads) k_cll_key(PartDev in, GridDev g, Workspace ws, float dt, float *mlo,
+                                                      float *mhi, long long maxm, int rec)
 {
     Counters *ctr = ws.ctr;
     const long long n = *in.n;
@@ -29,7 +58,9 @@ __global__ void __launch_bounds__(kThreads) k_cll_key(PartDev in, GridDev g, Wor
         ctr->epoch_cll += 1;
         ctr->ticket_cll = 0;
         ctr->n_in = n;
+        ctr->mig_base = n;
     }
+    long long moved = 0;
     const int lane = threadIdx.x & 31;
     const unsigned lt = lanemask_lt();
     const unsigned le = lt | (1u << lane);
@@ -72,6 +103,16 @@ __global__ void __launch_bounds__(kThreads) k_cll_key(PartDev in, GridDev g, Wor
                     }
                 }
                 if (lab[it] > -2) {
+                    if (Migrate) {
+                        int o2 = 0;
+                        const int cxr = cell_axis(x[it], g.lo[0], g.inv_cs, 0, g.ncell[0], o2);
+                        if (cxr < g.cx_begin || cxr >= g.cx_end) {
+                            pack_record(in, g.dim, i, x[it], y[it], z[it], lab[it], cxr < g.cx_begin ? mlo : mhi,
+                                        maxm, rec, ctr);
+                            ++moved;
+                            continue;
+                        }
+                    }
                     int oob = 0;
                     key[it] = cell_of(g, x[it], y[it], z[it], oob);
                     oob_acc += oob;
@@ -101,6 +142,54 @@ __global__ void __launch_bounds__(kThreads) k_cll_key(PartDev in, GridDev g, Wor
     }
     const unsigned o = warp_sum((unsigned)oob_acc);
     if (lane == 0 && o) atomicAdd((unsigned long long *)&ctr->out_of_grid, (unsigned long long)o);
+    if (Migrate) {
+        moved = warp_sum_ll(moved);
+        if (lane == 0 && moved) atomicAdd((unsigned long long *)&ctr->migrated, (unsigned long long)moved);
+    }
+}
+
+// K1b (multi-GPU): append the particles received from the neighbour slabs after
+// the local ones (index mig_base + s) with their keys and ranks, before the scan.
+__global__ void __launch_bounds__(kThreads) k_cll_unpack_key(PartDev in, GridDev g, Workspace ws, const float *blo,
+                                                             const float *bhi, long long maxm, int rec)
+{
+    Counters *ctr = ws.ctr;
+    const long long nlo = blo ? min((long long)__float_as_int(blo[0]), maxm) : 0;
+    const long long nhi = bhi ? min((long long)__float_as_int(bhi[0]), maxm) : 0;
+    const long long base = ctr->mig_base;
+    long long R = nlo + nhi;
+    if (base + R > in.cap) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(&ctr->status, kStCapacity);
+        R = in.cap - base;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) ctr->n_in = base + R;
+    const int dim = g.dim;
+    int oob_acc = 0;
+    for (long long s = (long long)blockIdx.x * blockDim.x + threadIdx.x; s < R; s += (long long)gridDim.x * blockDim.x) {
+        const float *r = s < nlo ? blo + 4 + s * rec : bhi + 4 + (s - nlo) * rec;
+        const long long d = base + s;
+        int w = 0;
+        const float x = r[w++], y = r[w++], z = dim == 3 ? r[w++] : 0.0f;
+        in.x[d] = x;
+        in.y[d] = y;
+        if (dim == 3) in.z[d] = z;
+        in.vx[d] = r[w++];
+        in.vy[d] = r[w++];
+        if (dim == 3) in.vz[d] = r[w++];
+        for (int e = 0; e < in.n_extra; ++e) in.extra[e][d] = r[w++];
+        const long long lo = (unsigned)__float_as_int(r[w++]);
+        const long long hi = __float_as_int(r[w++]);
+        in.id[d] = (hi << 32) | lo;
+        const int lab = __float_as_int(r[w++]);
+        in.label[d] = lab;
+        int oob = 0;
+        const int key = cell_of(g, x, y, z, oob);
+        oob_acc += oob;
+        ws.key[d] = key;
+        ws.rank[d] = atomicAdd(&ws.cell_count[key], 1);
+    }
+    const unsigned o = warp_sum((unsigned)oob_acc);
+    if ((threadIdx.x & 31) == 0 && o) atomicAdd((unsigned long long *)&ctr->out_of_grid, (unsigned long long)o);
 }
 
 __global__ void __launch_bounds__(kThreads) k_cell_scan(GridDev g, Workspace ws, int *cell_start, int *cell_end,
@@ -269,22 +358,54 @@ __global__ void __launch_bounds__(kThreads, MINB) k_cll_gather(PartDev in, PartD
 
 int sm_count() { return sm_count_cached(); }
 
+template <bool A, bool M>
+static void key_launch(const PartDev &in, const GridDev &g, const Workspace &ws, float dt, float *lo, float *hi,
+                       long long maxm, int rec, cudaStream_t s)
+{
+    static int grid = 0;
+    if (!grid) grid = occ_grid(k_cll_key<A, M>, kThreads);
+    k_cll_key<A, M><<<cap_grid(grid, in.cap, kThreads * kKeyItems), kThreads, 0, s>>>(in, g, ws, dt, lo, hi, maxm,
+                                                                                        rec);
+}
+
+cudaError_t launch_cll_key(const PartDev &in, const GridDev &g, const Workspace &ws, float dt, bool advect,
+                           float *send_lo, float *send_hi, long long maxm, int rec, cudaStream_t s, Launch *L)
+{
+    const bool mig = send_lo && send_hi;
+    if (mig) {
+        cudaError_t e = cudaMemsetAsync(send_lo, 0, 16, s);
+        if (e == cudaSuccess) e = cudaMemsetAsync(send_hi, 0, 16, s);
+        if (e != cudaSuccess) return e;
+    }
+    L->before(s);
+    if (advect && mig) key_launch<true, true>(in, g, ws, dt, send_lo, send_hi, maxm, rec, s);
+    else if (advect) key_launch<true, false>(in, g, ws, dt, nullptr, nullptr, 0, rec, s);
+    else if (mig) key_launch<false, true>(in, g, ws, 0.0f, send_lo, send_hi, maxm, rec, s);
+    else key_launch<false, false>(in, g, ws, 0.0f, nullptr, nullptr, 0, rec, s);
+    L->after(s, KID_CLL_KEY);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_cll(const PartDev &in, const PartDev &out, const GridDev &g, const Workspace &ws, int *cell_start,
                        int *cell_end, int *perm, float dt, bool advect, cudaStream_t s, Launch *L)
 {
+    cudaError_t e = launch_cll_key(in, g, ws, dt, advect, nullptr, nullptr, 0, 0, s, L);
+    if (e != cudaSuccess) return e;
+    return launch_cll_finish(in, out, g, ws, nullptr, nullptr, 0, 0, cell_start, cell_end, perm, s, L);
+}
+
+cudaError_t launch_cll_finish(const PartDev &in, const PartDev &out, const GridDev &g, const Workspace &ws,
+                              const float *recv_lo, const float *recv_hi, long long maxm, int rec, int *cell_start,
+                              int *cell_end, int *perm, cudaStream_t s, Launch *L)
+{
     const long long ntiles = (g.ncells + kCellTile - 1) / kCellTile;
     const long long cap = in.cap;
-    L->before(s);
-    if (advect) {
-        static int grid = 0;
-        if (!grid) grid = occ_grid(k_cll_key<true>, kThreads);
-        k_cll_key<true><<<cap_grid(grid, cap, kThreads * kKeyItems), kThreads, 0, s>>>(in, g, ws, dt);
-    } else {
-        static int grid = 0;
-        if (!grid) grid = occ_grid(k_cll_key<false>, kThreads);
-        k_cll_key<false><<<cap_grid(grid, cap, kThreads * kKeyItems), kThreads, 0, s>>>(in, g, ws, 0.0f);
+    if (recv_lo || recv_hi) {
+        L->before(s);
+        k_cll_unpack_key<<<cap_grid(sm_count_cached() * 2, maxm * 2, kThreads), kThreads, 0, s>>>(
+            in, g, ws, recv_lo, recv_hi, maxm, rec);
+        L->after(s, KID_MIG_UNPACK);
     }
-    L->after(s, KID_CLL_KEY);
     L->before(s);
     k_cell_scan<<<(unsigned)(ntiles > 0 ? ntiles : 1), kThreads, 0, s>>>(g, ws, cell_start, cell_end, out.n, ntiles);
     L->after(s, KID_CELL_SCAN);

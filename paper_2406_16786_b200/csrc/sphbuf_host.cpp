@@ -572,6 +572,36 @@ sph_status sph_advect_cll_build(sph_ctx *c, sph_particles *in, sph_particles *ou
     return cll_build(c, in, out, cell_start, cell_end, perm, dt, true, stream);
 }
 
+sph_status sph_cll_key(sph_ctx *c, sph_particles *in, float dt, int32_t advect, float *send_lo, float *send_hi,
+                       void *stream)
+{
+    if (!c) return SPH_ERR_ARG;
+    sph_status st = check_particles(c, in);
+    if (st != SPH_OK) return st;
+    if ((send_lo == nullptr) != (send_hi == nullptr)) return fail(c, SPH_ERR_ARG, "give both send buffers or none");
+    cudaError_t e = launch_cll_key(part_dev(in), c->gd, c->W, dt, advect != 0, send_lo, send_hi, c->max_migrate,
+                                   sph_migrate_record_floats(c), static_cast<cudaStream_t>(stream), &c->L);
+    return e == cudaSuccess ? SPH_OK : cuda_fail(c, e, "cll_key");
+}
+
+sph_status sph_cll_finish(sph_ctx *c, sph_particles *in, sph_particles *out, const float *recv_lo,
+                          const float *recv_hi, int32_t *cell_start, int32_t *cell_end, int32_t *perm, void *stream)
+{
+    if (!c) return SPH_ERR_ARG;
+    sph_status st = check_particles(c, in);
+    if (st == SPH_OK) st = check_particles(c, out);
+    if (st != SPH_OK) return st;
+    if (!cell_start || !cell_end) return fail(c, SPH_ERR_ARG, "NULL cell table");
+    if (in->x == out->x || in->id == out->id || in->label == out->label)
+        return fail(c, SPH_ERR_ARG, "cll_finish needs distinct input and output arrays");
+    if ((reinterpret_cast<size_t>(cell_start) | reinterpret_cast<size_t>(cell_end)) % 16)
+        return fail(c, SPH_ERR_ARG, "cell tables must be 16-byte aligned");
+    cudaError_t e = launch_cll_finish(part_dev(in), part_dev(out), c->gd, c->W, recv_lo, recv_hi, c->max_migrate,
+                                      sph_migrate_record_floats(c), cell_start, cell_end, perm,
+                                      static_cast<cudaStream_t>(stream), &c->L);
+    return e == cudaSuccess ? SPH_OK : cuda_fail(c, e, "cll_finish");
+}
+
 sph_status sph_buffer_update(sph_ctx *c, sph_particles *p, const int32_t *cell_start, const int32_t *cell_end,
                              int32_t *port_counts, void *stream)
 {

@@ -82,7 +82,8 @@ struct Counters {
     long long motion;      // cumulative
     long long cmp_n;       // compaction: N before
     long long cmp_next_id; // compaction: next_id before
-    long long migrated;    // last pack
+    long long migrated;    // cumulative packed for neighbour slabs
+    long long mig_base;    // cll: local count before the received particles are appended
     int status;            // sticky bits
     int dummy;
 };
@@ -139,6 +140,11 @@ cudaError_t launch_register(const PartDev &p, const GridDev &g, const PortTable 
                             cudaStream_t s, Launch *L);
 cudaError_t launch_cll(const PartDev &in, const PartDev &out, const GridDev &g, const Workspace &ws,
                        int *cell_start, int *cell_end, int *perm, float dt, bool advect, cudaStream_t s, Launch *L);
+cudaError_t launch_cll_key(const PartDev &in, const GridDev &g, const Workspace &ws, float dt, bool advect,
+                           float *send_lo, float *send_hi, long long maxm, int rec, cudaStream_t s, Launch *L);
+cudaError_t launch_cll_finish(const PartDev &in, const PartDev &out, const GridDev &g, const Workspace &ws,
+                              const float *recv_lo, const float *recv_hi, long long maxm, int rec, int *cell_start,
+                              int *cell_end, int *perm, cudaStream_t s, Launch *L);
 cudaError_t launch_update(const PartDev &p, const GridDev &g, const PortTable &pt, const Workspace &ws, int n_runs,
                           const int *cell_start, const int *cell_end, int *port_counts, cudaStream_t s,
                           Launch *L);

@@ -87,22 +87,21 @@ class SlabUpdater:
 
     # phases (LoopbackGroup interleaves them across slabs)
     def phase_advect_pack(self, dt):
-        self._dt = None
+        """advection + cell keys + migration pack in one pass (sph_cll_key)"""
+        bu = self.bu
         if self.world > 1:
-            if dt is not None:
-                self.bu.advect(dt)
-            sphbuf.sph_migrate_pack(self.bu.ctx, self.bu.A, self.send_lo, self.send_hi)
+            sphbuf.sph_cll_key(bu.ctx, bu.A, dt, self.send_lo, self.send_hi)
         else:
-            self._dt = dt       # single slab: advection fused into the cell-list build
+            sphbuf.sph_cll_key(bu.ctx, bu.A, dt)
 
     def phase_unpack_update(self):
-        if self.world > 1:
-            if self.rank > 0:
-                sphbuf.sph_migrate_unpack(self.bu.ctx, self.bu.A, self.recv_lo)
-            if self.rank < self.world - 1:
-                sphbuf.sph_migrate_unpack(self.bu.ctx, self.bu.A, self.recv_hi)
-        self.bu.cll_build(dt=self._dt)
-        self.bu.update()
+        """received particles appended + rest of the build (sph_cll_finish), update"""
+        bu = self.bu
+        rlo = self.recv_lo if (self.world > 1 and self.rank > 0) else None
+        rhi = self.recv_hi if (self.world > 1 and self.rank < self.world - 1) else None
+        sphbuf.sph_cll_finish(bu.ctx, bu.A, bu.B, bu.cell_start, bu.cell_end, rlo, rhi)
+        bu.A, bu.B = bu.B, bu.A
+        bu.update()
 
     def phase_compact(self):
         if self.world > 1:

@@ -55,7 +55,7 @@ EXPORTS = ["sph_ctx_create", "sph_ctx_destroy", "sph_last_error", "sph_workspace
            "sph_port_check", "sph_buffer_register", "sph_advect", "sph_cll_build", "sph_buffer_update",
            "sph_compact", "sph_migrate_record_floats", "sph_migrate_pack", "sph_migrate_unpack", "sph_status_sync",
            "sph_launch_count", "sph_port_cells", "sph_frame_from_axis", "sph_profile", "sph_profile_read",
-           "sph_kernel_name", "sph_advect_cll_build", "sph_compact_deferred"]
+           "sph_kernel_name", "sph_advect_cll_build", "sph_compact_deferred", "sph_cll_key", "sph_cll_finish"]
 NKERNELS = 14
 
 
@@ -84,6 +84,10 @@ def lib():
     L.sph_cll_build.argtypes = [vp, P(sph_particles), P(sph_particles), vp, vp, vp, vp]
     L.sph_advect_cll_build.argtypes = [vp, P(sph_particles), P(sph_particles), f32, vp, vp, vp, vp]
     L.sph_advect_cll_build.restype = C.c_int
+    L.sph_cll_key.argtypes = [vp, P(sph_particles), f32, i32, vp, vp, vp]
+    L.sph_cll_key.restype = C.c_int
+    L.sph_cll_finish.argtypes = [vp, P(sph_particles), P(sph_particles), vp, vp, vp, vp, vp, vp]
+    L.sph_cll_finish.restype = C.c_int
     L.sph_buffer_update.argtypes = [vp, P(sph_particles), vp, vp, vp, vp]
     L.sph_compact.argtypes = [vp, P(sph_particles), vp, i32, i32, vp, vp, vp]
     L.sph_compact_deferred.argtypes = [vp, P(sph_particles), vp, i32, i32, vp, vp]
@@ -202,6 +206,16 @@ def sph_cll_build(ctx, pin, pout, cell_start, cell_end, perm=None, stream=None):
 def sph_advect_cll_build(ctx, pin, pout, dt, cell_start, cell_end, perm=None, stream=None):
     _check(lib().sph_advect_cll_build(ctx.h, C.byref(pin.abi), C.byref(pout.abi), float(dt), _ptr(cell_start),
                                       _ptr(cell_end), _ptr(perm), _stream(stream)), ctx.h)
+
+
+def sph_cll_key(ctx, pin, dt=None, send_lo=None, send_hi=None, stream=None):
+    _check(lib().sph_cll_key(ctx.h, C.byref(pin.abi), float(dt or 0.0), 0 if dt is None else 1, _ptr(send_lo),
+                             _ptr(send_hi), _stream(stream)), ctx.h)
+
+
+def sph_cll_finish(ctx, pin, pout, cell_start, cell_end, recv_lo=None, recv_hi=None, perm=None, stream=None):
+    _check(lib().sph_cll_finish(ctx.h, C.byref(pin.abi), C.byref(pout.abi), _ptr(recv_lo), _ptr(recv_hi),
+                                _ptr(cell_start), _ptr(cell_end), _ptr(perm), _stream(stream)), ctx.h)
 
 
 def sph_buffer_update(ctx, parts, cell_start, cell_end, port_counts, stream=None):

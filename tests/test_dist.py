@@ -170,6 +170,37 @@ def test_gloo_two_ranks_match_single_process():
 
 
 @pytest.mark.gpu
+def test_migrate_pack_unpack_abi_roundtrip():
+    """sph_migrate_pack tombstones and packs exactly the particles whose pinned cell
+    x-index lies outside the slab; sph_migrate_unpack appends them unchanged."""
+    from paper_2406_16786_b200 import sphbuf
+    w = inputs.c4(scale=0.25, nports=4, n_updates=10)
+    st = oracle.to_numpy_state(w.state)
+    ncx = w.grid.ncell[0]
+    g = w.grid.slab(ncx // 3, 2 * ncx // 3)
+    a = sphbuf.BufferUpdater(g, w.h, w.dp, [], inputs.capacity_for(w, 0.1), max_migrate=1 << 19)
+    b = sphbuf.BufferUpdater(g, w.h, w.dp, [], inputs.capacity_for(w, 0.1), max_migrate=1 << 19)
+    a.load(w.state, w.next_id)
+    rec = sphbuf.sph_migrate_record_floats(a.ctx)
+    lo = torch.zeros(4 + (1 << 19) * rec, device="cuda")
+    hi = torch.zeros_like(lo)
+    sphbuf.sph_migrate_pack(a.ctx, a.A, lo, hi)
+    cx = cell_x(w.grid, st["x"])
+    exp_lo, exp_hi = int((cx < ncx // 3).sum()), int((cx >= 2 * ncx // 3).sum())
+    assert int(lo[:4].view(torch.int32)[0]) == exp_lo and int(hi[:4].view(torch.int32)[0]) == exp_hi
+    lab = a.A.label[:w.n].cpu().numpy()
+    assert int((lab == -3).sum()) == exp_lo + exp_hi
+    b.load({k: v[:0] for k, v in w.state.items()}, w.next_id)
+    sphbuf.sph_migrate_unpack(b.ctx, b.A, lo)
+    sphbuf.sph_migrate_unpack(b.ctx, b.A, hi)
+    got = by_id({k: v.numpy() for k, v in b.state().items()})
+    sel = (cx < ncx // 3) | (cx >= 2 * ncx // 3)
+    ref = by_id({k: v[sel] for k, v in st.items()})
+    for k in ref:
+        np.testing.assert_array_equal(got[k], ref[k], err_msg=k)
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("P", [2, 3])
 def test_loopback_slabs_match_oracle(P):
     from paper_2406_16786_b200.dist import LoopbackGroup, SlabUpdater
