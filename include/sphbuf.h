@@ -137,6 +137,32 @@ sph_status sph_buffer_register(sph_ctx *ctx, sph_particles *p, const float origi
                                const float half_extents[3], int32_t kind, int32_t layers, float dp,
                                int32_t *port_id_out, int64_t *members_out_dev, void *stream);
 
+/* Boundary-condition state of a port's buffer particles (paper §IV, SURVEY
+ * §8(f) rank 1), applied by sph_buffer_update to every particle that is a
+ * buffer particle of the port at the end of the update (after generation,
+ * recycling and relabel; duplicates keep the pre-BC state):
+ *   SPH_BC_PRESSURE: v <- (v.u) u (Eq. velocity_correction); a
+ *     particle recycled in this update gets density rho0 + p_b / c0^2 in extra
+ *     column rho_column (Eq. postulate-density; -1: no density column);
+ *   SPH_BC_VELOCITY: v <- Q^T (v_X', 0, 0) (Eqs. 2D/3D_velocity_transformation,
+ *     P:605-636) with v_X' = u0 (plug), u0 (1 - (Y'/R)^2) (Eqs. 2D/3D_velocity_
+ *     profile, literal) or u0 (1 - (Y'^2 + Z'^2)/R^2) (3-D pipe reading
+ *     R23); recycled density and pressure unchanged.
+ * Pinned arithmetic as everywhere. */
+typedef enum { SPH_BC_NONE = 0, SPH_BC_PRESSURE = 1, SPH_BC_VELOCITY = 2 } sph_bc_kind;
+typedef enum { SPH_PROFILE_PLUG = 0, SPH_PROFILE_PARABOLIC = 1, SPH_PROFILE_PARABOLIC_RADIAL = 2 } sph_profile_kind;
+typedef struct {
+    int32_t kind;          /* sph_bc_kind */
+    float rho0, c0, p_b;   /* PRESSURE */
+    int32_t rho_column;    /* PRESSURE: extra column index of the density, -1 none */
+    int32_t profile;       /* VELOCITY: sph_profile_kind */
+    float u0, radius;      /* VELOCITY: axial speed scale and R */
+} sph_bc;
+
+/* Set (or clear with kind SPH_BC_NONE) the boundary condition of registered
+ * port port_id.  Host only; takes effect at the next sph_buffer_update. */
+sph_status sph_port_set_bc(sph_ctx *ctx, int32_t port_id, const sph_bc *bc);
+
 /* Driver step (not the method): x <- fl(x + fl(v dt)) per component. */
 sph_status sph_advect(sph_ctx *ctx, sph_particles *p, float dt, void *stream);
 

@@ -39,7 +39,9 @@ class Grid(C.Structure):
 
 
 class Port(C.Structure):
-    _fields_ = [("o", C.c_float * 3), ("Q", C.c_float * 9), ("he", C.c_float * 3), ("kind", C.c_int32)]
+    _fields_ = [("o", C.c_float * 3), ("Q", C.c_float * 9), ("he", C.c_float * 3), ("kind", C.c_int32),
+                ("bc", C.c_int32), ("profile", C.c_int32), ("rho_col", C.c_int32), ("rho_b", C.c_float),
+                ("u0", C.c_float), ("R", C.c_float), ("R2", C.c_float)]
 
 
 class State(C.Structure):
@@ -169,6 +171,18 @@ def cport(p) -> Port:
     P.Q[:] = list(p.Q)
     P.he[:] = list(p.half_extents)
     P.kind = p.kind
+    P.bc, P.rho_col = 0, -1
+    bc = getattr(p, "bc", None)
+    if bc is not None and bc.kind:
+        P.bc = bc.kind
+        P.rho_col = bc.rho_column
+        # Eq. postulate-density formed in f64, rounded once to binary32
+        P.rho_b = float(np.float32(float(np.float32(bc.rho0)) + float(np.float32(bc.p_b)) /
+                                   (float(np.float32(bc.c0)) * float(np.float32(bc.c0)))))
+        P.profile = bc.profile
+        P.u0 = float(np.float32(bc.u0))
+        P.R = float(np.float32(bc.radius))
+        P.R2 = float(np.float32(bc.radius) * np.float32(bc.radius))
     return P
 
 

@@ -56,6 +56,12 @@ typedef struct {
                              coordinates; X' = Q (x - o)  (Eq. 2D/3D_transformation) */
     float he[3];          /* half extents a/2, b/2, c/2 */
     int32_t kind;         /* 0 = inlet (Alg. 1), 1 = outlet (Alg. 2), 2 = bidirectional (Alg. 3) */
+    /* boundary condition of the port's buffer particles (§IV; 0 none, 1 pressure, 2 velocity) */
+    int32_t bc;
+    int32_t profile;      /* velocity BC: 0 plug, 1 u0 (1-(Y'/R)^2), 2 u0 (1-(Y'^2+Z'^2)/R^2) */
+    int32_t rho_col;      /* pressure BC: extra column of the density, -1 none */
+    float rho_b;          /* pressure BC: fl32(rho0 + p_b / c0^2) formed in f64 (Eq. postulate-density) */
+    float u0, R, R2;      /* velocity BC: speed scale, radius, fl(R*R) */
 } orc_port;
 
 typedef struct {
@@ -583,6 +589,58 @@ int orc_update(const orc_grid *g, const orc_port *ports, int32_t K, const orc_st
         }
         free(mask);
         mask = NULL;
+    }
+
+    /* O5b: boundary-condition state of every buffer particle of port k after the
+     * update (paper §IV).  The duplicates staged in O4 keep the
+     * pre-BC state.
+     *  pressure BC: v = (v.u) u, u = row 0 of Q (Eq. velocity_correction);
+     *    a particle recycled in this update gets rho = rho0 + p_b / c0^2
+     *    (Eq. postulate-density);
+     *  velocity BC: v_X' = u0 (1 - (Y'/R)^2) in the local frame (Eqs. 2D/3D_velocity_
+     *    profile; plug and radial variants), v = Q^T (v_X', 0, 0)
+     *    (Eqs. 2D/3D_velocity_transformation); recycled density unchanged
+     *    (P:639-643).  Pinned fp32 (Q^T (v_X',0,0)_j = fl(v_X' Q_0j) since the other
+     *    terms are exact zeros). */
+    for (int32_t k = 0; k < K; ++k) {
+        const orc_port *p = &ports[k];
+        if (p->bc == 0) continue;
+        for (int64_t j = 0; j < n; ++j) {
+            if (out->delete_port[j] >= 0 || S->label[j] != k) continue;
+            float u;
+            if (p->bc == 1) {
+                float a0 = S->vx[j] * p->Q[0];
+                float a1 = S->vy[j] * p->Q[1];
+                u = a0 + a1;
+                if (dim == 3) {
+                    float a2 = S->vz[j] * p->Q[2];
+                    u = u + a2;
+                }
+                if (out->create_port[j] == k && p->rho_col >= 0) S->extra[p->rho_col][j] = p->rho_b;
+            } else {
+                float X[3];
+                orc_to_local_f32(p, dim, S->x[j], S->y[j], dim == 3 ? S->z[j] : 0.0f, X);
+                u = p->u0;
+                if (p->profile == 1) {
+                    float t = X[1] / p->R;
+                    float tt = t * t;
+                    float q = 1.0f - tt;
+                    u = p->u0 * q;
+                } else if (p->profile == 2) {
+                    float r2 = X[1] * X[1];
+                    if (dim == 3) {
+                        float zz = X[2] * X[2];
+                        r2 = r2 + zz;
+                    }
+                    float t = r2 / p->R2;
+                    float q = 1.0f - t;
+                    u = p->u0 * q;
+                }
+            }
+            S->vx[j] = u * p->Q[0];
+            S->vy[j] = u * p->Q[1];
+            if (dim == 3) S->vz[j] = u * p->Q[2];
+        }
     }
     return 0;
 }

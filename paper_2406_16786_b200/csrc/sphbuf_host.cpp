@@ -500,6 +500,8 @@ sph_status sph_buffer_register(sph_ctx *c, sph_particles *p, const float origin[
         D.s[j] = (dim == 2 && j == 2) ? 0.f : prod;
     }
     D.kind = kind;
+    D.bc = SPH_BC_NONE;
+    D.rho_col = -1;
     // host geometry and this slab's runs (inflated by 1e-3 cs to absorb fp32 rounding)
     PortHost P = make_port_host(origin, Q, he, c->grid.cs, dim, 0.0);
     PortHost Pi = make_port_host(origin, Q, he, c->grid.cs, dim, 1e-3 * (double)c->grid.cs);
@@ -531,6 +533,38 @@ sph_status sph_buffer_register(sph_ctx *c, sph_particles *p, const float origin[
     e = launch_register(part_dev(p), c->gd, c->pt, k, reinterpret_cast<long long *>(members_out_dev), s, &c->L);
     if (e != cudaSuccess) return cuda_fail(c, e, "register: identification kernel");
     if (port_id_out) *port_id_out = k;
+    return SPH_OK;
+}
+
+sph_status sph_port_set_bc(sph_ctx *c, int32_t port_id, const sph_bc *bc)
+{
+    if (!c || !bc) return SPH_ERR_ARG;
+    if (port_id < 0 || port_id >= c->pt.n) return fail(c, SPH_ERR_ARG, "unknown port");
+    PortDev &D = c->pt.p[port_id];
+    if (bc->kind == SPH_BC_NONE) {
+        D.bc = SPH_BC_NONE;
+        return SPH_OK;
+    }
+    if (bc->kind == SPH_BC_PRESSURE) {
+        if (!(bc->c0 > 0.f) || bc->rho_column < -1 || bc->rho_column >= c->n_extra)
+            return fail(c, SPH_ERR_ARG, "pressure BC: c0 <= 0 or bad density column");
+        D.rho_col = bc->rho_column;
+        // Eq. postulate-density, formed in f64, rounded once
+        D.rho_b = (float)((double)bc->rho0 + (double)bc->p_b / ((double)bc->c0 * (double)bc->c0));
+    } else if (bc->kind == SPH_BC_VELOCITY) {
+        if (bc->profile < SPH_PROFILE_PLUG || bc->profile > SPH_PROFILE_PARABOLIC_RADIAL)
+            return fail(c, SPH_ERR_ARG, "velocity BC: bad profile");
+        if (bc->profile != SPH_PROFILE_PLUG && !(bc->radius > 0.f))
+            return fail(c, SPH_ERR_ARG, "velocity BC: radius <= 0");
+        D.profile = bc->profile;
+        D.u0 = bc->u0;
+        D.R = bc->radius;
+        volatile float r2 = bc->radius * bc->radius;
+        D.R2 = r2;
+    } else {
+        return fail(c, SPH_ERR_ARG, "bad BC kind");
+    }
+    D.bc = bc->kind;
     return SPH_OK;
 }
 

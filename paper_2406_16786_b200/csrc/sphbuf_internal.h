@@ -40,7 +40,13 @@ struct PortDev {
     float heP[3];    // fl(he + cs): decision region P_k (reading R4)
     float s[3];      // recycle shift fl(a * u)
     int kind;
-    int pad;
+    int bc;          // sph_bc_kind
+    int profile;     // sph_profile_kind
+    int rho_col;     // extra column of the density (-1 none)
+    float rho_b;     // fl32(rho0 + p_b / c0^2), formed in f64
+    float u0;        // velocity BC speed scale
+    float R;         // profile radius
+    float R2;        // fl(R * R)
 };
 
 struct PortTable {

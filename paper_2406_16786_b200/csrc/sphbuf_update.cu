@@ -119,12 +119,13 @@ __global__ void __launch_bounds__(kThreads) k_upd_main(PartDev p, int dim, const
         __syncthreads();
         const long long tile = s_tile;
         if (tile >= ntiles || tile >= ws.upd_tiles) break;
-        bool cr[kUpdItems];
+        bool cr[kUpdItems], bcm[kUpdItems];
         int pidx[kUpdItems], kk[kUpdItems];
-        float ox[kUpdItems], oy[kUpdItems], oz[kUpdItems];
+        float ox[kUpdItems], oy[kUpdItems], oz[kUpdItems], bY[kUpdItems], bZ[kUpdItems];
 #pragma unroll
         for (int it = 0; it < kUpdItems; ++it) {
             cr[it] = false;
+            bcm[it] = false;
             pidx[it] = -1;
             kk[it] = 0;
             ox[it] = oy[it] = oz[it] = 0.0f;
@@ -174,28 +175,34 @@ __global__ void __launch_bounds__(kThreads) k_upd_main(PartDev p, int dim, const
                     p.z[pi] = pz;
                 }
                 cr[it] = true;
-                pidx[it] = pi;
-                kk[it] = k;
                 ox[it] = x;
                 oy[it] = y;
                 oz[it] = z;
                 atomicAdd(&port_counts[k], 1);
             }
+            pidx[it] = pi;
+            kk[it] = k;
+            float Xp[3] = {X[0], X[1], X[2]};
+            if (create) to_local(P, dim, px, py, pz, Xp);      // post-recycle local frame
+            bool fin = member;                                 // a buffer particle of k after the update
             if (del) {
                 p.label[pi] = -2;                                // tombstone, removed by sph_compact
                 atomicAdd(&port_counts[max_ports + k], 1);
                 ++del_cnt;
                 del_min = pi < del_min ? pi : del_min;
+                fin = false;
             } else if (P.kind != SPH_INLET) {
                 // relabel on post-recycle positions (R9)
-                float Xp[3] = {X[0], X[1], X[2]};
-                if (create) to_local(P, dim, px, py, pz, Xp);
-                if (in_box(Xp, P.he, dim)) {
+                fin = in_box(Xp, P.he, dim);
+                if (fin) {
                     if (lab != k) p.label[pi] = k;
                 } else if (lab == k) {
                     p.label[pi] = -1;
                 }
             }
+            bcm[it] = fin && P.bc != SPH_BC_NONE;
+            bY[it] = Xp[1];
+            bZ[it] = Xp[2];
         }
         unsigned excl[kUpdItems], total;
         striped_scan<kThreads, kUpdItems>(cr, excl, total, s_warp);
@@ -225,6 +232,36 @@ __global__ void __launch_bounds__(kThreads) k_upd_main(PartDev p, int dim, const
             } else {
                 atomicOr(&ctr->status, kStStaging);
             }
+        }
+        // boundary-condition state of the port's buffer particles, after the duplicates
+        // were staged with the pre-BC state (paper §IV)
+#pragma unroll
+        for (int it = 0; it < kUpdItems; ++it) {
+            if (!bcm[it]) continue;
+            const int pi = pidx[it];
+            const PortDev &P = s_ports[kk[it]];
+            float u;
+            if (P.bc == SPH_BC_PRESSURE) {
+                // v <- (v.u) u (Eq. velocity_correction)
+                u = __fadd_rn(__fmul_rn(p.vx[pi], P.Q[0]), __fmul_rn(p.vy[pi], P.Q[1]));
+                if (dim == 3) u = __fadd_rn(u, __fmul_rn(p.vz[pi], P.Q[2]));
+                // recycled particles: rho = rho0 + p_b / c0^2 (Eq. postulate-density)
+                if (cr[it] && P.rho_col >= 0) p.extra[P.rho_col][pi] = P.rho_b;
+            } else {
+                // v_X' from the profile (Eqs. 2D/3D_velocity_profile), v = Q^T (v_X', 0, 0)
+                u = P.u0;
+                if (P.profile == SPH_PROFILE_PARABOLIC) {
+                    const float t = __fdiv_rn(bY[it], P.R);
+                    u = __fmul_rn(P.u0, __fsub_rn(1.0f, __fmul_rn(t, t)));
+                } else if (P.profile == SPH_PROFILE_PARABOLIC_RADIAL) {
+                    float r2 = __fmul_rn(bY[it], bY[it]);
+                    if (dim == 3) r2 = __fadd_rn(r2, __fmul_rn(bZ[it], bZ[it]));
+                    u = __fmul_rn(P.u0, __fsub_rn(1.0f, __fdiv_rn(r2, P.R2)));
+                }
+            }
+            p.vx[pi] = __fmul_rn(u, P.Q[0]);
+            p.vy[pi] = __fmul_rn(u, P.Q[1]);
+            if (dim == 3) p.vz[pi] = __fmul_rn(u, P.Q[2]);
         }
         if (tile == ntiles - 1 && threadIdx.x == 0) ctr->n_stage = (long long)s_prefix + total;
         __syncthreads();

@@ -38,6 +38,23 @@ def f32(v: float) -> float:
     return float(np.float32(v))
 
 
+BC_NONE, BC_PRESSURE, BC_VELOCITY = 0, 1, 2
+PROFILE_PLUG, PROFILE_PARABOLIC, PROFILE_PARABOLIC_RADIAL = 0, 1, 2
+
+
+@dataclass
+class BC:
+    """Boundary-condition parameters of a port (paper §IV), as plain data."""
+    kind: int = BC_NONE
+    rho0: float = 1.0
+    c0: float = 10.0
+    p_b: float = 0.0
+    rho_column: int = -1
+    profile: int = PROFILE_PLUG
+    u0: float = 1.0
+    radius: float = 1.0
+
+
 @dataclass
 class Port:
     origin: tuple            # O' (global), binary32 values
@@ -45,6 +62,7 @@ class Port:
     half_extents: tuple      # (a/2, b/2, c/2)
     kind: int                # INLET / OUTLET / BIDIRECTIONAL
     layers: int
+    bc: BC = None            # optional boundary condition of its buffer particles
 
 
 @dataclass

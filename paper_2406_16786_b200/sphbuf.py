@@ -43,6 +43,11 @@ class sph_particles(C.Structure):
                 ("label", C.c_void_p), ("n_dev", C.c_void_p), ("capacity", C.c_int64)]
 
 
+class sph_bc(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("rho0", C.c_float), ("c0", C.c_float), ("p_b", C.c_float),
+                ("rho_column", C.c_int32), ("profile", C.c_int32), ("u0", C.c_float), ("radius", C.c_float)]
+
+
 class sph_stats(C.Structure):
     _fields_ = [("n", C.c_int64), ("candidates", C.c_int64), ("created", C.c_int64), ("deleted", C.c_int64),
                 ("checked_total", C.c_int64), ("out_of_grid", C.c_int64), ("motion_errors", C.c_int64),
@@ -55,7 +60,8 @@ EXPORTS = ["sph_ctx_create", "sph_ctx_destroy", "sph_last_error", "sph_workspace
            "sph_port_check", "sph_buffer_register", "sph_advect", "sph_cll_build", "sph_buffer_update",
            "sph_compact", "sph_migrate_record_floats", "sph_migrate_pack", "sph_migrate_unpack", "sph_status_sync",
            "sph_launch_count", "sph_port_cells", "sph_frame_from_axis", "sph_profile", "sph_profile_read",
-           "sph_kernel_name", "sph_advect_cll_build", "sph_compact_deferred", "sph_cll_key", "sph_cll_finish"]
+           "sph_kernel_name", "sph_advect_cll_build", "sph_compact_deferred", "sph_cll_key", "sph_cll_finish",
+           "sph_port_set_bc"]
 NKERNELS = 14
 
 
@@ -84,6 +90,8 @@ def lib():
     L.sph_cll_build.argtypes = [vp, P(sph_particles), P(sph_particles), vp, vp, vp, vp]
     L.sph_advect_cll_build.argtypes = [vp, P(sph_particles), P(sph_particles), f32, vp, vp, vp, vp]
     L.sph_advect_cll_build.restype = C.c_int
+    L.sph_port_set_bc.argtypes = [vp, i32, P(sph_bc)]
+    L.sph_port_set_bc.restype = C.c_int
     L.sph_cll_key.argtypes = [vp, P(sph_particles), f32, i32, vp, vp, vp]
     L.sph_cll_key.restype = C.c_int
     L.sph_cll_finish.argtypes = [vp, P(sph_particles), P(sph_particles), vp, vp, vp, vp, vp, vp]
@@ -192,6 +200,14 @@ def sph_buffer_register(ctx, parts, origin, Q, half_extents, kind, layers, dp, m
     _check(lib().sph_buffer_register(ctx.h, C.byref(parts.abi), _f3(origin), _f9(Q), _f3(half_extents), int(kind),
                                      int(layers), float(dp), C.byref(pid), _ptr(members_out), _stream(stream)), ctx.h)
     return pid.value
+
+
+def sph_port_set_bc(ctx, port_id, bc):
+    """bc: an object with kind, rho0, c0, p_b, rho_column, profile, u0, radius (inputs.BC)."""
+    B = sph_bc()
+    for f, _ in sph_bc._fields_:
+        setattr(B, f, getattr(bc, f))
+    _check(lib().sph_port_set_bc(ctx.h, int(port_id), C.byref(B)), ctx.h)
 
 
 def sph_advect(ctx, parts, dt, stream=None):
@@ -383,6 +399,8 @@ class BufferUpdater:
             pid = sph_buffer_register(self.ctx, self.A, p.origin, p.Q, p.half_extents, p.kind, p.layers, self.dp,
                                       self.members[k:k + 1], stream)
             assert pid == k
+            if getattr(p, "bc", None) is not None and p.bc.kind:
+                sph_port_set_bc(self.ctx, k, p.bc)
         self.registered = True
 
     # --- one update (the hot path); nothing here synchronises
