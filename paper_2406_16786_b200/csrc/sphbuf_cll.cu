@@ -92,15 +92,12 @@ __global__ void __launch_bounds__(kThreads) k_cll_key(PartDev in, GridDev g, Wor
             key[it] = -1;
             if (i < n) {
                 if (Advect) {
-                    // driver step fused in: x <- fl(x + fl(v dt))
-                    x[it] = __fadd_rn(x[it], __fmul_rn(vx[it], dt));
-                    y[it] = __fadd_rn(y[it], __fmul_rn(vy[it], dt));
-                    in.x[i] = x[it];
-                    in.y[i] = y[it];
-                    if (g.dim == 3) {
-                        z[it] = __fadd_rn(z[it], __fmul_rn(vz[it], dt));
-                        in.z[i] = z[it];
-                    }
+                    // driver step fused in: x <- fl(x + fl(v dt)), kept in registers
+                    // for the key; the gather recomputes it bit-identically when it
+                    // moves the particle, so `in` is never written here
+                    x[it] = advect1(x[it], vx[it], dt);
+                    y[it] = advect1(y[it], vy[it], dt);
+                    if (g.dim == 3) z[it] = advect1(z[it], vz[it], dt);
                 }
                 if (lab[it] > -2) {
                     if (Migrate) {
@@ -192,9 +189,12 @@ __global__ void __launch_bounds__(kThreads) k_cll_unpack_key(PartDev in, GridDev
     if ((threadIdx.x & 31) == 0 && o) atomicAdd((unsigned long long *)&ctr->out_of_grid, (unsigned long long)o);
 }
 
+// K2: kCellItems cells per thread (kCellTile per block: one wave of blocks even
+// at C5's 8.5M cells, so the look-back chain never waits on an unlaunched tile).
 __global__ void __launch_bounds__(kThreads) k_cell_scan(GridDev g, Workspace ws, int *cell_start, int *cell_end,
                                                         long long *n_out, long long ntiles)
 {
+    constexpr int V = kCellItems / 4;
     __shared__ unsigned s_warp[kThreads / 32 + 1];
     __shared__ long long s_tile;
     __shared__ unsigned s_prefix;
@@ -205,23 +205,27 @@ __global__ void __launch_bounds__(kThreads) k_cell_scan(GridDev g, Workspace ws,
     const unsigned epoch = ctr->epoch_cll;
     const long long nc = g.ncells;
     const long long base = tile * kCellTile + (long long)threadIdx.x * kCellItems;
-    int c[kCellItems];
-    if (base + kCellItems <= nc) {
+    const bool full = base + kCellItems <= nc;
+    int4 c[V];
+    if (full) {
         int4 *pc = reinterpret_cast<int4 *>(ws.cell_count + base);
-        int4 a = pc[0], b = pc[1];
-        c[0] = a.x; c[1] = a.y; c[2] = a.z; c[3] = a.w; c[4] = b.x; c[5] = b.y; c[6] = b.z; c[7] = b.w;
-        pc[0] = make_int4(0, 0, 0, 0);
-        pc[1] = make_int4(0, 0, 0, 0);
+#pragma unroll
+        for (int v = 0; v < V; ++v) c[v] = pc[v];
+#pragma unroll
+        for (int v = 0; v < V; ++v) pc[v] = make_int4(0, 0, 0, 0);
     } else {
+        int t[kCellItems];
 #pragma unroll
         for (int j = 0; j < kCellItems; ++j) {
-            c[j] = (base + j < nc) ? ws.cell_count[base + j] : 0;
+            t[j] = (base + j < nc) ? ws.cell_count[base + j] : 0;
             if (base + j < nc) ws.cell_count[base + j] = 0;
         }
+#pragma unroll
+        for (int v = 0; v < V; ++v) c[v] = make_int4(t[4 * v], t[4 * v + 1], t[4 * v + 2], t[4 * v + 3]);
     }
     unsigned sum = 0;
 #pragma unroll
-    for (int j = 0; j < kCellItems; ++j) sum += (unsigned)c[j];
+    for (int v = 0; v < V; ++v) sum += (unsigned)(c[v].x + c[v].y + c[v].z + c[v].w);
     unsigned total;
     const unsigned excl = block_excl_scan<kThreads>(sum, total, s_warp);
     if (threadIdx.x < 32) {
@@ -231,33 +235,40 @@ __global__ void __launch_bounds__(kThreads) k_cell_scan(GridDev g, Workspace ws,
     __syncthreads();
     const unsigned prefix = s_prefix;
     int run = (int)(prefix + excl);
-    int st[kCellItems], en[kCellItems];
-#pragma unroll
-    for (int j = 0; j < kCellItems; ++j) {
-        st[j] = run;
-        run += c[j];
-        en[j] = run;
-    }
-    if (base + kCellItems <= nc) {
+    if (full) {
         int4 *ps = reinterpret_cast<int4 *>(cell_start + base);
         int4 *pe = reinterpret_cast<int4 *>(cell_end + base);
-        ps[0] = make_int4(st[0], st[1], st[2], st[3]);
-        ps[1] = make_int4(st[4], st[5], st[6], st[7]);
-        pe[0] = make_int4(en[0], en[1], en[2], en[3]);
-        pe[1] = make_int4(en[4], en[5], en[6], en[7]);
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            int4 st, en;
+            st.x = run; run += c[v].x; en.x = run;
+            st.y = run; run += c[v].y; en.y = run;
+            st.z = run; run += c[v].z; en.z = run;
+            st.w = run; run += c[v].w; en.w = run;
+            ps[v] = st;
+            pe[v] = en;
+        }
     } else {
 #pragma unroll
-        for (int j = 0; j < kCellItems; ++j)
-            if (base + j < nc) {
-                cell_start[base + j] = st[j];
-                cell_end[base + j] = en[j];
+        for (int v = 0; v < V; ++v) {
+            const int cv[4] = {c[v].x, c[v].y, c[v].z, c[v].w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const long long j = base + 4 * v + q;
+                if (j < nc) {
+                    cell_start[j] = run;
+                    cell_end[j] = run + cv[q];
+                }
+                run += cv[q];
             }
+        }
     }
     if (tile == ntiles - 1 && threadIdx.x == 0) *n_out = (long long)(prefix + total);
 }
 
 constexpr int kScatterItems = 4;
 
+// K3: source index of every sorted slot (slot = cell_start[key] + atomic rank).
 __global__ void __launch_bounds__(kThreads) k_cll_scatter(Workspace ws, const int *cell_start, int *perm)
 {
     const long long n = ws.ctr->n_in;
@@ -277,64 +288,83 @@ __global__ void __launch_bounds__(kThreads) k_cll_scatter(Workspace ws, const in
         for (int it = 0; it < kScatterItems; ++it) {
             const long long i = base + it * kThreads + threadIdx.x;
             if (i >= n) continue;
-            if (key[it] >= 0) ws.pair[cell_start[key[it]] + rk[it]] = make_int2((int)i, key[it]);
+            if (key[it] >= 0) ws.src[__ldg(cell_start + key[it]) + rk[it]] = (int)i;
             else if (perm) perm[i] = -1;                          // tombstone: dropped
         }
     }
 }
 
-// K4: one round of loads per output slot (the source's columns and its cell's
-// range, all independent), the rank by id among the cell's slots from ids staged
-// in shared memory (slots of a cell that straddles the tile edge are read from
-// global memory), and the store into the sorted position.  Loads are nearly
-// sequential (only particles that changed cell come from far away); stores stay
-// inside the cell.
+// K4: per output slot, one round of independent loads of the source's columns;
+// the (advected, when the build fused the driver's advection) position gives the
+// cell again by the pinned formula of K1, hence the cell's slot range; the rank
+// by id among the cell's slots comes from ids staged in shared memory (slots of
+// a cell that straddles the tile edge are read from global memory); the store
+// goes to the sorted position.  Loads are nearly sequential (only particles that
+// changed cell come from far away); stores stay inside the cell.
 template <bool HasExtra, int ITEMS, int MINB>
-__global__ void __launch_bounds__(kThreads, MINB) k_cll_gather(PartDev in, PartDev out, int dim, Workspace ws,
-                                                         const int *cell_start, const int *cell_end, int *perm)
+__global__ void __launch_bounds__(kThreads, MINB) k_cll_gather(PartDev in, PartDev out, GridDev g, Workspace ws,
+                                                               const int *cell_start, const int *cell_end, int *perm,
+                                                               int advect, float dt)
 {
-    __shared__ long long s_id[(kThreads * ITEMS)];
+    constexpr int T = kThreads * ITEMS;
+    __shared__ long long s_id[T];
     const long long n = *out.n;
-    for (long long j0 = (long long)blockIdx.x * (kThreads * ITEMS); j0 < n; j0 += (long long)gridDim.x * (kThreads * ITEMS)) {
+    const int dim = g.dim;
+    // sources below mig_base are this slab's own particles (advected here when the
+    // build fused the advection); received migrants were advected by their sender
+    const long long adv_lim = advect ? ws.ctr->mig_base : 0;
+    for (long long j0 = (long long)blockIdx.x * T; j0 < n; j0 += (long long)gridDim.x * T) {
         int src[ITEMS], cb[ITEMS], ce[ITEMS], lab[ITEMS];
-        float x[ITEMS], y[ITEMS], z[ITEMS], vx[ITEMS], vy[ITEMS],
-            vz[ITEMS];
+        float x[ITEMS], y[ITEMS], z[ITEMS], vx[ITEMS], vy[ITEMS], vz[ITEMS];
         long long id[ITEMS];
-        int2 pr[ITEMS];
 #pragma unroll
         for (int it = 0; it < ITEMS; ++it) {
             const long long j = j0 + it * kThreads + threadIdx.x;
-            pr[it] = j < n ? ws.pair[j] : make_int2(-1, -1);
+            src[it] = j < n ? ws.src[j] : -1;
         }
 #pragma unroll
         for (int it = 0; it < ITEMS; ++it) {
-            src[it] = pr[it].x;
             if (src[it] < 0) continue;
             const int s = src[it];
-            cb[it] = cell_start[pr[it].y];
-            ce[it] = cell_end[pr[it].y];
             x[it] = in.x[s];
             y[it] = in.y[s];
             vx[it] = in.vx[s];
             vy[it] = in.vy[s];
+            z[it] = 0.0f;
             if (dim == 3) {
                 z[it] = in.z[s];
                 vz[it] = in.vz[s];
             }
             id[it] = in.id[s];
             lab[it] = in.label[s];
+        }
+#pragma unroll
+        for (int it = 0; it < ITEMS; ++it) {
+            if (src[it] < 0) continue;
+            if (src[it] < adv_lim) {
+                x[it] = advect1(x[it], vx[it], dt);
+                y[it] = advect1(y[it], vy[it], dt);
+                if (dim == 3) z[it] = advect1(z[it], vz[it], dt);
+            }
+            int oob = 0;
+            const int key = cell_of(g, x[it], y[it], z[it], oob);
+            cb[it] = __ldg(cell_start + key);
+            ce[it] = __ldg(cell_end + key);
             s_id[it * kThreads + threadIdx.x] = id[it];
         }
         __syncthreads();
 #pragma unroll
         for (int it = 0; it < ITEMS; ++it) {
             if (src[it] < 0) continue;
+            // slot indices fit in int32 (cell tables are int32)
+            const int t0 = (int)j0;
+            const int a = max(cb[it] - t0, 0), b = min(ce[it] - t0, T);
+            const long long me = id[it];
             int r = 0;
-            const long long lo = cb[it] > j0 ? cb[it] : j0;
-            const long long hi = ce[it] < j0 + (kThreads * ITEMS) ? ce[it] : j0 + (kThreads * ITEMS);
-            for (long long q = lo; q < hi; ++q) r += (s_id[q - j0] < id[it]);
-            for (long long q = cb[it]; q < lo; ++q) r += (in.id[ws.pair[q].x] < id[it]);
-            for (long long q = hi; q < ce[it]; ++q) r += (in.id[ws.pair[q].x] < id[it]);
+#pragma unroll 4
+            for (int q = a; q < b; ++q) r += (s_id[q] < me);
+            for (int q = cb[it]; q < t0 + a; ++q) r += (in.id[ws.src[q]] < me);
+            for (int q = t0 + b; q < ce[it]; ++q) r += (in.id[ws.src[q]] < me);
             const int d = cb[it] + r;
             out.x[d] = x[it];
             out.y[d] = y[it];
@@ -391,13 +421,14 @@ cudaError_t launch_cll(const PartDev &in, const PartDev &out, const GridDev &g, 
 {
     cudaError_t e = launch_cll_key(in, g, ws, dt, advect, nullptr, nullptr, 0, 0, s, L);
     if (e != cudaSuccess) return e;
-    return launch_cll_finish(in, out, g, ws, nullptr, nullptr, 0, 0, cell_start, cell_end, perm, s, L);
+    return launch_cll_finish(in, out, g, ws, nullptr, nullptr, 0, 0, cell_start, cell_end, perm, advect, dt, s, L);
 }
 
 cudaError_t launch_cll_finish(const PartDev &in, const PartDev &out, const GridDev &g, const Workspace &ws,
                               const float *recv_lo, const float *recv_hi, long long maxm, int rec, int *cell_start,
-                              int *cell_end, int *perm, cudaStream_t s, Launch *L)
+                              int *cell_end, int *perm, bool advect_b, float dt, cudaStream_t s, Launch *L)
 {
+    const int advect = advect_b ? 1 : 0;
     const long long ntiles = (g.ncells + kCellTile - 1) / kCellTile;
     const long long cap = in.cap;
     if (recv_lo || recv_hi) {
@@ -422,13 +453,13 @@ cudaError_t launch_cll_finish(const PartDev &in, const PartDev &out, const GridD
     if (in.n_extra > 0) {
         static int grid = 0;
         if (!grid) grid = occ_grid(k_cll_gather<true, 3, 4>, kThreads);
-        k_cll_gather<true, 3, 4><<<cap_grid(grid, cap, kThreads * 3), kThreads, 0, s>>>(in, out, g.dim, ws, cell_start,
-                                                                                         cell_end, perm);
+        k_cll_gather<true, 3, 4><<<cap_grid(grid, cap, kThreads * 3), kThreads, 0, s>>>(in, out, g, ws, cell_start,
+                                                                                         cell_end, perm, advect, dt);
     } else {
         static int grid = 0;
         if (!grid) grid = occ_grid(k_cll_gather<false, 3, 4>, kThreads);
-        k_cll_gather<false, 3, 4><<<cap_grid(grid, cap, kThreads * 3), kThreads, 0, s>>>(in, out, g.dim, ws,
-                                                                                          cell_start, cell_end, perm);
+        k_cll_gather<false, 3, 4><<<cap_grid(grid, cap, kThreads * 3), kThreads, 0, s>>>(in, out, g, ws, cell_start,
+                                                                                          cell_end, perm, advect, dt);
     }
     L->after(s, KID_CLL_GATHER);
     return cudaGetLastError();

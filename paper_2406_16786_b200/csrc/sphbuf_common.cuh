@@ -234,6 +234,9 @@ __device__ __forceinline__ bool in_box(const float X[3], const float he[3], int 
     return r;
 }
 
+// Pinned advection (the driver step): x <- fl(x + fl(v dt)).
+__device__ __forceinline__ float advect1(float x, float v, float dt) { return __fadd_rn(x, __fmul_rn(v, dt)); }
+
 // Pinned cell index along one axis: floor(fl(fl(x - lo) * inv_cs)), clamped.
 __device__ __forceinline__ int cell_axis(float x, float lo, float inv, int lo_c, int hi_c, int &oob)
 {

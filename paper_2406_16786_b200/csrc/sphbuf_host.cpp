@@ -92,6 +92,9 @@ struct sph_ctx {
     Workspace W{};
     Launch L;
     std::string err;
+    // advection of the last sph_cll_key, applied by the gather of sph_cll_finish
+    bool key_advect = false;
+    float key_dt = 0.f;
 };
 
 namespace {
@@ -135,8 +138,7 @@ size_t layout(const sph_ctx *c, char *base, Workspace *W)
     w.sub_off = (unsigned *)take(4 * cmp_subs);
     w.key = (int *)take(sizeof(int) * cap);
     w.rank = (int *)take(sizeof(int) * cap);
-    w.pair = (int2 *)take(sizeof(int2) * cap);
-    w.dst = (int *)take(sizeof(int) * cap);
+    w.src = (int *)take(sizeof(int) * cap);
     const long long mn = c->max_new;
     w.sx = (float *)take(4 * mn);
     w.sy = (float *)take(4 * mn);
@@ -613,6 +615,8 @@ sph_status sph_cll_key(sph_ctx *c, sph_particles *in, float dt, int32_t advect, 
     sph_status st = check_particles(c, in);
     if (st != SPH_OK) return st;
     if ((send_lo == nullptr) != (send_hi == nullptr)) return fail(c, SPH_ERR_ARG, "give both send buffers or none");
+    c->key_advect = advect != 0;
+    c->key_dt = dt;
     cudaError_t e = launch_cll_key(part_dev(in), c->gd, c->W, dt, advect != 0, send_lo, send_hi, c->max_migrate,
                                    sph_migrate_record_floats(c), static_cast<cudaStream_t>(stream), &c->L);
     return e == cudaSuccess ? SPH_OK : cuda_fail(c, e, "cll_key");
@@ -631,8 +635,8 @@ sph_status sph_cll_finish(sph_ctx *c, sph_particles *in, sph_particles *out, con
     if ((reinterpret_cast<size_t>(cell_start) | reinterpret_cast<size_t>(cell_end)) % 16)
         return fail(c, SPH_ERR_ARG, "cell tables must be 16-byte aligned");
     cudaError_t e = launch_cll_finish(part_dev(in), part_dev(out), c->gd, c->W, recv_lo, recv_hi, c->max_migrate,
-                                      sph_migrate_record_floats(c), cell_start, cell_end, perm,
-                                      static_cast<cudaStream_t>(stream), &c->L);
+                                      sph_migrate_record_floats(c), cell_start, cell_end, perm, c->key_advect,
+                                      c->key_dt, static_cast<cudaStream_t>(stream), &c->L);
     return e == cudaSuccess ? SPH_OK : cuda_fail(c, e, "cll_finish");
 }
 

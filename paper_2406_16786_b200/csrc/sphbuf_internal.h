@@ -14,7 +14,7 @@ namespace sphbuf {
 
 // ---------------------------------------------------------------- tiling
 constexpr int kThreads = 256;            // block size of the O(N) kernels
-constexpr int kCellItems = 8;            // cells per thread in the cell scan
+constexpr int kCellItems = 32;           // cells per thread in the cell scan (multiple of 4)
 constexpr int kCellTile = kThreads * kCellItems;
 constexpr int kUpdItems = 2;             // candidates per thread in the update
 constexpr int kUpdTile = kThreads * kUpdItems;
@@ -100,8 +100,7 @@ struct Workspace {
     unsigned long long *tile_cells;  // [cell tiles]
     int *key;                        // [capacity]
     int *rank;                       // [capacity]
-    int2 *pair;                      // [capacity]: (source index, cell) per sorted slot
-    int *dst;                        // [capacity]: sorted position of each input particle (-1 dropped)
+    int *src;                        // [capacity]: source index of each sorted slot
     unsigned long long *tile_upd;    // [upd tiles]
     unsigned long long *tile_cmp;    // [cmp count tiles]
     unsigned *sub_off;               // [cmp sub-tiles]: tombstones before each sub-tile
@@ -146,11 +145,13 @@ cudaError_t launch_register(const PartDev &p, const GridDev &g, const PortTable 
                             cudaStream_t s, Launch *L);
 cudaError_t launch_cll(const PartDev &in, const PartDev &out, const GridDev &g, const Workspace &ws,
                        int *cell_start, int *cell_end, int *perm, float dt, bool advect, cudaStream_t s, Launch *L);
+// advect / dt: the advection of the key pass (launch_cll_key) that this build
+// finishes; the gather applies it to the slab's own particles as it moves them.
 cudaError_t launch_cll_key(const PartDev &in, const GridDev &g, const Workspace &ws, float dt, bool advect,
                            float *send_lo, float *send_hi, long long maxm, int rec, cudaStream_t s, Launch *L);
 cudaError_t launch_cll_finish(const PartDev &in, const PartDev &out, const GridDev &g, const Workspace &ws,
                               const float *recv_lo, const float *recv_hi, long long maxm, int rec, int *cell_start,
-                              int *cell_end, int *perm, cudaStream_t s, Launch *L);
+                              int *cell_end, int *perm, bool advect, float dt, cudaStream_t s, Launch *L);
 cudaError_t launch_update(const PartDev &p, const GridDev &g, const PortTable &pt, const Workspace &ws, int n_runs,
                           const int *cell_start, const int *cell_end, int *port_counts, cudaStream_t s,
                           Launch *L);
