@@ -13,6 +13,8 @@
 //                    memory, store into the sorted position.
 #include <climits>
 #include <cstdint>
+#include <cstdlib>
+#include <cstring>
 
 #include "sphbuf_common.cuh"
 
@@ -294,20 +296,41 @@ __global__ void __launch_bounds__(kThreads) k_cll_scatter(Workspace ws, const in
     }
 }
 
-// K4: per output slot, one round of independent loads of the source's columns;
-// the (advected, when the build fused the driver's advection) position gives the
-// cell again by the pinned formula of K1, hence the cell's slot range; the rank
-// by id among the cell's slots comes from ids staged in shared memory (slots of
-// a cell that straddles the tile edge are read from global memory); the store
-// goes to the sorted position.  Loads are nearly sequential (only particles that
-// changed cell come from far away); stores stay inside the cell.
+constexpr int kHalo = 64;   // slots staged on either side of a gather tile
+
+// Rank by id of slot p (id me) among its cell's slots [cb, ce).  The ids of the
+// slots [w0, w1) are in shared memory at sid[q - w0]; a cell reaching past them
+// (more than kHalo slots outside the tile) reads the rest from global memory.
+__device__ __forceinline__ int rank_in_cell(const PartDev &in, const Workspace &ws, const long long *sid, int w0,
+                                            int w1, int cb, int ce, long long me)
+{
+    int r = 0;
+    if (cb >= w0 && ce <= w1) {
+        const long long *sc = sid - w0;
+#pragma unroll 4
+        for (int q = cb; q < ce; ++q) r += (sc[q] < me);
+        return r;
+    }
+    for (int q = cb; q < ce; ++q) r += (((q >= w0 && q < w1) ? sid[q - w0] : in.id[ws.src[q]]) < me);
+    return r;
+}
+
+// K4: one round of independent loads per output slot (all columns of the
+// source); the (advected, when the build fused the driver's advection) position
+// gives the cell again by the pinned formula of K1, hence the cell's slot range;
+// the rank by id among the cell's slots comes from ids staged in shared memory —
+// the tile's and kHalo slots on either side, so a cell straddling the tile edge
+// is ranked from shared memory as well; the store goes to the sorted position.
+// Loads are nearly sequential (only particles that changed cell come from far
+// away); stores stay inside the cell.
 template <bool HasExtra, int ITEMS, int MINB>
 __global__ void __launch_bounds__(kThreads, MINB) k_cll_gather(PartDev in, PartDev out, GridDev g, Workspace ws,
                                                                const int *cell_start, const int *cell_end, int *perm,
                                                                int advect, float dt)
 {
     constexpr int T = kThreads * ITEMS;
-    __shared__ long long s_id[T];
+    static_assert(2 * kHalo <= kThreads, "one halo slot per thread");
+    __shared__ long long s_id[kHalo + T + kHalo];
     const long long n = *out.n;
     const int dim = g.dim;
     // sources below mig_base are this slab's own particles (advected here when the
@@ -317,11 +340,16 @@ __global__ void __launch_bounds__(kThreads, MINB) k_cll_gather(PartDev in, PartD
         int src[ITEMS], cb[ITEMS], ce[ITEMS], lab[ITEMS];
         float x[ITEMS], y[ITEMS], z[ITEMS], vx[ITEMS], vy[ITEMS], vz[ITEMS];
         long long id[ITEMS];
+        // halo ids (threads 0 .. 2 kHalo - 1): two dependent loads, issued first
+        const long long jh = threadIdx.x < kHalo ? j0 - kHalo + threadIdx.x : j0 + T + (threadIdx.x - kHalo);
+        const bool hv = threadIdx.x < 2 * kHalo && jh >= 0 && jh < n;
+        const int hsrc = hv ? ws.src[jh] : 0;
 #pragma unroll
         for (int it = 0; it < ITEMS; ++it) {
             const long long j = j0 + it * kThreads + threadIdx.x;
             src[it] = j < n ? ws.src[j] : -1;
         }
+        const long long hid = hv ? in.id[hsrc] : 0;
 #pragma unroll
         for (int it = 0; it < ITEMS; ++it) {
             if (src[it] < 0) continue;
@@ -338,6 +366,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_cll_gather(PartDev in, PartD
             id[it] = in.id[s];
             lab[it] = in.label[s];
         }
+        if (threadIdx.x < 2 * kHalo) s_id[threadIdx.x < kHalo ? threadIdx.x : T + threadIdx.x] = hid;
 #pragma unroll
         for (int it = 0; it < ITEMS; ++it) {
             if (src[it] < 0) continue;
@@ -350,22 +379,19 @@ __global__ void __launch_bounds__(kThreads, MINB) k_cll_gather(PartDev in, PartD
             const int key = cell_of(g, x[it], y[it], z[it], oob);
             cb[it] = __ldg(cell_start + key);
             ce[it] = __ldg(cell_end + key);
-            s_id[it * kThreads + threadIdx.x] = id[it];
+            s_id[kHalo + it * kThreads + threadIdx.x] = id[it];
         }
         __syncthreads();
+        // slot indices fit in int32 (cell tables are int32); staged window [w0, w1)
+        const int t0 = (int)j0;
+        const int w0 = t0 - kHalo > 0 ? t0 - kHalo : 0;
+        const int w1 = (long long)t0 + T + kHalo < n ? t0 + T + kHalo : (int)n;
+        const long long *sid = s_id + (w0 - (t0 - kHalo));
 #pragma unroll
         for (int it = 0; it < ITEMS; ++it) {
             if (src[it] < 0) continue;
-            // slot indices fit in int32 (cell tables are int32)
-            const int t0 = (int)j0;
-            const int a = max(cb[it] - t0, 0), b = min(ce[it] - t0, T);
             const long long me = id[it];
-            int r = 0;
-#pragma unroll 4
-            for (int q = a; q < b; ++q) r += (s_id[q] < me);
-            for (int q = cb[it]; q < t0 + a; ++q) r += (in.id[ws.src[q]] < me);
-            for (int q = t0 + b; q < ce[it]; ++q) r += (in.id[ws.src[q]] < me);
-            const int d = cb[it] + r;
+            const int d = cb[it] + rank_in_cell(in, ws, sid, w0, w1, cb[it], ce[it], me);
             out.x[d] = x[it];
             out.y[d] = y[it];
             out.vx[d] = vx[it];
@@ -376,7 +402,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_cll_gather(PartDev in, PartD
             }
             if (HasExtra)
                 for (int e = 0; e < in.n_extra; ++e) out.extra[e][d] = in.extra[e][src[it]];
-            out.id[d] = id[it];
+            out.id[d] = me;
             out.label[d] = lab[it];
             if (perm) perm[src[it]] = d;
         }
@@ -386,7 +412,53 @@ __global__ void __launch_bounds__(kThreads, MINB) k_cll_gather(PartDev in, PartD
 
 // ------------------------------------------------------------------ launchers
 
+// Gather variants (template instances), chosen by SPHBUF_GATHER=<slots>:<min blocks>
+// for tuning runs (tools/gather_sweep.py); the default is the measured best.
+template <bool HasExtra, int ITEMS, int MINB>
+static void gather_fused(const PartDev &in, const PartDev &out, const GridDev &g, const Workspace &ws,
+                         const int *cs, const int *ce, int *perm, int advect, float dt, long long cap, cudaStream_t s)
+{
+    static int grid = 0;
+    if (!grid) grid = occ_grid(k_cll_gather<HasExtra, ITEMS, MINB>, kThreads);
+    k_cll_gather<HasExtra, ITEMS, MINB><<<cap_grid(grid, cap, kThreads * ITEMS), kThreads, 0, s>>>(
+        in, out, g, ws, cs, ce, perm, advect, dt);
+}
+
+template <bool HasExtra>
+static void gather_variant(const char *v, const PartDev &in, const PartDev &out, const GridDev &g,
+                           const Workspace &ws, const int *cs, const int *ce, int *perm, int advect, float dt,
+                           long long cap, cudaStream_t s)
+{
+#define SPH_GV(name, I, M)                                                              \
+    if (!strcmp(v, name)) {                                                             \
+        gather_fused<HasExtra, I, M>(in, out, g, ws, cs, ce, perm, advect, dt, cap, s); \
+        return;                                                                         \
+    }
+    SPH_GV("1:8", 1, 8)
+    SPH_GV("3:4", 3, 4)
+    SPH_GV("2:8", 2, 8)
+    SPH_GV("4:3", 4, 3)
+    SPH_GV("4:4", 4, 4)
+#undef SPH_GV
+    // default: 2 slots per thread at <= 40 registers (6 blocks/SM), measured best
+    // on C5 among the variants above (tools/gather_sweep.py)
+    gather_fused<HasExtra, 2, 6>(in, out, g, ws, cs, ce, perm, advect, dt, cap, s);
+}
+
+static void launch_gather(const PartDev &in, const PartDev &out, const GridDev &g, const Workspace &ws,
+                          const int *cs, const int *ce, int *perm, int advect, float dt, long long cap, cudaStream_t s)
+{
+    static const char *v = nullptr;
+    if (!v) {
+        v = getenv("SPHBUF_GATHER");
+        if (!v) v = "";
+    }
+    if (in.n_extra > 0) gather_variant<true>(v, in, out, g, ws, cs, ce, perm, advect, dt, cap, s);
+    else gather_variant<false>(v, in, out, g, ws, cs, ce, perm, advect, dt, cap, s);
+}
+
 int sm_count() { return sm_count_cached(); }
+
 
 template <bool A, bool M>
 static void key_launch(const PartDev &in, const GridDev &g, const Workspace &ws, float dt, float *lo, float *hi,
@@ -448,19 +520,7 @@ cudaError_t launch_cll_finish(const PartDev &in, const PartDev &out, const GridD
         L->after(s, KID_CLL_SCATTER);
     }
     L->before(s);
-    // 3 slots per thread at <= 64 registers (4 blocks/SM): measured best on C5
-    // among 1-4 slots x 1-8 min blocks (profiles/r1_summary.md)
-    if (in.n_extra > 0) {
-        static int grid = 0;
-        if (!grid) grid = occ_grid(k_cll_gather<true, 3, 4>, kThreads);
-        k_cll_gather<true, 3, 4><<<cap_grid(grid, cap, kThreads * 3), kThreads, 0, s>>>(in, out, g, ws, cell_start,
-                                                                                         cell_end, perm, advect, dt);
-    } else {
-        static int grid = 0;
-        if (!grid) grid = occ_grid(k_cll_gather<false, 3, 4>, kThreads);
-        k_cll_gather<false, 3, 4><<<cap_grid(grid, cap, kThreads * 3), kThreads, 0, s>>>(in, out, g, ws, cell_start,
-                                                                                          cell_end, perm, advect, dt);
-    }
+    launch_gather(in, out, g, ws, cell_start, cell_end, perm, advect, dt, cap, s);
     L->after(s, KID_CLL_GATHER);
     return cudaGetLastError();
 }

@@ -237,14 +237,15 @@ __device__ __forceinline__ bool in_box(const float X[3], const float he[3], int 
 // Pinned advection (the driver step): x <- fl(x + fl(v dt)).
 __device__ __forceinline__ float advect1(float x, float v, float dt) { return __fadd_rn(x, __fmul_rn(v, dt)); }
 
-// Pinned cell index along one axis: floor(fl(fl(x - lo) * inv_cs)), clamped.
+// Pinned cell index along one axis: floor(fl(fl(x - lo) * inv_cs)), clamped
+// (branch-free: min/max of the floored value; oob is set when clamping changed it).
 __device__ __forceinline__ int cell_axis(float x, float lo, float inv, int lo_c, int hi_c, int &oob)
 {
     const float t = __fmul_rn(__fsub_rn(x, lo), inv);
     const float f = floorf(t);
-    if (f < (float)lo_c) { oob = 1; return lo_c; }
-    if (f > (float)(hi_c - 1)) { oob = 1; return hi_c - 1; }
-    return (int)f;
+    const float c = fminf(fmaxf(f, (float)lo_c), (float)(hi_c - 1));
+    oob |= (c != f);
+    return (int)c;
 }
 
 __device__ __forceinline__ int cell_of(const GridDev &g, float x, float y, float z, int &oob)
