@@ -301,11 +301,20 @@ constexpr int kHalo = 64;   // slots staged on either side of a gather tile
 // Rank by id of slot p (id me) among its cell's slots [cb, ce).  The ids of the
 // slots [w0, w1) are in shared memory at sid[q - w0]; a cell reaching past them
 // (more than kHalo slots outside the tile) reads the rest from global memory.
-__device__ __forceinline__ int rank_in_cell(const PartDev &in, const Workspace &ws, const long long *sid, int w0,
-                                            int w1, int cb, int ce, long long me)
+// narrow: every id of the window is below 2^32, and slo holds their low words.
+__device__ __forceinline__ int rank_in_cell(const PartDev &in, const Workspace &ws, const long long *sid,
+                                            const unsigned *slo, bool narrow, int w0, int w1, int cb, int ce,
+                                            long long me)
 {
     int r = 0;
     if (cb >= w0 && ce <= w1) {
+        if (narrow) {
+            const unsigned *sc = slo - w0;
+            const unsigned m32 = (unsigned)me;
+#pragma unroll 4
+            for (int q = cb; q < ce; ++q) r += (sc[q] < m32);
+            return r;
+        }
         const long long *sc = sid - w0;
 #pragma unroll 4
         for (int q = cb; q < ce; ++q) r += (sc[q] < me);
@@ -323,14 +332,15 @@ __device__ __forceinline__ int rank_in_cell(const PartDev &in, const Workspace &
 // is ranked from shared memory as well; the store goes to the sorted position.
 // Loads are nearly sequential (only particles that changed cell come from far
 // away); stores stay inside the cell.
-template <bool HasExtra, int ITEMS, int MINB>
-__global__ void __launch_bounds__(kThreads, MINB) k_cll_gather(PartDev in, PartDev out, GridDev g, Workspace ws,
+template <bool HasExtra, int ITEMS, int MINB, int NT = kThreads>
+__global__ void __launch_bounds__(NT, MINB) k_cll_gather(PartDev in, PartDev out, GridDev g, Workspace ws,
                                                                const int *cell_start, const int *cell_end, int *perm,
                                                                int advect, float dt)
 {
-    constexpr int T = kThreads * ITEMS;
-    static_assert(2 * kHalo <= kThreads, "one halo slot per thread");
+    constexpr int T = NT * ITEMS;
+    static_assert(2 * kHalo <= NT, "one halo slot per thread");
     __shared__ long long s_id[kHalo + T + kHalo];
+    __shared__ unsigned s_lo[kHalo + T + kHalo];
     const long long n = *out.n;
     const int dim = g.dim;
     // sources below mig_base are this slab's own particles (advected here when the
@@ -346,7 +356,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_cll_gather(PartDev in, PartD
         const int hsrc = hv ? ws.src[jh] : 0;
 #pragma unroll
         for (int it = 0; it < ITEMS; ++it) {
-            const long long j = j0 + it * kThreads + threadIdx.x;
+            const long long j = j0 + it * NT + threadIdx.x;
             src[it] = j < n ? ws.src[j] : -1;
         }
         const long long hid = hv ? in.id[hsrc] : 0;
@@ -366,7 +376,12 @@ __global__ void __launch_bounds__(kThreads, MINB) k_cll_gather(PartDev in, PartD
             id[it] = in.id[s];
             lab[it] = in.label[s];
         }
-        if (threadIdx.x < 2 * kHalo) s_id[threadIdx.x < kHalo ? threadIdx.x : T + threadIdx.x] = hid;
+        bool wide = hv && (hid >> 32) != 0;
+        if (threadIdx.x < 2 * kHalo) {
+            const int hq = threadIdx.x < kHalo ? threadIdx.x : T + threadIdx.x;
+            s_id[hq] = hid;
+            s_lo[hq] = (unsigned)hid;
+        }
 #pragma unroll
         for (int it = 0; it < ITEMS; ++it) {
             if (src[it] < 0) continue;
@@ -379,19 +394,23 @@ __global__ void __launch_bounds__(kThreads, MINB) k_cll_gather(PartDev in, PartD
             const int key = cell_of(g, x[it], y[it], z[it], oob);
             cb[it] = __ldg(cell_start + key);
             ce[it] = __ldg(cell_end + key);
-            s_id[kHalo + it * kThreads + threadIdx.x] = id[it];
+            s_id[kHalo + it * NT + threadIdx.x] = id[it];
+            s_lo[kHalo + it * NT + threadIdx.x] = (unsigned)id[it];
+            wide |= (id[it] >> 32) != 0;
         }
-        __syncthreads();
+        // 32-bit compares when no id of the window needs its high word
+        const bool narrow = !__syncthreads_or(wide);
         // slot indices fit in int32 (cell tables are int32); staged window [w0, w1)
         const int t0 = (int)j0;
         const int w0 = t0 - kHalo > 0 ? t0 - kHalo : 0;
         const int w1 = (long long)t0 + T + kHalo < n ? t0 + T + kHalo : (int)n;
         const long long *sid = s_id + (w0 - (t0 - kHalo));
+        const unsigned *slo = s_lo + (w0 - (t0 - kHalo));
 #pragma unroll
         for (int it = 0; it < ITEMS; ++it) {
             if (src[it] < 0) continue;
             const long long me = id[it];
-            const int d = cb[it] + rank_in_cell(in, ws, sid, w0, w1, cb[it], ce[it], me);
+            const int d = cb[it] + rank_in_cell(in, ws, sid, slo, narrow, w0, w1, cb[it], ce[it], me);
             out.x[d] = x[it];
             out.y[d] = y[it];
             out.vx[d] = vx[it];
@@ -414,14 +433,14 @@ __global__ void __launch_bounds__(kThreads, MINB) k_cll_gather(PartDev in, PartD
 
 // Gather variants (template instances), chosen by SPHBUF_GATHER=<slots>:<min blocks>
 // for tuning runs (tools/gather_sweep.py); the default is the measured best.
-template <bool HasExtra, int ITEMS, int MINB>
+template <bool HasExtra, int ITEMS, int MINB, int NT = kThreads>
 static void gather_fused(const PartDev &in, const PartDev &out, const GridDev &g, const Workspace &ws,
                          const int *cs, const int *ce, int *perm, int advect, float dt, long long cap, cudaStream_t s)
 {
     static int grid = 0;
-    if (!grid) grid = occ_grid(k_cll_gather<HasExtra, ITEMS, MINB>, kThreads);
-    k_cll_gather<HasExtra, ITEMS, MINB><<<cap_grid(grid, cap, kThreads * ITEMS), kThreads, 0, s>>>(
-        in, out, g, ws, cs, ce, perm, advect, dt);
+    if (!grid) grid = occ_grid(k_cll_gather<HasExtra, ITEMS, MINB, NT>, NT);
+    k_cll_gather<HasExtra, ITEMS, MINB, NT><<<cap_grid(grid, cap, NT * ITEMS), NT, 0, s>>>(in, out, g, ws, cs, ce,
+                                                                                         perm, advect, dt);
 }
 
 template <bool HasExtra>
@@ -441,7 +460,8 @@ static void gather_variant(const char *v, const PartDev &in, const PartDev &out,
     SPH_GV("4:4", 4, 4)
 #undef SPH_GV
     // default: 2 slots per thread at <= 40 registers (6 blocks/SM), measured best
-    // on C5 among the variants above (tools/gather_sweep.py)
+    // on C5 among the variants above and 128- / 512-thread blocks
+    // (tools/gather_sweep.py)
     gather_fused<HasExtra, 2, 6>(in, out, g, ws, cs, ce, perm, advect, dt, cap, s);
 }
 
