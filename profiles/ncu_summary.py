@@ -22,6 +22,8 @@ METRICS = [
     ("sm__warps_active.avg.pct_of_peak_sustained_active", "occupancy %"),
     ("launch__registers_per_thread", "regs"),
     ("smsp__thread_inst_executed_per_inst_executed.ratio", "threads/inst"),
+    ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue active %"),
+    ("smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio", "long-scoreboard stalls / issue"),
 ]
 
 
