@@ -163,6 +163,23 @@ typedef struct {
  * port port_id.  Host only; takes effect at the next sph_buffer_update. */
 sph_status sph_port_set_bc(sph_ctx *ctx, int32_t port_id, const sph_bc *bc);
 
+/* Moving port (rotating sprinkler, §V.C): re-establish port port_id
+ * at the pose (origin, Q) — e.g. theta = omega t + theta0 about a pivot,
+ * computed by the caller — after this step's generation in the old pose
+ * (Fig. rotation_procedure).  Every buffer particle of the port keeps its local
+ * coordinates and local velocity (reading R23):
+ *     x <- o1 + Q1^T (Q0 (x - o0)),  v <- Q1^T (Q0 v)      (pinned fp32)
+ * and the port's candidate cells are enumerated on the device for the new pose
+ * (the first move turns the port's runs into a fixed slice of one slot per cell
+ * column around its bounding sphere).  Half extents, kind and BC are kept.
+ * Call after sph_buffer_update with the same cell tables (the buffer particles
+ * are found among the port's candidates) and before the next sph_cll_build.
+ * Host-side errors, nothing enqueued: SPH_ERR_ARG (unknown port, NULL),
+ * SPH_ERR_NOT_ORTHONORMAL, SPH_ERR_OUT_OF_GRID, SPH_ERR_OVERLAP (the new P_k meets
+ * another port's). */
+sph_status sph_port_move(sph_ctx *ctx, sph_particles *p, int32_t port_id, const float origin[3], const float Q[9],
+                         const int32_t *cell_start, const int32_t *cell_end, void *stream);
+
 /* Driver step (not the method): x <- fl(x + fl(v dt)) per component. */
 sph_status sph_advect(sph_ctx *ctx, sph_particles *p, float dt, void *stream);
 

@@ -78,6 +78,8 @@ def lib():
         L.orc_port_cells.argtypes = [C.POINTER(Grid), C.POINTER(Port), C.c_void_p]
         L.orc_port_cells.restype = C.c_int64
         L.orc_advect.argtypes = [C.POINTER(State), C.c_int32, C.c_float]
+        L.orc_port_move.argtypes = [C.POINTER(State), C.c_int32, C.POINTER(Port), C.POINTER(Port), C.c_int32]
+        L.orc_port_move.restype = C.c_int64
         L.orc_register.argtypes = [C.POINTER(State), C.POINTER(Grid), C.POINTER(Port), C.c_int32, C.c_int32]
         L.orc_register.restype = C.c_int64
         L.orc_update.argtypes = [C.POINTER(Grid), C.POINTER(Port), C.c_int32, C.POINTER(State), C.c_int32,
@@ -250,6 +252,14 @@ def port_cells(grid, port) -> np.ndarray:
 def advect(st: dict, dim: int, dt: float):
     r = _StateRef(st)
     lib().orc_advect(C.byref(r.s), dim, dt)
+
+
+def port_move(st: dict, dim: int, port_from, port_to, k: int) -> int:
+    """Moving port (rotating sprinkler): the buffer particles of port k keep
+    their local coordinates and velocities from frame ``port_from`` to ``port_to``."""
+    r = _StateRef(st)
+    A, B = cport(port_from), cport(port_to)
+    return int(lib().orc_port_move(C.byref(r.s), dim, C.byref(A), C.byref(B), k))
 
 
 def register(st: dict, grid, port, k: int, prec: int = 0) -> int:

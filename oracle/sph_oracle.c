@@ -372,6 +372,71 @@ void orc_advect(orc_state *s, int32_t dim, float dt)
     }
 }
 
+/* ------------------------------------------- moving ports (rotating sprinkler) */
+
+/* Rotating sprinkler (§V.C, Fig. rotation_procedure): after this
+ * step's generation in the established local frame, "the positions and
+ * velocities of buffer particles are transformed to new ones through coordinate
+ * rotation", and "the local coordinate system is reestablished according to the
+ * new position of sprinkler".  Reading R23: every buffer particle of
+ * the port keeps its local coordinates and its local velocity; `from` is the
+ * established frame, `to` the re-established one (the caller computes it, e.g.
+ * theta = omega t + theta0):
+ *     X' = Q0 (x - o0)      Eq. 2D/3D_transformation     (pinned as orc_to_local_f32)
+ *     x  = o1 + Q1^T X'     Eq. 2D/3D_Inverse_transformation
+ *     V' = Q0 v,  v = Q1^T V'   (velocities rotate without the translation)
+ * Pinned fp32, one rounding per operation, sums in index order:
+ *     x_j = fl(o1_j + fl(fl(fl(Q1[0][j] X'_0) + fl(Q1[1][j] X'_1)) + fl(Q1[2][j] X'_2)))
+ *     (2-D: fl(o1_j + fl(fl(Q1[0][j] X'_0) + fl(Q1[1][j] X'_1))))
+ * Brute force over every particle labelled k.  Returns how many moved. */
+int64_t orc_port_move(orc_state *s, int32_t dim, const orc_port *from, const orc_port *to, int32_t k)
+{
+    int64_t moved = 0;
+    for (int64_t i = 0; i < s->n; ++i) {
+        if (s->label[i] != k) continue;
+        float X[3], V[3];
+        orc_to_local_f32(from, dim, s->x[i], s->y[i], dim == 3 ? s->z[i] : 0.0f, X);
+        /* local velocity: the linear part of the same transform */
+        for (int r = 0; r < dim; ++r) {
+            float acc = from->Q[3 * r + 0] * s->vx[i];
+            float t1 = from->Q[3 * r + 1] * s->vy[i];
+            acc = acc + t1;
+            if (dim == 3) {
+                float t2 = from->Q[3 * r + 2] * s->vz[i];
+                acc = acc + t2;
+            }
+            V[r] = acc;
+        }
+        float xn[3] = {0.0f, 0.0f, 0.0f}, vn[3] = {0.0f, 0.0f, 0.0f};
+        for (int j = 0; j < dim; ++j) {
+            float gx = to->Q[0 * 3 + j] * X[0];
+            float gv = to->Q[0 * 3 + j] * V[0];
+            float t = to->Q[1 * 3 + j] * X[1];
+            float tv = to->Q[1 * 3 + j] * V[1];
+            gx = gx + t;
+            gv = gv + tv;
+            if (dim == 3) {
+                float t2 = to->Q[2 * 3 + j] * X[2];
+                float tv2 = to->Q[2 * 3 + j] * V[2];
+                gx = gx + t2;
+                gv = gv + tv2;
+            }
+            xn[j] = to->o[j] + gx;
+            vn[j] = gv;
+        }
+        s->x[i] = xn[0];
+        s->y[i] = xn[1];
+        s->vx[i] = vn[0];
+        s->vy[i] = vn[1];
+        if (dim == 3) {
+            s->z[i] = xn[2];
+            s->vz[i] = vn[2];
+        }
+        ++moved;
+    }
+    return moved;
+}
+
 /* ---------------------------------------------------- O0: registration */
 
 /* Alg. 1 "Buffer particle identification ... Execute only once":

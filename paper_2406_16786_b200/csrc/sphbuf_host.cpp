@@ -86,7 +86,9 @@ struct sph_ctx {
     GridDev gd{};
     PortTable pt{};
     std::vector<PortHost> ports;
-    std::vector<int> runs;   // 3 ints per run: c0, c1, port
+    std::vector<int> runs;   // 3 ints per run: c0, c1, port (ports in registration order)
+    std::vector<int> run_base, run_cnt;   // per port: first run and run count in `runs`
+    std::vector<int> run_cap;             // per port: > 0 once movable (device-enumerated slice)
     void *ws = nullptr;
     size_t ws_bytes = 0;
     Workspace W{};
@@ -392,6 +394,8 @@ const char *sph_last_error(const sph_ctx *c) { return c ? c->err.c_str() : "null
 
 size_t sph_workspace_bytes(const sph_ctx *c) { return c ? layout(c, nullptr, nullptr) : 0; }
 
+static cudaError_t enumerate_slice(sph_ctx *c, int k, const float o[3], const float Q[9], cudaStream_t s);
+
 sph_status sph_set_workspace(sph_ctx *c, void *d_ws, size_t bytes)
 {
     if (!c || !d_ws) return SPH_ERR_ARG;
@@ -406,25 +410,19 @@ sph_status sph_set_workspace(sph_ctx *c, void *d_ws, size_t bytes)
     if (!c->runs.empty()) {
         e = cudaMemcpy(c->W.runs, c->runs.data(), sizeof(int) * c->runs.size(), cudaMemcpyHostToDevice);
         if (e != cudaSuccess) return cuda_fail(c, e, "sph_set_workspace runs");
+        for (int q = 0; q < c->pt.n; ++q)   // movable ports: their slices live on the device only
+            if (c->run_cap[q] > 0 && (e = enumerate_slice(c, q, c->pt.p[q].o, c->pt.p[q].Q, 0)) != cudaSuccess)
+                return cuda_fail(c, e, "sph_set_workspace enumeration");
     }
     return SPH_OK;
 }
 
-sph_status sph_port_check(const sph_ctx *cc, const float origin[3], const float Q[9], const float he[3], int32_t kind,
-                          int32_t layers, float dp)
+// Pose checks shared by registration and sph_port_move: Q a rotation (planar in
+// 2-D), P_k strictly inside the grid, P_k disjoint from every other port's
+// (port `skip` excluded: the port being moved).
+static sph_status check_pose(sph_ctx *c, const float origin[3], const float Q[9], const float he[3], int skip)
 {
-    sph_ctx *c = const_cast<sph_ctx *>(cc);
-    if (!c || !origin || !Q || !he) return fail(c, SPH_ERR_ARG, "NULL argument");
     const int dim = c->grid.dim;
-    if (kind < SPH_INLET || kind > SPH_BIDIRECTIONAL) return fail(c, SPH_ERR_ARG, "bad kind");
-    if (c->pt.n >= c->max_ports) return fail(c, SPH_ERR_ARG, "too many ports");
-    // at least three layers of particles (P:226-229); a = layers * dp
-    if (layers < 3 || !(dp > 0.f)) return fail(c, SPH_ERR_ARG, "layers < 3 or dp <= 0");
-    for (int r = 0; r < dim; ++r)
-        if (!(he[r] > 0.f)) return fail(c, SPH_ERR_ARG, "half extents must be positive");
-    const double a = 2.0 * (double)he[0];
-    if (std::fabs(a - layers * (double)dp) > 1e-5 * layers * (double)dp)
-        return fail(c, SPH_ERR_ARG, "2*half_extents[0] != layers*dp");
     // orthonormality and handedness
     double M[9];
     for (int i = 0; i < 9; ++i) M[i] = Q[i];
@@ -452,9 +450,28 @@ sph_status sph_port_check(const sph_ctx *cc, const float origin[3], const float 
     }
     // disjoint decision regions (the paper never overlaps buffers; each particle
     // then gets at most one decision)
-    for (const PortHost &B : c->ports)
-        if (obb_obb_overlap(P, B, dim)) return fail(c, SPH_ERR_OVERLAP, "P_k overlaps an existing port");
+    for (size_t j = 0; j < c->ports.size(); ++j)
+        if ((int)j != skip && obb_obb_overlap(P, c->ports[j], dim))
+            return fail(c, SPH_ERR_OVERLAP, "P_k overlaps an existing port");
     return SPH_OK;
+}
+
+sph_status sph_port_check(const sph_ctx *cc, const float origin[3], const float Q[9], const float he[3], int32_t kind,
+                          int32_t layers, float dp)
+{
+    sph_ctx *c = const_cast<sph_ctx *>(cc);
+    if (!c || !origin || !Q || !he) return fail(c, SPH_ERR_ARG, "NULL argument");
+    const int dim = c->grid.dim;
+    if (kind < SPH_INLET || kind > SPH_BIDIRECTIONAL) return fail(c, SPH_ERR_ARG, "bad kind");
+    if (c->pt.n >= c->max_ports) return fail(c, SPH_ERR_ARG, "too many ports");
+    // at least three layers of particles (P:226-229); a = layers * dp
+    if (layers < 3 || !(dp > 0.f)) return fail(c, SPH_ERR_ARG, "layers < 3 or dp <= 0");
+    for (int r = 0; r < dim; ++r)
+        if (!(he[r] > 0.f)) return fail(c, SPH_ERR_ARG, "half extents must be positive");
+    const double a = 2.0 * (double)he[0];
+    if (std::fabs(a - layers * (double)dp) > 1e-5 * layers * (double)dp)
+        return fail(c, SPH_ERR_ARG, "2*half_extents[0] != layers*dp");
+    return check_pose(c, origin, Q, he, -1);
 }
 
 sph_status sph_port_cells(const sph_grid *grid, const float origin[3], const float Q[9], const float he[3],
@@ -527,6 +544,9 @@ sph_status sph_buffer_register(sph_ctx *c, sph_particles *p, const float origin[
         return cuda_fail(c, e, "register: upload runs");
     }
     c->ports.push_back(P);
+    c->run_base.push_back((int)(before / 3));
+    c->run_cnt.push_back((int)(r2.size() / 2));
+    c->run_cap.push_back(0);
     c->pt.n = k + 1;
     if (members_out_dev) {
         e = cudaMemsetAsync(members_out_dev, 0, sizeof(int64_t), s);
@@ -535,6 +555,132 @@ sph_status sph_buffer_register(sph_ctx *c, sph_particles *p, const float origin[
     e = launch_register(part_dev(p), c->gd, c->pt, k, reinterpret_cast<long long *>(members_out_dev), s, &c->L);
     if (e != cudaSuccess) return cuda_fail(c, e, "register: identification kernel");
     if (port_id_out) *port_id_out = k;
+    return SPH_OK;
+}
+
+// Movable ports (sph_port_move): the slice of one run slot per cell column of a
+// window of `span` columns per axis around the bounding sphere of the inflated
+// decision region; any pose of the port fits in it.
+static int move_span(const sph_ctx *c, int k)
+{
+    const PortDev &D = c->pt.p[k];
+    const double cs = (double)c->grid.cs, inf = 1e-3 * cs;
+    double r2 = 0.0;
+    for (int j = 0; j < c->grid.dim; ++j) {
+        const double H = (double)D.he[j] + cs + inf;
+        r2 += H * H;
+    }
+    return (int)std::floor(2.0 * std::sqrt(r2) / cs) + 3;
+}
+
+static int move_slice_cap(const sph_ctx *c, int k)
+{
+    const int span = move_span(c, k);
+    return c->grid.dim == 3 ? span * span : span;
+}
+
+// K10 launch for port k at pose (o, Q) into its slice.
+static cudaError_t enumerate_slice(sph_ctx *c, int k, const float o[3], const float Q[9], cudaStream_t s)
+{
+    const int dim = c->grid.dim;
+    float he[3];
+    for (int j = 0; j < 3; ++j) he[j] = c->pt.p[k].he[j];
+    const PortHost Pi = make_port_host(o, Q, he, c->grid.cs, dim, 1e-3 * (double)c->grid.cs);
+    const double cs = (double)c->grid.cs;
+    double r2 = 0.0;
+    for (int j = 0; j < dim; ++j) r2 += Pi.H[j] * Pi.H[j];
+    const double R = std::sqrt(r2);
+    const int span = move_span(c, k);
+    PortEnum E{};
+    for (int r = 0; r < 3; ++r) {
+        E.o[r] = Pi.o[r];
+        E.H[r] = Pi.H[r];
+        for (int j = 0; j < 3; ++j) E.ax[r][j] = Pi.ax[r][j];
+    }
+    auto first_cell = [&](int j) { return (int)std::floor((Pi.o[j] - R - (double)c->grid.lo[j]) / cs) - 1; };
+    const int fast = dim - 1;
+    E.cx0 = first_cell(0);
+    E.ncx = span;
+    E.cy0 = dim == 3 ? first_cell(1) : 0;
+    E.ncy = dim == 3 ? span : 1;
+    E.f0 = std::max(first_cell(fast), 0);
+    E.f1 = std::min(first_cell(fast) + span - 1, c->grid.ncell[fast] - 1);
+    E.k = k;
+    return launch_port_enum(c->gd, E, c->grid.cs, c->W.runs + 3 * (size_t)c->run_base[k], c->run_cap[k], s, &c->L);
+}
+
+sph_status sph_port_move(sph_ctx *c, sph_particles *p, int32_t k, const float origin[3], const float Q[9],
+                         const int32_t *cell_start, const int32_t *cell_end, void *stream)
+{
+    if (!c) return SPH_ERR_ARG;
+    if (!origin || !Q || !cell_start || !cell_end) return fail(c, SPH_ERR_ARG, "NULL argument");
+    if (k < 0 || k >= c->pt.n) return fail(c, SPH_ERR_ARG, "unknown port");
+    if (!c->ws) return fail(c, SPH_ERR_STATE, "no workspace set");
+    sph_status st = check_particles(c, p);
+    if (st != SPH_OK) return st;
+    const int dim = c->grid.dim;
+    PortDev P1 = c->pt.p[k];
+    float o1[3], he[3];
+    for (int j = 0; j < 3; ++j) {
+        o1[j] = (dim == 2 && j == 2) ? 0.f : origin[j];
+        he[j] = P1.he[j];
+    }
+    st = check_pose(c, o1, Q, he, k);
+    if (st != SPH_OK) return st;
+    for (int j = 0; j < 3; ++j) P1.o[j] = o1[j];
+    for (int i = 0; i < 9; ++i) P1.Q[i] = Q[i];
+    const float a = 2.0f * P1.he[0];
+    for (int j = 0; j < 3; ++j) {
+        volatile float prod = a * Q[j];            // recycle shift s = fl(a u) of the new axis (R10)
+        P1.s[j] = (dim == 2 && j == 2) ? 0.f : prod;
+    }
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    // 1. the buffer particles, found among the port's candidates of the current build
+    cudaError_t e = launch_port_move(part_dev(p), dim, c->pt.p[k], P1, c->W.runs + 3 * (size_t)c->run_base[k],
+                                     c->run_cnt[k], cell_start, cell_end, k, nullptr, s, &c->L);
+    if (e != cudaSuccess) return cuda_fail(c, e, "port_move");
+    // 2. first move: the port's runs become a fixed device slice, one slot per cell
+    //    column of a window around its bounding sphere (any pose fits); the table is
+    //    re-laid out, so the other movable ports' slices are enumerated again
+    if (c->run_cap[k] == 0) {
+        const int cap = move_slice_cap(c, k);
+        std::vector<int> nr;
+        std::vector<int> base(c->pt.n), cnt(c->pt.n);
+        for (int q = 0; q < c->pt.n; ++q) {
+            base[q] = (int)(nr.size() / 3);
+            const int m = q == k ? cap : c->run_cnt[q];
+            if (q == k || c->run_cap[q] > 0) {
+                for (int i = 0; i < m; ++i) {
+                    nr.push_back(0);
+                    nr.push_back(-1);
+                    nr.push_back(q);
+                }
+            } else {
+                nr.insert(nr.end(), c->runs.begin() + 3 * (size_t)c->run_base[q],
+                          c->runs.begin() + 3 * (size_t)(c->run_base[q] + c->run_cnt[q]));
+            }
+            cnt[q] = m;
+        }
+        if (nr.size() / 3 > (size_t)kMaxRuns) return fail(c, SPH_ERR_ARG, "too many port runs");
+        // pageable source: staged before return, so later host edits cannot race it
+        e = cudaMemcpyAsync(c->W.runs, nr.data(), sizeof(int) * nr.size(), cudaMemcpyHostToDevice, s);
+        if (e != cudaSuccess) return cuda_fail(c, e, "port_move: upload runs");
+        c->runs.swap(nr);
+        c->run_base = base;
+        c->run_cnt = cnt;
+        c->run_cap[k] = cap;
+        for (int q = 0; q < c->pt.n; ++q) {
+            if (q == k || c->run_cap[q] == 0) continue;
+            e = enumerate_slice(c, q, c->pt.p[q].o, c->pt.p[q].Q, s);
+            if (e != cudaSuccess) return cuda_fail(c, e, "port_move: enumeration");
+        }
+    }
+    // 3. the candidate cells of the new pose, enumerated on the device
+    e = enumerate_slice(c, k, o1, Q, s);
+    if (e != cudaSuccess) return cuda_fail(c, e, "port_move: enumeration");
+    // 4. the re-established frame for the next update
+    c->pt.p[k] = P1;
+    c->ports[k] = make_port_host(o1, Q, he, c->grid.cs, dim, 0.0);
     return SPH_OK;
 }
 
@@ -737,7 +883,8 @@ int64_t sph_launch_count(const sph_ctx *c) { return c ? c->L.count : 0; }
 
 static const char *kKernelNames[KID_COUNT] = {
     "advect", "register", "cll_key", "cell_scan", "cll_scatter", "cll_gather", "upd_prologue",
-    "upd_main", "compact", "compact_append", "mig_pack", "mig_unpack", "compact_count", "cll_rank"};
+    "upd_main", "compact", "compact_append", "mig_pack", "mig_unpack", "compact_count", "cll_rank",
+    "port_move", "port_enum"};
 
 const char *sph_kernel_name(int32_t i) { return (i >= 0 && i < KID_COUNT) ? kKernelNames[i] : ""; }
 

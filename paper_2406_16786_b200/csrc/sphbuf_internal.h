@@ -49,6 +49,18 @@ struct PortDev {
     float R2;        // fl(R * R)
 };
 
+// Pose of a movable port for the device cell enumeration (sphbuf_motion.cu):
+// f64 decision region (centre, unit axes, half sizes he + cs + 1e-3 cs) and the
+// cell window covering its bounding sphere: columns [cx0, cx0 + ncx) x
+// [cy0, cy0 + ncy) (3-D; 2-D: columns along y, ncy = 1), fast-axis cells [f0, f1].
+struct PortEnum {
+    double o[3];
+    double ax[3][3];
+    double H[3];
+    int cx0, cy0, ncx, ncy, f0, f1;
+    int k;
+};
+
 struct PortTable {
     int n;
     int max_ports;
@@ -120,7 +132,7 @@ struct Workspace {
 enum KernelId {
     KID_ADVECT, KID_REGISTER, KID_CLL_KEY, KID_CELL_SCAN, KID_CLL_SCATTER, KID_CLL_GATHER, KID_UPD_PROLOGUE,
     KID_UPD_MAIN, KID_COMPACT, KID_COMPACT_APPEND, KID_MIG_PACK, KID_MIG_UNPACK, KID_COMPACT_COUNT, KID_CLL_RANK,
-    KID_COUNT
+    KID_PORT_MOVE, KID_PORT_ENUM, KID_COUNT
 };
 
 // Counts launches; when profiling is on, brackets every launch with a pair of
@@ -162,6 +174,11 @@ cudaError_t launch_migrate_pack(const PartDev &p, const GridDev &g, const Worksp
                                 long long max_migrate, int rec, cudaStream_t s, Launch *L);
 cudaError_t launch_migrate_unpack(const PartDev &p, const GridDev &g, const Workspace &ws, const float *buf,
                                   long long max_migrate, int rec, cudaStream_t s, Launch *L);
+cudaError_t launch_port_move(const PartDev &p, int dim, const PortDev &P0, const PortDev &P1, const int *runs,
+                             int nrun, const int *cell_start, const int *cell_end, int k, long long *moved,
+                             cudaStream_t s, Launch *L);
+cudaError_t launch_port_enum(const GridDev &g, const PortEnum &P, float cs, int *runs, int cap, cudaStream_t s,
+                             Launch *L);
 int sm_count();
 
 }  // namespace sphbuf

@@ -71,7 +71,9 @@ __global__ void __launch_bounds__(1024) k_upd_prologue(Workspace ws, int n_runs,
     for (int r0 = 0; r0 < n_runs; r0 += 1024) {
         const int r = r0 + threadIdx.x;
         long long len = 0;
-        if (r < n_runs) len = (long long)cell_end[ws.runs[3 * r + 1]] - (long long)cell_start[ws.runs[3 * r]];
+        // (c1 < c0: an empty slot of a movable port's run slice)
+        if (r < n_runs && ws.runs[3 * r + 1] >= ws.runs[3 * r])
+            len = (long long)cell_end[ws.runs[3 * r + 1]] - (long long)cell_start[ws.runs[3 * r]];
         long long total;
         const long long ex = block_excl_scan_ll<1024>(len, total, s_warp);
         if (r < n_runs) ws.run_off[r] = carry + ex;

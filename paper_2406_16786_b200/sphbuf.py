@@ -61,8 +61,8 @@ EXPORTS = ["sph_ctx_create", "sph_ctx_destroy", "sph_last_error", "sph_workspace
            "sph_compact", "sph_migrate_record_floats", "sph_migrate_pack", "sph_migrate_unpack", "sph_status_sync",
            "sph_launch_count", "sph_port_cells", "sph_frame_from_axis", "sph_profile", "sph_profile_read",
            "sph_kernel_name", "sph_advect_cll_build", "sph_compact_deferred", "sph_cll_key", "sph_cll_finish",
-           "sph_port_set_bc"]
-NKERNELS = 14
+           "sph_port_set_bc", "sph_port_move"]
+NKERNELS = 16
 
 
 def lib():
@@ -92,6 +92,8 @@ def lib():
     L.sph_advect_cll_build.restype = C.c_int
     L.sph_port_set_bc.argtypes = [vp, i32, P(sph_bc)]
     L.sph_port_set_bc.restype = C.c_int
+    L.sph_port_move.argtypes = [vp, P(sph_particles), i32, vp, vp, vp, vp, vp]
+    L.sph_port_move.restype = C.c_int
     L.sph_cll_key.argtypes = [vp, P(sph_particles), f32, i32, vp, vp, vp]
     L.sph_cll_key.restype = C.c_int
     L.sph_cll_finish.argtypes = [vp, P(sph_particles), P(sph_particles), vp, vp, vp, vp, vp, vp]
@@ -222,6 +224,12 @@ def sph_cll_build(ctx, pin, pout, cell_start, cell_end, perm=None, stream=None):
 def sph_advect_cll_build(ctx, pin, pout, dt, cell_start, cell_end, perm=None, stream=None):
     _check(lib().sph_advect_cll_build(ctx.h, C.byref(pin.abi), C.byref(pout.abi), float(dt), _ptr(cell_start),
                                       _ptr(cell_end), _ptr(perm), _stream(stream)), ctx.h)
+
+
+def sph_port_move(ctx, parts, port_id, origin, Q, cell_start, cell_end, stream=None):
+    o, q = _f3(origin), _f9(Q)
+    _check(lib().sph_port_move(ctx.h, C.byref(parts.abi), int(port_id), o, q, _ptr(cell_start), _ptr(cell_end),
+                               _stream(stream)), ctx.h)
 
 
 def sph_cll_key(ctx, pin, dt=None, send_lo=None, send_hi=None, stream=None):
@@ -417,6 +425,14 @@ class BufferUpdater:
 
     def update(self, stream=None):
         sph_buffer_update(self.ctx, self.A, self.cell_start, self.cell_end, self.port_counts, stream)
+
+    def move_port(self, k, origin, Q, stream=None):
+        """Re-establish port k at the pose (origin, Q) after this step's update (moving
+        port): its buffer particles keep local coordinates and velocities."""
+        sph_port_move(self.ctx, self.A, k, origin, Q, self.cell_start, self.cell_end, stream)
+        p = self.ports[k]
+        self.ports[k] = type(p)(tuple(float(v) for v in origin), tuple(float(v) for v in Q), p.half_extents,
+                                p.kind, p.layers, getattr(p, "bc", None))
 
     def compact(self, all_counts=None, nranks=1, rank=0, perm=None, stream=None, deferred=False):
         """IDs + compaction (sph_compact), or IDs + append with the removal left to
