@@ -107,16 +107,17 @@ __device__ bool cell_meets_port(const double c[3], const double e[3], const Port
     return true;
 }
 
-// K10: thread i -> column i of the window (cx0 + i % ncx, cy0 + i / ncx) in 3-D,
+// K10: thread i -> column i of the window (cx0 + i / ncy, cy0 + i % ncy) in 3-D,
 // (cx0 + i) in 2-D; the run is written to slot i of the port's slice, or marked
-// empty (c1 < c0).  Runs come out in increasing cell order (x-major columns).
+// empty (c1 < c0).  Slots follow the x-major cell order (cx slowest), so the
+// port's candidates stay in cell order and creations in canonical order (R14).
 __global__ void __launch_bounds__(kThreads) k_port_enum(GridDev g, PortEnum P, float cs, int *runs, int cap)
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= cap) return;
     const int dim = g.dim;
-    const int cx = P.cx0 + (dim == 3 ? i % P.ncx : i);
-    const int cy = dim == 3 ? P.cy0 + i / P.ncx : 0;
+    const int cx = P.cx0 + (dim == 3 ? i / P.ncy : i);
+    const int cy = dim == 3 ? P.cy0 + i % P.ncy : 0;
     int first = -1, last = -1;
     const bool col_ok = cx >= g.cx_begin && cx < g.cx_end && (dim == 2 || (cy >= 0 && cy < g.ncell[1]));
     if (col_ok) {

@@ -508,6 +508,53 @@ def sprinkler_pose(port0: Port, pivot, theta: float) -> tuple:
     return o, frame_rows_2d(phi0 + theta)
 
 
+def rotation_pose_3d(port0: Port, pivot, axis, theta: float) -> tuple:
+    """Pose (origin, Q) of a 3-D port turned by theta about the line through `pivot`
+    along `axis` (Rodrigues, f64): origin pivot + R(o0 - pivot), every local axis
+    rotated (Q = Q0 R^T); rounded once to binary32 (input data for both sides)."""
+    a = np.asarray(axis, dtype=np.float64)
+    a = a / np.linalg.norm(a)
+    K = np.array([[0.0, -a[2], a[1]], [a[2], 0.0, -a[0]], [-a[1], a[0], 0.0]])
+    R = np.eye(3) + math.sin(theta) * K + (1.0 - math.cos(theta)) * (K @ K)
+    pv = np.asarray(pivot, dtype=np.float64)
+    o = pv + R @ (np.asarray(port0.origin, dtype=np.float64) - pv)
+    Q = np.asarray(port0.Q, dtype=np.float64).reshape(3, 3) @ R.T
+    return tuple(f32(v) for v in o), tuple(f32(v) for v in Q.reshape(-1))
+
+
+def c7(device="cpu", n_updates=100) -> Workload:
+    """3-D rotating port (the sprinkler's moving frame in 3-D): a 0.3^3 box of fluid
+    at dp = 0.01 (27,000 particles, lattice + jitter + N(0,0.05) noise), one inlet
+    (he = (2 dp, 0.04, 0.03), 4 layers) turning at omega = 2 rad/s about the axis
+    (1, 1, 1) through the box centre, and a static outlet.  Velocities: 1.0 along
+    the nearest port axis + noise, axial only near the ports.  dt = 0.0005."""
+    dim, dp = 3, 0.01
+    h = 1.3 * dp
+    cs = f32(2 * h)
+    dt = 0.0005
+    g = _gen(SEED_BASE + 7, device)
+    xyz, ids = _lattice((30, 30, 30), dp, device)
+    n = ids.numel()
+    for j in range(dim):
+        xyz[j] = xyz[j] + _jitter(n, g, device, dp)
+    ports = [_port((0.15 + 0.07, 0.15 - 0.03, 0.15 - 0.04), frame_rows_3d((0.3, 1.0, -0.2), 0.4),
+                   (2 * dp, 0.04, 0.03), INLET, 4),
+             _port((0.06, 0.24, 0.22), frame_rows_3d((-1.0, 0.2, 0.5), 1.1), (2 * dp, 0.03, 0.03), OUTLET, 4)]
+    v = [_noise(n, g, device) for _ in range(dim)]
+    d2 = [sum((xyz[j] - p.origin[j]) ** 2 for j in range(dim)) for p in ports]
+    near0 = d2[0] <= d2[1]
+    for j in range(dim):
+        u0 = torch.tensor(ports[0].Q[j], dtype=torch.float64, device=device)
+        u1 = torch.tensor(ports[1].Q[j], dtype=torch.float64, device=device)
+        v[j] = v[j] + torch.where(near0, u0, u1)
+    v = _project_near_ports(xyz, v, ports, dim, 2 * dp)
+    lo = (f32(-2 * cs), f32(-2 * cs), f32(-2 * cs))
+    nc = int(math.ceil(0.3 / cs)) + 4
+    grid = Grid(dim, lo, cs, (nc, nc, nc))
+    return Workload("C7", dim, dp, h, grid, ports, _pack_state(xyz, v, ids, dim), f32(dt), n_updates, n,
+                    notes="3-D rotating inlet about (1,1,1) through the box centre, static outlet")
+
+
 def c6(device="cpu", n_updates=200, nozzles=4) -> Workload:
     """2-D rotating sprinkler (paper §V.C): dp = 0.005, nozzles of
     half-width 0.02 with the inflow profile v_X' = 2500 (0.02^2 - Y'^2) (u0 = 1.0,
@@ -551,7 +598,7 @@ def c6(device="cpu", n_updates=200, nozzles=4) -> Workload:
                     notes=f"{nozzles} nozzles of 32 buffer particles, omega = {SPRINKLER_OMEGA} rad/s")
 
 
-CONFIGS = {"C1": c1, "C1e": c1e, "C2": c2, "C3": c3, "C4": c4, "C5": c5, "C6": c6}
+CONFIGS = {"C1": c1, "C1e": c1e, "C2": c2, "C3": c3, "C4": c4, "C5": c5, "C6": c6, "C7": c7}
 
 
 def make(name: str, device="cpu", **kw) -> Workload:

@@ -180,3 +180,68 @@ def test_sprinkler_gpu_parity():
         assert int(bu.next_id.item()) == nid
         st = new
     assert s["motion_errors"] == 0
+
+
+C7_PIVOT, C7_AXIS = (0.15, 0.15, 0.15), (1.0, 1.0, 1.0)
+
+
+def _c7_pose(w, step):
+    t = (step + 1) * w.dt
+    return inputs.rotation_pose_3d(w.ports[0], C7_PIVOT, C7_AXIS, inputs.sprinkler_angle(t))
+
+
+def test_rotating_port_3d_oracle_invariants():
+    """3-D port turning about (1,1,1) (C7), 60 updates on the oracle: inlet member
+    count constant, brute force = cell-restricted decisions at every pose, no
+    particle with two decisions, no motion error."""
+    w = inputs.make("C7")
+    K = len(w.ports)
+    st = oracle.to_numpy_state(w.state)
+    m0 = [oracle.register(st, w.grid, p, k) for k, p in enumerate(w.ports)]
+    assert m0[0] > 0
+    ports = list(w.ports)
+    nid = w.next_id
+    for step in range(60):
+        oracle.advect(st, 3, w.dt)
+        res = oracle.update(w.grid, ports, st)
+        res1 = oracle.update(w.grid, ports, oracle.to_numpy_state(st), mode=1)
+        assert (res.port_counts == res1.port_counts).all() and (res.delete_port == res1.delete_port).all()
+        assert res.multi_decision == 0 and res.motion_errors == 0
+        new, perm, nid = oracle.compact(res, 3, K, res.port_counts[None, :], 0, nid)
+        o, Q = _c7_pose(w, step)
+        nxt = Port(o, Q, ports[0].half_extents, ports[0].kind, ports[0].layers)
+        assert oracle.port_move(new, 3, ports[0], nxt, 0) == m0[0]
+        ports[0] = nxt
+        st = new
+
+
+@pytest.mark.gpu
+def test_rotating_port_3d_gpu_parity():
+    """C7 on the GPU (3-D K9 move, 3-D K10 enumeration) vs the oracle, 100 updates,
+    bit-exact; the in-place compaction every update."""
+    w = inputs.make("C7", device="cuda")
+    K = len(w.ports)
+    st = oracle.to_numpy_state(w.state)
+    for k, p in enumerate(w.ports):
+        oracle.register(st, w.grid, p, k)
+    bu = make_updater(w)
+    bu.load(w.state, w.next_id)
+    bu.register_ports()
+    ports = list(w.ports)
+    nid = w.next_id
+    for step in range(100):
+        oracle.advect(st, 3, w.dt)
+        res = oracle.update(w.grid, ports, st)
+        new, perm, nid = oracle.compact(res, 3, K, res.port_counts[None, :], 0, nid)
+        o, Q = _c7_pose(w, step)
+        nxt = Port(o, Q, ports[0].half_extents, ports[0].kind, ports[0].layers)
+        oracle.port_move(new, 3, ports[0], nxt, 0)
+        ports[0] = nxt
+        bu.cll_build(dt=w.dt)
+        bu.update()
+        bu.move_port(0, o, Q)
+        bu.compact()
+        assert (gpu_counts_to_oracle(bu.port_counts, K) == res.port_counts).all(), step
+        assert_state_equal(bu.state(), new, f"step {step}")
+        st = new
+    assert bu.stats()["motion_errors"] == 0
