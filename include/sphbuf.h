@@ -163,6 +163,47 @@ typedef struct {
  * port port_id.  Host only; takes effect at the next sph_buffer_update. */
 sph_status sph_port_set_bc(sph_ctx *ctx, int32_t port_id, const sph_bc *bc);
 
+/* Time-dependent port drivers (aorta flow, §V.D).
+ *   FOURIER    (port with a velocity BC): its speed scale follows
+ *              u0(t) = a0 + sum_{n=1..8} a_n cos(n t omega) + sum_{n=1..8} b_n sin(n t omega)
+ *              (Eq. Fourier_Series, Table I), evaluated in f64 on the host in that
+ *              order and rounded once;
+ *   WINDKESSEL (port with a pressure BC): its boundary pressure P(t) follows the
+ *              3-element RCR model (1 + Rp/Rd) Q + C Rp dQ/dt = P/Rd + C dP/dt
+ *              (Eq. windkessel, Table II; SI units), driven by the flow rate Q out
+ *              of the port measured on the device every step: Q = V/a * sum over
+ *              the port's buffer particles of v.n (n = +u for an outlet, -u for an
+ *              inlet or bidirectional port; reading R26), summed exactly in 32.32
+ *              fixed point; P advances by one explicit step (R27); the recycled
+ *              density becomes fl32(rho0 + P / c0^2) of the port's pressure BC.
+ * The driver state (P, Q) stays on the device (sph_driver_read synchronises). */
+typedef enum { SPH_DRIVER_NONE = 0, SPH_DRIVER_FOURIER = 1, SPH_DRIVER_WINDKESSEL = 2 } sph_driver_kind;
+typedef struct {
+    int32_t kind;      /* sph_driver_kind */
+    double a[9];       /* FOURIER: a0 .. a8 */
+    double b[9];       /* FOURIER: b[1] .. b[8] (b[0] unused) */
+    double omega;      /* FOURIER: rad/s */
+    double Rp, C, Rd;  /* WINDKESSEL: Pa s/m^3, m^3/Pa, Pa s/m^3 */
+    double P0;         /* WINDKESSEL: pressure at the first step, Pa */
+    double volume;     /* WINDKESSEL: particle volume dp^dim for the flow rate */
+} sph_driver;
+
+/* Attach (or detach with kind NONE) a driver to port port_id; FOURIER needs a
+ * velocity BC, WINDKESSEL a pressure BC on the port (sph_port_set_bc first).
+ * Initialises the device state (P = P0); synchronous. */
+sph_status sph_port_set_driver(sph_ctx *ctx, int32_t port_id, const sph_driver *d);
+
+/* Advance every driver to time t (step dt): Fourier speeds set on the host,
+ * Windkessel ports measured and advanced on the device (one block per port over
+ * its candidates in the current cell tables).  Call after sph_cll_build and
+ * before sph_buffer_update. */
+sph_status sph_drivers_step(sph_ctx *ctx, sph_particles *p, double t, double dt, const int32_t *cell_start,
+                            const int32_t *cell_end, void *stream);
+
+/* out[0] = P, out[1] = Q of the last step, out[2] = the u0 in use (FOURIER).
+ * Synchronises `stream`. */
+sph_status sph_driver_read(sph_ctx *ctx, int32_t port_id, double out[3], void *stream);
+
 /* Moving port (rotating sprinkler, §V.C): re-establish port port_id
  * at the pose (origin, Q) — e.g. theta = omega t + theta0 about a pivot,
  * computed by the caller — after this step's generation in the old pose

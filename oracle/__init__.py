@@ -78,6 +78,12 @@ def lib():
         L.orc_port_cells.argtypes = [C.POINTER(Grid), C.POINTER(Port), C.c_void_p]
         L.orc_port_cells.restype = C.c_int64
         L.orc_advect.argtypes = [C.POINTER(State), C.c_int32, C.c_float]
+        L.orc_fourier.argtypes = [C.c_double, C.c_void_p, C.c_void_p, C.c_double]
+        L.orc_fourier.restype = C.c_double
+        L.orc_port_flux.argtypes = [C.POINTER(State), C.c_int32, C.POINTER(Port), C.c_int32]
+        L.orc_port_flux.restype = C.c_int64
+        L.orc_windkessel.argtypes = [C.c_double] * 7
+        L.orc_windkessel.restype = C.c_double
         L.orc_port_move.argtypes = [C.POINTER(State), C.c_int32, C.POINTER(Port), C.POINTER(Port), C.c_int32]
         L.orc_port_move.restype = C.c_int64
         L.orc_register.argtypes = [C.POINTER(State), C.POINTER(Grid), C.POINTER(Port), C.c_int32, C.c_int32]
@@ -254,6 +260,25 @@ def advect(st: dict, dim: int, dt: float):
     lib().orc_advect(C.byref(r.s), dim, dt)
 
 
+def fourier(t: float, a, b, omega: float) -> float:
+    """Eq. Fourier_Series (Table I coefficients a0..a8, b1..b8; b[0] unused)."""
+    aa = np.ascontiguousarray(a, dtype=np.float64)
+    bb = np.ascontiguousarray(b, dtype=np.float64)
+    return float(lib().orc_fourier(float(t), aa.ctypes.data, bb.ctypes.data, float(omega)))
+
+
+def port_flux(st: dict, dim: int, port, k: int) -> int:
+    """Exact 32.32 fixed-point sum of v.u over the buffer particles of port k (R26)."""
+    r = _StateRef(st)
+    P = cport(port)
+    return int(lib().orc_port_flux(C.byref(r.s), dim, C.byref(P), k))
+
+
+def windkessel(P: float, Q: float, Qprev: float, dt: float, Rp: float, Cc: float, Rd: float) -> float:
+    """One explicit step of the RCR Windkessel (Eq. windkessel; reading R27)."""
+    return float(lib().orc_windkessel(P, Q, Qprev, dt, Rp, Cc, Rd))
+
+
 def port_move(st: dict, dim: int, port_from, port_to, k: int) -> int:
     """Moving port (rotating sprinkler): the buffer particles of port k keep
     their local coordinates and velocities from frame ``port_from`` to ``port_to``."""
@@ -287,8 +312,10 @@ class UpdateResult:
     motion_errors: int
 
 
-def update(grid, ports, st: dict, mode: int = 0, prec: int = 0, cap_stage: int | None = None) -> UpdateResult:
-    """O2-O5 on one slab: cell list, decisions, duplicate + recycle, relabel."""
+def update(grid, ports, st: dict, mode: int = 0, prec: int = 0, cap_stage: int | None = None,
+           rho_b: dict | None = None) -> UpdateResult:
+    """O2-O5 on one slab: cell list, decisions, duplicate + recycle, relabel.
+    rho_b: {port: recycled density} overriding the pressure BC's (a Windkessel driver)."""
     dim = grid.dim
     n = len(st["x"])
     K = len(ports)
@@ -316,6 +343,8 @@ def update(grid, ports, st: dict, mode: int = 0, prec: int = 0, cap_stage: int |
     ri = _StateRef(st)
     G = cgrid(grid)
     P = cports(ports)
+    for k, v in (rho_b or {}).items():
+        P[k].rho_b = float(v)
     rc = lib().orc_update(C.byref(G), P, K, C.byref(ri.s), mode, prec, C.byref(o))
     if rc != 0:
         raise RuntimeError("oracle staging overflow")

@@ -437,6 +437,62 @@ int64_t orc_port_move(orc_state *s, int32_t dim, const orc_port *from, const orc
     return moved;
 }
 
+/* ------------------------------------------ port drivers (aorta flow, §V.D) */
+
+/* Eq. Fourier_Series: v_inlet(t) = a0 + sum_{n=1..8} a_n cos(n t w)
+ * + sum_{n=1..8} b_n sin(n t w), Table I.  f64, the two sums in the order
+ * written, argument (n t) w. */
+double orc_fourier(double t, const double *a, const double *b, double omega)
+{
+    double u = a[0];
+    for (int n = 1; n <= 8; ++n) u = u + a[n] * cos(((double)n * t) * omega);
+    for (int n = 1; n <= 8; ++n) u = u + b[n] * sin(((double)n * t) * omega);
+    return u;
+}
+
+/* Flow through a port (reading R26): sum over the port's buffer particles of
+ * v . u, u = row 0 of Q, each term pinned fp32 fl(fl(fl(vx ux) + fl(vy uy)) +
+ * fl(vz uz)) scaled by 2^32 and rounded to the nearest integer (ties to even),
+ * summed exactly in int64 (so the order of the sum does not matter).  The caller
+ * forms Q = +-(S 2^-32) V / a.  Brute force over every particle. */
+int64_t orc_port_flux(const orc_state *s, int32_t dim, const orc_port *p, int32_t k)
+{
+    int64_t S = 0;
+    for (int64_t i = 0; i < s->n; ++i) {
+        if (s->label[i] != k) continue;
+        float d = s->vx[i] * p->Q[0];
+        float e = s->vy[i] * p->Q[1];
+        d = d + e;
+        if (dim == 3) {
+            float f = s->vz[i] * p->Q[2];
+            d = d + f;
+        }
+        float sc = d * 4294967296.0f;
+        S += (int64_t)llrintf(sc);
+    }
+    return S;
+}
+
+/* One explicit step of the 3-element Windkessel (Eq. windkessel):
+ *     (1 + Rp/Rd) Q + C Rp dQ/dt = P/Rd + C dP/dt
+ * reading R27: dQ/dt = (Q - Qprev)/dt, P_next = P + dt dP/dt with
+ * dP/dt = ((1 + Rp/Rd) Q + C Rp dQ/dt - P/Rd) / C.  f64, in the order written. */
+double orc_windkessel(double P, double Q, double Qprev, double dt, double Rp, double C, double Rd)
+{
+    double dQ = (Q - Qprev) / dt;
+    double t1 = Rp / Rd;
+    double t2 = 1.0 + t1;
+    double t3 = t2 * Q;
+    double t4 = C * Rp;
+    double t5 = t4 * dQ;
+    double t6 = t3 + t5;
+    double t7 = P / Rd;
+    double t8 = t6 - t7;
+    double dP = t8 / C;
+    double m = dt * dP;
+    return P + m;
+}
+
 /* ---------------------------------------------------- O0: registration */
 
 /* Alg. 1 "Buffer particle identification ... Execute only once":

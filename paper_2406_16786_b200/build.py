@@ -11,7 +11,7 @@ CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(HERE, "libsphbuf.so")
 SOURCES = ["sphbuf_cll.cu", "sphbuf_update.cu", "sphbuf_compact.cu", "sphbuf_migrate.cu", "sphbuf_motion.cu",
-           "sphbuf_host.cpp"]
+           "sphbuf_drivers.cu", "sphbuf_host.cpp"]
 DEPS = SOURCES + ["sphbuf_internal.h", "sphbuf_common.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "--fmad=false",

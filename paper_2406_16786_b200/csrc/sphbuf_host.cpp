@@ -89,6 +89,10 @@ struct sph_ctx {
     std::vector<int> runs;   // 3 ints per run: c0, c1, port (ports in registration order)
     std::vector<int> run_base, run_cnt;   // per port: first run and run count in `runs`
     std::vector<int> run_cap;             // per port: > 0 once movable (device-enumerated slice)
+    std::vector<sph_bc> bcs;              // per port: the last BC set
+    std::vector<sph_driver> drivers;      // per port: time-dependent driver (kind NONE if none)
+    std::vector<double> drv_u0;           // per port: the Fourier speed in use
+    DriverLaunch drv_launch{};            // staging of the Windkessel kernel parameter
     void *ws = nullptr;
     size_t ws_bytes = 0;
     Workspace W{};
@@ -135,6 +139,8 @@ size_t layout(const sph_ctx *c, char *base, Workspace *W)
     w.tile_cmp = (unsigned long long *)take(8 * cmp_tiles);
     w.rd = (unsigned *)take(4 * cmp_subs);
     w.runs = (int *)take(sizeof(int) * 3 * kMaxRuns);
+    w.drv = (DriverDev *)take(sizeof(DriverDev) * SPH_MAX_PORTS);
+    w.drv_rho = (float *)take(sizeof(float) * SPH_MAX_PORTS);
     w.run_off = (long long *)take(sizeof(long long) * (kMaxRuns + 1));
     const size_t zero_end = off;   // everything above must start zeroed
     w.sub_off = (unsigned *)take(4 * cmp_subs);
@@ -547,6 +553,9 @@ sph_status sph_buffer_register(sph_ctx *c, sph_particles *p, const float origin[
     c->run_base.push_back((int)(before / 3));
     c->run_cnt.push_back((int)(r2.size() / 2));
     c->run_cap.push_back(0);
+    c->bcs.push_back(sph_bc{});
+    c->drivers.push_back(sph_driver{});
+    c->drv_u0.push_back(0.0);
     c->pt.n = k + 1;
     if (members_out_dev) {
         e = cudaMemsetAsync(members_out_dev, 0, sizeof(int64_t), s);
@@ -713,6 +722,104 @@ sph_status sph_port_set_bc(sph_ctx *c, int32_t port_id, const sph_bc *bc)
         return fail(c, SPH_ERR_ARG, "bad BC kind");
     }
     D.bc = bc->kind;
+    c->bcs[port_id] = *bc;
+    return SPH_OK;
+}
+
+sph_status sph_port_set_driver(sph_ctx *c, int32_t k, const sph_driver *d)
+{
+    if (!c || !d) return SPH_ERR_ARG;
+    if (k < 0 || k >= c->pt.n) return fail(c, SPH_ERR_ARG, "unknown port");
+    if (!c->ws) return fail(c, SPH_ERR_STATE, "no workspace set");
+    PortDev &D = c->pt.p[k];
+    if (d->kind == SPH_DRIVER_NONE) {
+        D.rho_dev = 0;
+        c->drivers[k] = *d;
+        return SPH_OK;
+    }
+    if (d->kind == SPH_DRIVER_FOURIER) {
+        if (D.bc != SPH_BC_VELOCITY) return fail(c, SPH_ERR_ARG, "Fourier driver needs a velocity BC");
+    } else if (d->kind == SPH_DRIVER_WINDKESSEL) {
+        if (D.bc != SPH_BC_PRESSURE) return fail(c, SPH_ERR_ARG, "Windkessel driver needs a pressure BC");
+        if (!(d->Rp > 0.0) || !(d->C > 0.0) || !(d->Rd > 0.0) || !(d->volume > 0.0))
+            return fail(c, SPH_ERR_ARG, "Windkessel: Rp, C, Rd, volume must be positive");
+        DriverDev st{};
+        st.P = d->P0;
+        st.first = 1;
+        const sph_bc &bc = c->bcs[k];
+        const float rho = (float)((double)bc.rho0 + d->P0 / ((double)bc.c0 * (double)bc.c0));
+        cudaError_t e = cudaMemcpy(c->W.drv + k, &st, sizeof(st), cudaMemcpyHostToDevice);
+        if (e == cudaSuccess) e = cudaMemcpy(c->W.drv_rho + k, &rho, sizeof(rho), cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) return cuda_fail(c, e, "set_driver");
+        D.rho_dev = 1;
+    } else {
+        return fail(c, SPH_ERR_ARG, "bad driver kind");
+    }
+    c->drivers[k] = *d;
+    return SPH_OK;
+}
+
+// Eq. Fourier_Series: a0 + sum a_n cos(n t w) + sum b_n sin(n t w), the
+// two sums in that order, f64.
+static double fourier_speed(const sph_driver &d, double t)
+{
+    double u = d.a[0];
+    for (int n = 1; n <= 8; ++n) u = u + d.a[n] * std::cos(((double)n * t) * d.omega);
+    for (int n = 1; n <= 8; ++n) u = u + d.b[n] * std::sin(((double)n * t) * d.omega);
+    return u;
+}
+
+sph_status sph_drivers_step(sph_ctx *c, sph_particles *p, double t, double dt, const int32_t *cell_start,
+                            const int32_t *cell_end, void *stream)
+{
+    if (!c) return SPH_ERR_ARG;
+    if (!cell_start || !cell_end) return fail(c, SPH_ERR_ARG, "NULL cell table");
+    if (!(dt > 0.0)) return fail(c, SPH_ERR_ARG, "dt <= 0");
+    sph_status st = check_particles(c, p);
+    if (st != SPH_OK) return st;
+    DriverLaunch &L = c->drv_launch;   // host staging of the kernel parameter
+    L.n = 0;
+    for (int k = 0; k < c->pt.n; ++k) {
+        const sph_driver &d = c->drivers[k];
+        PortDev &D = c->pt.p[k];
+        if (d.kind == SPH_DRIVER_FOURIER) {
+            const double u = fourier_speed(d, t);
+            c->drv_u0[k] = u;
+            D.u0 = (float)u;
+        } else if (d.kind == SPH_DRIVER_WINDKESSEL) {
+            DriverEntry &E = L.e[L.n++];
+            E = DriverEntry{};
+            E.k = k;
+            E.run0 = c->run_base[k];
+            E.nrun = c->run_cnt[k];
+            for (int j = 0; j < 3; ++j) E.u[j] = D.Q[j];
+            E.sign = D.kind == SPH_OUTLET ? 1.0 : -1.0;   // flow out of the domain (R26)
+            E.scale = d.volume / (2.0 * (double)D.he[0]);
+            E.Rp = d.Rp;
+            E.C = d.C;
+            E.Rd = d.Rd;
+            E.rho0 = (double)c->bcs[k].rho0;
+            E.c0sq = (double)c->bcs[k].c0 * (double)c->bcs[k].c0;
+            E.dt = dt;
+        }
+    }
+    cudaError_t e = launch_drivers(part_dev(p), c->W, L, cell_start, cell_end, static_cast<cudaStream_t>(stream),
+                                   &c->L);
+    return e == cudaSuccess ? SPH_OK : cuda_fail(c, e, "drivers_step");
+}
+
+sph_status sph_driver_read(sph_ctx *c, int32_t k, double out[3], void *stream)
+{
+    if (!c || !out) return SPH_ERR_ARG;
+    if (k < 0 || k >= c->pt.n) return fail(c, SPH_ERR_ARG, "unknown port");
+    DriverDev st{};
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    cudaError_t e = cudaMemcpyAsync(&st, c->W.drv + k, sizeof(st), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_fail(c, e, "driver_read");
+    out[0] = st.P;
+    out[1] = st.Q;
+    out[2] = c->drv_u0[k];
     return SPH_OK;
 }
 
@@ -884,7 +991,7 @@ int64_t sph_launch_count(const sph_ctx *c) { return c ? c->L.count : 0; }
 static const char *kKernelNames[KID_COUNT] = {
     "advect", "register", "cll_key", "cell_scan", "cll_scatter", "cll_gather", "upd_prologue",
     "upd_main", "compact", "compact_append", "mig_pack", "mig_unpack", "compact_count", "cll_rank",
-    "port_move", "port_enum"};
+    "port_move", "port_enum", "drivers"};
 
 const char *sph_kernel_name(int32_t i) { return (i >= 0 && i < KID_COUNT) ? kKernelNames[i] : ""; }
 

@@ -47,6 +47,7 @@ struct PortDev {
     float u0;        // velocity BC speed scale
     float R;         // profile radius
     float R2;        // fl(R * R)
+    int rho_dev;     // pressure BC driven by a Windkessel: rho_b read from Workspace::drv_rho[k]
 };
 
 // Pose of a movable port for the device cell enumeration (sphbuf_motion.cu):
@@ -59,6 +60,30 @@ struct PortEnum {
     double H[3];
     int cx0, cy0, ncx, ncy, f0, f1;
     int k;
+};
+
+// Device state of a Windkessel driver (sph_drivers_step).
+struct DriverDev {
+    double P;        // boundary pressure
+    double Q;        // flow rate of the last step
+    double Qprev;    // flow rate of the step before
+    int first;       // no step taken yet (Qprev := Q)
+    int pad;
+};
+
+// One Windkessel port for the driver kernel (by value).
+struct DriverEntry {
+    int k, run0, nrun, pad;
+    float u[3];      // the port's axis (row 0 of Q)
+    float pad2;
+    double sign;     // +1 outlet, -1 inlet / bidirectional (flow out of the domain is positive)
+    double scale;    // V / a
+    double Rp, C, Rd, rho0, c0sq, dt;
+};
+
+struct DriverLaunch {
+    int n;
+    DriverEntry e[SPH_MAX_PORTS];
 };
 
 struct PortTable {
@@ -118,6 +143,8 @@ struct Workspace {
     unsigned *sub_off;               // [cmp sub-tiles]: tombstones before each sub-tile
     unsigned *rd;                    // [cmp sub-tiles]: "read done" epoch flags
     int *runs;                       // [kMaxRuns * 3]: c0, c1, port
+    DriverDev *drv;                  // [SPH_MAX_PORTS]: Windkessel state
+    float *drv_rho;                  // [SPH_MAX_PORTS]: recycled density of driven pressure BCs
     long long *run_off;              // [kMaxRuns + 1]
     float *sx, *sy, *sz, *svx, *svy, *svz;
     float *sextra[SPH_MAX_EXTRA];
@@ -132,7 +159,7 @@ struct Workspace {
 enum KernelId {
     KID_ADVECT, KID_REGISTER, KID_CLL_KEY, KID_CELL_SCAN, KID_CLL_SCATTER, KID_CLL_GATHER, KID_UPD_PROLOGUE,
     KID_UPD_MAIN, KID_COMPACT, KID_COMPACT_APPEND, KID_MIG_PACK, KID_MIG_UNPACK, KID_COMPACT_COUNT, KID_CLL_RANK,
-    KID_PORT_MOVE, KID_PORT_ENUM, KID_COUNT
+    KID_PORT_MOVE, KID_PORT_ENUM, KID_DRIVERS, KID_COUNT
 };
 
 // Counts launches; when profiling is on, brackets every launch with a pair of
@@ -179,6 +206,8 @@ cudaError_t launch_port_move(const PartDev &p, int dim, const PortDev &P0, const
                              cudaStream_t s, Launch *L);
 cudaError_t launch_port_enum(const GridDev &g, const PortEnum &P, float cs, int *runs, int cap, cudaStream_t s,
                              Launch *L);
+cudaError_t launch_drivers(const PartDev &p, const Workspace &ws, const DriverLaunch &D, const int *cell_start,
+                           const int *cell_end, cudaStream_t s, Launch *L);
 int sm_count();
 
 }  // namespace sphbuf

@@ -248,7 +248,8 @@ __global__ void __launch_bounds__(kThreads) k_upd_main(PartDev p, int dim, const
                 u = __fadd_rn(__fmul_rn(p.vx[pi], P.Q[0]), __fmul_rn(p.vy[pi], P.Q[1]));
                 if (dim == 3) u = __fadd_rn(u, __fmul_rn(p.vz[pi], P.Q[2]));
                 // recycled particles: rho = rho0 + p_b / c0^2 (Eq. postulate-density)
-                if (cr[it] && P.rho_col >= 0) p.extra[P.rho_col][pi] = P.rho_b;
+                // (a Windkessel-driven port reads the density of this step from the device)
+                if (cr[it] && P.rho_col >= 0) p.extra[P.rho_col][pi] = P.rho_dev ? ws.drv_rho[kk[it]] : P.rho_b;
             } else {
                 // v_X' from the profile (Eqs. 2D/3D_velocity_profile), v = Q^T (v_X', 0, 0)
                 u = P.u0;

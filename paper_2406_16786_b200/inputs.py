@@ -55,6 +55,41 @@ class BC:
     radius: float = 1.0
 
 
+DRIVER_NONE, DRIVER_FOURIER, DRIVER_WINDKESSEL = 0, 1, 2
+
+# Table I: Fourier coefficients of the aortic inflow speed; the
+# duplicated label "b_7" of the last row is read as b_8.
+TABLE_I_A = (0.3782, -0.1812, 0.1276, -0.08981, 0.04347, -0.05412, 0.02642, 0.008946, -0.009005)
+TABLE_I_B = (0.0, -0.07725, 0.01466, 0.04295, -0.06679, 0.05679, -0.01878, 0.01869, -0.01888)
+TABLE_I_OMEGA = 8.302
+# Table II: RCR Windkessel parameters, CGS units (dyn s/cm^5, cm^5/dyn)
+TABLE_II = {"right common carotid": (1180.0, 7.70e-5, 18400.0), "right subclavian": (1040.0, 8.74e-5, 16300.0),
+            "left common carotid": (1180.0, 7.70e-5, 18400.0), "left subclavian": (970.0, 9.34e-5, 15200.0),
+            "descending aorta": (188.0, 4.82e-4, 2950.0)}
+DYN_S_CM5 = 1e5              # 1 dyn s/cm^5 = 1e5 Pa s/m^3
+CM5_DYN = 1e-5               # 1 cm^5/dyn = 1e-5 m^3/Pa
+
+
+def windkessel_si(vessel: str) -> tuple:
+    """(Rp, C, Rd) of a Table II vessel in SI units."""
+    Rp, Cc, Rd = TABLE_II[vessel]
+    return Rp * DYN_S_CM5, Cc * CM5_DYN, Rd * DYN_S_CM5
+
+
+@dataclass
+class Driver:
+    """Time-dependent port driver (aorta flow, §V.D), as plain data."""
+    kind: int = DRIVER_NONE
+    a: tuple = (0.0,) * 9
+    b: tuple = (0.0,) * 9
+    omega: float = 0.0
+    Rp: float = 0.0
+    C: float = 0.0
+    Rd: float = 0.0
+    P0: float = 0.0
+    volume: float = 0.0
+
+
 @dataclass
 class Port:
     origin: tuple            # O' (global), binary32 values
@@ -63,6 +98,7 @@ class Port:
     kind: int                # INLET / OUTLET / BIDIRECTIONAL
     layers: int
     bc: BC = None            # optional boundary condition of its buffer particles
+    driver: Driver = None    # optional time-dependent driver of that boundary condition
 
 
 @dataclass

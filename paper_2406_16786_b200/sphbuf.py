@@ -11,6 +11,7 @@ workspace, and runs advect -> sph_cll_build -> sph_buffer_update -> sph_compact.
 from __future__ import annotations
 
 import ctypes as C
+import dataclasses
 import os
 
 import torch
@@ -48,6 +49,12 @@ class sph_bc(C.Structure):
                 ("rho_column", C.c_int32), ("profile", C.c_int32), ("u0", C.c_float), ("radius", C.c_float)]
 
 
+class sph_driver(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("a", C.c_double * 9), ("b", C.c_double * 9), ("omega", C.c_double),
+                ("Rp", C.c_double), ("C", C.c_double), ("Rd", C.c_double), ("P0", C.c_double),
+                ("volume", C.c_double)]
+
+
 class sph_stats(C.Structure):
     _fields_ = [("n", C.c_int64), ("candidates", C.c_int64), ("created", C.c_int64), ("deleted", C.c_int64),
                 ("checked_total", C.c_int64), ("out_of_grid", C.c_int64), ("motion_errors", C.c_int64),
@@ -61,7 +68,8 @@ EXPORTS = ["sph_ctx_create", "sph_ctx_destroy", "sph_last_error", "sph_workspace
            "sph_compact", "sph_migrate_record_floats", "sph_migrate_pack", "sph_migrate_unpack", "sph_status_sync",
            "sph_launch_count", "sph_port_cells", "sph_frame_from_axis", "sph_profile", "sph_profile_read",
            "sph_kernel_name", "sph_advect_cll_build", "sph_compact_deferred", "sph_cll_key", "sph_cll_finish",
-           "sph_port_set_bc", "sph_port_move"]
+           "sph_port_set_bc", "sph_port_move", "sph_port_set_driver",
+           "sph_drivers_step", "sph_driver_read"]
 NKERNELS = 16
 
 
@@ -92,6 +100,12 @@ def lib():
     L.sph_advect_cll_build.restype = C.c_int
     L.sph_port_set_bc.argtypes = [vp, i32, P(sph_bc)]
     L.sph_port_set_bc.restype = C.c_int
+    L.sph_port_set_driver.argtypes = [vp, i32, P(sph_driver)]
+    L.sph_port_set_driver.restype = C.c_int
+    L.sph_drivers_step.argtypes = [vp, P(sph_particles), C.c_double, C.c_double, vp, vp, vp]
+    L.sph_drivers_step.restype = C.c_int
+    L.sph_driver_read.argtypes = [vp, i32, vp, vp]
+    L.sph_driver_read.restype = C.c_int
     L.sph_port_move.argtypes = [vp, P(sph_particles), i32, vp, vp, vp, vp, vp]
     L.sph_port_move.restype = C.c_int
     L.sph_cll_key.argtypes = [vp, P(sph_particles), f32, i32, vp, vp, vp]
@@ -210,6 +224,28 @@ def sph_port_set_bc(ctx, port_id, bc):
     for f, _ in sph_bc._fields_:
         setattr(B, f, getattr(bc, f))
     _check(lib().sph_port_set_bc(ctx.h, int(port_id), C.byref(B)), ctx.h)
+
+
+def sph_port_set_driver(ctx, port_id, drv):
+    """drv: an object with kind, a, b, omega, Rp, C, Rd, P0, volume (inputs.Driver)."""
+    D = sph_driver()
+    D.kind = int(drv.kind)
+    D.a[:] = [float(v) for v in drv.a]
+    D.b[:] = [float(v) for v in drv.b]
+    for f in ("omega", "Rp", "C", "Rd", "P0", "volume"):
+        setattr(D, f, float(getattr(drv, f)))
+    _check(lib().sph_port_set_driver(ctx.h, int(port_id), C.byref(D)), ctx.h)
+
+
+def sph_drivers_step(ctx, parts, t, dt, cell_start, cell_end, stream=None):
+    _check(lib().sph_drivers_step(ctx.h, C.byref(parts.abi), float(t), float(dt), _ptr(cell_start), _ptr(cell_end),
+                                  _stream(stream)), ctx.h)
+
+
+def sph_driver_read(ctx, port_id, stream=None) -> dict:
+    out = (C.c_double * 3)()
+    _check(lib().sph_driver_read(ctx.h, int(port_id), out, _stream(stream)), ctx.h)
+    return {"P": out[0], "Q": out[1], "u0": out[2]}
 
 
 def sph_advect(ctx, parts, dt, stream=None):
@@ -409,6 +445,8 @@ class BufferUpdater:
             assert pid == k
             if getattr(p, "bc", None) is not None and p.bc.kind:
                 sph_port_set_bc(self.ctx, k, p.bc)
+            if getattr(p, "driver", None) is not None and p.driver.kind:
+                sph_port_set_driver(self.ctx, k, p.driver)
         self.registered = True
 
     # --- one update (the hot path); nothing here synchronises
@@ -426,13 +464,23 @@ class BufferUpdater:
     def update(self, stream=None):
         sph_buffer_update(self.ctx, self.A, self.cell_start, self.cell_end, self.port_counts, stream)
 
+    def drivers_step(self, t, dt, stream=None):
+        """Advance the ports' time-dependent drivers to time t (after the build)."""
+        sph_drivers_step(self.ctx, self.A, t, dt, self.cell_start, self.cell_end, stream)
+
+    def driver_state(self, k) -> dict:
+        return sph_driver_read(self.ctx, k)
+
     def move_port(self, k, origin, Q, stream=None):
         """Re-establish port k at the pose (origin, Q) after this step's update (moving
         port): its buffer particles keep local coordinates and velocities."""
         sph_port_move(self.ctx, self.A, k, origin, Q, self.cell_start, self.cell_end, stream)
         p = self.ports[k]
-        self.ports[k] = type(p)(tuple(float(v) for v in origin), tuple(float(v) for v in Q), p.half_extents,
-                                p.kind, p.layers, getattr(p, "bc", None))
+        o, q = tuple(float(v) for v in origin), tuple(float(v) for v in Q)
+        if dataclasses.is_dataclass(p):
+            self.ports[k] = dataclasses.replace(p, origin=o, Q=q)
+        else:
+            p.origin, p.Q = o, q
 
     def compact(self, all_counts=None, nranks=1, rank=0, perm=None, stream=None, deferred=False):
         """IDs + compaction (sph_compact), or IDs + append with the removal left to
