@@ -332,7 +332,7 @@ __device__ __forceinline__ int rank_in_cell(const PartDev &in, const Workspace &
 // is ranked from shared memory as well; the store goes to the sorted position.
 // Loads are nearly sequential (only particles that changed cell come from far
 // away); stores stay inside the cell.
-template <bool HasExtra, int ITEMS, int MINB, int NT = kThreads>
+template <bool HasExtra, int ITEMS, int MINB, int NT = kThreads, bool PF = false>
 __global__ void __launch_bounds__(NT, MINB) k_cll_gather(PartDev in, PartDev out, GridDev g, Workspace ws,
                                                                const int *cell_start, const int *cell_end, int *perm,
                                                                int advect, float dt)
@@ -346,18 +346,39 @@ __global__ void __launch_bounds__(NT, MINB) k_cll_gather(PartDev in, PartDev out
     // sources below mig_base are this slab's own particles (advected here when the
     // build fused the advection); received migrants were advected by their sender
     const long long adv_lim = advect ? ws.ctr->mig_base : 0;
-    for (long long j0 = (long long)blockIdx.x * T; j0 < n; j0 += (long long)gridDim.x * T) {
+    const long long stride = (long long)gridDim.x * T;
+    // PF: the slot -> source map of the next tile is loaded while this tile's
+    // columns are in flight (one dependent DRAM round trip less per tile)
+    int nsrc[ITEMS], nhsrc = 0;
+    auto load_map = [&](long long jb, int (&sv)[ITEMS], int &hs) {
+#pragma unroll
+        for (int it = 0; it < ITEMS; ++it) {
+            const long long j = jb + it * NT + threadIdx.x;
+            sv[it] = j < n ? ws.src[j] : -1;
+        }
+        const long long jh = threadIdx.x < kHalo ? jb - kHalo + threadIdx.x : jb + T + (threadIdx.x - kHalo);
+        hs = (threadIdx.x < 2 * kHalo && jh >= 0 && jh < n) ? ws.src[jh] : -1;
+    };
+    if (PF) load_map((long long)blockIdx.x * T, nsrc, nhsrc);
+    for (long long j0 = (long long)blockIdx.x * T; j0 < n; j0 += stride) {
         int src[ITEMS], cb[ITEMS], ce[ITEMS], lab[ITEMS];
         float x[ITEMS], y[ITEMS], z[ITEMS], vx[ITEMS], vy[ITEMS], vz[ITEMS];
         long long id[ITEMS];
         // halo ids (threads 0 .. 2 kHalo - 1): two dependent loads, issued first
         const long long jh = threadIdx.x < kHalo ? j0 - kHalo + threadIdx.x : j0 + T + (threadIdx.x - kHalo);
         const bool hv = threadIdx.x < 2 * kHalo && jh >= 0 && jh < n;
-        const int hsrc = hv ? ws.src[jh] : 0;
+        int hsrc;
+        if (PF) {
+            hsrc = nhsrc;
 #pragma unroll
-        for (int it = 0; it < ITEMS; ++it) {
-            const long long j = j0 + it * NT + threadIdx.x;
-            src[it] = j < n ? ws.src[j] : -1;
+            for (int it = 0; it < ITEMS; ++it) src[it] = nsrc[it];
+        } else {
+            hsrc = hv ? ws.src[jh] : 0;
+#pragma unroll
+            for (int it = 0; it < ITEMS; ++it) {
+                const long long j = j0 + it * NT + threadIdx.x;
+                src[it] = j < n ? ws.src[j] : -1;
+            }
         }
         const long long hid = hv ? in.id[hsrc] : 0;
 #pragma unroll
@@ -376,6 +397,7 @@ __global__ void __launch_bounds__(NT, MINB) k_cll_gather(PartDev in, PartDev out
             id[it] = in.id[s];
             lab[it] = in.label[s];
         }
+        if (PF) load_map(j0 + stride, nsrc, nhsrc);
         bool wide = hv && (hid >> 32) != 0;
         if (threadIdx.x < 2 * kHalo) {
             const int hq = threadIdx.x < kHalo ? threadIdx.x : T + threadIdx.x;
@@ -433,13 +455,13 @@ __global__ void __launch_bounds__(NT, MINB) k_cll_gather(PartDev in, PartDev out
 
 // Gather variants (template instances), chosen by SPHBUF_GATHER=<slots>:<min blocks>
 // for tuning runs (tools/gather_sweep.py); the default is the measured best.
-template <bool HasExtra, int ITEMS, int MINB, int NT = kThreads>
+template <bool HasExtra, int ITEMS, int MINB, int NT = kThreads, bool PF = false>
 static void gather_fused(const PartDev &in, const PartDev &out, const GridDev &g, const Workspace &ws,
                          const int *cs, const int *ce, int *perm, int advect, float dt, long long cap, cudaStream_t s)
 {
     static int grid = 0;
-    if (!grid) grid = occ_grid(k_cll_gather<HasExtra, ITEMS, MINB, NT>, NT);
-    k_cll_gather<HasExtra, ITEMS, MINB, NT><<<cap_grid(grid, cap, NT * ITEMS), NT, 0, s>>>(in, out, g, ws, cs, ce,
+    if (!grid) grid = occ_grid(k_cll_gather<HasExtra, ITEMS, MINB, NT, PF>, NT);
+    k_cll_gather<HasExtra, ITEMS, MINB, NT, PF><<<cap_grid(grid, cap, NT * ITEMS), NT, 0, s>>>(in, out, g, ws, cs, ce,
                                                                                          perm, advect, dt);
 }
 
@@ -454,15 +476,15 @@ static void gather_variant(const char *v, const PartDev &in, const PartDev &out,
         return;                                                                         \
     }
     SPH_GV("1:8", 1, 8)
+    SPH_GV("2:6", 2, 6)
     SPH_GV("3:4", 3, 4)
-    SPH_GV("2:8", 2, 8)
     SPH_GV("4:3", 4, 3)
-    SPH_GV("4:4", 4, 4)
+    if (!strcmp(v, "pf3:4")) return gather_fused<HasExtra, 3, 4, kThreads, true>(in, out, g, ws, cs, ce, perm, advect, dt, cap, s);
 #undef SPH_GV
-    // default: 2 slots per thread at <= 40 registers (6 blocks/SM), measured best
-    // on C5 among the variants above and 128- / 512-thread blocks
-    // (tools/gather_sweep.py)
-    gather_fused<HasExtra, 2, 6>(in, out, g, ws, cs, ce, perm, advect, dt, cap, s);
+    // default: 2 slots per thread, the next tile's slot map prefetched, <= 48
+    // registers (5 blocks/SM): measured best on C5 among the variants above,
+    // 128- / 512-thread blocks and cp.async / warp-chunk designs
+    gather_fused<HasExtra, 2, 5, kThreads, true>(in, out, g, ws, cs, ce, perm, advect, dt, cap, s);
 }
 
 static void launch_gather(const PartDev &in, const PartDev &out, const GridDev &g, const Workspace &ws,

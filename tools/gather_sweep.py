@@ -16,7 +16,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-VARIANTS = ["", "1:8", "3:4", "2:8", "4:3", "4:4"]
+VARIANTS = ["", "1:8", "2:6", "3:4", "4:3", "pf3:4"]
 
 
 def child(config, steps):
