@@ -54,6 +54,7 @@ template <bool Advect, bool Migrate>
 __global__ void __launch_bounds__(kThreads) k_cll_key(PartDev in, GridDev g, Workspace ws, float dt, float *mlo,
                                                       float *mhi, long long maxm, int rec)
 {
+    pdl_entry();
     Counters *ctr = ws.ctr;
     const long long n = *in.n;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -152,6 +153,7 @@ __global__ void __launch_bounds__(kThreads) k_cll_key(PartDev in, GridDev g, Wor
 __global__ void __launch_bounds__(kThreads) k_cll_unpack_key(PartDev in, GridDev g, Workspace ws, const float *blo,
                                                              const float *bhi, long long maxm, int rec)
 {
+    pdl_entry();
     Counters *ctr = ws.ctr;
     const long long nlo = blo ? min((long long)__float_as_int(blo[0]), maxm) : 0;
     const long long nhi = bhi ? min((long long)__float_as_int(bhi[0]), maxm) : 0;
@@ -196,6 +198,7 @@ __global__ void __launch_bounds__(kThreads) k_cll_unpack_key(PartDev in, GridDev
 __global__ void __launch_bounds__(kThreads) k_cell_scan(GridDev g, Workspace ws, int *cell_start, int *cell_end,
                                                         long long *n_out, long long ntiles)
 {
+    pdl_entry();
     constexpr int V = kCellItems / 4;
     __shared__ unsigned s_warp[kThreads / 32 + 1];
     __shared__ long long s_tile;
@@ -273,6 +276,7 @@ constexpr int kScatterItems = 4;
 // K3: source index of every sorted slot (slot = cell_start[key] + atomic rank).
 __global__ void __launch_bounds__(kThreads) k_cll_scatter(Workspace ws, const int *cell_start, int *perm)
 {
+    pdl_entry();
     const long long n = ws.ctr->n_in;
     const long long stride = (long long)gridDim.x * kThreads * kScatterItems;
     for (long long base = (long long)blockIdx.x * kThreads * kScatterItems; base < n; base += stride) {
@@ -337,6 +341,7 @@ __global__ void __launch_bounds__(NT, MINB) k_cll_gather(PartDev in, PartDev out
                                                                const int *cell_start, const int *cell_end, int *perm,
                                                                int advect, float dt)
 {
+    pdl_entry();
     constexpr int T = NT * ITEMS;
     static_assert(2 * kHalo <= NT, "one halo slot per thread");
     __shared__ long long s_id[kHalo + T + kHalo];
@@ -461,7 +466,7 @@ static void gather_fused(const PartDev &in, const PartDev &out, const GridDev &g
 {
     static int grid = 0;
     if (!grid) grid = occ_grid(k_cll_gather<HasExtra, ITEMS, MINB, NT, PF>, NT);
-    k_cll_gather<HasExtra, ITEMS, MINB, NT, PF><<<cap_grid(grid, cap, NT * ITEMS), NT, 0, s>>>(in, out, g, ws, cs, ce,
+    launch_k(k_cll_gather<HasExtra, ITEMS, MINB, NT, PF>, dim3(cap_grid(grid, cap, NT * ITEMS)), dim3(NT), 0, s, in, out, g, ws, cs, ce,
                                                                                          perm, advect, dt);
 }
 
@@ -508,7 +513,7 @@ static void key_launch(const PartDev &in, const GridDev &g, const Workspace &ws,
 {
     static int grid = 0;
     if (!grid) grid = occ_grid(k_cll_key<A, M>, kThreads);
-    k_cll_key<A, M><<<cap_grid(grid, in.cap, kThreads * kKeyItems), kThreads, 0, s>>>(in, g, ws, dt, lo, hi, maxm,
+    launch_k(k_cll_key<A, M>, dim3(cap_grid(grid, in.cap, kThreads * kKeyItems)), dim3(kThreads), 0, s, in, g, ws, dt, lo, hi, maxm,
                                                                                         rec);
 }
 
@@ -547,18 +552,18 @@ cudaError_t launch_cll_finish(const PartDev &in, const PartDev &out, const GridD
     const long long cap = in.cap;
     if (recv_lo || recv_hi) {
         L->before(s);
-        k_cll_unpack_key<<<cap_grid(sm_count_cached() * 2, maxm * 2, kThreads), kThreads, 0, s>>>(
+        launch_k(k_cll_unpack_key, dim3(cap_grid(sm_count_cached() * 2, maxm * 2, kThreads)), dim3(kThreads), 0, s, 
             in, g, ws, recv_lo, recv_hi, maxm, rec);
         L->after(s, KID_MIG_UNPACK);
     }
     L->before(s);
-    k_cell_scan<<<(unsigned)(ntiles > 0 ? ntiles : 1), kThreads, 0, s>>>(g, ws, cell_start, cell_end, out.n, ntiles);
+    launch_k(k_cell_scan, dim3((unsigned)(ntiles > 0 ? ntiles : 1)), dim3(kThreads), 0, s, g, ws, cell_start, cell_end, out.n, ntiles);
     L->after(s, KID_CELL_SCAN);
     {
         static int grid = 0;
         if (!grid) grid = occ_grid(k_cll_scatter, kThreads);
         L->before(s);
-        k_cll_scatter<<<cap_grid(grid, cap, kThreads * kScatterItems), kThreads, 0, s>>>(ws, cell_start, perm);
+        launch_k(k_cll_scatter, dim3(cap_grid(grid, cap, kThreads * kScatterItems)), dim3(kThreads), 0, s, ws, cell_start, perm);
         L->after(s, KID_CLL_SCATTER);
     }
     L->before(s);

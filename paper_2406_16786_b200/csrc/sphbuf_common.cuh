@@ -9,12 +9,22 @@
 #pragma once
 #include <climits>
 #include <cstdint>
+#include <cstdlib>
+#include <utility>
 
 #include "sphbuf_internal.h"
 
 namespace sphbuf {
 
 // ------------------------------------------------------------------ helpers
+
+// Programmatic dependent launch (sm_90+): every kernel of the path is launched
+// with launch_k() below and waits here for the kernel before it on the stream to
+// complete with its memory visible.  The dependent grid is released as this
+// grid's blocks exit (no early trigger: early-launched blocks would take SM
+// slots from the running grid), so only the launch gap between kernels is
+// hidden.  Without the launch attribute the instruction is a no-op.
+__device__ __forceinline__ void pdl_entry() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 __device__ __forceinline__ unsigned lanemask_lt()
 {
@@ -258,6 +268,35 @@ __device__ __forceinline__ int cell_of(const GridDev &g, float x, float y, float
 }
 
 // ------------------------------------------------------------------ launch helpers (host)
+
+// Launch with the programmatic-stream-serialization attribute (see pdl_entry);
+// SPHBUF_PDL=0 in the environment launches plainly (A/B timing).
+inline bool pdl_enabled()
+{
+    static int on = -1;
+    if (on < 0) {
+        const char *v = getenv("SPHBUF_PDL");
+        on = (v && v[0] == '0') ? 0 : 1;
+    }
+    return on == 1;
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                            Args &&...args)
+{
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 inline int sm_count_cached()
 {

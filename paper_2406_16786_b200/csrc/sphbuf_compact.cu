@@ -32,6 +32,7 @@ __device__ __forceinline__ long long cmp_begin(long long i_first) { return (i_fi
 
 __global__ void __launch_bounds__(kThreads) k_compact_count(PartDev p, Workspace ws, const long long *next_id)
 {
+    pdl_entry();
     __shared__ unsigned s_sub[kCntSub][kThreads / 32];
     __shared__ unsigned s_tot[kCntSub + 1];
     __shared__ long long s_tile;
@@ -93,6 +94,7 @@ __global__ void __launch_bounds__(kThreads) k_compact_count(PartDev p, Workspace
 template <bool HasExtra>
 __global__ void __launch_bounds__(kThreads) k_compact_move(PartDev p, int dim, Workspace ws, int *perm)
 {
+    pdl_entry();
     __shared__ unsigned s_cnt[kCmpItems * kThreads / 32 + 1];
     __shared__ long long s_tile;
     Counters *ctr = ws.ctr;
@@ -210,6 +212,7 @@ __global__ void __launch_bounds__(kThreads) k_compact_append(PartDev p, int dim,
                                                              Workspace ws, const int *all_counts, int nranks,
                                                              int rank, long long *next_id, int *perm, bool defer)
 {
+    pdl_entry();
     __shared__ long long s_off[SPH_MAX_PORTS];
     __shared__ long long s_beg[SPH_MAX_PORTS];
     __shared__ long long s_total;
@@ -281,7 +284,7 @@ cudaError_t launch_compact(const PartDev &p, const PortTable &pt, const Workspac
     const int dim = p.z ? 3 : 2;
     if (defer) {
         L->before(s);
-        k_compact_append<<<1, kThreads, 0, s>>>(p, dim, pt.n, pt.max_ports, ws, all_counts, nranks, rank, next_id,
+        launch_k(k_compact_append, dim3(1), dim3(kThreads), 0, s, p, dim, pt.n, pt.max_ports, ws, all_counts, nranks, rank, next_id,
                                                 nullptr, true);
         L->after(s, KID_COMPACT_APPEND);
         return cudaGetLastError();
@@ -290,22 +293,22 @@ cudaError_t launch_compact(const PartDev &p, const PortTable &pt, const Workspac
         static int grid = 0;
         if (!grid) grid = occ_grid(k_compact_count, kThreads);
         L->before(s);
-        k_compact_count<<<cap_grid(grid, p.cap, kCntTile), kThreads, 0, s>>>(p, ws, next_id);
+        launch_k(k_compact_count, dim3(cap_grid(grid, p.cap, kCntTile)), dim3(kThreads), 0, s, p, ws, next_id);
         L->after(s, KID_COMPACT_COUNT);
     }
     L->before(s);
     if (p.n_extra > 0) {
         static int grid = 0;
         if (!grid) grid = occ_grid(k_compact_move<true>, kThreads);
-        k_compact_move<true><<<cap_grid(grid, p.cap, kCmpTile), kThreads, 0, s>>>(p, dim, ws, perm);
+        launch_k(k_compact_move<true>, dim3(cap_grid(grid, p.cap, kCmpTile)), dim3(kThreads), 0, s, p, dim, ws, perm);
     } else {
         static int grid = 0;
         if (!grid) grid = occ_grid(k_compact_move<false>, kThreads);
-        k_compact_move<false><<<cap_grid(grid, p.cap, kCmpTile), kThreads, 0, s>>>(p, dim, ws, perm);
+        launch_k(k_compact_move<false>, dim3(cap_grid(grid, p.cap, kCmpTile)), dim3(kThreads), 0, s, p, dim, ws, perm);
     }
     L->after(s, KID_COMPACT);
     L->before(s);
-    k_compact_append<<<cap_grid(sm_count_cached() * 4, perm ? p.cap : ws.max_new, kThreads), kThreads, 0, s>>>(
+    launch_k(k_compact_append, dim3(cap_grid(sm_count_cached() * 4, perm ? p.cap : ws.max_new, kThreads)), dim3(kThreads), 0, s, 
         p, dim, pt.n, pt.max_ports, ws, all_counts, nranks, rank, next_id, perm, false);
     L->after(s, KID_COMPACT_APPEND);
     return cudaGetLastError();

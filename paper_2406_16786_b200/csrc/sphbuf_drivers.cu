@@ -30,6 +30,7 @@ __device__ __forceinline__ long long flux_fixed(float vx, float vy, float vz, co
 __global__ void __launch_bounds__(256) k_drivers(PartDev p, int dim, Workspace ws, const __grid_constant__ DriverLaunch D,
                                                  const int *cell_start, const int *cell_end)
 {
+    pdl_entry();
     __shared__ long long s_part[256 / 32];
     const DriverEntry &E = D.e[blockIdx.x];
     long long sum = 0;
@@ -76,7 +77,7 @@ cudaError_t launch_drivers(const PartDev &p, const Workspace &ws, const DriverLa
 {
     if (D.n <= 0) return cudaSuccess;
     L->before(s);
-    k_drivers<<<D.n, 256, 0, s>>>(p, p.z ? 3 : 2, ws, D, cell_start, cell_end);
+    launch_k(k_drivers, dim3(D.n), dim3(256), 0, s, p, p.z ? 3 : 2, ws, D, cell_start, cell_end);
     L->after(s, KID_DRIVERS);
     return cudaGetLastError();
 }

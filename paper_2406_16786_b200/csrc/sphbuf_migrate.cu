@@ -13,6 +13,7 @@ namespace sphbuf {
 __global__ void __launch_bounds__(kThreads) k_mig_pack(PartDev p, GridDev g, Workspace ws, float *blo, float *bhi,
                                                        long long maxm, int rec)
 {
+    pdl_entry();
     const long long n = *p.n;
     long long moved = 0;
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
@@ -50,6 +51,7 @@ __global__ void __launch_bounds__(kThreads) k_mig_pack(PartDev p, GridDev g, Wor
 __global__ void __launch_bounds__(1024) k_mig_unpack(PartDev p, int dim, Workspace ws, const float *buf,
                                                      long long maxm, int rec)
 {
+    pdl_entry();
     const long long n = *p.n;
     long long cnt = __float_as_int(buf[0]);
     if (cnt > maxm) cnt = maxm;
@@ -87,7 +89,7 @@ cudaError_t launch_migrate_pack(const PartDev &p, const GridDev &g, const Worksp
     if (e == cudaSuccess) e = cudaMemsetAsync(hi, 0, 16, s);
     if (e != cudaSuccess) return e;
     L->before(s);
-    k_mig_pack<<<cap_grid(sm_count_cached() * 8, p.cap, kThreads), kThreads, 0, s>>>(p, g, ws, lo, hi, max_migrate, rec);
+    launch_k(k_mig_pack, dim3(cap_grid(sm_count_cached() * 8, p.cap, kThreads)), dim3(kThreads), 0, s, p, g, ws, lo, hi, max_migrate, rec);
     L->after(s, KID_MIG_PACK);
     return cudaGetLastError();
 }
@@ -96,7 +98,7 @@ cudaError_t launch_migrate_unpack(const PartDev &p, const GridDev &g, const Work
                                   long long max_migrate, int rec, cudaStream_t s, Launch *L)
 {
     L->before(s);
-    k_mig_unpack<<<1, 1024, 0, s>>>(p, g.dim, ws, buf, max_migrate, rec);
+    launch_k(k_mig_unpack, dim3(1), dim3(1024), 0, s, p, g.dim, ws, buf, max_migrate, rec);
     L->after(s, KID_MIG_UNPACK);
     return cudaGetLastError();
 }

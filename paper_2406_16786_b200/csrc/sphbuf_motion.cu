@@ -50,6 +50,7 @@ __global__ void __launch_bounds__(kThreads) k_port_move(PartDev p, int dim, Port
                                                         int nrun, const int *cell_start, const int *cell_end, int k,
                                                         long long *moved)
 {
+    pdl_entry();
     long long cnt = 0;
     for (int r = blockIdx.x; r < nrun; r += gridDim.x) {
         const int c0 = runs[3 * r], c1 = runs[3 * r + 1];
@@ -113,6 +114,7 @@ __device__ bool cell_meets_port(const double c[3], const double e[3], const Port
 // port's candidates stay in cell order and creations in canonical order (R14).
 __global__ void __launch_bounds__(kThreads) k_port_enum(GridDev g, PortEnum P, float cs, int *runs, int cap)
 {
+    pdl_entry();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= cap) return;
     const int dim = g.dim;
@@ -156,7 +158,7 @@ cudaError_t launch_port_move(const PartDev &p, int dim, const PortDev &P0, const
 {
     if (nrun <= 0) return cudaSuccess;
     L->before(s);
-    k_port_move<<<nrun < 4 * sm_count_cached() ? nrun : 4 * sm_count_cached(), 128, 0, s>>>(
+    launch_k(k_port_move, dim3(nrun < 4 * sm_count_cached() ? nrun : 4 * sm_count_cached()), dim3(128), 0, s, 
         p, dim, P0, P1, runs, nrun, cell_start, cell_end, k, moved);
     L->after(s, KID_PORT_MOVE);
     return cudaGetLastError();
@@ -167,7 +169,7 @@ cudaError_t launch_port_enum(const GridDev &g, const PortEnum &P, float cs, int 
 {
     if (cap <= 0) return cudaSuccess;
     L->before(s);
-    k_port_enum<<<(cap + kThreads - 1) / kThreads, kThreads, 0, s>>>(g, P, cs, runs, cap);
+    launch_k(k_port_enum, dim3((cap + kThreads - 1) / kThreads), dim3(kThreads), 0, s, g, P, cs, runs, cap);
     L->after(s, KID_PORT_ENUM);
     return cudaGetLastError();
 }

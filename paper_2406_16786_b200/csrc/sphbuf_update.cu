@@ -13,6 +13,7 @@ namespace sphbuf {
 
 __global__ void __launch_bounds__(kThreads) k_advect(PartDev p, int dim, float dt)
 {
+    pdl_entry();
     const long long n = *p.n;
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
         p.x[i] = __fadd_rn(p.x[i], __fmul_rn(p.vx[i], dt));
@@ -28,6 +29,7 @@ __global__ void __launch_bounds__(kThreads) k_advect(PartDev p, int dim, float d
 // the initial relabel of outlet / bidirectional ports.
 __global__ void __launch_bounds__(kThreads) k_register(PartDev p, int dim, PortDev P, int k, long long *members)
 {
+    pdl_entry();
     const long long n = *p.n;
     long long cnt = 0;
     const int lane = threadIdx.x & 31;
@@ -57,6 +59,7 @@ __global__ void __launch_bounds__(kThreads) k_register(PartDev p, int dim, PortD
 __global__ void __launch_bounds__(1024) k_upd_prologue(Workspace ws, int n_runs, const int *cell_start,
                                                        const int *cell_end, int *port_counts, int max_ports)
 {
+    pdl_entry();
     __shared__ long long s_warp[1024 / 32 + 1];
     Counters *ctr = ws.ctr;
     if (threadIdx.x == 0) {
@@ -94,6 +97,7 @@ __global__ void __launch_bounds__(kThreads) k_upd_main(PartDev p, int dim, const
                                                        Workspace ws, int n_runs, const int *cell_start,
                                                        int *port_counts)
 {
+    pdl_entry();
     __shared__ PortDev s_ports[SPH_MAX_PORTS];
     __shared__ unsigned s_warp[kUpdItems * kThreads / 32 + 1];
     __shared__ long long s_tile;
@@ -291,7 +295,7 @@ __global__ void __launch_bounds__(kThreads) k_upd_main(PartDev p, int dim, const
 cudaError_t launch_advect(const PartDev &p, int dim, float dt, cudaStream_t s, Launch *L)
 {
     L->before(s);
-    k_advect<<<cap_grid(sm_count_cached() * 8, p.cap, kThreads), kThreads, 0, s>>>(p, dim, dt);
+    launch_k(k_advect, dim3(cap_grid(sm_count_cached() * 8, p.cap, kThreads)), dim3(kThreads), 0, s, p, dim, dt);
     L->after(s, KID_ADVECT);
     return cudaGetLastError();
 }
@@ -300,7 +304,7 @@ cudaError_t launch_register(const PartDev &p, const GridDev &g, const PortTable 
                             cudaStream_t s, Launch *L)
 {
     L->before(s);
-    k_register<<<cap_grid(sm_count_cached() * 8, p.cap, kThreads), kThreads, 0, s>>>(p, g.dim, pt.p[k], k, members);
+    launch_k(k_register, dim3(cap_grid(sm_count_cached() * 8, p.cap, kThreads)), dim3(kThreads), 0, s, p, g.dim, pt.p[k], k, members);
     L->after(s, KID_REGISTER);
     return cudaGetLastError();
 }
@@ -309,12 +313,12 @@ cudaError_t launch_update(const PartDev &p, const GridDev &g, const PortTable &p
                           const int *cell_start, const int *cell_end, int *port_counts, cudaStream_t s, Launch *L)
 {
     L->before(s);
-    k_upd_prologue<<<1, 1024, 0, s>>>(ws, n_runs, cell_start, cell_end, port_counts, pt.max_ports);
+    launch_k(k_upd_prologue, dim3(1), dim3(1024), 0, s, ws, n_runs, cell_start, cell_end, port_counts, pt.max_ports);
     L->after(s, KID_UPD_PROLOGUE);
     static int grid = 0;
     if (!grid) grid = occ_grid(k_upd_main, kThreads);
     L->before(s);
-    k_upd_main<<<cap_grid(grid, ws.upd_tiles, 1), kThreads, 0, s>>>(p, g.dim, pt, ws, n_runs, cell_start, port_counts);
+    launch_k(k_upd_main, dim3(cap_grid(grid, ws.upd_tiles, 1)), dim3(kThreads), 0, s, p, g.dim, pt, ws, n_runs, cell_start, port_counts);
     L->after(s, KID_UPD_MAIN);
     return cudaGetLastError();
 }
