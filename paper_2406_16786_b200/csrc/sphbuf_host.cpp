@@ -136,6 +136,7 @@ size_t layout(const sph_ctx *c, char *base, Workspace *W)
     w.cell_count = (int *)take(sizeof(int) * ncells);
     w.tile_cells = (unsigned long long *)take(8 * cell_tiles);
     w.tile_upd = (unsigned long long *)take(8 * upd_tiles);
+    w.tile_runs = (unsigned long long *)take(8 * (kMaxRuns / 1024 + 1));
     w.tile_cmp = (unsigned long long *)take(8 * cmp_tiles);
     w.rd = (unsigned *)take(4 * cmp_subs);
     w.runs = (int *)take(sizeof(int) * 3 * kMaxRuns);

@@ -128,6 +128,8 @@ struct Counters {
     long long migrated;    // cumulative packed for neighbour slabs
     long long mig_base;    // cll: local count before the received particles are appended
     int status;            // sticky bits
+    int ticket_runs;       // update prologue: tile tickets (reset by its last block)
+    int done_runs;         // update prologue: finished blocks
     int dummy;
 };
 
@@ -139,6 +141,7 @@ struct Workspace {
     int *rank;                       // [capacity]
     int *src;                        // [capacity]: source index of each sorted slot
     unsigned long long *tile_upd;    // [upd tiles]
+    unsigned long long *tile_runs;   // [kMaxRuns / 1024 + 1]: update prologue look-back
     unsigned long long *tile_cmp;    // [cmp count tiles]
     unsigned *sub_off;               // [cmp sub-tiles]: tombstones before each sub-tile
     unsigned *rd;                    // [cmp sub-tiles]: "read done" epoch flags

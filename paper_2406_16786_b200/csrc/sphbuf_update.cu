@@ -55,38 +55,65 @@ __global__ void __launch_bounds__(kThreads) k_register(PartDev p, int dim, PortD
 // ------------------------------------------------------------------ a3-a6: buffer update
 
 // K5: candidate count per port run (cell ranges from the current cell list) and
-// their exclusive scan; resets the per-update counters.  One block.
+// their exclusive scan over 1024-run tiles (ticket order, decoupled look-back),
+// so any number of runs is scanned by many blocks at once; resets the
+// per-update counters.  The tile tickets and the epoch are advanced by the last
+// block to finish (done counter), so the kernel needs no other launch.
 __global__ void __launch_bounds__(1024) k_upd_prologue(Workspace ws, int n_runs, const int *cell_start,
                                                        const int *cell_end, int *port_counts, int max_ports)
 {
     pdl_entry();
-    __shared__ long long s_warp[1024 / 32 + 1];
+    __shared__ unsigned s_warp[1024 / 32 + 1];
+    __shared__ int s_tile;
+    __shared__ unsigned s_prefix;
     Counters *ctr = ws.ctr;
-    if (threadIdx.x == 0) {
-        ctr->epoch_upd += 1;
-        ctr->ticket_upd = 0;
-        ctr->n_stage = 0;
-        ctr->n_del = 0;
-        ctr->i_first = LLONG_MAX;
+    const int ntiles = (n_runs + 1023) / 1024;
+    const unsigned epoch = ctr->epoch_upd + 1;
+    if (threadIdx.x == 0) s_tile = atomicAdd(&ctr->ticket_runs, 1);
+    __syncthreads();
+    const int tile = s_tile;
+    if (tile == 0) {
+        if (threadIdx.x == 0) {
+            ctr->ticket_upd = 0;
+            ctr->n_stage = 0;
+            ctr->n_del = 0;
+            ctr->i_first = LLONG_MAX;
+        }
+        for (int i = threadIdx.x; i < 2 * max_ports; i += blockDim.x) port_counts[i] = 0;
     }
-    for (int i = threadIdx.x; i < 2 * max_ports; i += blockDim.x) port_counts[i] = 0;
-    long long carry = 0;
-    for (int r0 = 0; r0 < n_runs; r0 += 1024) {
-        const int r = r0 + threadIdx.x;
-        long long len = 0;
+    if (tile < ntiles) {
+        const int r = tile * 1024 + threadIdx.x;
+        unsigned len = 0;
         // (c1 < c0: an empty slot of a movable port's run slice)
         if (r < n_runs && ws.runs[3 * r + 1] >= ws.runs[3 * r])
-            len = (long long)cell_end[ws.runs[3 * r + 1]] - (long long)cell_start[ws.runs[3 * r]];
-        long long total;
-        const long long ex = block_excl_scan_ll<1024>(len, total, s_warp);
-        if (r < n_runs) ws.run_off[r] = carry + ex;
-        carry += total;
+            len = (unsigned)(cell_end[ws.runs[3 * r + 1]] - cell_start[ws.runs[3 * r]]);
+        unsigned total;
+        const unsigned ex = block_excl_scan<1024>(len, total, s_warp);
+        if (threadIdx.x < 32) {
+            const unsigned pre = tile_prefix(ws.tile_runs, tile, epoch, total);
+            if (threadIdx.x == 0) s_prefix = pre;
+        }
+        __syncthreads();
+        if (r < n_runs) ws.run_off[r] = (long long)s_prefix + ex;
+        if (tile == ntiles - 1 && threadIdx.x == 0) {
+            const long long carry = (long long)s_prefix + total;
+            ws.run_off[n_runs] = carry;
+            ctr->n_cand = carry;
+            ctr->checked += carry;
+            if ((carry + kUpdTile - 1) / kUpdTile > ws.upd_tiles) ctr->status |= kStCapacity;
+        }
+    }
+    if (ntiles == 0 && tile == 0 && threadIdx.x == 0) {
+        ws.run_off[0] = 0;
+        ctr->n_cand = 0;
     }
     if (threadIdx.x == 0) {
-        ws.run_off[n_runs] = carry;
-        ctr->n_cand = carry;
-        ctr->checked += carry;
-        if ((carry + kUpdTile - 1) / kUpdTile > ws.upd_tiles) ctr->status |= kStCapacity;
+        __threadfence();
+        if (atomicAdd(&ctr->done_runs, 1) == (int)gridDim.x - 1) {
+            ctr->done_runs = 0;
+            ctr->ticket_runs = 0;
+            ctr->epoch_upd = epoch;
+        }
     }
 }
 
@@ -313,7 +340,9 @@ cudaError_t launch_update(const PartDev &p, const GridDev &g, const PortTable &p
                           const int *cell_start, const int *cell_end, int *port_counts, cudaStream_t s, Launch *L)
 {
     L->before(s);
-    launch_k(k_upd_prologue, dim3(1), dim3(1024), 0, s, ws, n_runs, cell_start, cell_end, port_counts, pt.max_ports);
+    const int pro_blocks = n_runs > 0 ? (n_runs + 1023) / 1024 : 1;
+    launch_k(k_upd_prologue, dim3(pro_blocks), dim3(1024), 0, s, ws, n_runs, cell_start, cell_end, port_counts,
+             pt.max_ports);
     L->after(s, KID_UPD_PROLOGUE);
     static int grid = 0;
     if (!grid) grid = occ_grid(k_upd_main, kThreads);
