@@ -158,8 +158,8 @@ def test_drivers_oracle_run():
 
 
 @pytest.mark.gpu
-def test_drivers_gpu_parity():
-    w = duct_with_drivers()
+def test_drivers_gpu_parity(n_updates=40):
+    w = duct_with_drivers(n_updates=n_updates)
     st = oracle.to_numpy_state(w.state)
     for k, p in enumerate(w.ports):
         oracle.register(st, w.grid, p, k)

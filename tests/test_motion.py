@@ -144,7 +144,7 @@ def test_sprinkler_oracle_invariants():
 
 
 @pytest.mark.gpu
-def test_sprinkler_gpu_parity():
+def test_sprinkler_gpu_parity(n_steps=200):
     """Lock-step GPU (sph_port_move through the C ABI) vs oracle, 200 updates,
     bit-exact state after every update."""
     w = inputs.make("C6", device="cuda")
@@ -159,7 +159,7 @@ def test_sprinkler_gpu_parity():
     assert_state_equal(bu.state(), st, "after register")
     ports = list(w.ports)
     nid = w.next_id
-    for step in range(200):
+    for step in range(n_steps):
         oracle.advect(st, 2, w.dt)
         res = oracle.update(w.grid, ports, st)
         new, perm, nid = oracle.compact(res, 2, K, res.port_counts[None, :], 0, nid)
@@ -216,7 +216,7 @@ def test_rotating_port_3d_oracle_invariants():
 
 
 @pytest.mark.gpu
-def test_rotating_port_3d_gpu_parity():
+def test_rotating_port_3d_gpu_parity(n_steps=100):
     """C7 on the GPU (3-D K9 move, 3-D K10 enumeration) vs the oracle, 100 updates,
     bit-exact; the in-place compaction every update."""
     w = inputs.make("C7", device="cuda")
@@ -229,7 +229,7 @@ def test_rotating_port_3d_gpu_parity():
     bu.register_ports()
     ports = list(w.ports)
     nid = w.next_id
-    for step in range(100):
+    for step in range(n_steps):
         oracle.advect(st, 3, w.dt)
         res = oracle.update(w.grid, ports, st)
         new, perm, nid = oracle.compact(res, 3, K, res.port_counts[None, :], 0, nid)
