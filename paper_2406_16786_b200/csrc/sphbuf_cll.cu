@@ -294,6 +294,7 @@ __global__ void __launch_bounds__(kThreads) k_cll_scatter(Workspace ws, const in
         for (int it = 0; it < kScatterItems; ++it) {
             const long long i = base + it * kThreads + threadIdx.x;
             if (i >= n) continue;
+            SPH_CHECK(key[it] < 0 || __ldg(cell_start + key[it]) + rk[it] < n);
             if (key[it] >= 0) ws.src[__ldg(cell_start + key[it]) + rk[it]] = (int)i;
             else if (perm) perm[i] = -1;                          // tombstone: dropped
         }
@@ -438,6 +439,7 @@ __global__ void __launch_bounds__(NT, MINB) k_cll_gather(PartDev in, PartDev out
             if (src[it] < 0) continue;
             const long long me = id[it];
             const int d = cb[it] + rank_in_cell(in, ws, sid, slo, narrow, w0, w1, cb[it], ce[it], me);
+            SPH_CHECK(d >= cb[it] && d < ce[it] && ce[it] <= n && src[it] < in.cap);
             out.x[d] = x[it];
             out.y[d] = y[it];
             out.vx[d] = vx[it];

@@ -7,6 +7,7 @@
 // __fadd_rn/__fsub_rn/__fmul_rn (one binary32 round-to-nearest op each, never
 // contracted), in the order fixed by DESIGN.md §3 "Pinned arithmetic".
 #pragma once
+#include <cassert>
 #include <climits>
 #include <cstdint>
 #include <cstdlib>
@@ -17,6 +18,15 @@
 namespace sphbuf {
 
 // ------------------------------------------------------------------ helpers
+
+// Device bounds checks of the debug build (-DSPHBUF_DEBUG, build.py --debug):
+// compute-sanitizer is not available on the GPU pool, so index invariants are
+// asserted in the kernels themselves; compiled out otherwise.
+#ifdef SPHBUF_DEBUG
+#define SPH_CHECK(cond) assert(cond)
+#else
+#define SPH_CHECK(cond) ((void)0)
+#endif
 
 // Programmatic dependent launch (sm_90+): every kernel of the path is launched
 // with launch_k() below and waits here for the kernel before it on the stream to

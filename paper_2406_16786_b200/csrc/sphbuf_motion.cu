@@ -56,6 +56,7 @@ __global__ void __launch_bounds__(kThreads) k_port_move(PartDev p, int dim, Port
         const int c0 = runs[3 * r], c1 = runs[3 * r + 1];
         if (c1 < c0) continue;                                   // empty run of a movable port
         const int b = cell_start[c0], e = cell_end[c1];
+        SPH_CHECK(b >= 0 && e <= p.cap);
         for (int i = b + threadIdx.x; i < e; i += blockDim.x) {
             if (p.label[i] != k) continue;
             float X[3], V[3];
@@ -147,6 +148,7 @@ __global__ void __launch_bounds__(kThreads) k_port_enum(GridDev g, PortEnum P, f
             c1 = (cx - g.cx_begin) * g.ny + last;
         }
     }
+    SPH_CHECK(c1 < c0 || (c0 >= 0 && c1 < (int)g.ncells));
     runs[3 * i] = c0;
     runs[3 * i + 1] = c1;
     runs[3 * i + 2] = P.k;

@@ -174,6 +174,7 @@ __global__ void __launch_bounds__(kThreads) k_upd_main(PartDev p, int dim, const
             const int r = lo;
             const int k = ws.runs[3 * r + 2];
             const int pi = cell_start[ws.runs[3 * r]] + (int)(g - ws.run_off[r]);
+            SPH_CHECK(pi >= 0 && pi < p.cap && k >= 0 && k < pt.n);
             const PortDev &P = s_ports[k];
             const float x = p.x[pi], y = p.y[pi], z = dim == 3 ? p.z[pi] : 0.0f;
             const int lab = p.label[pi];

@@ -78,9 +78,10 @@ def lib():
     global _L
     if _L is not None:
         return _L
-    path = _build.LIB
+    debug = os.environ.get("SPHBUF_DEBUG") == "1"     # the bounds-asserting build (tests only)
+    path = _build.LIB_DEBUG if debug else _build.LIB
     if not os.path.exists(path) or os.environ.get("SPHBUF_REBUILD"):
-        path = _build.build()
+        path = _build.build(debug=debug)
     L = C.CDLL(path)
     vp, i32, i64, f32 = C.c_void_p, C.c_int32, C.c_int64, C.c_float
     P = C.POINTER
