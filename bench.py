@@ -123,8 +123,9 @@ def algorithmic_bytes(kernel, dim, n, ncells, cand, created, deleted, moved):
         "advect": n * (2 * dim * 4 + dim * 4),
         "cll_key": n * (4 * dim + 4),
         "cell_scan": ncells * 12,
-        "cll_scatter": n * 8,
-        "cll_gather": n * 2 * S,
+        "cll_scatter": n * 8,   # key read + slot -> source write
+        # + 4 B: the next build's key, written by the gather (key carry-over)
+        "cll_gather": n * (2 * S + 4),
         "cll_rank": n * (8 + 8),
         "compact_count": moved * 4,
         "upd_main": cand * (4 * dim + 4) + created * (2 * S + 4 * dim),

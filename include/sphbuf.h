@@ -233,11 +233,26 @@ sph_status sph_advect(sph_ctx *ctx, sph_particles *p, float dt, void *stream);
 sph_status sph_cll_build(sph_ctx *ctx, const sph_particles *in, sph_particles *out, int32_t *cell_start,
                          int32_t *cell_end, int32_t *perm_or_null, void *stream);
 
-/* sph_advect (the driver's step) fused into the key pass of sph_cll_build: the
- * advected positions are written back to `in` and the build proceeds as above.
- * Identical results to sph_advect followed by sph_cll_build, one pass less. */
+/* sph_advect (the driver's step) fused into the build: the advected positions
+ * are computed in the key pass and again, bit-identically, where the gather
+ * moves each particle into `out`; `in` is not written.  `out` is identical to
+ * sph_advect followed by sph_cll_build.
+ *
+ * Key carry-over: a build that advects (and does not migrate) also prepares
+ * the keys of the next build — each particle's cell after advecting its new
+ * position by the same dt — and that build's histogram; sph_buffer_update,
+ * sph_compact(_deferred) and sph_port_move keep them current for the particles
+ * they change.  The next sph_advect_cll_build (or sph_cll_key) of `out` with the
+ * same dt then skips its key pass; any other build clears them.  Results are
+ * identical either way.  A caller that changes positions, velocities or the
+ * particle set of `out` itself (other than through this library) must call
+ * sph_cll_invalidate first. */
 sph_status sph_advect_cll_build(sph_ctx *ctx, sph_particles *in, sph_particles *out, float dt, int32_t *cell_start,
                                 int32_t *cell_end, int32_t *perm_or_null, void *stream);
+
+/* Drop the carried-over keys (see above): the next build runs its key pass.
+ * Host only. */
+sph_status sph_cll_invalidate(sph_ctx *ctx);
 
 /* The same build in two halves around the multi-GPU neighbour exchange (§8(e)),
  * so migration costs no extra pass over the particles:

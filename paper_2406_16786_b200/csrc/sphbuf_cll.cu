@@ -65,8 +65,6 @@ __global__ void __launch_bounds__(kThreads) k_cll_key(PartDev in, GridDev g, Wor
     }
     long long moved = 0;
     const int lane = threadIdx.x & 31;
-    const unsigned lt = lanemask_lt();
-    const unsigned le = lt | (1u << lane);
     int oob_acc = 0;
     const long long stride = (long long)gridDim.x * kThreads * kKeyItems;
     for (long long base = (long long)blockIdx.x * kThreads * kKeyItems; base < n; base += stride) {
@@ -119,25 +117,11 @@ __global__ void __launch_bounds__(kThreads) k_cll_key(PartDev in, GridDev g, Wor
                 }
             }
         }
-        int cbase[kKeyItems], head_lane[kKeyItems];
 #pragma unroll
         for (int it = 0; it < kKeyItems; ++it) {
-            const int prev = __shfl_up_sync(0xffffffffu, key[it], 1);
-            const bool head = (lane == 0) || (key[it] != prev);
-            const unsigned heads = __ballot_sync(0xffffffffu, head);
-            head_lane[it] = 31 - __clz(heads & le);
-            const unsigned above = heads & ~le;
-            const int next = above ? __ffs(above) - 1 : 32;
-            cbase[it] = (head && key[it] >= 0) ? atomicAdd(&ws.cell_count[key[it]], next - lane) : 0;
-        }
-#pragma unroll
-        for (int it = 0; it < kKeyItems; ++it) {
-            const int b = __shfl_sync(0xffffffffu, cbase[it], head_lane[it]);
+            hist_count_runs(ws.cell_count, key[it]);     // one atomic per run of equal keys
             const long long i = base + it * kThreads + threadIdx.x;
-            if (i < n) {
-                ws.key[i] = key[it];
-                ws.rank[i] = b + lane - head_lane[it];
-            }
+            if (i < n) ws.key[i] = key[it];
         }
     }
     const unsigned o = warp_sum((unsigned)oob_acc);
@@ -146,6 +130,20 @@ __global__ void __launch_bounds__(kThreads) k_cll_key(PartDev in, GridDev g, Wor
         moved = warp_sum_ll(moved);
         if (lane == 0 && moved) atomicAdd((unsigned long long *)&ctr->migrated, (unsigned long long)moved);
     }
+}
+
+// K1 in key carry-over mode: the keys and the histogram of this build were made
+// by the previous build's gather (and kept up to date by the update, the
+// compaction and moving ports), so only the build's counters are set.
+__global__ void k_cll_begin(PartDev in, Workspace ws)
+{
+    pdl_entry();
+    Counters *ctr = ws.ctr;
+    const long long n = *in.n;
+    ctr->epoch_cll += 1;
+    ctr->ticket_cll = 0;
+    ctr->n_in = n;
+    ctr->mig_base = n;
 }
 
 // K1b (multi-GPU): append the particles received from the neighbour slabs after
@@ -187,7 +185,7 @@ __global__ void __launch_bounds__(kThreads) k_cll_unpack_key(PartDev in, GridDev
         const int key = cell_of(g, x, y, z, oob);
         oob_acc += oob;
         ws.key[d] = key;
-        ws.rank[d] = atomicAdd(&ws.cell_count[key], 1);
+        atomicAdd(&ws.cell_count[key], 1);
     }
     const unsigned o = warp_sum((unsigned)oob_acc);
     if ((threadIdx.x & 31) == 0 && o) atomicAdd((unsigned long long *)&ctr->out_of_grid, (unsigned long long)o);
@@ -212,18 +210,27 @@ __global__ void __launch_bounds__(kThreads) k_cell_scan(GridDev g, Workspace ws,
     const long long base = tile * kCellTile + (long long)threadIdx.x * kCellItems;
     const bool full = base + kCellItems <= nc;
     int4 c[V];
+    // the histogram is read and re-zeroed (the next build's, or the gather's key
+    // carry-over, accumulates into it); the scatter's cursors start from zero
     if (full) {
         int4 *pc = reinterpret_cast<int4 *>(ws.cell_count + base);
+        int4 *pk = reinterpret_cast<int4 *>(ws.cursor + base);
 #pragma unroll
         for (int v = 0; v < V; ++v) c[v] = pc[v];
 #pragma unroll
-        for (int v = 0; v < V; ++v) pc[v] = make_int4(0, 0, 0, 0);
+        for (int v = 0; v < V; ++v) {
+            pc[v] = make_int4(0, 0, 0, 0);
+            pk[v] = make_int4(0, 0, 0, 0);
+        }
     } else {
         int t[kCellItems];
 #pragma unroll
         for (int j = 0; j < kCellItems; ++j) {
             t[j] = (base + j < nc) ? ws.cell_count[base + j] : 0;
-            if (base + j < nc) ws.cell_count[base + j] = 0;
+            if (base + j < nc) {
+                ws.cell_count[base + j] = 0;
+                ws.cursor[base + j] = 0;
+            }
         }
 #pragma unroll
         for (int v = 0; v < V; ++v) c[v] = make_int4(t[4 * v], t[4 * v + 1], t[4 * v + 2], t[4 * v + 3]);
@@ -271,32 +278,49 @@ __global__ void __launch_bounds__(kThreads) k_cell_scan(GridDev g, Workspace ws,
     if (tile == ntiles - 1 && threadIdx.x == 0) *n_out = (long long)(prefix + total);
 }
 
-constexpr int kScatterItems = 4;
+constexpr int kScatterItems = 8;
 
-// K3: source index of every sorted slot (slot = cell_start[key] + atomic rank).
+// K3: source index of every sorted slot: slot = cell_start[key] + a per-cell
+// cursor (one atomic per run of equal keys in a warp; the order inside a cell is
+// arbitrary here, the gather ranks by id).
 __global__ void __launch_bounds__(kThreads) k_cll_scatter(Workspace ws, const int *cell_start, int *perm)
 {
     pdl_entry();
     const long long n = ws.ctr->n_in;
     const long long stride = (long long)gridDim.x * kThreads * kScatterItems;
     for (long long base = (long long)blockIdx.x * kThreads * kScatterItems; base < n; base += stride) {
-        int key[kScatterItems], rk[kScatterItems];
+        int key[kScatterItems];
 #pragma unroll
         for (int it = 0; it < kScatterItems; ++it) {
             const long long i = base + it * kThreads + threadIdx.x;
-            key[it] = -1;
-            if (i < n) {
-                key[it] = ws.key[i];
-                rk[it] = ws.rank[i];
-            }
+            key[it] = i < n ? ws.key[i] : -1;
+        }
+        // run heads of all items first, then all their atomics in flight together
+        const int lane = threadIdx.x & 31;
+        const unsigned le = lanemask_lt() | (1u << lane);
+        int b[kScatterItems], hl[kScatterItems];
+#pragma unroll
+        for (int it = 0; it < kScatterItems; ++it) {
+            const int prev = __shfl_up_sync(0xffffffffu, key[it], 1);
+            const bool head = (lane == 0) || (key[it] != prev);
+            const unsigned heads = __ballot_sync(0xffffffffu, head);
+            const unsigned above = heads & ~le;
+            const int next = above ? __ffs(above) - 1 : 32;
+            hl[it] = 31 - __clz(heads & le);
+            b[it] = (head && key[it] >= 0) ? atomicAdd(&ws.cursor[key[it]], next - lane) : 0;
         }
 #pragma unroll
         for (int it = 0; it < kScatterItems; ++it) {
+            const int rk = __shfl_sync(0xffffffffu, b[it], hl[it]) + lane - hl[it];
             const long long i = base + it * kThreads + threadIdx.x;
             if (i >= n) continue;
-            SPH_CHECK(key[it] < 0 || __ldg(cell_start + key[it]) + rk[it] < n);
-            if (key[it] >= 0) ws.src[__ldg(cell_start + key[it]) + rk[it]] = (int)i;
-            else if (perm) perm[i] = -1;                          // tombstone: dropped
+            if (key[it] >= 0) {
+                const int slot = __ldg(cell_start + key[it]) + rk;
+                SPH_CHECK(slot < n);
+                ws.src[slot] = (int)i;
+            } else if (perm) {
+                perm[i] = -1;                                     // tombstone: dropped
+            }
         }
     }
 }
@@ -340,7 +364,7 @@ __device__ __forceinline__ int rank_in_cell(const PartDev &in, const Workspace &
 template <bool HasExtra, int ITEMS, int MINB, int NT = kThreads, bool PF = false>
 __global__ void __launch_bounds__(NT, MINB) k_cll_gather(PartDev in, PartDev out, GridDev g, Workspace ws,
                                                                const int *cell_start, const int *cell_end, int *perm,
-                                                               int advect, float dt)
+                                                               int advect, float dt, int carry, float cdt)
 {
     pdl_entry();
     constexpr int T = NT * ITEMS;
@@ -353,6 +377,7 @@ __global__ void __launch_bounds__(NT, MINB) k_cll_gather(PartDev in, PartDev out
     // build fused the advection); received migrants were advected by their sender
     const long long adv_lim = advect ? ws.ctr->mig_base : 0;
     const long long stride = (long long)gridDim.x * T;
+    int oob_next = 0;
     // PF: the slot -> source map of the next tile is loaded while this tile's
     // columns are in flight (one dependent DRAM round trip less per tile)
     int nsrc[ITEMS], nhsrc = 0;
@@ -434,11 +459,22 @@ __global__ void __launch_bounds__(NT, MINB) k_cll_gather(PartDev in, PartDev out
         const int w1 = (long long)t0 + T + kHalo < n ? t0 + T + kHalo : (int)n;
         const long long *sid = s_id + (w0 - (t0 - kHalo));
         const unsigned *slo = s_lo + (w0 - (t0 - kHalo));
+        int kn[ITEMS];
 #pragma unroll
         for (int it = 0; it < ITEMS; ++it) {
+            kn[it] = -1;
             if (src[it] < 0) continue;
             const long long me = id[it];
             const int d = cb[it] + rank_in_cell(in, ws, sid, slo, narrow, w0, w1, cb[it], ce[it], me);
+            if (carry) {
+                // key carry-over: the next build's key of the particle now at d (its
+                // position advected again by cdt), so that build needs no key pass
+                int oobn = 0;
+                kn[it] = cell_of(g, advect1(x[it], vx[it], cdt), advect1(y[it], vy[it], cdt),
+                                 dim == 3 ? advect1(z[it], vz[it], cdt) : 0.0f, oobn);
+                oob_next += oobn;
+                ws.key[d] = kn[it];
+            }
             SPH_CHECK(d >= cb[it] && d < ce[it] && ce[it] <= n && src[it] < in.cap);
             out.x[d] = x[it];
             out.y[d] = y[it];
@@ -454,7 +490,15 @@ __global__ void __launch_bounds__(NT, MINB) k_cll_gather(PartDev in, PartDev out
             out.label[d] = lab[it];
             if (perm) perm[src[it]] = d;
         }
+        if (carry) {
+#pragma unroll
+            for (int it = 0; it < ITEMS; ++it) hist_count_runs(ws.cell_count, kn[it]);   // next histogram
+        }
         __syncthreads();
+    }
+    if (carry) {
+        const unsigned o = warp_sum((unsigned)oob_next);
+        if ((threadIdx.x & 31) == 0 && o) atomicAdd((unsigned long long *)&ws.ctr->out_of_grid, (unsigned long long)o);
     }
 }
 
@@ -464,46 +508,48 @@ __global__ void __launch_bounds__(NT, MINB) k_cll_gather(PartDev in, PartDev out
 // for tuning runs (tools/gather_sweep.py); the default is the measured best.
 template <bool HasExtra, int ITEMS, int MINB, int NT = kThreads, bool PF = false>
 static void gather_fused(const PartDev &in, const PartDev &out, const GridDev &g, const Workspace &ws,
-                         const int *cs, const int *ce, int *perm, int advect, float dt, long long cap, cudaStream_t s)
+                         const int *cs, const int *ce, int *perm, int advect, float dt, int carry, float cdt,
+                         long long cap, cudaStream_t s)
 {
     static int grid = 0;
     if (!grid) grid = occ_grid(k_cll_gather<HasExtra, ITEMS, MINB, NT, PF>, NT);
     launch_k(k_cll_gather<HasExtra, ITEMS, MINB, NT, PF>, dim3(cap_grid(grid, cap, NT * ITEMS)), dim3(NT), 0, s, in, out, g, ws, cs, ce,
-                                                                                         perm, advect, dt);
+             perm, advect, dt, carry, cdt);
 }
 
 template <bool HasExtra>
 static void gather_variant(const char *v, const PartDev &in, const PartDev &out, const GridDev &g,
                            const Workspace &ws, const int *cs, const int *ce, int *perm, int advect, float dt,
-                           long long cap, cudaStream_t s)
+                           int carry, float cdt, long long cap, cudaStream_t s)
 {
 #define SPH_GV(name, I, M)                                                              \
     if (!strcmp(v, name)) {                                                             \
-        gather_fused<HasExtra, I, M>(in, out, g, ws, cs, ce, perm, advect, dt, cap, s); \
+        gather_fused<HasExtra, I, M>(in, out, g, ws, cs, ce, perm, advect, dt, carry, cdt, cap, s); \
         return;                                                                         \
     }
     SPH_GV("1:8", 1, 8)
     SPH_GV("2:6", 2, 6)
     SPH_GV("3:4", 3, 4)
     SPH_GV("4:3", 4, 3)
-    if (!strcmp(v, "pf3:4")) return gather_fused<HasExtra, 3, 4, kThreads, true>(in, out, g, ws, cs, ce, perm, advect, dt, cap, s);
+    if (!strcmp(v, "pf3:4")) return gather_fused<HasExtra, 3, 4, kThreads, true>(in, out, g, ws, cs, ce, perm, advect, dt, carry, cdt, cap, s);
 #undef SPH_GV
     // default: 2 slots per thread, the next tile's slot map prefetched, <= 48
     // registers (5 blocks/SM): measured best on C5 among the variants above,
     // 128- / 512-thread blocks and cp.async / warp-chunk designs
-    gather_fused<HasExtra, 2, 5, kThreads, true>(in, out, g, ws, cs, ce, perm, advect, dt, cap, s);
+    gather_fused<HasExtra, 2, 5, kThreads, true>(in, out, g, ws, cs, ce, perm, advect, dt, carry, cdt, cap, s);
 }
 
 static void launch_gather(const PartDev &in, const PartDev &out, const GridDev &g, const Workspace &ws,
-                          const int *cs, const int *ce, int *perm, int advect, float dt, long long cap, cudaStream_t s)
+                          const int *cs, const int *ce, int *perm, int advect, float dt, int carry, float cdt,
+                          long long cap, cudaStream_t s)
 {
     static const char *v = nullptr;
     if (!v) {
         v = getenv("SPHBUF_GATHER");
         if (!v) v = "";
     }
-    if (in.n_extra > 0) gather_variant<true>(v, in, out, g, ws, cs, ce, perm, advect, dt, cap, s);
-    else gather_variant<false>(v, in, out, g, ws, cs, ce, perm, advect, dt, cap, s);
+    if (in.n_extra > 0) gather_variant<true>(v, in, out, g, ws, cs, ce, perm, advect, dt, carry, cdt, cap, s);
+    else gather_variant<false>(v, in, out, g, ws, cs, ce, perm, advect, dt, carry, cdt, cap, s);
 }
 
 int sm_count() { return sm_count_cached(); }
@@ -520,8 +566,20 @@ static void key_launch(const PartDev &in, const GridDev &g, const Workspace &ws,
 }
 
 cudaError_t launch_cll_key(const PartDev &in, const GridDev &g, const Workspace &ws, float dt, bool advect,
-                           float *send_lo, float *send_hi, long long maxm, int rec, cudaStream_t s, Launch *L)
+                           float *send_lo, float *send_hi, long long maxm, int rec, const CllCarry &cc, cudaStream_t s,
+                           Launch *L)
 {
+    if (cc.use) {
+        L->before(s);
+        launch_k(k_cll_begin, dim3(1), dim3(1), 0, s, in, ws);
+        L->after(s, KID_CLL_KEY);
+        return cudaGetLastError();
+    }
+    if (cc.clear) {
+        // the previous gather left a carried-over histogram this build does not use
+        cudaError_t e = cudaMemsetAsync(ws.cell_count, 0, sizeof(int) * (size_t)g.ncells, s);
+        if (e != cudaSuccess) return e;
+    }
     const bool mig = send_lo && send_hi;
     if (mig) {
         cudaError_t e = cudaMemsetAsync(send_lo, 0, 16, s);
@@ -538,16 +596,17 @@ cudaError_t launch_cll_key(const PartDev &in, const GridDev &g, const Workspace 
 }
 
 cudaError_t launch_cll(const PartDev &in, const PartDev &out, const GridDev &g, const Workspace &ws, int *cell_start,
-                       int *cell_end, int *perm, float dt, bool advect, cudaStream_t s, Launch *L)
+                       int *cell_end, int *perm, float dt, bool advect, const CllCarry &cc, cudaStream_t s, Launch *L)
 {
-    cudaError_t e = launch_cll_key(in, g, ws, dt, advect, nullptr, nullptr, 0, 0, s, L);
+    cudaError_t e = launch_cll_key(in, g, ws, dt, advect, nullptr, nullptr, 0, 0, cc, s, L);
     if (e != cudaSuccess) return e;
-    return launch_cll_finish(in, out, g, ws, nullptr, nullptr, 0, 0, cell_start, cell_end, perm, advect, dt, s, L);
+    return launch_cll_finish(in, out, g, ws, nullptr, nullptr, 0, 0, cell_start, cell_end, perm, advect, dt, cc, s, L);
 }
 
 cudaError_t launch_cll_finish(const PartDev &in, const PartDev &out, const GridDev &g, const Workspace &ws,
                               const float *recv_lo, const float *recv_hi, long long maxm, int rec, int *cell_start,
-                              int *cell_end, int *perm, bool advect_b, float dt, cudaStream_t s, Launch *L)
+                              int *cell_end, int *perm, bool advect_b, float dt, const CllCarry &cc,
+                              cudaStream_t s, Launch *L)
 {
     const int advect = advect_b ? 1 : 0;
     const long long ntiles = (g.ncells + kCellTile - 1) / kCellTile;
@@ -569,7 +628,7 @@ cudaError_t launch_cll_finish(const PartDev &in, const PartDev &out, const GridD
         L->after(s, KID_CLL_SCATTER);
     }
     L->before(s);
-    launch_gather(in, out, g, ws, cell_start, cell_end, perm, advect, dt, cap, s);
+    launch_gather(in, out, g, ws, cell_start, cell_end, perm, advect, dt, cc.make ? 1 : 0, cc.dt, cap, s);
     L->after(s, KID_CLL_GATHER);
     return cudaGetLastError();
 }

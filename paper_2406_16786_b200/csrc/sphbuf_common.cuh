@@ -134,6 +134,21 @@ static __device__ unsigned tile_prefix(unsigned long long *status, long long til
     return excl;
 }
 
+// Cell histogram from a warp whose lanes hold consecutive particles (keys mostly
+// equal in runs): one atomic per run of equal keys; key < 0 is not counted.  All
+// 32 lanes must call it.
+__device__ __forceinline__ void hist_count_runs(int *cnt, int key)
+{
+    const int lane = threadIdx.x & 31;
+    const unsigned le = lanemask_lt() | (1u << lane);
+    const int prev = __shfl_up_sync(0xffffffffu, key, 1);
+    const bool head = (lane == 0) || (key != prev);
+    const unsigned heads = __ballot_sync(0xffffffffu, head);
+    const unsigned above = heads & ~le;
+    const int next = above ? __ffs(above) - 1 : 32;
+    if (head && key >= 0) atomicAdd(&cnt[key], next - lane);
+}
+
 // Block-wide exclusive scan of one unsigned per thread (NT threads).
 template <int NT>
 __device__ __forceinline__ unsigned block_excl_scan(unsigned v, unsigned &total, unsigned *s_warp)
@@ -275,6 +290,25 @@ __device__ __forceinline__ int cell_of(const GridDev &g, float x, float y, float
     int cz = 0;
     if (g.dim == 3) cz = cell_axis(z, g.lo[2], g.inv_cs, 0, g.ncell[2], oob);
     return ((cx - g.cx_begin) * g.ny + cy) * g.nz + cz;
+}
+
+// Key carry-over fix-up (sphbuf_cll.cu): particle i, whose next-build key
+// ws.key[i] the gather computed, now has position x and velocity v (or was
+// deleted): its key for advection by cdt and the next histogram follow.
+__device__ __forceinline__ void carry_fix(const GridDev &g, const Workspace &ws, long long i, bool del, float x,
+                                          float y, float z, float vx, float vy, float vz, float cdt)
+{
+    const int kold = ws.key[i];
+    int knew = -1;
+    if (!del) {
+        int oob = 0;
+        knew = cell_of(g, advect1(x, vx, cdt), advect1(y, vy, cdt), g.dim == 3 ? advect1(z, vz, cdt) : 0.0f, oob);
+    }
+    if (knew != kold) {
+        if (kold >= 0) atomicSub(&ws.cell_count[kold], 1);
+        if (knew >= 0) atomicAdd(&ws.cell_count[knew], 1);
+        ws.key[i] = knew;
+    }
 }
 
 // ------------------------------------------------------------------ launch helpers (host)

@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(kThreads) k_compact_count(PartDev p, Workspace
 }
 
 template <bool HasExtra>
-__global__ void __launch_bounds__(kThreads) k_compact_move(PartDev p, int dim, Workspace ws, int *perm)
+__global__ void __launch_bounds__(kThreads) k_compact_move(PartDev p, int dim, Workspace ws, int *perm, int carry)
 {
     pdl_entry();
     __shared__ unsigned s_cnt[kCmpItems * kThreads / 32 + 1];
@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(kThreads) k_compact_move(PartDev p, int dim, W
         float x[kCmpItems], y[kCmpItems], z[kCmpItems], vx[kCmpItems], vy[kCmpItems], vz[kCmpItems];
         float ex[kCmpItems][SPH_MAX_EXTRA];
         long long id[kCmpItems];
-        int lab[kCmpItems];
+        int lab[kCmpItems], kc[kCmpItems];
         unsigned mine = 0;
 #pragma unroll
         for (int it = 0; it < kCmpItems; ++it) {
@@ -122,6 +122,7 @@ __global__ void __launch_bounds__(kThreads) k_compact_move(PartDev p, int dim, W
             alive[it] = false;
             if (i < N) {
                 lab[it] = p.label[i];
+                kc[it] = carry ? ws.key[i] : 0;   // key carry-over: the next-build key moves along
                 x[it] = p.x[i];
                 y[it] = p.y[i];
                 vx[it] = p.vx[i];
@@ -140,7 +141,7 @@ __global__ void __launch_bounds__(kThreads) k_compact_move(PartDev p, int dim, W
                 alive[it] = lab[it] > -2;
                 mine += alive[it];
                 // consume every loaded word so the loads are complete before "read done"
-                dep ^= __float_as_int(x[it]) ^ __float_as_int(y[it]) ^ __float_as_int(z[it]) ^
+                dep ^= kc[it] ^ __float_as_int(x[it]) ^ __float_as_int(y[it]) ^ __float_as_int(z[it]) ^
                        __float_as_int(vx[it]) ^ __float_as_int(vy[it]) ^ __float_as_int(vz[it]) ^ (int)id[it] ^
                        (int)(id[it] >> 32);
                 if (HasExtra) {
@@ -196,6 +197,7 @@ __global__ void __launch_bounds__(kThreads) k_compact_move(PartDev p, int dim, W
                 for (int e = 0; e < p.n_extra; ++e) p.extra[e][o] = ex[it][e];
             p.id[o] = id[it];
             p.label[o] = lab[it];
+            if (carry) ws.key[o] = kc[it];
             if (perm) perm[i] = (int)o;
         }
         __syncthreads();
@@ -208,10 +210,12 @@ __global__ void __launch_bounds__(kThreads) k_compact_move(PartDev p, int dim, W
 // defer: the tombstones stay in place (the next sph_cll_build drops them) and the
 // staged particles go to [N, N + C); launched with one block, so N and next_id
 // can be read directly.
-__global__ void __launch_bounds__(kThreads) k_compact_append(PartDev p, int dim, int n_ports, int max_ports,
+__global__ void __launch_bounds__(kThreads) k_compact_append(PartDev p, GridDev g, int n_ports, int max_ports,
                                                              Workspace ws, const int *all_counts, int nranks,
-                                                             int rank, long long *next_id, int *perm, bool defer)
+                                                             int rank, long long *next_id, int *perm, bool defer,
+                                                             int carry, float cdt)
 {
+    const int dim = g.dim;
     pdl_entry();
     __shared__ long long s_off[SPH_MAX_PORTS];
     __shared__ long long s_beg[SPH_MAX_PORTS];
@@ -264,6 +268,14 @@ __global__ void __launch_bounds__(kThreads) k_compact_append(PartDev p, int dim,
         for (int e = 0; e < p.n_extra; ++e) p.extra[e][d] = ws.sextra[e][s];
         p.id[d] = s_off[k] + (s - s_beg[k]);
         p.label[d] = -1;
+        if (carry) {
+            // key carry-over: the new particle's key for the next build
+            int oob = 0;
+            const int key = cell_of(g, advect1(ws.sx[s], ws.svx[s], cdt), advect1(ws.sy[s], ws.svy[s], cdt),
+                                    dim == 3 ? advect1(ws.sz[s], ws.svz[s], cdt) : 0.0f, oob);
+            ws.key[d] = key;
+            atomicAdd(&ws.cell_count[key], 1);
+        }
     }
     if (perm) {
         const long long ibeg = D ? cmp_begin(ctr->i_first) : N;
@@ -277,18 +289,18 @@ __global__ void __launch_bounds__(kThreads) k_compact_append(PartDev p, int dim,
 
 // ------------------------------------------------------------------ launcher
 
-cudaError_t launch_compact(const PartDev &p, const PortTable &pt, const Workspace &ws, const int *all_counts,
-                           int nranks, int rank, long long *next_id, int *perm, bool defer, cudaStream_t s,
-                           Launch *L)
+cudaError_t launch_compact(const PartDev &p, const GridDev &g, const PortTable &pt, const Workspace &ws,
+                           const int *all_counts, int nranks, int rank, long long *next_id, int *perm, bool defer,
+                           int carry, float cdt, cudaStream_t s, Launch *L)
 {
-    const int dim = p.z ? 3 : 2;
     if (defer) {
         L->before(s);
-        launch_k(k_compact_append, dim3(1), dim3(kThreads), 0, s, p, dim, pt.n, pt.max_ports, ws, all_counts, nranks, rank, next_id,
-                                                nullptr, true);
+        launch_k(k_compact_append, dim3(1), dim3(kThreads), 0, s, p, g, pt.n, pt.max_ports, ws, all_counts, nranks,
+                 rank, next_id, nullptr, true, carry, cdt);
         L->after(s, KID_COMPACT_APPEND);
         return cudaGetLastError();
     }
+    const int dim = g.dim;
     {
         static int grid = 0;
         if (!grid) grid = occ_grid(k_compact_count, kThreads);
@@ -300,16 +312,19 @@ cudaError_t launch_compact(const PartDev &p, const PortTable &pt, const Workspac
     if (p.n_extra > 0) {
         static int grid = 0;
         if (!grid) grid = occ_grid(k_compact_move<true>, kThreads);
-        launch_k(k_compact_move<true>, dim3(cap_grid(grid, p.cap, kCmpTile)), dim3(kThreads), 0, s, p, dim, ws, perm);
+        launch_k(k_compact_move<true>, dim3(cap_grid(grid, p.cap, kCmpTile)), dim3(kThreads), 0, s, p, dim, ws, perm,
+                 carry);
     } else {
         static int grid = 0;
         if (!grid) grid = occ_grid(k_compact_move<false>, kThreads);
-        launch_k(k_compact_move<false>, dim3(cap_grid(grid, p.cap, kCmpTile)), dim3(kThreads), 0, s, p, dim, ws, perm);
+        launch_k(k_compact_move<false>, dim3(cap_grid(grid, p.cap, kCmpTile)), dim3(kThreads), 0, s, p, dim, ws, perm,
+                 carry);
     }
     L->after(s, KID_COMPACT);
     L->before(s);
-    launch_k(k_compact_append, dim3(cap_grid(sm_count_cached() * 4, perm ? p.cap : ws.max_new, kThreads)), dim3(kThreads), 0, s, 
-        p, dim, pt.n, pt.max_ports, ws, all_counts, nranks, rank, next_id, perm, false);
+    launch_k(k_compact_append, dim3(cap_grid(sm_count_cached() * 4, perm ? p.cap : ws.max_new, kThreads)),
+             dim3(kThreads), 0, s, p, g, pt.n, pt.max_ports, ws, all_counts, nranks, rank, next_id, perm, false, carry,
+             cdt);
     L->after(s, KID_COMPACT_APPEND);
     return cudaGetLastError();
 }

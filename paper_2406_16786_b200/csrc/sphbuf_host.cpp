@@ -101,6 +101,14 @@ struct sph_ctx {
     // advection of the last sph_cll_key, applied by the gather of sph_cll_finish
     bool key_advect = false;
     float key_dt = 0.f;
+    // key carry-over (sphbuf_cll.cu): the last build's gather prepared the keys and
+    // histogram of a next build that advects by carry_dt the arrays (carry_x,
+    // carry_id) it wrote; the update, compaction and port moves keep them current
+    bool carry_next = false;
+    float carry_dt = 0.f;
+    const float *carry_x = nullptr;
+    const int64_t *carry_id = nullptr;
+    CllCarry key_cc{};
 };
 
 namespace {
@@ -134,6 +142,7 @@ size_t layout(const sph_ctx *c, char *base, Workspace *W)
     Workspace w{};
     w.ctr = (Counters *)take(sizeof(Counters));
     w.cell_count = (int *)take(sizeof(int) * ncells);
+    w.cursor = (int *)take(sizeof(int) * ncells);
     w.tile_cells = (unsigned long long *)take(8 * cell_tiles);
     w.tile_upd = (unsigned long long *)take(8 * upd_tiles);
     w.tile_runs = (unsigned long long *)take(8 * (kMaxRuns / 1024 + 1));
@@ -146,7 +155,6 @@ size_t layout(const sph_ctx *c, char *base, Workspace *W)
     const size_t zero_end = off;   // everything above must start zeroed
     w.sub_off = (unsigned *)take(4 * cmp_subs);
     w.key = (int *)take(sizeof(int) * cap);
-    w.rank = (int *)take(sizeof(int) * cap);
     w.src = (int *)take(sizeof(int) * cap);
     const long long mn = c->max_new;
     w.sx = (float *)take(4 * mn);
@@ -401,6 +409,48 @@ const char *sph_last_error(const sph_ctx *c) { return c ? c->err.c_str() : "null
 
 size_t sph_workspace_bytes(const sph_ctx *c) { return c ? layout(c, nullptr, nullptr) : 0; }
 
+// Key carry-over plan of a build of `in` (see sph_ctx): reuse the carried keys
+// when `in` is the array they were made for and the advection is the same; make
+// new ones when this build advects and does not migrate (SPHBUF_CARRY=0: never).
+static CllCarry carry_plan(const sph_ctx *c, const sph_particles *in, bool advect, float dt, bool migrating)
+{
+    static int enabled = -1;
+    if (enabled < 0) {
+        const char *v = getenv("SPHBUF_CARRY");
+        enabled = (v && v[0] == '0') ? 0 : 1;
+    }
+    CllCarry cc;
+    const bool match = c->carry_next && advect && !migrating && in->x == c->carry_x && in->id == c->carry_id &&
+                       dt == c->carry_dt;
+    cc.use = match;
+    cc.clear = c->carry_next && !match;
+    cc.make = enabled && advect && !migrating;
+    cc.dt = dt;
+    return cc;
+}
+
+static void carry_after_build(sph_ctx *c, const CllCarry &cc, const sph_particles *out)
+{
+    c->carry_next = cc.make;
+    c->carry_dt = cc.dt;
+    c->carry_x = out->x;
+    c->carry_id = out->id;
+}
+
+// 1 when the carried keys describe `p` (the arrays the last build wrote).
+static int carry_on(const sph_ctx *c, const sph_particles *p)
+{
+    return (c->carry_next && p->x == c->carry_x && p->id == c->carry_id) ? 1 : 0;
+}
+
+// Positions or arrays changed behind the carried keys: the next build clears the
+// carried histogram and runs the key pass.
+static void carry_drop(sph_ctx *c)
+{
+    c->carry_x = nullptr;
+    c->carry_id = nullptr;
+}
+
 static cudaError_t enumerate_slice(sph_ctx *c, int k, const float o[3], const float Q[9], cudaStream_t s);
 
 sph_status sph_set_workspace(sph_ctx *c, void *d_ws, size_t bytes)
@@ -410,6 +460,7 @@ sph_status sph_set_workspace(sph_ctx *c, void *d_ws, size_t bytes)
     if (reinterpret_cast<size_t>(d_ws) % 256) return fail(c, SPH_ERR_ARG, "workspace not 256-byte aligned");
     c->ws = d_ws;
     c->ws_bytes = bytes;
+    c->carry_next = false;   // the histogram is zeroed below
     layout(c, static_cast<char *>(d_ws), &c->W);
     cudaError_t e = cudaMemset(d_ws, 0, zero_bytes(c));
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
@@ -646,8 +697,9 @@ sph_status sph_port_move(sph_ctx *c, sph_particles *p, int32_t k, const float or
     }
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     // 1. the buffer particles, found among the port's candidates of the current build
-    cudaError_t e = launch_port_move(part_dev(p), dim, c->pt.p[k], P1, c->W.runs + 3 * (size_t)c->run_base[k],
-                                     c->run_cnt[k], cell_start, cell_end, k, nullptr, s, &c->L);
+    cudaError_t e = launch_port_move(part_dev(p), c->gd, c->pt.p[k], P1, c->W.runs + 3 * (size_t)c->run_base[k],
+                                     c->run_cnt[k], cell_start, cell_end, k, nullptr, c->W, carry_on(c, p),
+                                     c->carry_dt, s, &c->L);
     if (e != cudaSuccess) return cuda_fail(c, e, "port_move");
     // 2. first move: the port's runs become a fixed device slice, one slot per cell
     //    column of a window around its bounding sphere (any pose fits); the table is
@@ -829,6 +881,7 @@ sph_status sph_advect(sph_ctx *c, sph_particles *p, float dt, void *stream)
     if (!c) return SPH_ERR_ARG;
     sph_status st = check_particles(c, p);
     if (st != SPH_OK) return st;
+    carry_drop(c);
     cudaError_t e = launch_advect(part_dev(p), c->grid.dim, dt, static_cast<cudaStream_t>(stream), &c->L);
     return e == cudaSuccess ? SPH_OK : cuda_fail(c, e, "advect");
 }
@@ -845,9 +898,12 @@ static sph_status cll_build(sph_ctx *c, const sph_particles *in, sph_particles *
         return fail(c, SPH_ERR_ARG, "cll_build needs distinct input and output arrays");
     if ((reinterpret_cast<size_t>(cell_start) | reinterpret_cast<size_t>(cell_end)) % 16)
         return fail(c, SPH_ERR_ARG, "cell tables must be 16-byte aligned");
-    cudaError_t e = launch_cll(part_dev(in), part_dev(out), c->gd, c->W, cell_start, cell_end, perm, dt, advect,
+    const CllCarry cc = carry_plan(c, in, advect, dt, false);
+    cudaError_t e = launch_cll(part_dev(in), part_dev(out), c->gd, c->W, cell_start, cell_end, perm, dt, advect, cc,
                                static_cast<cudaStream_t>(stream), &c->L);
-    return e == cudaSuccess ? SPH_OK : cuda_fail(c, e, "cll_build");
+    if (e != cudaSuccess) return cuda_fail(c, e, "cll_build");
+    carry_after_build(c, cc, out);
+    return SPH_OK;
 }
 
 sph_status sph_cll_build(sph_ctx *c, const sph_particles *in, sph_particles *out, int32_t *cell_start,
@@ -862,6 +918,13 @@ sph_status sph_advect_cll_build(sph_ctx *c, sph_particles *in, sph_particles *ou
     return cll_build(c, in, out, cell_start, cell_end, perm, dt, true, stream);
 }
 
+sph_status sph_cll_invalidate(sph_ctx *c)
+{
+    if (!c) return SPH_ERR_ARG;
+    carry_drop(c);
+    return SPH_OK;
+}
+
 sph_status sph_cll_key(sph_ctx *c, sph_particles *in, float dt, int32_t advect, float *send_lo, float *send_hi,
                        void *stream)
 {
@@ -871,8 +934,11 @@ sph_status sph_cll_key(sph_ctx *c, sph_particles *in, float dt, int32_t advect, 
     if ((send_lo == nullptr) != (send_hi == nullptr)) return fail(c, SPH_ERR_ARG, "give both send buffers or none");
     c->key_advect = advect != 0;
     c->key_dt = dt;
+    c->key_cc = carry_plan(c, in, advect != 0, dt, send_lo != nullptr);
     cudaError_t e = launch_cll_key(part_dev(in), c->gd, c->W, dt, advect != 0, send_lo, send_hi, c->max_migrate,
-                                   sph_migrate_record_floats(c), static_cast<cudaStream_t>(stream), &c->L);
+                                   sph_migrate_record_floats(c), c->key_cc, static_cast<cudaStream_t>(stream),
+                                   &c->L);
+    if (e == cudaSuccess && c->key_cc.clear) c->carry_next = false;   // cleared: nothing carried any more
     return e == cudaSuccess ? SPH_OK : cuda_fail(c, e, "cll_key");
 }
 
@@ -890,8 +956,10 @@ sph_status sph_cll_finish(sph_ctx *c, sph_particles *in, sph_particles *out, con
         return fail(c, SPH_ERR_ARG, "cell tables must be 16-byte aligned");
     cudaError_t e = launch_cll_finish(part_dev(in), part_dev(out), c->gd, c->W, recv_lo, recv_hi, c->max_migrate,
                                       sph_migrate_record_floats(c), cell_start, cell_end, perm, c->key_advect,
-                                      c->key_dt, static_cast<cudaStream_t>(stream), &c->L);
-    return e == cudaSuccess ? SPH_OK : cuda_fail(c, e, "cll_finish");
+                                      c->key_dt, c->key_cc, static_cast<cudaStream_t>(stream), &c->L);
+    if (e != cudaSuccess) return cuda_fail(c, e, "cll_finish");
+    carry_after_build(c, c->key_cc, out);
+    return SPH_OK;
 }
 
 sph_status sph_buffer_update(sph_ctx *c, sph_particles *p, const int32_t *cell_start, const int32_t *cell_end,
@@ -903,7 +971,7 @@ sph_status sph_buffer_update(sph_ctx *c, sph_particles *p, const int32_t *cell_s
     if (!cell_start || !cell_end || !port_counts) return fail(c, SPH_ERR_ARG, "NULL argument");
     const int n_runs = (int)(c->runs.size() / 3);
     cudaError_t e = launch_update(part_dev(p), c->gd, c->pt, c->W, n_runs, cell_start, cell_end, port_counts,
-                                  static_cast<cudaStream_t>(stream), &c->L);
+                                  carry_on(c, p), c->carry_dt, static_cast<cudaStream_t>(stream), &c->L);
     return e == cudaSuccess ? SPH_OK : cuda_fail(c, e, "buffer_update");
 }
 
@@ -915,9 +983,9 @@ static sph_status compact(sph_ctx *c, sph_particles *p, const int32_t *all_count
     if (st != SPH_OK) return st;
     if (!all_counts || !next_id_dev || nranks <= 0 || rank < 0 || rank >= nranks)
         return fail(c, SPH_ERR_ARG, "bad count matrix / rank");
-    cudaError_t e = launch_compact(part_dev(p), c->pt, c->W, all_counts, nranks, rank,
-                                   reinterpret_cast<long long *>(next_id_dev), perm, defer,
-                                   static_cast<cudaStream_t>(stream), &c->L);
+    cudaError_t e = launch_compact(part_dev(p), c->gd, c->pt, c->W, all_counts, nranks, rank,
+                                   reinterpret_cast<long long *>(next_id_dev), perm, defer, carry_on(c, p),
+                                   c->carry_dt, static_cast<cudaStream_t>(stream), &c->L);
     return e == cudaSuccess ? SPH_OK : cuda_fail(c, e, "compact");
 }
 
@@ -941,6 +1009,7 @@ sph_status sph_migrate_pack(sph_ctx *c, sph_particles *p, float *send_lo, float 
     sph_status st = check_particles(c, p);
     if (st != SPH_OK) return st;
     if (!send_lo || !send_hi) return fail(c, SPH_ERR_ARG, "NULL send buffer");
+    carry_drop(c);
     cudaError_t e = launch_migrate_pack(part_dev(p), c->gd, c->W, send_lo, send_hi, c->max_migrate,
                                         sph_migrate_record_floats(c), static_cast<cudaStream_t>(stream),
                                         &c->L);
@@ -953,6 +1022,7 @@ sph_status sph_migrate_unpack(sph_ctx *c, sph_particles *p, const float *recv, v
     sph_status st = check_particles(c, p);
     if (st != SPH_OK) return st;
     if (!recv) return fail(c, SPH_ERR_ARG, "NULL receive buffer");
+    carry_drop(c);
     cudaError_t e = launch_migrate_unpack(part_dev(p), c->gd, c->W, recv, c->max_migrate,
                                           sph_migrate_record_floats(c), static_cast<cudaStream_t>(stream),
                                           &c->L);

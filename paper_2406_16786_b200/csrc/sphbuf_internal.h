@@ -135,10 +135,10 @@ struct Counters {
 
 struct Workspace {
     Counters *ctr;
-    int *cell_count;                 // [ncells]
+    int *cell_count;                 // [ncells]: build histogram
+    int *cursor;                     // [ncells]: scatter cursors
     unsigned long long *tile_cells;  // [cell tiles]
     int *key;                        // [capacity]
-    int *rank;                       // [capacity]
     int *src;                        // [capacity]: source index of each sorted slot
     unsigned long long *tile_upd;    // [upd tiles]
     unsigned long long *tile_runs;   // [kMaxRuns / 1024 + 1]: update prologue look-back
@@ -185,28 +185,40 @@ struct Launch {
 cudaError_t launch_advect(const PartDev &p, int dim, float dt, cudaStream_t s, Launch *L);
 cudaError_t launch_register(const PartDev &p, const GridDev &g, const PortTable &pt, int k, long long *members,
                             cudaStream_t s, Launch *L);
+// Key carry-over of the cell-list build (sphbuf_cll.cu): `use` — this build's keys
+// and histogram were made by the previous build's gather (skip the key pass);
+// `clear` — the previous gather left a histogram this build does not use (zero
+// it first); `make` — this build's gather prepares the next build's keys for
+// advection by `dt`.
+struct CllCarry {
+    bool use = false, clear = false, make = false;
+    float dt = 0.f;
+};
 cudaError_t launch_cll(const PartDev &in, const PartDev &out, const GridDev &g, const Workspace &ws,
-                       int *cell_start, int *cell_end, int *perm, float dt, bool advect, cudaStream_t s, Launch *L);
+                       int *cell_start, int *cell_end, int *perm, float dt, bool advect, const CllCarry &cc,
+                       cudaStream_t s, Launch *L);
 // advect / dt: the advection of the key pass (launch_cll_key) that this build
 // finishes; the gather applies it to the slab's own particles as it moves them.
 cudaError_t launch_cll_key(const PartDev &in, const GridDev &g, const Workspace &ws, float dt, bool advect,
-                           float *send_lo, float *send_hi, long long maxm, int rec, cudaStream_t s, Launch *L);
+                           float *send_lo, float *send_hi, long long maxm, int rec, const CllCarry &cc,
+                           cudaStream_t s, Launch *L);
 cudaError_t launch_cll_finish(const PartDev &in, const PartDev &out, const GridDev &g, const Workspace &ws,
                               const float *recv_lo, const float *recv_hi, long long maxm, int rec, int *cell_start,
-                              int *cell_end, int *perm, bool advect, float dt, cudaStream_t s, Launch *L);
+                              int *cell_end, int *perm, bool advect, float dt, const CllCarry &cc,
+                              cudaStream_t s, Launch *L);
 cudaError_t launch_update(const PartDev &p, const GridDev &g, const PortTable &pt, const Workspace &ws, int n_runs,
-                          const int *cell_start, const int *cell_end, int *port_counts, cudaStream_t s,
-                          Launch *L);
-cudaError_t launch_compact(const PartDev &p, const PortTable &pt, const Workspace &ws, const int *all_counts,
-                           int nranks, int rank, long long *next_id, int *perm, bool defer, cudaStream_t s,
-                           Launch *L);
+                          const int *cell_start, const int *cell_end, int *port_counts, int carry, float cdt,
+                          cudaStream_t s, Launch *L);
+cudaError_t launch_compact(const PartDev &p, const GridDev &g, const PortTable &pt, const Workspace &ws,
+                           const int *all_counts, int nranks, int rank, long long *next_id, int *perm, bool defer,
+                           int carry, float cdt, cudaStream_t s, Launch *L);
 cudaError_t launch_migrate_pack(const PartDev &p, const GridDev &g, const Workspace &ws, float *lo, float *hi,
                                 long long max_migrate, int rec, cudaStream_t s, Launch *L);
 cudaError_t launch_migrate_unpack(const PartDev &p, const GridDev &g, const Workspace &ws, const float *buf,
                                   long long max_migrate, int rec, cudaStream_t s, Launch *L);
-cudaError_t launch_port_move(const PartDev &p, int dim, const PortDev &P0, const PortDev &P1, const int *runs,
-                             int nrun, const int *cell_start, const int *cell_end, int k, long long *moved,
-                             cudaStream_t s, Launch *L);
+cudaError_t launch_port_move(const PartDev &p, const GridDev &g, const PortDev &P0, const PortDev &P1,
+                             const int *runs, int nrun, const int *cell_start, const int *cell_end, int k,
+                             long long *moved, const Workspace &ws, int carry, float cdt, cudaStream_t s, Launch *L);
 cudaError_t launch_port_enum(const GridDev &g, const PortEnum &P, float cs, int *runs, int cap, cudaStream_t s,
                              Launch *L);
 cudaError_t launch_drivers(const PartDev &p, const Workspace &ws, const DriverLaunch &D, const int *cell_start,

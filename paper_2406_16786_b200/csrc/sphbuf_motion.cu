@@ -46,10 +46,11 @@ __device__ __forceinline__ float rot_global(const PortDev &P, int dim, const flo
 }
 
 // K9: one block per run (grid-stride), threads over the run's particle range.
-__global__ void __launch_bounds__(kThreads) k_port_move(PartDev p, int dim, PortDev P0, PortDev P1, const int *runs,
+__global__ void __launch_bounds__(kThreads) k_port_move(PartDev p, GridDev g, PortDev P0, PortDev P1, const int *runs,
                                                         int nrun, const int *cell_start, const int *cell_end, int k,
-                                                        long long *moved)
+                                                        long long *moved, Workspace ws, int carry, float cdt)
 {
+    const int dim = g.dim;
     pdl_entry();
     long long cnt = 0;
     for (int r = blockIdx.x; r < nrun; r += gridDim.x) {
@@ -71,6 +72,9 @@ __global__ void __launch_bounds__(kThreads) k_port_move(PartDev p, int dim, Port
                 p.z[i] = to_global(P1, dim, X, 2);
                 p.vz[i] = rot_global(P1, dim, V, 2);
             }
+            if (carry)
+                carry_fix(g, ws, i, false, p.x[i], p.y[i], dim == 3 ? p.z[i] : 0.0f, p.vx[i], p.vy[i],
+                          dim == 3 ? p.vz[i] : 0.0f, cdt);
             ++cnt;
         }
     }
@@ -154,14 +158,14 @@ __global__ void __launch_bounds__(kThreads) k_port_enum(GridDev g, PortEnum P, f
     runs[3 * i + 2] = P.k;
 }
 
-cudaError_t launch_port_move(const PartDev &p, int dim, const PortDev &P0, const PortDev &P1, const int *runs,
-                             int nrun, const int *cell_start, const int *cell_end, int k, long long *moved,
-                             cudaStream_t s, Launch *L)
+cudaError_t launch_port_move(const PartDev &p, const GridDev &g, const PortDev &P0, const PortDev &P1,
+                             const int *runs, int nrun, const int *cell_start, const int *cell_end, int k,
+                             long long *moved, const Workspace &ws, int carry, float cdt, cudaStream_t s, Launch *L)
 {
     if (nrun <= 0) return cudaSuccess;
     L->before(s);
-    launch_k(k_port_move, dim3(nrun < 4 * sm_count_cached() ? nrun : 4 * sm_count_cached()), dim3(128), 0, s, 
-        p, dim, P0, P1, runs, nrun, cell_start, cell_end, k, moved);
+    launch_k(k_port_move, dim3(nrun < 4 * sm_count_cached() ? nrun : 4 * sm_count_cached()), dim3(128), 0, s, p, g,
+             P0, P1, runs, nrun, cell_start, cell_end, k, moved, ws, carry, cdt);
     L->after(s, KID_PORT_MOVE);
     return cudaGetLastError();
 }

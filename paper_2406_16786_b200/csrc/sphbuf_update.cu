@@ -120,10 +120,11 @@ __global__ void __launch_bounds__(1024) k_upd_prologue(Workspace ws, int n_runs,
 // K6: the candidate check (a3) with generation (a4), deletion (a5) and relabel
 // (a6) fused; CREATEs are appended to the staging area in canonical order
 // (port, cell, id) by a ballot/block scan + decoupled look-back over ordered tiles.
-__global__ void __launch_bounds__(kThreads) k_upd_main(PartDev p, int dim, const __grid_constant__ PortTable pt,
+__global__ void __launch_bounds__(kThreads) k_upd_main(PartDev p, GridDev g, const __grid_constant__ PortTable pt,
                                                        Workspace ws, int n_runs, const int *cell_start,
-                                                       int *port_counts)
+                                                       int *port_counts, int carry, float cdt)
 {
+    const int dim = g.dim;
     pdl_entry();
     __shared__ PortDev s_ports[SPH_MAX_PORTS];
     __shared__ unsigned s_warp[kUpdItems * kThreads / 32 + 1];
@@ -152,13 +153,14 @@ __global__ void __launch_bounds__(kThreads) k_upd_main(PartDev p, int dim, const
         __syncthreads();
         const long long tile = s_tile;
         if (tile >= ntiles || tile >= ws.upd_tiles) break;
-        bool cr[kUpdItems], bcm[kUpdItems];
+        bool cr[kUpdItems], bcm[kUpdItems], dl[kUpdItems];
         int pidx[kUpdItems], kk[kUpdItems];
         float ox[kUpdItems], oy[kUpdItems], oz[kUpdItems], bY[kUpdItems], bZ[kUpdItems];
 #pragma unroll
         for (int it = 0; it < kUpdItems; ++it) {
             cr[it] = false;
             bcm[it] = false;
+            dl[it] = false;
             pidx[it] = -1;
             kk[it] = 0;
             ox[it] = oy[it] = oz[it] = 0.0f;
@@ -219,6 +221,7 @@ __global__ void __launch_bounds__(kThreads) k_upd_main(PartDev p, int dim, const
             float Xp[3] = {X[0], X[1], X[2]};
             if (create) to_local(P, dim, px, py, pz, Xp);      // post-recycle local frame
             bool fin = member;                                 // a buffer particle of k after the update
+            dl[it] = del;
             if (del) {
                 p.label[pi] = -2;                                // tombstone, removed by sph_compact
                 atomicAdd(&port_counts[max_ports + k], 1);
@@ -298,6 +301,17 @@ __global__ void __launch_bounds__(kThreads) k_upd_main(PartDev p, int dim, const
             p.vy[pi] = __fmul_rn(u, P.Q[1]);
             if (dim == 3) p.vz[pi] = __fmul_rn(u, P.Q[2]);
         }
+        // key carry-over: particles whose position or velocity changed here (or that
+        // were deleted) get their next-build key and histogram entry corrected
+        if (carry) {
+#pragma unroll
+            for (int it = 0; it < kUpdItems; ++it) {
+                if (!(cr[it] || dl[it] || bcm[it])) continue;
+                const int pi = pidx[it];
+                carry_fix(g, ws, pi, dl[it], p.x[pi], p.y[pi], dim == 3 ? p.z[pi] : 0.0f, p.vx[pi], p.vy[pi],
+                          dim == 3 ? p.vz[pi] : 0.0f, cdt);
+            }
+        }
         if (tile == ntiles - 1 && threadIdx.x == 0) ctr->n_stage = (long long)s_prefix + total;
         __syncthreads();
     }
@@ -338,7 +352,8 @@ cudaError_t launch_register(const PartDev &p, const GridDev &g, const PortTable 
 }
 
 cudaError_t launch_update(const PartDev &p, const GridDev &g, const PortTable &pt, const Workspace &ws, int n_runs,
-                          const int *cell_start, const int *cell_end, int *port_counts, cudaStream_t s, Launch *L)
+                          const int *cell_start, const int *cell_end, int *port_counts, int carry, float cdt,
+                          cudaStream_t s, Launch *L)
 {
     L->before(s);
     const int pro_blocks = n_runs > 0 ? (n_runs + 1023) / 1024 : 1;
@@ -348,7 +363,8 @@ cudaError_t launch_update(const PartDev &p, const GridDev &g, const PortTable &p
     static int grid = 0;
     if (!grid) grid = occ_grid(k_upd_main, kThreads);
     L->before(s);
-    launch_k(k_upd_main, dim3(cap_grid(grid, ws.upd_tiles, 1)), dim3(kThreads), 0, s, p, g.dim, pt, ws, n_runs, cell_start, port_counts);
+    launch_k(k_upd_main, dim3(cap_grid(grid, ws.upd_tiles, 1)), dim3(kThreads), 0, s, p, g, pt, ws, n_runs, cell_start,
+             port_counts, carry, cdt);
     L->after(s, KID_UPD_MAIN);
     return cudaGetLastError();
 }

@@ -68,7 +68,7 @@ EXPORTS = ["sph_ctx_create", "sph_ctx_destroy", "sph_last_error", "sph_workspace
            "sph_compact", "sph_migrate_record_floats", "sph_migrate_pack", "sph_migrate_unpack", "sph_status_sync",
            "sph_launch_count", "sph_port_cells", "sph_frame_from_axis", "sph_profile", "sph_profile_read",
            "sph_kernel_name", "sph_advect_cll_build", "sph_compact_deferred", "sph_cll_key", "sph_cll_finish",
-           "sph_port_set_bc", "sph_port_move", "sph_port_set_driver",
+           "sph_port_set_bc", "sph_port_move", "sph_port_set_driver", "sph_cll_invalidate",
            "sph_drivers_step", "sph_driver_read"]
 NKERNELS = 16
 
@@ -109,6 +109,8 @@ def lib():
     L.sph_driver_read.restype = C.c_int
     L.sph_port_move.argtypes = [vp, P(sph_particles), i32, vp, vp, vp, vp, vp]
     L.sph_port_move.restype = C.c_int
+    L.sph_cll_invalidate.argtypes = [vp]
+    L.sph_cll_invalidate.restype = C.c_int
     L.sph_cll_key.argtypes = [vp, P(sph_particles), f32, i32, vp, vp, vp]
     L.sph_cll_key.restype = C.c_int
     L.sph_cll_finish.argtypes = [vp, P(sph_particles), P(sph_particles), vp, vp, vp, vp, vp, vp]
@@ -267,6 +269,10 @@ def sph_port_move(ctx, parts, port_id, origin, Q, cell_start, cell_end, stream=N
     o, q = _f3(origin), _f9(Q)
     _check(lib().sph_port_move(ctx.h, C.byref(parts.abi), int(port_id), o, q, _ptr(cell_start), _ptr(cell_end),
                                _stream(stream)), ctx.h)
+
+
+def sph_cll_invalidate(ctx):
+    _check(lib().sph_cll_invalidate(ctx.h), ctx.h)
 
 
 def sph_cll_key(ctx, pin, dt=None, send_lo=None, send_hi=None, stream=None):
@@ -438,6 +444,7 @@ class BufferUpdater:
     def load(self, state: dict, next_id: int):
         self.A.load(state)
         self.next_id.fill_(int(next_id))
+        sph_cll_invalidate(self.ctx)   # new particles: no carried-over keys apply
 
     def register_ports(self, stream=None):
         for k, p in enumerate(self.ports):
