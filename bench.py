@@ -332,6 +332,7 @@ def run_e2e(su, w, args, dev, world):
         bu.A.id[:n].copy_(host_in["id"][:n], non_blocking=True)
         bu.A.label[:n].copy_(host_in["label"][:n], non_blocking=True)
         bu.A.n.fill_(n)
+        sphbuf.sph_cll_invalidate(bu.ctx)   # uploaded state: no carried-over keys (ABI contract)
         h2d += n * (4 * len(cols) + 12)
         su.step(w.dt)
         n = int(bu.A.n.item())
