@@ -278,21 +278,21 @@ __global__ void __launch_bounds__(kThreads) k_cell_scan(GridDev g, Workspace ws,
     if (tile == ntiles - 1 && threadIdx.x == 0) *n_out = (long long)(prefix + total);
 }
 
-constexpr int kScatterItems = 8;
 
 // K3: source index of every sorted slot: slot = cell_start[key] + a per-cell
 // cursor (one atomic per run of equal keys in a warp; the order inside a cell is
 // arbitrary here, the gather ranks by id).
-__global__ void __launch_bounds__(kThreads) k_cll_scatter(Workspace ws, const int *cell_start, int *perm)
+template <int kScatterItems, int NT>
+__global__ void __launch_bounds__(NT) k_cll_scatter(Workspace ws, const int *cell_start, int *perm)
 {
     pdl_entry();
     const long long n = ws.ctr->n_in;
-    const long long stride = (long long)gridDim.x * kThreads * kScatterItems;
-    for (long long base = (long long)blockIdx.x * kThreads * kScatterItems; base < n; base += stride) {
+    const long long stride = (long long)gridDim.x * NT * kScatterItems;
+    for (long long base = (long long)blockIdx.x * NT * kScatterItems; base < n; base += stride) {
         int key[kScatterItems];
 #pragma unroll
         for (int it = 0; it < kScatterItems; ++it) {
-            const long long i = base + it * kThreads + threadIdx.x;
+            const long long i = base + it * NT + threadIdx.x;
             key[it] = i < n ? ws.key[i] : -1;
         }
         // run heads of all items first, then all their atomics in flight together
@@ -312,7 +312,7 @@ __global__ void __launch_bounds__(kThreads) k_cll_scatter(Workspace ws, const in
 #pragma unroll
         for (int it = 0; it < kScatterItems; ++it) {
             const int rk = __shfl_sync(0xffffffffu, b[it], hl[it]) + lane - hl[it];
-            const long long i = base + it * kThreads + threadIdx.x;
+            const long long i = base + it * NT + threadIdx.x;
             if (i >= n) continue;
             if (key[it] >= 0) {
                 const int slot = __ldg(cell_start + key[it]) + rk;
@@ -327,6 +327,13 @@ __global__ void __launch_bounds__(kThreads) k_cll_scatter(Workspace ws, const in
 
 constexpr int kHalo = 64;   // slots staged on either side of a gather tile
 
+// acc + [a >= m] (unsigned): the carry of a - m, two instructions per element.
+__device__ __forceinline__ unsigned add_ge(unsigned acc, unsigned a, unsigned m)
+{
+    asm("{\n\t.reg .u32 t;\n\tsub.cc.u32 t, %1, %2;\n\taddc.u32 %0, %0, 0;\n\t}" : "+r"(acc) : "r"(a), "r"(m));
+    return acc;
+}
+
 // Rank by id of slot p (id me) among its cell's slots [cb, ce).  The ids of the
 // slots [w0, w1) are in shared memory at sid[q - w0]; a cell reaching past them
 // (more than kHalo slots outside the tile) reads the rest from global memory.
@@ -338,10 +345,22 @@ __device__ __forceinline__ int rank_in_cell(const PartDev &in, const Workspace &
     int r = 0;
     if (cb >= w0 && ce <= w1) {
         if (narrow) {
+            // 8-byte pairs of low words over the range padded to even slots (the
+            // staged window starts on an even slot), each compare folded into a
+            // carry-add (count of ids >= me), the padding slots taken back out
             const unsigned *sc = slo - w0;
             const unsigned m32 = (unsigned)me;
-#pragma unroll 4
-            for (int q = cb; q < ce; ++q) r += (sc[q] < m32);
+            const int q0 = cb & ~1, q1 = (ce + 1) & ~1;
+            unsigned ge = 0;
+#pragma unroll 2
+            for (int q = q0; q < q1; q += 2) {
+                const uint2 v = *reinterpret_cast<const uint2 *>(sc + q);
+                ge = add_ge(ge, v.x, m32);
+                ge = add_ge(ge, v.y, m32);
+            }
+            r = (q1 - q0) - (int)ge;
+            if (cb & 1) r -= (sc[cb - 1] < m32);
+            if (ce & 1) r -= (sc[ce] < m32);
             return r;
         }
         const long long *sc = sid - w0;
@@ -370,7 +389,7 @@ __global__ void __launch_bounds__(NT, MINB) k_cll_gather(PartDev in, PartDev out
     constexpr int T = NT * ITEMS;
     static_assert(2 * kHalo <= NT, "one halo slot per thread");
     __shared__ long long s_id[kHalo + T + kHalo];
-    __shared__ unsigned s_lo[kHalo + T + kHalo];
+    __shared__ __align__(16) unsigned s_lo[kHalo + T + kHalo];
     const long long n = *out.n;
     const int dim = g.dim;
     // sources below mig_base are this slab's own particles (advected here when the
@@ -504,6 +523,14 @@ __global__ void __launch_bounds__(NT, MINB) k_cll_gather(PartDev in, PartDev out
 
 // ------------------------------------------------------------------ launchers
 
+template <int I, int NT>
+static void scatter_launch(const Workspace &ws, const int *cell_start, int *perm, long long cap, cudaStream_t s)
+{
+    static int grid = 0;
+    if (!grid) grid = occ_grid(k_cll_scatter<I, NT>, NT);
+    launch_k(k_cll_scatter<I, NT>, dim3(cap_grid(grid, cap, NT * I)), dim3(NT), 0, s, ws, cell_start, perm);
+}
+
 // Gather variants (template instances), chosen by SPHBUF_GATHER=<slots>:<min blocks>
 // for tuning runs (tools/gather_sweep.py); the default is the measured best.
 template <bool HasExtra, int ITEMS, int MINB, int NT = kThreads, bool PF = false>
@@ -621,10 +648,16 @@ cudaError_t launch_cll_finish(const PartDev &in, const PartDev &out, const GridD
     launch_k(k_cell_scan, dim3((unsigned)(ntiles > 0 ? ntiles : 1)), dim3(kThreads), 0, s, g, ws, cell_start, cell_end, out.n, ntiles);
     L->after(s, KID_CELL_SCAN);
     {
-        static int grid = 0;
-        if (!grid) grid = occ_grid(k_cll_scatter, kThreads);
+        // scatter variants for tuning (SPHBUF_SCATTER=<items>:<threads>); default 4 x 256,
+        // measured best on C5 among 1-16 items x 128-512 threads
+        static const char *sv = getenv("SPHBUF_SCATTER");
+        const char *v = sv ? sv : "";
         L->before(s);
-        launch_k(k_cll_scatter, dim3(cap_grid(grid, cap, kThreads * kScatterItems)), dim3(kThreads), 0, s, ws, cell_start, perm);
+        if (!strcmp(v, "8:256")) scatter_launch<8, 256>(ws, cell_start, perm, cap, s);
+        else if (!strcmp(v, "2:256")) scatter_launch<2, 256>(ws, cell_start, perm, cap, s);
+        else if (!strcmp(v, "1:256")) scatter_launch<1, 256>(ws, cell_start, perm, cap, s);
+        else if (!strcmp(v, "2:512")) scatter_launch<2, 512>(ws, cell_start, perm, cap, s);
+        else scatter_launch<4, 256>(ws, cell_start, perm, cap, s);
         L->after(s, KID_CLL_SCATTER);
     }
     L->before(s);
