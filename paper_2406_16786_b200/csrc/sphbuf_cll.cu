@@ -146,6 +146,39 @@ __global__ void k_cll_begin(PartDev in, Workspace ws)
     ctr->mig_base = n;
 }
 
+// K1 in key carry-over mode with slab migration: the listed leavers (still keyed
+// kLeaver; a later fix-up may have kept one inside, a duplicate entry is claimed
+// once) are packed for the neighbour ranks with their advected positions, as the
+// key pass would have; everything else was keyed by the previous build.
+__global__ void __launch_bounds__(kThreads) k_mig_pack_list(PartDev in, GridDev g, Workspace ws, float dt,
+                                                            float *mlo, float *mhi, long long maxm, int rec)
+{
+    pdl_entry();
+    Counters *ctr = ws.ctr;
+    const long long n = *in.n;
+    long long nl = ctr->n_leave;
+    if (nl > ws.max_leave) nl = ws.max_leave;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        ctr->epoch_cll += 1;
+        ctr->ticket_cll = 0;
+        ctr->n_in = n;
+        ctr->mig_base = n;
+    }
+    long long moved = 0;
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < nl; e += (long long)gridDim.x * blockDim.x) {
+        const int i = ws.leave[e];
+        if (atomicCAS(&ws.key[i], kLeaver, kPacked) != kLeaver) continue;
+        const float x = advect1(in.x[i], in.vx[i], dt), y = advect1(in.y[i], in.vy[i], dt),
+                    z = g.dim == 3 ? advect1(in.z[i], in.vz[i], dt) : 0.0f;
+        int o2 = 0;
+        const int cxr = cell_axis(x, g.lo[0], g.inv_cs, 0, g.ncell[0], o2);
+        pack_record(in, g.dim, i, x, y, z, in.label[i], cxr < g.cx_begin ? mlo : mhi, maxm, rec, ctr);
+        ++moved;
+    }
+    moved = warp_sum_ll(moved);
+    if ((threadIdx.x & 31) == 0 && moved) atomicAdd((unsigned long long *)&ctr->migrated, (unsigned long long)moved);
+}
+
 // K1b (multi-GPU): append the particles received from the neighbour slabs after
 // the local ones (index mig_base + s) with their keys and ranks, before the scan.
 __global__ void __launch_bounds__(kThreads) k_cll_unpack_key(PartDev in, GridDev g, Workspace ws, const float *blo,
@@ -275,7 +308,10 @@ __global__ void __launch_bounds__(kThreads) k_cell_scan(GridDev g, Workspace ws,
             }
         }
     }
-    if (tile == ntiles - 1 && threadIdx.x == 0) *n_out = (long long)(prefix + total);
+    if (tile == ntiles - 1 && threadIdx.x == 0) {
+        *n_out = (long long)(prefix + total);
+        ctr->n_leave = 0;   // the leaver list of the next build starts here (pack-from-list ran before)
+    }
 }
 
 
@@ -487,12 +523,13 @@ __global__ void __launch_bounds__(NT, MINB) k_cll_gather(PartDev in, PartDev out
             const int d = cb[it] + rank_in_cell(in, ws, sid, slo, narrow, w0, w1, cb[it], ce[it], me);
             if (carry) {
                 // key carry-over: the next build's key of the particle now at d (its
-                // position advected again by cdt), so that build needs no key pass
+                // position advected again by cdt), so that build needs no key pass;
+                // with slab migration a particle about to leave the slab is listed
                 int oobn = 0;
-                kn[it] = cell_of(g, advect1(x[it], vx[it], cdt), advect1(y[it], vy[it], cdt),
-                                 dim == 3 ? advect1(z[it], vz[it], cdt) : 0.0f, oobn);
+                kn[it] = carry_key(g, x[it], y[it], z[it], vx[it], vy[it], vz[it], cdt, carry, oobn);
                 oob_next += oobn;
                 ws.key[d] = kn[it];
+                if (kn[it] == kLeaver) leaver_append(ws, d);
             }
             SPH_CHECK(d >= cb[it] && d < ce[it] && ce[it] <= n && src[it] < in.cap);
             out.x[d] = x[it];
@@ -596,9 +633,19 @@ cudaError_t launch_cll_key(const PartDev &in, const GridDev &g, const Workspace 
                            float *send_lo, float *send_hi, long long maxm, int rec, const CllCarry &cc, cudaStream_t s,
                            Launch *L)
 {
-    if (cc.use) {
+    if (cc.use && !(send_lo && send_hi)) {
         L->before(s);
         launch_k(k_cll_begin, dim3(1), dim3(1), 0, s, in, ws);
+        L->after(s, KID_CLL_KEY);
+        return cudaGetLastError();
+    }
+    if (cc.use) {
+        cudaError_t e = cudaMemsetAsync(send_lo, 0, 16, s);
+        if (e == cudaSuccess) e = cudaMemsetAsync(send_hi, 0, 16, s);
+        if (e != cudaSuccess) return e;
+        L->before(s);
+        launch_k(k_mig_pack_list, dim3(cap_grid(sm_count_cached() * 2, ws.max_leave, kThreads)), dim3(kThreads), 0, s,
+                 in, g, ws, dt, send_lo, send_hi, maxm, rec);
         L->after(s, KID_CLL_KEY);
         return cudaGetLastError();
     }
@@ -661,7 +708,8 @@ cudaError_t launch_cll_finish(const PartDev &in, const PartDev &out, const GridD
         L->after(s, KID_CLL_SCATTER);
     }
     L->before(s);
-    launch_gather(in, out, g, ws, cell_start, cell_end, perm, advect, dt, cc.make ? 1 : 0, cc.dt, cap, s);
+    launch_gather(in, out, g, ws, cell_start, cell_end, perm, advect, dt, cc.make ? (cc.mig ? 2 : 1) : 0, cc.dt, cap,
+                  s);
     L->after(s, KID_CLL_GATHER);
     return cudaGetLastError();
 }

@@ -292,21 +292,45 @@ __device__ __forceinline__ int cell_of(const GridDev &g, float x, float y, float
     return ((cx - g.cx_begin) * g.ny + cy) * g.nz + cz;
 }
 
-// Key carry-over fix-up (sphbuf_cll.cu): particle i, whose next-build key
-// ws.key[i] the gather computed, now has position x and velocity v (or was
-// deleted): its key for advection by cdt and the next histogram follow.
+// Key carry-over (sphbuf_cll.cu).  carry: 0 off, 1 on, 2 on with slab
+// migration — a particle whose next cell x-index leaves the slab gets the key
+// kLeaver (not counted; its index goes to the leaver list, packed for the
+// neighbour rank by the next build).
+constexpr int kLeaver = -2;
+constexpr int kPacked = -3;
+
+__device__ __forceinline__ int carry_key(const GridDev &g, float x, float y, float z, float vx, float vy, float vz,
+                                         float cdt, int carry, int &oob)
+{
+    const float xa = advect1(x, vx, cdt), ya = advect1(y, vy, cdt), za = g.dim == 3 ? advect1(z, vz, cdt) : 0.0f;
+    if (carry == 2) {
+        int o2 = 0;
+        const int cxr = cell_axis(xa, g.lo[0], g.inv_cs, 0, g.ncell[0], o2);
+        if (cxr < g.cx_begin || cxr >= g.cx_end) return kLeaver;
+    }
+    return cell_of(g, xa, ya, za, oob);
+}
+
+__device__ __forceinline__ void leaver_append(const Workspace &ws, long long i)
+{
+    const long long e = atomicAdd((unsigned long long *)&ws.ctr->n_leave, 1ull);
+    if (e < ws.max_leave) ws.leave[e] = (int)i;
+    else atomicOr(&ws.ctr->status, kStMigrate);
+}
+
+// Fix-up: particle i, whose next-build key ws.key[i] the gather computed, now has
+// position x and velocity v (or was deleted): its key and the next histogram
+// follow (a leaver key leaves the histogram alone and lists the particle).
 __device__ __forceinline__ void carry_fix(const GridDev &g, const Workspace &ws, long long i, bool del, float x,
-                                          float y, float z, float vx, float vy, float vz, float cdt)
+                                          float y, float z, float vx, float vy, float vz, float cdt, int carry)
 {
     const int kold = ws.key[i];
-    int knew = -1;
-    if (!del) {
-        int oob = 0;
-        knew = cell_of(g, advect1(x, vx, cdt), advect1(y, vy, cdt), g.dim == 3 ? advect1(z, vz, cdt) : 0.0f, oob);
-    }
+    int oob = 0;
+    const int knew = del ? -1 : carry_key(g, x, y, z, vx, vy, vz, cdt, carry, oob);
     if (knew != kold) {
         if (kold >= 0) atomicSub(&ws.cell_count[kold], 1);
         if (knew >= 0) atomicAdd(&ws.cell_count[knew], 1);
+        if (knew == kLeaver) leaver_append(ws, i);      // (a stale entry is skipped when packing)
         ws.key[i] = knew;
     }
 }

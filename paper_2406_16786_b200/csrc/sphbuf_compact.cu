@@ -271,10 +271,11 @@ __global__ void __launch_bounds__(kThreads) k_compact_append(PartDev p, GridDev 
         if (carry) {
             // key carry-over: the new particle's key for the next build
             int oob = 0;
-            const int key = cell_of(g, advect1(ws.sx[s], ws.svx[s], cdt), advect1(ws.sy[s], ws.svy[s], cdt),
-                                    dim == 3 ? advect1(ws.sz[s], ws.svz[s], cdt) : 0.0f, oob);
+            const int key = carry_key(g, ws.sx[s], ws.sy[s], dim == 3 ? ws.sz[s] : 0.0f, ws.svx[s], ws.svy[s],
+                                      dim == 3 ? ws.svz[s] : 0.0f, cdt, carry, oob);
             ws.key[d] = key;
-            atomicAdd(&ws.cell_count[key], 1);
+            if (key >= 0) atomicAdd(&ws.cell_count[key], 1);
+            else leaver_append(ws, d);
         }
     }
     if (perm) {

@@ -105,6 +105,7 @@ struct sph_ctx {
     // histogram of a next build that advects by carry_dt the arrays (carry_x,
     // carry_id) it wrote; the update, compaction and port moves keep them current
     bool carry_next = false;
+    bool carry_mig = false;   // made with slab migration (leaver list)
     float carry_dt = 0.f;
     const float *carry_x = nullptr;
     const int64_t *carry_id = nullptr;
@@ -156,6 +157,8 @@ size_t layout(const sph_ctx *c, char *base, Workspace *W)
     w.sub_off = (unsigned *)take(4 * cmp_subs);
     w.key = (int *)take(sizeof(int) * cap);
     w.src = (int *)take(sizeof(int) * cap);
+    w.max_leave = 2 * c->max_migrate + 1024;
+    w.leave = (int *)take(sizeof(int) * w.max_leave);
     const long long mn = c->max_new;
     w.sx = (float *)take(4 * mn);
     w.sy = (float *)take(4 * mn);
@@ -420,11 +423,12 @@ static CllCarry carry_plan(const sph_ctx *c, const sph_particles *in, bool advec
         enabled = (v && v[0] == '0') ? 0 : 1;
     }
     CllCarry cc;
-    const bool match = c->carry_next && advect && !migrating && in->x == c->carry_x && in->id == c->carry_id &&
-                       dt == c->carry_dt;
+    const bool match = c->carry_next && advect && migrating == c->carry_mig && in->x == c->carry_x &&
+                       in->id == c->carry_id && dt == c->carry_dt;
     cc.use = match;
     cc.clear = c->carry_next && !match;
-    cc.make = enabled && advect && !migrating;
+    cc.make = enabled && advect;
+    cc.mig = migrating;
     cc.dt = dt;
     return cc;
 }
@@ -432,15 +436,18 @@ static CllCarry carry_plan(const sph_ctx *c, const sph_particles *in, bool advec
 static void carry_after_build(sph_ctx *c, const CllCarry &cc, const sph_particles *out)
 {
     c->carry_next = cc.make;
+    c->carry_mig = cc.mig;
     c->carry_dt = cc.dt;
     c->carry_x = out->x;
     c->carry_id = out->id;
 }
 
-// 1 when the carried keys describe `p` (the arrays the last build wrote).
+// The carry mode of the kernels that change particles of `p` (0 when the carried
+// keys do not describe `p`, the arrays the last build wrote; 2 with migration).
 static int carry_on(const sph_ctx *c, const sph_particles *p)
 {
-    return (c->carry_next && p->x == c->carry_x && p->id == c->carry_id) ? 1 : 0;
+    if (!(c->carry_next && p->x == c->carry_x && p->id == c->carry_id)) return 0;
+    return c->carry_mig ? 2 : 1;
 }
 
 // Positions or arrays changed behind the carried keys: the next build clears the
@@ -983,9 +990,16 @@ static sph_status compact(sph_ctx *c, sph_particles *p, const int32_t *all_count
     if (st != SPH_OK) return st;
     if (!all_counts || !next_id_dev || nranks <= 0 || rank < 0 || rank >= nranks)
         return fail(c, SPH_ERR_ARG, "bad count matrix / rank");
+    int carry = carry_on(c, p);
+    if (carry == 2 && !defer) {
+        // an in-place compaction renumbers particles behind the leaver list: the
+        // next build runs its own key pass instead
+        carry_drop(c);
+        carry = 0;
+    }
     cudaError_t e = launch_compact(part_dev(p), c->gd, c->pt, c->W, all_counts, nranks, rank,
-                                   reinterpret_cast<long long *>(next_id_dev), perm, defer, carry_on(c, p),
-                                   c->carry_dt, static_cast<cudaStream_t>(stream), &c->L);
+                                   reinterpret_cast<long long *>(next_id_dev), perm, defer, carry, c->carry_dt,
+                                   static_cast<cudaStream_t>(stream), &c->L);
     return e == cudaSuccess ? SPH_OK : cuda_fail(c, e, "compact");
 }
 

@@ -127,6 +127,7 @@ struct Counters {
     long long cmp_next_id; // compaction: next_id before
     long long migrated;    // cumulative packed for neighbour slabs
     long long mig_base;    // cll: local count before the received particles are appended
+    long long n_leave;     // key carry-over: leavers listed for the next build's migration
     int status;            // sticky bits
     int ticket_runs;       // update prologue: tile tickets (reset by its last block)
     int done_runs;         // update prologue: finished blocks
@@ -139,6 +140,7 @@ struct Workspace {
     int *cursor;                     // [ncells]: scatter cursors
     unsigned long long *tile_cells;  // [cell tiles]
     int *key;                        // [capacity]
+    int *leave;                      // [max_leave]: indices of listed leavers (key carry-over + migration)
     int *src;                        // [capacity]: source index of each sorted slot
     unsigned long long *tile_upd;    // [upd tiles]
     unsigned long long *tile_runs;   // [kMaxRuns / 1024 + 1]: update prologue look-back
@@ -154,6 +156,7 @@ struct Workspace {
     long long *sid;                  // source id of each staged particle (diagnostic)
     int *sport;                      // port of each staged particle
     long long max_new;
+    long long max_leave;
     long long upd_tiles;
     long long cmp_tiles;
 };
@@ -192,6 +195,7 @@ cudaError_t launch_register(const PartDev &p, const GridDev &g, const PortTable 
 // advection by `dt`.
 struct CllCarry {
     bool use = false, clear = false, make = false;
+    bool mig = false;   // with slab migration (leaver list)
     float dt = 0.f;
 };
 cudaError_t launch_cll(const PartDev &in, const PartDev &out, const GridDev &g, const Workspace &ws,

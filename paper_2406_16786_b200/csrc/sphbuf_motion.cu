@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(kThreads) k_port_move(PartDev p, GridDev g, Po
             }
             if (carry)
                 carry_fix(g, ws, i, false, p.x[i], p.y[i], dim == 3 ? p.z[i] : 0.0f, p.vx[i], p.vy[i],
-                          dim == 3 ? p.vz[i] : 0.0f, cdt);
+                          dim == 3 ? p.vz[i] : 0.0f, cdt, carry);
             ++cnt;
         }
     }

@@ -309,7 +309,7 @@ __global__ void __launch_bounds__(kThreads) k_upd_main(PartDev p, GridDev g, con
                 if (!(cr[it] || dl[it] || bcm[it])) continue;
                 const int pi = pidx[it];
                 carry_fix(g, ws, pi, dl[it], p.x[pi], p.y[pi], dim == 3 ? p.z[pi] : 0.0f, p.vx[pi], p.vy[pi],
-                          dim == 3 ? p.vz[pi] : 0.0f, cdt);
+                          dim == 3 ? p.vz[pi] : 0.0f, cdt, carry);
             }
         }
         if (tile == ntiles - 1 && threadIdx.x == 0) ctr->n_stage = (long long)s_prefix + total;
