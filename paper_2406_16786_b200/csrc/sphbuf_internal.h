@@ -14,7 +14,7 @@ namespace sphbuf {
 
 // ---------------------------------------------------------------- tiling
 constexpr int kThreads = 256;            // block size of the O(N) kernels
-constexpr int kCellItems = 64;           // cells per thread in the cell scan (multiple of 4)
+constexpr int kCellItems = 32;           // cells per thread in the cell scan (multiple of 4)
 constexpr int kCellTile = kThreads * kCellItems;
 constexpr int kUpdItems = 2;             // candidates per thread in the update
 constexpr int kUpdTile = kThreads * kUpdItems;
