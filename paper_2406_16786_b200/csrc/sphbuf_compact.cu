@@ -221,12 +221,7 @@ __global__ void __launch_bounds__(kThreads) k_compact_append(PartDev p, GridDev 
     __shared__ long long s_beg[SPH_MAX_PORTS];
     __shared__ long long s_total;
     Counters *ctr = ws.ctr;
-    if (defer && threadIdx.x == 0) {
-        ctr->cmp_n = *p.n;
-        ctr->cmp_next_id = *next_id;
-    }
-    __syncthreads();
-    const long long nid0 = ctr->cmp_next_id;
+    const long long nid0 = ctr->cmp_next_id;   // N and next_id before: k_compact_prep / k_compact_count
     if (threadIdx.x == 0) {
         long long acc = nid0, beg = 0;
         for (int k = 0; k < n_ports; ++k) {
@@ -288,6 +283,15 @@ __global__ void __launch_bounds__(kThreads) k_compact_append(PartDev p, GridDev 
     }
 }
 
+// Deferred mode: N and next_id before the append, for every block of the append
+// (which writes both at its end).
+__global__ void k_compact_prep(PartDev p, Workspace ws, const long long *next_id)
+{
+    pdl_entry();
+    ws.ctr->cmp_n = *p.n;
+    ws.ctr->cmp_next_id = *next_id;
+}
+
 // ------------------------------------------------------------------ launcher
 
 cudaError_t launch_compact(const PartDev &p, const GridDev &g, const PortTable &pt, const Workspace &ws,
@@ -296,8 +300,9 @@ cudaError_t launch_compact(const PartDev &p, const GridDev &g, const PortTable &
 {
     if (defer) {
         L->before(s);
-        launch_k(k_compact_append, dim3(1), dim3(kThreads), 0, s, p, g, pt.n, pt.max_ports, ws, all_counts, nranks,
-                 rank, next_id, nullptr, true, carry, cdt);
+        launch_k(k_compact_prep, dim3(1), dim3(1), 0, s, p, ws, (const long long *)next_id);
+        launch_k(k_compact_append, dim3(cap_grid(sm_count_cached() * 2, ws.max_new, kThreads)), dim3(kThreads), 0, s,
+                 p, g, pt.n, pt.max_ports, ws, all_counts, nranks, rank, next_id, nullptr, true, carry, cdt);
         L->after(s, KID_COMPACT_APPEND);
         return cudaGetLastError();
     }
