@@ -302,46 +302,59 @@ def run_ours(args):
 
 
 def run_e2e(su, w, args, dev, world):
-    """The same metric end to end: each step copies the rank's particle state from
-    pinned host memory to the device (H2D), runs the update through the public
-    API, and reads the updated state back (D2H).  Host-resident simulation loop."""
+    """The same metric end to end: every step uploads the rank's particle state from
+    pinned host memory (H2D), runs the update through the public API, and reads
+    the updated state back (D2H) — a host-resident simulation loop.  The read-back
+    of one step and the upload of the next are pipelined per column on two copy
+    streams (the two PCIe directions run concurrently): column c goes up again as
+    soon as it has come down, and the next step starts once every column is up."""
     bu = su.bu
     n = bu.A.count()
-    cols = list(bu.A.cols.items())
-    host_in = {c: torch.empty(bu.capacity, dtype=t.dtype, pin_memory=True) for c, t in cols}
-    host_in["id"] = torch.empty(bu.capacity, dtype=torch.int64, pin_memory=True)
-    host_in["label"] = torch.empty(bu.capacity, dtype=torch.int32, pin_memory=True)
-    host_out = {c: torch.empty_like(v).pin_memory() for c, v in host_in.items()}
-    for c, t in cols:
-        host_in[c][:n].copy_(t[:n])
-    host_in["id"][:n].copy_(bu.A.id[:n])
-    host_in["label"][:n].copy_(bu.A.label[:n])
+    names = [c for c, _ in bu.A.cols.items()] + ["id", "label"]
+
+    def col(name):
+        return bu.A.cols[name] if name in bu.A.cols else getattr(bu.A, name)
+
+    host = {c: torch.empty(bu.capacity, dtype=col(c).dtype, pin_memory=True) for c in names}
+    for c in names:
+        host[c][:n].copy_(col(c)[:n])
     steps = max(2, min(args.steps, args.e2e_steps))
     stream = torch.cuda.current_stream()
+    up, down = torch.cuda.Stream(), torch.cuda.Stream()
+    evs = {c: torch.cuda.Event() for c in names}
     checked0 = bu.stats()["checked_total"]
     h2d = d2h = 0
+    per = sum(col(c).element_size() for c in names)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    t0 = time.perf_counter()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    for _ in range(steps):
-        for c, t in cols:
-            t[:n].copy_(host_in[c][:n], non_blocking=True)
-        bu.A.id[:n].copy_(host_in["id"][:n], non_blocking=True)
-        bu.A.label[:n].copy_(host_in["label"][:n], non_blocking=True)
+    up.wait_stream(stream)
+    with torch.cuda.stream(up):                      # first step's inputs
+        for c in names:
+            col(c)[:n].copy_(host[c][:n], non_blocking=True)
+    h2d += n * per
+    for s in range(steps):
+        stream.wait_stream(up)
         bu.A.n.fill_(n)
         sphbuf.sph_cll_invalidate(bu.ctx)   # uploaded state: no carried-over keys (ABI contract)
-        h2d += n * (4 * len(cols) + 12)
         su.step(w.dt)
         n = int(bu.A.n.item())
-        for c, t in cols:
-            host_out[c][:n].copy_(t[:n], non_blocking=True)
-        host_out["id"][:n].copy_(bu.A.id[:n], non_blocking=True)
-        host_out["label"][:n].copy_(bu.A.label[:n], non_blocking=True)
-        d2h += n * (4 * len(cols) + 12) + 8
-        host_in, host_out = host_out, host_in
+        down.wait_stream(stream)
+        last = s == steps - 1
+        for c in names:
+            with torch.cuda.stream(down):            # this step's result
+                host[c][:n].copy_(col(c)[:n], non_blocking=True)
+                evs[c].record(down)
+            if not last:
+                with torch.cuda.stream(up):          # the next step's input, column by column
+                    up.wait_event(evs[c])
+                    col(c)[:n].copy_(host[c][:n], non_blocking=True)
+        d2h += n * per + 8
+        if not last:
+            h2d += n * per
+    stream.wait_stream(down)
     e1.record(stream)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
@@ -355,7 +368,8 @@ def run_e2e(su, w, args, dev, world):
         ms, checked = float(a[0]), float(b[1])
     return {"value": checked / (ms / 1e3), "unit": "particles_checked/s", "ms_per_step": ms / steps,
             "steps": steps, "h2d_bytes_per_step": h2d // steps, "d2h_bytes_per_step": d2h // steps,
-            "what": "pinned host state -> device, update via BufferUpdater/SlabUpdater, state -> pinned host"}
+            "what": "pinned host state -> device, update via BufferUpdater/SlabUpdater, state -> pinned host; "
+                    "read-back and next upload pipelined per column on two copy streams"}
 
 
 # ------------------------------------------------------------------ CPU oracle (reference arm / cpu_baseline)
@@ -478,7 +492,7 @@ def main():
     ap.add_argument("--config", default="C5")
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--cpu-scale", type=float, default=0.5)
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-sweep", action="store_true", help="skip the per-config us/update sweep (C1-C4)")
