@@ -58,8 +58,6 @@ __global__ void __launch_bounds__(kThreads) k_cll_key(PartDev in, GridDev g, Wor
     Counters *ctr = ws.ctr;
     const long long n = *in.n;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
-        ctr->epoch_cll += 1;
-        ctr->ticket_cll = 0;
         ctr->n_in = n;
         ctr->mig_base = n;
     }
@@ -132,20 +130,6 @@ __global__ void __launch_bounds__(kThreads) k_cll_key(PartDev in, GridDev g, Wor
     }
 }
 
-// K1 in key carry-over mode: the keys and the histogram of this build were made
-// by the previous build's gather (and kept up to date by the update, the
-// compaction and moving ports), so only the build's counters are set.
-__global__ void k_cll_begin(PartDev in, Workspace ws)
-{
-    pdl_entry();
-    Counters *ctr = ws.ctr;
-    const long long n = *in.n;
-    ctr->epoch_cll += 1;
-    ctr->ticket_cll = 0;
-    ctr->n_in = n;
-    ctr->mig_base = n;
-}
-
 // K1 in key carry-over mode with slab migration: the listed leavers (still keyed
 // kLeaver; a later fix-up may have kept one inside, a duplicate entry is claimed
 // once) are packed for the neighbour ranks with their advected positions, as the
@@ -159,8 +143,6 @@ __global__ void __launch_bounds__(kThreads) k_mig_pack_list(PartDev in, GridDev 
     long long nl = ctr->n_leave;
     if (nl > ws.max_leave) nl = ws.max_leave;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
-        ctr->epoch_cll += 1;
-        ctr->ticket_cll = 0;
         ctr->n_in = n;
         ctr->mig_base = n;
     }
@@ -226,8 +208,11 @@ __global__ void __launch_bounds__(kThreads) k_cll_unpack_key(PartDev in, GridDev
 
 // K2: kCellItems cells per thread (kCellTile per block: one wave of blocks even
 // at C5's 8.5M cells, so the look-back chain never waits on an unlaunched tile).
+// n_src: with carried-over keys and no migration (no key pass ran), the input
+// count to record for the scatter and the gather.  The tile tickets and the
+// look-back epoch are advanced by the last block to finish, for the next build.
 __global__ void __launch_bounds__(kThreads) k_cell_scan(GridDev g, Workspace ws, int *cell_start, int *cell_end,
-                                                        long long *n_out, long long ntiles)
+                                                        long long *n_out, long long ntiles, const long long *n_src)
 {
     pdl_entry();
     constexpr int V = kCellItems / 4;
@@ -239,6 +224,10 @@ __global__ void __launch_bounds__(kThreads) k_cell_scan(GridDev g, Workspace ws,
     __syncthreads();
     const long long tile = s_tile;
     const unsigned epoch = ctr->epoch_cll;
+    if (n_src && tile == 0 && threadIdx.x == 0) {
+        ctr->n_in = *n_src;
+        ctr->mig_base = *n_src;
+    }
     const long long nc = g.ncells;
     const long long base = tile * kCellTile + (long long)threadIdx.x * kCellItems;
     const bool full = base + kCellItems <= nc;
@@ -311,6 +300,14 @@ __global__ void __launch_bounds__(kThreads) k_cell_scan(GridDev g, Workspace ws,
     if (tile == ntiles - 1 && threadIdx.x == 0) {
         *n_out = (long long)(prefix + total);
         ctr->n_leave = 0;   // the leaver list of the next build starts here (pack-from-list ran before)
+    }
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(&ctr->done_cll, 1) == (int)gridDim.x - 1) {
+            ctr->done_cll = 0;
+            ctr->ticket_cll = 0;
+            ctr->epoch_cll += 1;
+        }
     }
 }
 
@@ -633,12 +630,7 @@ cudaError_t launch_cll_key(const PartDev &in, const GridDev &g, const Workspace 
                            float *send_lo, float *send_hi, long long maxm, int rec, const CllCarry &cc, cudaStream_t s,
                            Launch *L)
 {
-    if (cc.use && !(send_lo && send_hi)) {
-        L->before(s);
-        launch_k(k_cll_begin, dim3(1), dim3(1), 0, s, in, ws);
-        L->after(s, KID_CLL_KEY);
-        return cudaGetLastError();
-    }
+    if (cc.use && !(send_lo && send_hi)) return cudaSuccess;   // the scan records the input count
     if (cc.use) {
         cudaError_t e = cudaMemsetAsync(send_lo, 0, 16, s);
         if (e == cudaSuccess) e = cudaMemsetAsync(send_hi, 0, 16, s);
@@ -692,7 +684,9 @@ cudaError_t launch_cll_finish(const PartDev &in, const PartDev &out, const GridD
         L->after(s, KID_MIG_UNPACK);
     }
     L->before(s);
-    launch_k(k_cell_scan, dim3((unsigned)(ntiles > 0 ? ntiles : 1)), dim3(kThreads), 0, s, g, ws, cell_start, cell_end, out.n, ntiles);
+    const bool no_key_pass = cc.use && !cc.mig;
+    launch_k(k_cell_scan, dim3((unsigned)(ntiles > 0 ? ntiles : 1)), dim3(kThreads), 0, s, g, ws, cell_start, cell_end,
+             out.n, ntiles, no_key_pass ? (const long long *)in.n : (const long long *)nullptr);
     L->after(s, KID_CELL_SCAN);
     {
         // scatter variants for tuning (SPHBUF_SCATTER=<items>:<threads>); default 4 x 256,

@@ -221,7 +221,9 @@ __global__ void __launch_bounds__(kThreads) k_compact_append(PartDev p, GridDev 
     __shared__ long long s_beg[SPH_MAX_PORTS];
     __shared__ long long s_total;
     Counters *ctr = ws.ctr;
-    const long long nid0 = ctr->cmp_next_id;   // N and next_id before: k_compact_prep / k_compact_count
+    // N and next_id before the append: read here by every block (deferred), or
+    // recorded by k_compact_count; the last block to finish writes the new ones
+    const long long nid0 = defer ? *next_id : ctr->cmp_next_id;
     if (threadIdx.x == 0) {
         long long acc = nid0, beg = 0;
         for (int k = 0; k < n_ports; ++k) {
@@ -239,7 +241,7 @@ __global__ void __launch_bounds__(kThreads) k_compact_append(PartDev p, GridDev 
         s_total = acc - nid0;
     }
     __syncthreads();
-    const long long N = ctr->cmp_n;
+    const long long N = defer ? *p.n : ctr->cmp_n;
     const long long D = defer ? 0 : ctr->n_del;
     long long C = ctr->n_stage;
     if (C > ws.max_new) C = ws.max_new;
@@ -277,19 +279,14 @@ __global__ void __launch_bounds__(kThreads) k_compact_append(PartDev p, GridDev 
         const long long ibeg = D ? cmp_begin(ctr->i_first) : N;
         for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < ibeg; i += stride) perm[i] = (int)i;
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        *p.n = dst0 + C;
-        *next_id = nid0 + s_total;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(&ctr->done_app, 1) == (int)gridDim.x - 1) {
+            ctr->done_app = 0;
+            *p.n = dst0 + C;
+            *next_id = nid0 + s_total;
+        }
     }
-}
-
-// Deferred mode: N and next_id before the append, for every block of the append
-// (which writes both at its end).
-__global__ void k_compact_prep(PartDev p, Workspace ws, const long long *next_id)
-{
-    pdl_entry();
-    ws.ctr->cmp_n = *p.n;
-    ws.ctr->cmp_next_id = *next_id;
 }
 
 // ------------------------------------------------------------------ launcher
@@ -300,7 +297,6 @@ cudaError_t launch_compact(const PartDev &p, const GridDev &g, const PortTable &
 {
     if (defer) {
         L->before(s);
-        launch_k(k_compact_prep, dim3(1), dim3(1), 0, s, p, ws, (const long long *)next_id);
         launch_k(k_compact_append, dim3(cap_grid(sm_count_cached() * 2, ws.max_new, kThreads)), dim3(kThreads), 0, s,
                  p, g, pt.n, pt.max_ports, ws, all_counts, nranks, rank, next_id, nullptr, true, carry, cdt);
         L->after(s, KID_COMPACT_APPEND);

@@ -130,6 +130,8 @@ struct Counters {
     long long n_leave;     // key carry-over: leavers listed for the next build's migration
     int status;            // sticky bits
     int ticket_runs;       // update prologue: tile tickets (reset by its last block)
+    int done_cll;          // cell scan: finished blocks
+    int done_app;          // compaction append: finished blocks
     int done_runs;         // update prologue: finished blocks
     int dummy;
 };
