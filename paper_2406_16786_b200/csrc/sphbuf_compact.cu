@@ -160,7 +160,8 @@ __global__ void __launch_bounds__(kThreads) k_compact_move(PartDev p, int dim, W
                 asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(ws.rd + u), "r"(epoch) : "memory");
             // wait only for the earlier sub-tiles whose input overlaps the output range
             // [dst0, dst0 + alive) (when the shift exceeds a sub-tile these are a few
-            // tiles back, claimed long ago); relaxed polling, one acquire fence after
+            // tiles back, claimed long ago); acquire polling (no full fence), the block
+            // barrier below orders the other threads' stores after it
             if (total > 0 && dst0 < start) {
                 const long long vlo = (dst0 - ibeg) / kCmpTile;
                 long long vhi = (dst0 + total - 1 - ibeg) / kCmpTile;
@@ -168,10 +169,9 @@ __global__ void __launch_bounds__(kThreads) k_compact_move(PartDev p, int dim, W
                 for (long long v = vlo + threadIdx.x; v <= vhi; v += 32) {
                     unsigned f;
                     do {
-                        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(ws.rd + v) : "memory");
+                        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(ws.rd + v) : "memory");
                     } while (f != epoch);
                 }
-                asm volatile("fence.acq_rel.gpu;" ::: "memory");
             }
             __syncwarp();
         }

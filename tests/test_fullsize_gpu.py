@@ -35,10 +35,11 @@ def test_C4_full_junction_two_updates():
     torch.cuda.empty_cache()
 
 
-def test_C5_full_slab_one_update():
+def test_C5_full_slab_two_updates():
+    """(the second build uses the keys the first build's gather carried over)"""
     w = inputs.c5(device="cuda", slab=0, nslabs=1)
     assert w.n > 120_000_000
-    tot, bu = lockstep(w, 1, check_every=1, fused=True, deferred=True)
+    tot, bu = lockstep(w, 2, check_every=1, fused=True, deferred=True)
     assert tot[0] > 0 and tot[1] > 0
     del bu
     torch.cuda.empty_cache()
