@@ -1,0 +1,130 @@
+"""Randomised lock-step parity: seeded random workloads that mix what the fixed
+configurations keep apart — 2-D and 3-D, 1-5 ports of every kind at random
+orientations and sizes, pressure / velocity boundary conditions (with a density
+column), bidirectional flow, random dt, and every build / compaction mode (key
+pass or carried keys, deferred or in-place compaction).  Each is compared with
+the oracle bit-exactly after every update (tests/parity_util.py::lockstep).
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2406_16786_b200 import inputs
+from paper_2406_16786_b200.inputs import (BC, BC_PRESSURE, BC_VELOCITY, BIDIRECTIONAL, INLET, OUTLET,
+                                          PROFILE_PARABOLIC, PROFILE_PARABOLIC_RADIAL, PROFILE_PLUG, Grid, Port,
+                                          Workload, f32, frame_rows_2d, frame_rows_3d)
+
+from parity_util import lockstep
+
+
+SEEDS = range(24)
+
+
+def random_workload(seed):
+    rng = np.random.default_rng(1000 + seed)
+    dim = 2 if rng.random() < 0.35 else 3
+    dp = float(rng.uniform(0.008, 0.012)) if dim == 3 else float(rng.uniform(0.002, 0.005))
+    h = 1.3 * dp
+    cs = f32(2 * h * float(rng.uniform(1.0, 1.3)))
+    L = float(rng.uniform(0.32, 0.42)) if dim == 3 else float(rng.uniform(0.3, 0.5))
+    counts = tuple(int(L / dp) for _ in range(dim))
+    n = int(np.prod(counts))
+    dt = float(rng.uniform(0.0002, 0.0008))
+    # ports: rejection-sampled bounding spheres (+1 cell), 2 cells apart, inside the fluid box
+    ports, placed = [], []
+    nports = int(rng.integers(1, 6))
+    while len(ports) < nports:
+        kind = [INLET, OUTLET, BIDIRECTIONAL][int(rng.integers(0, 3))]
+        layers = int(rng.integers(3, 6))
+        for _ in range(2000):
+            if dim == 3:
+                u = rng.standard_normal(3)
+                Q = frame_rows_3d(u / np.linalg.norm(u), float(rng.uniform(0, 2 * math.pi)))
+                b, c = rng.uniform(0.02, 0.05, size=2) * L / 0.3
+                he = (layers * dp / 2, b / 2, c / 2)
+            else:
+                Q = frame_rows_2d(float(rng.uniform(0, 2 * math.pi)))
+                he = (layers * dp / 2, float(rng.uniform(0.03, 0.1)) * L / 0.4, 0.0)
+            r = math.sqrt(sum(x * x for x in he[:dim])) + cs
+            lo, hi = r, L - r
+            if hi <= lo:
+                continue
+            o = rng.uniform(lo, hi, size=dim)
+            if all(np.linalg.norm(o - q) > r + rq + 2 * cs for q, rq in placed):
+                bc = None
+                roll = rng.random()
+                if roll < 0.25:
+                    bc = BC(BC_PRESSURE, rho0=1.0, c0=float(rng.uniform(5, 20)), p_b=float(rng.uniform(-1, 1)),
+                            rho_column=0)
+                elif roll < 0.5:
+                    prof = [PROFILE_PLUG, PROFILE_PARABOLIC, PROFILE_PARABOLIC_RADIAL][int(rng.integers(0, 3))]
+                    bc = BC(BC_VELOCITY, profile=prof, u0=float(rng.uniform(0.5, 1.5)), radius=float(2 * he[1]))
+                oo = tuple(float(x) for x in o) + ((0.0,) if dim == 2 else ())
+                ports.append(Port(tuple(f32(x) for x in oo), Q, tuple(f32(x) for x in he), kind, layers, bc))
+                placed.append((o, r))
+                break
+        else:
+            if ports:
+                break    # lattice + jitter; velocity along the nearest port's axis (random sign at
+    # bidirectional ports), noise, axial near the ports
+    g = torch.Generator().manual_seed(2000 + seed)
+    idx = torch.arange(n, dtype=torch.int64)
+    xyz, rem = [], idx
+    for a in range(dim):
+        stride = int(np.prod(counts[a + 1:])) if a < dim - 1 else 1
+        xyz.append(((rem // stride) % counts[a]).double() * dp + 0.5 * dp
+                   + (torch.rand(n, generator=g, dtype=torch.float64) * 2 - 1) * 0.1 * dp)
+    best = torch.full((n,), float("inf"), dtype=torch.float64)
+    v = [torch.zeros(n, dtype=torch.float64) for _ in range(dim)]
+    for p in ports:
+        sgn = -1.0 if (p.kind == BIDIRECTIONAL and rng.random() < 0.5) else 1.0
+        d2 = sum((xyz[j] - p.origin[j]) ** 2 for j in range(dim))
+        sel = d2 < best
+        best = torch.where(sel, d2, best)
+        for j in range(dim):
+            v[j] = torch.where(sel, torch.full_like(v[j], sgn * p.Q[j]), v[j])
+    v = [v[j] + (torch.randn(n, generator=g, dtype=torch.float64) * 0.05).clamp(-0.2, 0.2) for j in range(dim)]
+    v = inputs._project_near_ports(xyz, v, ports, dim, 2 * dp)
+    st = inputs._pack_state(xyz, v, idx, dim)
+    st["extra"] = [torch.full((n,), 1.0, dtype=torch.float32)]
+    pad = 4
+    lo = tuple(f32(-pad * cs) for _ in range(dim)) + ((0.0,) if dim == 2 else ())
+    ncell = tuple(int(math.ceil(L / cs)) + 2 * pad for _ in range(dim)) + ((1,) if dim == 2 else ())
+    grid = Grid(dim, lo, cs, ncell)
+    w = Workload(f"R{seed}", dim, dp, h, grid, ports, st, f32(dt), 8, n)
+    mode = dict(fused=bool(rng.random() < 0.7), deferred=bool(rng.random() < 0.5))
+    return w, int(rng.integers(4, 9)), mode
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", SEEDS)
+def test_random_workload_lockstep(seed):
+    w, steps, mode = random_workload(seed)
+    tot, bu = lockstep(w, steps, check_every=1, state=w.state, **mode)
+    assert bu.stats()["motion_errors"] == 0
+
+
+def test_random_workloads_are_valid_inputs():
+    """(CPU) every seed is deterministic, registers members in every port and runs
+    its updates on the oracle with no particle claimed by two ports; over all seeds
+    particles are both created and deleted, in 2-D and 3-D."""
+    import oracle
+    made = {2: [0, 0], 3: [0, 0]}
+    for seed in SEEDS:
+        w, steps, mode = random_workload(seed)
+        w2, _, _ = random_workload(seed)
+        assert torch.equal(w.state["x"], w2.state["x"]) and len(w.ports) == len(w2.ports) >= 1
+        st = oracle.to_numpy_state(w.state)
+        K = len(w.ports)
+        assert all(oracle.register(st, w.grid, p, k) > 0 for k, p in enumerate(w.ports)), seed
+        nid = w.next_id
+        for _ in range(steps):
+            oracle.advect(st, w.dim, w.dt)
+            res = oracle.update(w.grid, w.ports, st)
+            assert res.multi_decision == 0, seed
+            st, perm, nid = oracle.compact(res, w.dim, K, res.port_counts[None, :], 0, nid)
+            made[w.dim][0] += int(res.port_counts[:K].sum())
+            made[w.dim][1] += int(res.port_counts[K:].sum())
+    assert min(made[2] + made[3]) > 0, made
