@@ -128,3 +128,73 @@ def test_random_workloads_are_valid_inputs():
             made[w.dim][0] += int(res.port_counts[:K].sum())
             made[w.dim][1] += int(res.port_counts[K:].sum())
     assert min(made[2] + made[3]) > 0, made
+
+
+def random_motion(w, seed):
+    """Per port: a pivot within a third of a cell of its origin, a rotation axis
+    (3-D) and a turn per update of 0.5-3 degrees either way — the bounding sphere
+    moves by less than the 2-cell gap over the run, so ports stay disjoint."""
+    rng = np.random.default_rng(3000 + seed)
+    cs = w.grid.cs
+    mot = []
+    for p in w.ports:
+        off = rng.standard_normal(w.dim)
+        off = off / np.linalg.norm(off) * cs / 3
+        pivot = tuple(float(p.origin[j] + off[j]) for j in range(w.dim)) + ((0.0,) if w.dim == 2 else ())
+        axis = rng.standard_normal(3)
+        dth = math.radians(float(rng.uniform(0.5, 3.0))) * (1 if rng.random() < 0.5 else -1)
+        mot.append((pivot, axis, dth))
+    return mot
+
+
+def _pose(w, k, mot, step):
+    pivot, axis, dth = mot[k]
+    if w.dim == 2:
+        return inputs.sprinkler_pose(w.ports[k], pivot, dth * (step + 1))
+    return inputs.rotation_pose_3d(w.ports[k], pivot, axis, dth * (step + 1))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", SEEDS)
+def test_random_moving_ports_lockstep(seed):
+    """The same random workloads with every port turning about a nearby pivot after
+    each update (sph_port_move), compared with the oracle's port_move bit-exactly."""
+    import oracle
+    from parity_util import assert_state_equal, gpu_counts_to_oracle, make_updater
+    w, steps, mode = random_workload(seed)
+    mot = random_motion(w, seed)
+    K = len(w.ports)
+    st = oracle.to_numpy_state(w.state)
+    for k, p in enumerate(w.ports):
+        oracle.register(st, w.grid, p, k)
+    bu = make_updater(w, n_extra=1)
+    bu.load(w.state, w.next_id)
+    bu.register_ports()
+    ports = list(w.ports)
+    nid = w.next_id
+    for step in range(steps):
+        oracle.advect(st, w.dim, w.dt)
+        res = oracle.update(w.grid, ports, st)
+        assert res.multi_decision == 0
+        new, perm, nid = oracle.compact(res, w.dim, K, res.port_counts[None, :], 0, nid)
+        poses = [_pose(w, k, mot, step) for k in range(K)]
+        for k, (o, Q) in enumerate(poses):
+            nxt = Port(o, Q, ports[k].half_extents, ports[k].kind, ports[k].layers, ports[k].bc)
+            oracle.port_move(new, w.dim, ports[k], nxt, k)
+            ports[k] = nxt
+        if mode["fused"]:
+            bu.cll_build(dt=w.dt)
+        else:
+            bu.advect(w.dt)
+            bu.cll_build()
+        bu.update()
+        for k, (o, Q) in enumerate(poses):
+            bu.move_port(k, o, Q)
+        deferred = mode["deferred"] and step % 2 == 1
+        bu.compact(deferred=deferred)
+        assert (gpu_counts_to_oracle(bu.port_counts, K) == res.port_counts).all(), step
+        if not deferred:
+            assert_state_equal(bu.state(), new, f"step {step}")
+        assert int(bu.next_id.item()) == nid
+        st = new
+    assert bu.stats()["motion_errors"] == 0
