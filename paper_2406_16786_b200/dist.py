@@ -69,11 +69,11 @@ class SlabUpdater:
     """One rank: BufferUpdater + migration buffers + count matrix."""
 
     def __init__(self, w, rank: int, world: int, capacity: int, max_migrate: int, max_new=None, comm=None,
-                 device="cuda", deferred=False):
+                 device="cuda", deferred=False, n_extra=0):
         self.rank, self.world = rank, world
         self.deferred = deferred
         self.bu = sphbuf.BufferUpdater(w.grid, w.h, w.dp, w.ports, capacity, max_new=max_new,
-                                       max_migrate=max_migrate, device=device)
+                                       max_migrate=max_migrate, n_extra=n_extra, device=device)
         rec = sphbuf.sph_migrate_record_floats(self.bu.ctx)
         n = 4 + max_migrate * rec
         mk = lambda: torch.zeros(n, dtype=torch.float32, device=device)

@@ -198,3 +198,57 @@ def test_random_moving_ports_lockstep(seed):
         assert int(bu.next_id.item()) == nid
         st = new
     assert bu.stats()["motion_errors"] == 0
+
+
+def _flat(st):
+    """state dict with its extra columns as plain keys e0, e1, ... (numpy)."""
+    d = {k: (v.cpu().numpy() if isinstance(v, torch.Tensor) else v) for k, v in st.items() if k != "extra"}
+    for e, col in enumerate(st.get("extra") or []):
+        d[f"e{e}"] = col.cpu().numpy() if isinstance(col, torch.Tensor) else col
+    return d
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed,P", [(s, 2 + s % 2) for s in SEEDS])
+def test_random_slabs_lockstep(seed, P):
+    """The random workloads cut into P x-slabs run through the migration path
+    (sph_cll_key packing leavers / sph_cll_finish appending arrivals, density
+    column included) in one process (LoopbackGroup); the union of the slabs
+    equals the oracle's single-domain state after every update."""
+    import oracle
+    from paper_2406_16786_b200.dist import LoopbackGroup, SlabUpdater
+    from test_dist import by_id, cat, cell_x
+    w, steps, mode = random_workload(seed)
+    st = oracle.to_numpy_state(w.state)
+    ncx = w.grid.ncell[0]
+    cuts = [int(round(i * ncx / P)) for i in range(P + 1)]
+    cx = cell_x(w.grid, st["x"])
+    slabs = []
+    for r in range(P):
+        sel = (cx >= cuts[r]) & (cx < cuts[r + 1])
+        part = {k: torch.from_numpy(v[sel].copy()) for k, v in st.items() if k != "extra"}
+        part["extra"] = [torch.from_numpy(c[sel].copy()) for c in st["extra"]]
+        ws = inputs.Workload(w.name, w.dim, w.dp, w.h, w.grid.slab(cuts[r], cuts[r + 1]), w.ports, part, w.dt,
+                             w.n_updates, w.next_id)
+        su = SlabUpdater(ws, r, P, inputs.capacity_for(ws, 0.3) + 4096, max_migrate=1 << 15, comm=None,
+                         deferred=mode["deferred"], n_extra=1)
+        su.load(ws.state, w.next_id)
+        slabs.append(su)
+    grp = LoopbackGroup(slabs)
+    for k, p in enumerate(w.ports):
+        oracle.register(st, w.grid, p, k)
+    nid = w.next_id
+    for s in range(steps):
+        st, res, perm, nid = oracle.step(st, w.grid, w.ports, nid, w.dt)
+        grp.step(w.dt)
+        union = None
+        for su in slabs:
+            g = _flat(su.bu.state())
+            live = g["label"] > -2
+            g = {k: v[live] for k, v in g.items()}
+            union = g if union is None else cat(union, g)
+        union, ref = by_id(union), by_id(_flat(st))
+        for k in ref:
+            assert np.array_equal(union[k].view(np.uint8), ref[k].view(np.uint8)), f"P={P} step {s} column {k}"
+        for su in slabs:
+            assert int(su.bu.next_id.item()) == nid
