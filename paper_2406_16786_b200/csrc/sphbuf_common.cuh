@@ -100,6 +100,10 @@ __device__ __forceinline__ long long warp_min_ll(long long v)
 // happens-before what the caller does after this returns.
 static __device__ unsigned tile_prefix(unsigned long long *status, long long tile, unsigned epoch, unsigned aggregate)
 {
+    // each lane inspects kLB consecutive predecessors per round (loads issued
+    // together), so a wave of W tiles started at once resolves in ~W / (32 kLB)
+    // dependent rounds instead of W / 32
+    constexpr int kLB = 4;
     const int lane = threadIdx.x & 31;
     const unsigned ep = epoch & 0x3fffffffu;
     if (tile == 0) {
@@ -107,27 +111,37 @@ static __device__ unsigned tile_prefix(unsigned long long *status, long long til
         return 0;
     }
     if (lane == 0) st_release(&status[tile], pack_status(epoch, 1, aggregate));
+    auto flag_of = [&](unsigned long long s) -> unsigned {
+        return ((unsigned)(s >> 34) == ep) ? (unsigned)((s >> 32) & 3u) : 0u;
+    };
     unsigned excl = 0;
     long long base = tile - 1;
     while (true) {
-        long long t = base - lane;
-        unsigned long long s = 0;
-        unsigned flag;
-        if (t >= 0) {
-            do {
-                s = ld_relaxed(&status[t]);   // polled relaxed; one acquire fence below
-                flag = ((unsigned)(s >> 34) == ep) ? (unsigned)((s >> 32) & 3u) : 0u;
-            } while (flag == 0);
-        } else {
-            flag = 2;
-            s = 0;
+        unsigned long long s[kLB];
+#pragma unroll
+        for (int j = 0; j < kLB; ++j) {
+            const long long t = base - lane * kLB - j;
+            s[j] = t >= 0 ? ld_relaxed(&status[t]) : 0ull;     // polled relaxed; one acquire fence below
         }
-        unsigned pmask = __ballot_sync(0xffffffffu, flag == 2);
-        int first = pmask ? __ffs(pmask) - 1 : 32;
-        unsigned v = (lane <= first) ? (unsigned)(s & 0xffffffffu) : 0u;
-        excl += warp_sum(v);
+        unsigned v = 0;
+        bool incl = false;
+#pragma unroll
+        for (int j = 0; j < kLB; ++j) {
+            const long long t = base - lane * kLB - j;
+            unsigned f = 2;
+            if (t >= 0) {
+                while ((f = flag_of(s[j])) == 0) s[j] = ld_relaxed(&status[t]);
+            }
+            if (!incl) {
+                v += (unsigned)(s[j] & 0xffffffffu);          // aggregate, or the inclusive prefix
+                incl = f == 2;
+            }
+        }
+        const unsigned pmask = __ballot_sync(0xffffffffu, incl);
+        const int first = pmask ? __ffs(pmask) - 1 : 32;
+        excl += warp_sum(lane <= first ? v : 0u);
         if (pmask) break;
-        base -= 32;
+        base -= 32 * kLB;
     }
     asm volatile("fence.acq_rel.gpu;" ::: "memory");
     if (lane == 0) st_release(&status[tile], pack_status(epoch, 2, excl + aggregate));

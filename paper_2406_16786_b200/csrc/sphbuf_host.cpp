@@ -155,6 +155,8 @@ size_t layout(const sph_ctx *c, char *base, Workspace *W)
     w.run_off = (long long *)take(sizeof(long long) * (kMaxRuns + 1));
     const size_t zero_end = off;   // everything above must start zeroed
     w.sub_off = (unsigned *)take(4 * cmp_subs);
+    w.run_base = (int *)take(sizeof(int) * kMaxRuns);
+    w.tile_run = (int *)take(sizeof(int) * upd_tiles);
     w.key = (int *)take(sizeof(int) * cap);
     w.src = (int *)take(sizeof(int) * cap);
     w.max_leave = 2 * c->max_migrate + 1024;

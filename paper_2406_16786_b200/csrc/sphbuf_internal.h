@@ -153,6 +153,8 @@ struct Workspace {
     DriverDev *drv;                  // [SPH_MAX_PORTS]: Windkessel state
     float *drv_rho;                  // [SPH_MAX_PORTS]: recycled density of driven pressure BCs
     long long *run_off;              // [kMaxRuns + 1]
+    int *run_base;                   // [kMaxRuns]: first particle index of each run
+    int *tile_run;                   // [upd tiles]: run holding the first candidate of each K6 tile
     float *sx, *sy, *sz, *svx, *svy, *svz;
     float *sextra[SPH_MAX_EXTRA];
     long long *sid;                  // source id of each staged particle (diagnostic)

@@ -84,9 +84,12 @@ __global__ void __launch_bounds__(1024) k_upd_prologue(Workspace ws, int n_runs,
     if (tile < ntiles) {
         const int r = tile * 1024 + threadIdx.x;
         unsigned len = 0;
+        int base = 0;
         // (c1 < c0: an empty slot of a movable port's run slice)
-        if (r < n_runs && ws.runs[3 * r + 1] >= ws.runs[3 * r])
-            len = (unsigned)(cell_end[ws.runs[3 * r + 1]] - cell_start[ws.runs[3 * r]]);
+        if (r < n_runs && ws.runs[3 * r + 1] >= ws.runs[3 * r]) {
+            base = cell_start[ws.runs[3 * r]];
+            len = (unsigned)(cell_end[ws.runs[3 * r + 1]] - base);
+        }
         unsigned total;
         const unsigned ex = block_excl_scan<1024>(len, total, s_warp);
         if (threadIdx.x < 32) {
@@ -94,7 +97,14 @@ __global__ void __launch_bounds__(1024) k_upd_prologue(Workspace ws, int n_runs,
             if (threadIdx.x == 0) s_prefix = pre;
         }
         __syncthreads();
-        if (r < n_runs) ws.run_off[r] = (long long)s_prefix + ex;
+        if (r < n_runs) {
+            const long long off = (long long)s_prefix + ex;
+            ws.run_off[r] = off;
+            ws.run_base[r] = base;
+            // the run holding the first candidate of each K6 tile starting inside it
+            for (long long t = (off + kUpdTile - 1) / kUpdTile; t * kUpdTile < off + len && t < ws.upd_tiles; ++t)
+                ws.tile_run[t] = r;
+        }
         if (tile == ntiles - 1 && threadIdx.x == 0) {
             const long long carry = (long long)s_prefix + total;
             ws.run_off[n_runs] = carry;
@@ -117,6 +127,8 @@ __global__ void __launch_bounds__(1024) k_upd_prologue(Workspace ws, int n_runs,
     }
 }
 
+constexpr int kTileRuns = 256;   // runs of one K6 tile staged in shared memory (else global search)
+
 // K6: the candidate check (a3) with generation (a4), deletion (a5) and relabel
 // (a6) fused; CREATEs are appended to the staging area in canonical order
 // (port, cell, id) by a ballot/block scan + decoupled look-back over ordered tiles.
@@ -130,6 +142,7 @@ __global__ void __launch_bounds__(kThreads) k_upd_main(PartDev p, GridDev g, con
     __shared__ unsigned s_warp[kUpdItems * kThreads / 32 + 1];
     __shared__ long long s_tile;
     __shared__ unsigned s_prefix;
+    __shared__ int s_roff[kTileRuns], s_rbase[kTileRuns], s_rk[kTileRuns];
     {
         const int words = pt.n * (int)(sizeof(PortDev) / 4);
         const unsigned *src = reinterpret_cast<const unsigned *>(pt.p);
@@ -153,6 +166,21 @@ __global__ void __launch_bounds__(kThreads) k_upd_main(PartDev p, GridDev g, con
         __syncthreads();
         const long long tile = s_tile;
         if (tile >= ntiles || tile >= ws.upd_tiles) break;
+        // the tile's runs [r0, r1] (K5's tile_run) staged in shared memory: offsets
+        // relative to the tile, first particle index, port
+        const long long t0 = tile * kUpdTile;
+        const int r0 = ws.tile_run[tile];
+        const int r1 = tile + 1 < ntiles ? ws.tile_run[tile + 1] : n_runs - 1;
+        const int nr = r1 - r0 + 1;
+        const bool staged = nr <= kTileRuns;
+        if (staged) {
+            for (int i = threadIdx.x; i < nr; i += blockDim.x) {
+                s_roff[i] = (int)(ws.run_off[r0 + i] - t0);
+                s_rbase[i] = ws.run_base[r0 + i];
+                s_rk[i] = ws.runs[3 * (r0 + i) + 2];
+            }
+        }
+        __syncthreads();
         bool cr[kUpdItems], bcm[kUpdItems], dl[kUpdItems];
         int pidx[kUpdItems], kk[kUpdItems];
         float ox[kUpdItems], oy[kUpdItems], oz[kUpdItems], bY[kUpdItems], bZ[kUpdItems];
@@ -164,18 +192,31 @@ __global__ void __launch_bounds__(kThreads) k_upd_main(PartDev p, GridDev g, con
             pidx[it] = -1;
             kk[it] = 0;
             ox[it] = oy[it] = oz[it] = 0.0f;
-            const long long g = tile * kUpdTile + it * kThreads + threadIdx.x;
+            const int rel = it * kThreads + threadIdx.x;
+            const long long g = t0 + rel;
             if (g >= n_cand) continue;
-            // run containing g: largest r with run_off[r] <= g
-            int lo = 0, hi = n_runs - 1;
-            while (lo < hi) {
-                const int mid = (lo + hi + 1) >> 1;
-                if (ws.run_off[mid] <= g) lo = mid;
-                else hi = mid - 1;
+            // run containing g: the largest r with run_off[r] <= g (empty runs share
+            // their successor's offset, so the search lands on the non-empty one)
+            int k, pi;
+            if (staged) {
+                int lo = 0, hi = nr - 1;
+                while (lo < hi) {
+                    const int mid = (lo + hi + 1) >> 1;
+                    if (s_roff[mid] <= rel) lo = mid;
+                    else hi = mid - 1;
+                }
+                k = s_rk[lo];
+                pi = s_rbase[lo] + (rel - s_roff[lo]);
+            } else {
+                int lo = r0, hi = r1;
+                while (lo < hi) {
+                    const int mid = (lo + hi + 1) >> 1;
+                    if (ws.run_off[mid] <= g) lo = mid;
+                    else hi = mid - 1;
+                }
+                k = ws.runs[3 * lo + 2];
+                pi = ws.run_base[lo] + (int)(g - ws.run_off[lo]);
             }
-            const int r = lo;
-            const int k = ws.runs[3 * r + 2];
-            const int pi = cell_start[ws.runs[3 * r]] + (int)(g - ws.run_off[r]);
             SPH_CHECK(pi >= 0 && pi < p.cap && k >= 0 && k < pt.n);
             const PortDev &P = s_ports[k];
             const float x = p.x[pi], y = p.y[pi], z = dim == 3 ? p.z[pi] : 0.0f;
