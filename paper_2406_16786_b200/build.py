@@ -11,6 +11,7 @@ CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(HERE, "libsphbuf.so")
 LIB_DEBUG = os.path.join(HERE, "libsphbuf_debug.so")   # -DSPHBUF_DEBUG: device bounds asserts
+LIB_TRACE = os.path.join(HERE, "libsphbuf_trace.so")   # -DSPHBUF_TRACE: per-tile timestamps of the update (tools/)
 SOURCES = ["sphbuf_cll.cu", "sphbuf_update.cu", "sphbuf_compact.cu", "sphbuf_migrate.cu", "sphbuf_motion.cu",
            "sphbuf_drivers.cu", "sphbuf_host.cpp"]
 DEPS = SOURCES + ["sphbuf_internal.h", "sphbuf_common.cuh"]
@@ -27,14 +28,15 @@ def _stale(lib=LIB) -> bool:
     return any(os.path.getmtime(s) > t for s in srcs)
 
 
-def build(force: bool = False, verbose: bool = False, debug: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, debug: bool = False, trace: bool = False) -> str:
     """Compile libsphbuf.so (or, debug=True, libsphbuf_debug.so with device-side
-    bounds asserts: compute-sanitizer is not available on the GPU pool)."""
-    lib = LIB_DEBUG if debug else LIB
+    bounds asserts: compute-sanitizer is not available on the GPU pool; or,
+    trace=True, libsphbuf_trace.so with the update kernel's tile timeline)."""
+    lib = LIB_DEBUG if debug else LIB_TRACE if trace else LIB
     if not force and not _stale(lib):
         return lib
     tmp = lib + f".tmp{os.getpid()}"
-    extra = ["-DSPHBUF_DEBUG"] if debug else []
+    extra = ["-DSPHBUF_DEBUG"] if debug else ["-DSPHBUF_TRACE"] if trace else []
     cmd = [NVCC, *FLAGS, *extra, "-I", INCLUDE, "-I", CSRC, *[os.path.join(CSRC, s) for s in SOURCES], "-o", tmp]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
@@ -47,4 +49,4 @@ def build(force: bool = False, verbose: bool = False, debug: bool = False) -> st
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True, debug="--debug" in sys.argv)
+    build(force="--force" in sys.argv, verbose=True, debug="--debug" in sys.argv, trace="--trace" in sys.argv)

@@ -6,7 +6,8 @@
 //                    atomic per run of equal keys in a warp (the input is already
 //                    nearly sorted by cell, so runs are long);
 //   K2 k_cell_scan   single-pass decoupled look-back scan of the histogram ->
-//                    cell_start / cell_end; re-zeroes the histogram;
+//                    cell_start / cell_end (warp-striped, coalesced); re-zeroes
+//                    the histogram and the scatter's cursors;
 //   K3 k_cll_scatter (source index, cell) pairs into their slots;
 //   K4 k_cll_gather  one round of loads per slot (all columns of the source plus
 //                    the cell range), rank by id among the cell's slots in shared
@@ -211,6 +212,27 @@ __global__ void __launch_bounds__(kThreads) k_cll_unpack_key(PartDev in, GridDev
 // n_src: with carried-over keys and no migration (no key pass ran), the input
 // count to record for the scatter and the gather.  The tile tickets and the
 // look-back epoch are advanced by the last block to finish, for the next build.
+#ifdef SPHBUF_TRACE
+// K2 tile timeline (tools/upd_trace.py): start, loads + block scan done,
+// look-back done, end, block, SM.
+constexpr int kTraceScan = 1 << 12;
+__device__ unsigned long long g_trace_scan[kTraceScan][6];
+__device__ __forceinline__ unsigned long long gtimer2()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define SCAN_TRACE(slot)                                                                             \
+    do {                                                                                             \
+        if (threadIdx.x == 0 && tile < kTraceScan) g_trace_scan[tile][slot] = gtimer2();             \
+    } while (0)
+#else
+#define SCAN_TRACE(slot) \
+    do {                 \
+    } while (0)
+#endif
+
 __global__ void __launch_bounds__(kThreads) k_cell_scan(GridDev g, Workspace ws, int *cell_start, int *cell_end,
                                                         long long *n_out, long long ntiles, const long long *n_src)
 {
@@ -223,72 +245,104 @@ __global__ void __launch_bounds__(kThreads) k_cell_scan(GridDev g, Workspace ws,
     if (threadIdx.x == 0) s_tile = atomicAdd(&ctr->ticket_cll, 1);
     __syncthreads();
     const long long tile = s_tile;
+    SCAN_TRACE(0);
+#ifdef SPHBUF_TRACE
+    if (threadIdx.x == 0 && tile < kTraceScan) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        g_trace_scan[tile][4] = blockIdx.x;
+        g_trace_scan[tile][5] = smid;
+    }
+#endif
     const unsigned epoch = ctr->epoch_cll;
     if (n_src && tile == 0 && threadIdx.x == 0) {
         ctr->n_in = *n_src;
         ctr->mig_base = *n_src;
     }
     const long long nc = g.ncells;
-    const long long base = tile * kCellTile + (long long)threadIdx.x * kCellItems;
-    const bool full = base + kCellItems <= nc;
+    // warp-striped layout: warp w owns cells [tile base + w 32 kCellItems, +32 kCellItems);
+    // row v of it is int4 #(32 v + lane), so every load / store instruction of a
+    // warp covers 512 contiguous bytes
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const long long wbase = tile * kCellTile + (long long)warp * (32 * kCellItems);
+    const bool full = tile * kCellTile + kCellTile <= nc;
     int4 c[V];
     // the histogram is read and re-zeroed (the next build's, or the gather's key
     // carry-over, accumulates into it); the scatter's cursors start from zero
     if (full) {
-        int4 *pc = reinterpret_cast<int4 *>(ws.cell_count + base);
-        int4 *pk = reinterpret_cast<int4 *>(ws.cursor + base);
+        int4 *pc = reinterpret_cast<int4 *>(ws.cell_count + wbase) + lane;
+        int4 *pk = reinterpret_cast<int4 *>(ws.cursor + wbase) + lane;
 #pragma unroll
-        for (int v = 0; v < V; ++v) c[v] = pc[v];
+        for (int v = 0; v < V; ++v) c[v] = pc[32 * v];
 #pragma unroll
         for (int v = 0; v < V; ++v) {
-            pc[v] = make_int4(0, 0, 0, 0);
-            pk[v] = make_int4(0, 0, 0, 0);
+            pc[32 * v] = make_int4(0, 0, 0, 0);
+            pk[32 * v] = make_int4(0, 0, 0, 0);
         }
     } else {
-        int t[kCellItems];
 #pragma unroll
-        for (int j = 0; j < kCellItems; ++j) {
-            t[j] = (base + j < nc) ? ws.cell_count[base + j] : 0;
-            if (base + j < nc) {
-                ws.cell_count[base + j] = 0;
-                ws.cursor[base + j] = 0;
+        for (int v = 0; v < V; ++v) {
+            int t[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const long long j = wbase + 4 * (32 * v + lane) + q;
+                t[q] = j < nc ? ws.cell_count[j] : 0;
+                if (j < nc) {
+                    ws.cell_count[j] = 0;
+                    ws.cursor[j] = 0;
+                }
             }
+            c[v] = make_int4(t[0], t[1], t[2], t[3]);
         }
-#pragma unroll
-        for (int v = 0; v < V; ++v) c[v] = make_int4(t[4 * v], t[4 * v + 1], t[4 * v + 2], t[4 * v + 3]);
     }
-    unsigned sum = 0;
+    // per row: exclusive prefix of this lane's int4 inside the row, and the rows
+    // before it; then the warps of the block, then the tiles (look-back)
+    unsigned rowpre[V], wtot = 0;
 #pragma unroll
-    for (int v = 0; v < V; ++v) sum += (unsigned)(c[v].x + c[v].y + c[v].z + c[v].w);
+    for (int v = 0; v < V; ++v) {
+        const unsigned sv = (unsigned)(c[v].x + c[v].y + c[v].z + c[v].w);
+        unsigned inc = sv;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+        }
+        rowpre[v] = wtot + inc - sv;
+        wtot += __shfl_sync(0xffffffffu, inc, 31);
+    }
     unsigned total;
-    const unsigned excl = block_excl_scan<kThreads>(sum, total, s_warp);
+    const unsigned wexcl = block_excl_scan<kThreads>(lane == 0 ? wtot : 0u, total, s_warp);
+    const unsigned woff = __shfl_sync(0xffffffffu, wexcl, 0);
+    SCAN_TRACE(1);
     if (threadIdx.x < 32) {
         unsigned pre = tile_prefix(ws.tile_cells, tile, epoch, total);
         if (threadIdx.x == 0) s_prefix = pre;
     }
     __syncthreads();
+    SCAN_TRACE(2);
     const unsigned prefix = s_prefix;
-    int run = (int)(prefix + excl);
     if (full) {
-        int4 *ps = reinterpret_cast<int4 *>(cell_start + base);
-        int4 *pe = reinterpret_cast<int4 *>(cell_end + base);
+        int4 *ps = reinterpret_cast<int4 *>(cell_start + wbase) + lane;
+        int4 *pe = reinterpret_cast<int4 *>(cell_end + wbase) + lane;
 #pragma unroll
         for (int v = 0; v < V; ++v) {
+            int run = (int)(prefix + woff + rowpre[v]);
             int4 st, en;
             st.x = run; run += c[v].x; en.x = run;
             st.y = run; run += c[v].y; en.y = run;
             st.z = run; run += c[v].z; en.z = run;
             st.w = run; run += c[v].w; en.w = run;
-            ps[v] = st;
-            pe[v] = en;
+            ps[32 * v] = st;
+            pe[32 * v] = en;
         }
     } else {
 #pragma unroll
         for (int v = 0; v < V; ++v) {
+            int run = (int)(prefix + woff + rowpre[v]);
             const int cv[4] = {c[v].x, c[v].y, c[v].z, c[v].w};
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-                const long long j = base + 4 * v + q;
+                const long long j = wbase + 4 * (32 * v + lane) + q;
                 if (j < nc) {
                     cell_start[j] = run;
                     cell_end[j] = run + cv[q];
@@ -309,12 +363,30 @@ __global__ void __launch_bounds__(kThreads) k_cell_scan(GridDev g, Workspace ws,
             ctr->epoch_cll += 1;
         }
     }
+    SCAN_TRACE(3);
 }
+
+#ifdef SPHBUF_TRACE
+}  // namespace sphbuf
+extern "C" int sph_trace_scan(unsigned long long *host, int max_tiles, int reset)
+{
+    const int n = max_tiles < sphbuf::kTraceScan ? max_tiles : sphbuf::kTraceScan;
+    cudaError_t e = cudaMemcpyFromSymbol(host, sphbuf::g_trace_scan, sizeof(unsigned long long) * 6 * n);
+    if (reset) {
+        static unsigned long long zero[sphbuf::kTraceScan][6];
+        cudaMemcpyToSymbol(sphbuf::g_trace_scan, zero, sizeof(zero));
+    }
+    return (int)e;
+}
+namespace sphbuf {
+#endif
 
 
 // K3: source index of every sorted slot: slot = cell_start[key] + a per-cell
 // cursor (one atomic per run of equal keys in a warp; the order inside a cell is
-// arbitrary here, the gather ranks by id).
+// arbitrary here, the gather ranks by id).  (Counting the histogram itself back
+// down instead of zeroed cursors saves K2 two stores per cell but costs the
+// scatter and the gather more than it saves: measured.)
 template <int kScatterItems, int NT>
 __global__ void __launch_bounds__(NT) k_cll_scatter(Workspace ws, const int *cell_start, int *perm)
 {

@@ -48,6 +48,11 @@ __device__ __forceinline__ void st_release(unsigned long long *p, unsigned long 
     asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+__device__ __forceinline__ void st_relaxed(unsigned long long *p, unsigned long long v)
+{
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
 __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long *p)
 {
     unsigned long long v;
@@ -95,9 +100,10 @@ __device__ __forceinline__ long long warp_min_ll(long long v)
 // Decoupled look-back (single pass): called by all 32 lanes of warp 0 of a block
 // that owns `tile`.  Publishes the tile's aggregate, accumulates predecessors'
 // aggregates until an inclusive prefix is found, publishes its own inclusive
-// prefix and returns the exclusive prefix.  Publishing uses release stores and
-// reading acquire loads, so everything a predecessor did before publishing
-// happens-before what the caller does after this returns.
+// prefix and returns the exclusive prefix.  The flag, epoch and value travel in
+// one 64-bit word and callers use nothing else a predecessor wrote, so the
+// stores and polls are relaxed: no fence (a gpu-scope fence per tile costs
+// microseconds when the block still has stores and atomics in flight).
 static __device__ unsigned tile_prefix(unsigned long long *status, long long tile, unsigned epoch, unsigned aggregate)
 {
     // each lane inspects kLB consecutive predecessors per round (loads issued
@@ -107,10 +113,10 @@ static __device__ unsigned tile_prefix(unsigned long long *status, long long til
     const int lane = threadIdx.x & 31;
     const unsigned ep = epoch & 0x3fffffffu;
     if (tile == 0) {
-        if (lane == 0) st_release(&status[0], pack_status(epoch, 2, aggregate));
+        if (lane == 0) st_relaxed(&status[0], pack_status(epoch, 2, aggregate));
         return 0;
     }
-    if (lane == 0) st_release(&status[tile], pack_status(epoch, 1, aggregate));
+    if (lane == 0) st_relaxed(&status[tile], pack_status(epoch, 1, aggregate));
     auto flag_of = [&](unsigned long long s) -> unsigned {
         return ((unsigned)(s >> 34) == ep) ? (unsigned)((s >> 32) & 3u) : 0u;
     };
@@ -121,7 +127,7 @@ static __device__ unsigned tile_prefix(unsigned long long *status, long long til
 #pragma unroll
         for (int j = 0; j < kLB; ++j) {
             const long long t = base - lane * kLB - j;
-            s[j] = t >= 0 ? ld_relaxed(&status[t]) : 0ull;     // polled relaxed; one acquire fence below
+            s[j] = t >= 0 ? ld_relaxed(&status[t]) : 0ull;
         }
         unsigned v = 0;
         bool incl = false;
@@ -143,8 +149,7 @@ static __device__ unsigned tile_prefix(unsigned long long *status, long long til
         if (pmask) break;
         base -= 32 * kLB;
     }
-    asm volatile("fence.acq_rel.gpu;" ::: "memory");
-    if (lane == 0) st_release(&status[tile], pack_status(epoch, 2, excl + aggregate));
+    if (lane == 0) st_relaxed(&status[tile], pack_status(epoch, 2, excl + aggregate));
     return excl;
 }
 
@@ -332,6 +337,17 @@ __device__ __forceinline__ void leaver_append(const Workspace &ws, long long i)
     else atomicOr(&ws.ctr->status, kStMigrate);
 }
 
+// Key fix-up with the old key already loaded and the new one computed.
+__device__ __forceinline__ void carry_set(const Workspace &ws, long long i, int kold, int knew)
+{
+    if (knew != kold) {
+        if (kold >= 0) atomicSub(&ws.cell_count[kold], 1);
+        if (knew >= 0) atomicAdd(&ws.cell_count[knew], 1);
+        if (knew == kLeaver) leaver_append(ws, i);      // (a stale entry is skipped when packing)
+        ws.key[i] = knew;
+    }
+}
+
 // Fix-up: particle i, whose next-build key ws.key[i] the gather computed, now has
 // position x and velocity v (or was deleted): its key and the next histogram
 // follow (a leaver key leaves the histogram alone and lists the particle).
@@ -340,13 +356,7 @@ __device__ __forceinline__ void carry_fix(const GridDev &g, const Workspace &ws,
 {
     const int kold = ws.key[i];
     int oob = 0;
-    const int knew = del ? -1 : carry_key(g, x, y, z, vx, vy, vz, cdt, carry, oob);
-    if (knew != kold) {
-        if (kold >= 0) atomicSub(&ws.cell_count[kold], 1);
-        if (knew >= 0) atomicAdd(&ws.cell_count[knew], 1);
-        if (knew == kLeaver) leaver_append(ws, i);      // (a stale entry is skipped when packing)
-        ws.key[i] = knew;
-    }
+    carry_set(ws, i, kold, del ? -1 : carry_key(g, x, y, z, vx, vy, vz, cdt, carry, oob));
 }
 
 // ------------------------------------------------------------------ launch helpers (host)

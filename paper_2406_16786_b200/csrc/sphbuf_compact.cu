@@ -251,25 +251,29 @@ __global__ void __launch_bounds__(kThreads) k_compact_append(PartDev p, GridDev 
         C = p.cap - dst0 > 0 ? p.cap - dst0 : 0;
     }
     const long long stride = (long long)gridDim.x * blockDim.x;
-    for (long long s = (long long)blockIdx.x * blockDim.x + threadIdx.x; s < C; s += stride) {
-        const int k = ws.sport[s];
+    for (long long u = (long long)blockIdx.x * blockDim.x + threadIdx.x; u < C; u += stride) {
+        // staging slot u (filled in any order) -> canonical slot s (port, cell, id)
+        const long long s = (long long)ws.tile_pre[ws.stile[u]] + ws.sexcl[u];
+        if (s >= C) continue;                      // (staging overflow: reported, state undefined)
+        const int k = ws.sport[u];
         const long long d = dst0 + s;
-        p.x[d] = ws.sx[s];
-        p.y[d] = ws.sy[s];
-        p.vx[d] = ws.svx[s];
-        p.vy[d] = ws.svy[s];
+        const float sx = ws.sx[u], sy = ws.sy[u], sz = dim == 3 ? ws.sz[u] : 0.0f;
+        const float svx = ws.svx[u], svy = ws.svy[u], svz = dim == 3 ? ws.svz[u] : 0.0f;
+        p.x[d] = sx;
+        p.y[d] = sy;
+        p.vx[d] = svx;
+        p.vy[d] = svy;
         if (dim == 3) {
-            p.z[d] = ws.sz[s];
-            p.vz[d] = ws.svz[s];
+            p.z[d] = sz;
+            p.vz[d] = svz;
         }
-        for (int e = 0; e < p.n_extra; ++e) p.extra[e][d] = ws.sextra[e][s];
+        for (int e = 0; e < p.n_extra; ++e) p.extra[e][d] = ws.sextra[e][u];
         p.id[d] = s_off[k] + (s - s_beg[k]);
         p.label[d] = -1;
         if (carry) {
             // key carry-over: the new particle's key for the next build
             int oob = 0;
-            const int key = carry_key(g, ws.sx[s], ws.sy[s], dim == 3 ? ws.sz[s] : 0.0f, ws.svx[s], ws.svy[s],
-                                      dim == 3 ? ws.svz[s] : 0.0f, cdt, carry, oob);
+            const int key = carry_key(g, sx, sy, sz, svx, svy, svz, cdt, carry, oob);
             ws.key[d] = key;
             if (key >= 0) atomicAdd(&ws.cell_count[key], 1);
             else leaver_append(ws, d);

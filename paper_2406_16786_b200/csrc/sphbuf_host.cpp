@@ -145,7 +145,6 @@ size_t layout(const sph_ctx *c, char *base, Workspace *W)
     w.cell_count = (int *)take(sizeof(int) * ncells);
     w.cursor = (int *)take(sizeof(int) * ncells);
     w.tile_cells = (unsigned long long *)take(8 * cell_tiles);
-    w.tile_upd = (unsigned long long *)take(8 * upd_tiles);
     w.tile_runs = (unsigned long long *)take(8 * (kMaxRuns / 1024 + 1));
     w.tile_cmp = (unsigned long long *)take(8 * cmp_tiles);
     w.rd = (unsigned *)take(4 * cmp_subs);
@@ -157,6 +156,8 @@ size_t layout(const sph_ctx *c, char *base, Workspace *W)
     w.sub_off = (unsigned *)take(4 * cmp_subs);
     w.run_base = (int *)take(sizeof(int) * kMaxRuns);
     w.tile_run = (int *)take(sizeof(int) * upd_tiles);
+    w.tile_cr = (unsigned *)take(4 * upd_tiles);
+    w.tile_pre = (unsigned *)take(4 * upd_tiles);
     w.key = (int *)take(sizeof(int) * cap);
     w.src = (int *)take(sizeof(int) * cap);
     w.max_leave = 2 * c->max_migrate + 1024;
@@ -173,6 +174,8 @@ size_t layout(const sph_ctx *c, char *base, Workspace *W)
     for (int e = 0; e < c->n_extra; ++e) w.sextra[e] = (float *)take(4 * mn);
     w.sid = (long long *)take(8 * mn);
     w.sport = (int *)take(4 * mn);
+    w.stile = (int *)take(4 * mn);
+    w.sexcl = (int *)take(4 * mn);
     w.max_new = mn;
     w.upd_tiles = upd_tiles;
     w.cmp_tiles = cmp_tiles;

@@ -128,11 +128,13 @@ struct Counters {
     long long migrated;    // cumulative packed for neighbour slabs
     long long mig_base;    // cll: local count before the received particles are appended
     long long n_leave;     // key carry-over: leavers listed for the next build's migration
+    long long n_stage_raw; // update: staging slots handed out (unordered, one atomic per tile)
     int status;            // sticky bits
     int ticket_runs;       // update prologue: tile tickets (reset by its last block)
     int done_cll;          // cell scan: finished blocks
     int done_app;          // compaction append: finished blocks
     int done_runs;         // update prologue: finished blocks
+    int done_upd;          // update: finished blocks (the last one scans the tile counts)
     int dummy;
 };
 
@@ -144,7 +146,8 @@ struct Workspace {
     int *key;                        // [capacity]
     int *leave;                      // [max_leave]: indices of listed leavers (key carry-over + migration)
     int *src;                        // [capacity]: source index of each sorted slot
-    unsigned long long *tile_upd;    // [upd tiles]
+    unsigned *tile_cr;               // [upd tiles]: CREATEs of each update tile
+    unsigned *tile_pre;              // [upd tiles]: their exclusive prefix (canonical staging order)
     unsigned long long *tile_runs;   // [kMaxRuns / 1024 + 1]: update prologue look-back
     unsigned long long *tile_cmp;    // [cmp count tiles]
     unsigned *sub_off;               // [cmp sub-tiles]: tombstones before each sub-tile
@@ -159,6 +162,8 @@ struct Workspace {
     float *sextra[SPH_MAX_EXTRA];
     long long *sid;                  // source id of each staged particle (diagnostic)
     int *sport;                      // port of each staged particle
+    int *stile, *sexcl;              // update tile of each staged particle and its rank inside the tile:
+                                     // canonical slot = tile_pre[stile] + sexcl
     long long max_new;
     long long max_leave;
     long long upd_tiles;

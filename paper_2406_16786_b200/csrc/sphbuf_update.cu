@@ -76,6 +76,7 @@ __global__ void __launch_bounds__(1024) k_upd_prologue(Workspace ws, int n_runs,
         if (threadIdx.x == 0) {
             ctr->ticket_upd = 0;
             ctr->n_stage = 0;
+            ctr->n_stage_raw = 0;
             ctr->n_del = 0;
             ctr->i_first = LLONG_MAX;
         }
@@ -127,11 +128,63 @@ __global__ void __launch_bounds__(1024) k_upd_prologue(Workspace ws, int n_runs,
     }
 }
 
+#ifdef SPHBUF_TRACE
+// Tile timeline of K6 (tools/upd_trace.py): per tile, %globaltimer at its start,
+// after the run staging, before the scan, after the look-back, at its end; the
+// block and SM that ran it.
+constexpr int kTraceTiles = 1 << 14;
+__device__ unsigned long long g_trace[kTraceTiles][7];
+__device__ unsigned long long g_trace_k[4];   // K6: first block entry, last block entry, scan start, end
+__device__ __forceinline__ unsigned long long gtimer()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define SPH_TRACE(tile, slot)                                                            \
+    do {                                                                                 \
+        __syncthreads();                                                                 \
+        if (threadIdx.x == 0 && (tile) < kTraceTiles) g_trace[(tile)][(slot)] = gtimer(); \
+    } while (0)
+#else
+#define SPH_TRACE(tile, slot) \
+    do {                      \
+    } while (0)
+#endif
+
 constexpr int kTileRuns = 256;   // runs of one K6 tile staged in shared memory (else global search)
+
+// Boundary-condition velocity of a buffer particle of port P (paper §IV; SURVEY
+// §8(f) rank 1): pressure BC v <- (v.u) u (Eq. velocity_correction);
+// velocity BC v_X' from the profile (Eqs. 2D/3D_velocity_profile),
+// v = Q^T (v_X', 0, 0).  Y, Z: post-recycle lateral local coordinates.
+__device__ __forceinline__ float bc_speed(const PortDev &P, int dim, float vx, float vy, float vz, float Y, float Z)
+{
+    if (P.bc == SPH_BC_PRESSURE) {
+        float u = __fadd_rn(__fmul_rn(vx, P.Q[0]), __fmul_rn(vy, P.Q[1]));
+        if (dim == 3) u = __fadd_rn(u, __fmul_rn(vz, P.Q[2]));
+        return u;
+    }
+    float u = P.u0;
+    if (P.profile == SPH_PROFILE_PARABOLIC) {
+        const float t = __fdiv_rn(Y, P.R);
+        u = __fmul_rn(P.u0, __fsub_rn(1.0f, __fmul_rn(t, t)));
+    } else if (P.profile == SPH_PROFILE_PARABOLIC_RADIAL) {
+        float r2 = __fmul_rn(Y, Y);
+        if (dim == 3) r2 = __fadd_rn(r2, __fmul_rn(Z, Z));
+        u = __fmul_rn(P.u0, __fsub_rn(1.0f, __fdiv_rn(r2, P.R2)));
+    }
+    return u;
+}
 
 // K6: the candidate check (a3) with generation (a4), deletion (a5) and relabel
 // (a6) fused; CREATEs are appended to the staging area in canonical order
-// (port, cell, id) by a ballot/block scan + decoupled look-back over ordered tiles.
+// (port, cell, id) without any wait between tiles: a tile's CREATEs take staging
+// slots from one atomic per tile and record (tile, rank in the tile); the last
+// block to finish scans the per-tile counts, so the canonical slot of a staged
+// particle is tile_pre[tile] + rank (read by the compaction).  Per tile, every
+// load is issued before the stores it does not depend on, so a tile costs few
+// dependent memory round trips.
 __global__ void __launch_bounds__(kThreads) k_upd_main(PartDev p, GridDev g, const __grid_constant__ PortTable pt,
                                                        Workspace ws, int n_runs, const int *cell_start,
                                                        int *port_counts, int carry, float cdt)
@@ -140,18 +193,25 @@ __global__ void __launch_bounds__(kThreads) k_upd_main(PartDev p, GridDev g, con
     pdl_entry();
     __shared__ PortDev s_ports[SPH_MAX_PORTS];
     __shared__ unsigned s_warp[kUpdItems * kThreads / 32 + 1];
-    __shared__ long long s_tile;
-    __shared__ unsigned s_prefix;
+    __shared__ long long s_tile, s_u0;
     __shared__ int s_roff[kTileRuns], s_rbase[kTileRuns], s_rk[kTileRuns];
+    Counters *ctr = ws.ctr;
+#ifdef SPHBUF_TRACE
+    if (threadIdx.x == 0) {
+        const unsigned long long t = gtimer();
+        atomicMin(&g_trace_k[0], t);
+        atomicMax(&g_trace_k[1], t);
+    }
+#endif
+    long long next_ticket = 0;
+    if (threadIdx.x == 0) next_ticket = atomicAdd(&ctr->ticket_upd, 1);
     {
         const int words = pt.n * (int)(sizeof(PortDev) / 4);
         const unsigned *src = reinterpret_cast<const unsigned *>(pt.p);
         unsigned *dst = reinterpret_cast<unsigned *>(s_ports);
         for (int w = threadIdx.x; w < words; w += blockDim.x) dst[w] = src[w];
     }
-    Counters *ctr = ws.ctr;
     const long long n_cand = ctr->n_cand;
-    const unsigned epoch = ctr->epoch_upd;
     const long long ntiles = (n_cand + kUpdTile - 1) / kUpdTile;
     const int max_ports = pt.max_ports;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -160,12 +220,22 @@ __global__ void __launch_bounds__(kThreads) k_upd_main(PartDev p, GridDev g, con
         ctr->ticket_cmp2 = 0;
     }
     long long del_cnt = 0, del_min = LLONG_MAX, motion = 0;
-    __syncthreads();
     while (true) {
-        if (threadIdx.x == 0) s_tile = atomicAdd(&ctr->ticket_upd, 1);
+        if (threadIdx.x == 0) s_tile = next_ticket;
         __syncthreads();
         const long long tile = s_tile;
         if (tile >= ntiles || tile >= ws.upd_tiles) break;
+#ifdef SPHBUF_TRACE
+        if (threadIdx.x == 0 && tile < kTraceTiles) {
+            unsigned smid;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+            g_trace[tile][0] = gtimer();
+            g_trace[tile][5] = blockIdx.x;
+            g_trace[tile][6] = smid;
+        }
+#endif
+        // the ticket of this block's next tile, taken now (off the critical path)
+        if (threadIdx.x == 0) next_ticket = atomicAdd(&ctr->ticket_upd, 1);
         // the tile's runs [r0, r1] (K5's tile_run) staged in shared memory: offsets
         // relative to the tile, first particle index, port
         const long long t0 = tile * kUpdTile;
@@ -181,22 +251,19 @@ __global__ void __launch_bounds__(kThreads) k_upd_main(PartDev p, GridDev g, con
             }
         }
         __syncthreads();
-        bool cr[kUpdItems], bcm[kUpdItems], dl[kUpdItems];
-        int pidx[kUpdItems], kk[kUpdItems];
-        float ox[kUpdItems], oy[kUpdItems], oz[kUpdItems], bY[kUpdItems], bZ[kUpdItems];
+        SPH_TRACE(tile, 1);
+        // (A) candidate -> particle, loads of what the decisions need
+        int pidx[kUpdItems], kk[kUpdItems], lab[kUpdItems];
+        float x[kUpdItems], y[kUpdItems], z[kUpdItems];
 #pragma unroll
         for (int it = 0; it < kUpdItems; ++it) {
-            cr[it] = false;
-            bcm[it] = false;
-            dl[it] = false;
             pidx[it] = -1;
             kk[it] = 0;
-            ox[it] = oy[it] = oz[it] = 0.0f;
             const int rel = it * kThreads + threadIdx.x;
-            const long long g = t0 + rel;
-            if (g >= n_cand) continue;
-            // run containing g: the largest r with run_off[r] <= g (empty runs share
-            // their successor's offset, so the search lands on the non-empty one)
+            const long long gc = t0 + rel;
+            if (gc >= n_cand) continue;
+            // run containing gc: the largest r with run_off[r] <= gc (empty runs
+            // share their successor's offset, so the search lands on the non-empty one)
             int k, pi;
             if (staged) {
                 int lo = 0, hi = nr - 1;
@@ -211,20 +278,36 @@ __global__ void __launch_bounds__(kThreads) k_upd_main(PartDev p, GridDev g, con
                 int lo = r0, hi = r1;
                 while (lo < hi) {
                     const int mid = (lo + hi + 1) >> 1;
-                    if (ws.run_off[mid] <= g) lo = mid;
+                    if (ws.run_off[mid] <= gc) lo = mid;
                     else hi = mid - 1;
                 }
                 k = ws.runs[3 * lo + 2];
-                pi = ws.run_base[lo] + (int)(g - ws.run_off[lo]);
+                pi = ws.run_base[lo] + (int)(gc - ws.run_off[lo]);
             }
             SPH_CHECK(pi >= 0 && pi < p.cap && k >= 0 && k < pt.n);
+            pidx[it] = pi;
+            kk[it] = k;
+            x[it] = p.x[pi];
+            y[it] = p.y[pi];
+            z[it] = dim == 3 ? p.z[pi] : 0.0f;
+            lab[it] = p.label[pi];
+        }
+        // (B) decisions, pure arithmetic
+        bool cr[kUpdItems], dl[kUpdItems], bcm[kUpdItems];
+        int nlab[kUpdItems];                                   // label to write, or INT_MIN
+        float bY[kUpdItems], bZ[kUpdItems];
+#pragma unroll
+        for (int it = 0; it < kUpdItems; ++it) {
+            cr[it] = dl[it] = bcm[it] = false;
+            nlab[it] = INT_MIN;
+            bY[it] = bZ[it] = 0.0f;
+            if (pidx[it] < 0) continue;
+            const int k = kk[it];
             const PortDev &P = s_ports[k];
-            const float x = p.x[pi], y = p.y[pi], z = dim == 3 ? p.z[pi] : 0.0f;
-            const int lab = p.label[pi];
             float X[3];
-            to_local(P, dim, x, y, z, X);
+            to_local(P, dim, x[it], y[it], z[it], X);
             const bool inP = in_box(X, P.heP, dim);              // x in P_k (reading R4)
-            const bool member = (lab == k);
+            const bool member = (lab[it] == k);
             const bool beyond = X[0] > P.he[0];                  // X'_0 > a/2
             bool create = false, del = false;
             if (inP) {
@@ -240,120 +323,153 @@ __global__ void __launch_bounds__(kThreads) k_upd_main(PartDev p, GridDev g, con
             // R12: a buffer particle outside its decision region moved more than the
             // one-cell margin in one step; it can no longer be generated/deleted.
             if (member && !inP) ++motion;
-            float px = x, py = y, pz = z;
-            if (create) {
-                // recycle: x <- fl(x - fl(a u)) (Eqs. 2D/3D_Inverse_transformation, R10)
-                px = __fsub_rn(x, P.s[0]);
-                py = __fsub_rn(y, P.s[1]);
-                p.x[pi] = px;
-                p.y[pi] = py;
-                if (dim == 3) {
-                    pz = __fsub_rn(z, P.s[2]);
-                    p.z[pi] = pz;
-                }
-                cr[it] = true;
-                ox[it] = x;
-                oy[it] = y;
-                oz[it] = z;
-                atomicAdd(&port_counts[k], 1);
-            }
-            pidx[it] = pi;
-            kk[it] = k;
             float Xp[3] = {X[0], X[1], X[2]};
-            if (create) to_local(P, dim, px, py, pz, Xp);      // post-recycle local frame
-            bool fin = member;                                 // a buffer particle of k after the update
-            dl[it] = del;
+            if (create) {
+                // post-recycle local frame of x <- fl(x - fl(a u)) (R10)
+                to_local(P, dim, __fsub_rn(x[it], P.s[0]), __fsub_rn(y[it], P.s[1]),
+                         dim == 3 ? __fsub_rn(z[it], P.s[2]) : 0.0f, Xp);
+            }
+            bool fin = member;                                   // a buffer particle of k after the update
             if (del) {
-                p.label[pi] = -2;                                // tombstone, removed by sph_compact
-                atomicAdd(&port_counts[max_ports + k], 1);
-                ++del_cnt;
-                del_min = pi < del_min ? pi : del_min;
+                nlab[it] = -2;                                   // tombstone, removed by sph_compact
                 fin = false;
             } else if (P.kind != SPH_INLET) {
                 // relabel on post-recycle positions (R9)
                 fin = in_box(Xp, P.he, dim);
-                if (fin) {
-                    if (lab != k) p.label[pi] = k;
-                } else if (lab == k) {
-                    p.label[pi] = -1;
-                }
+                if (fin && !member) nlab[it] = k;
+                else if (!fin && member) nlab[it] = -1;
             }
+            cr[it] = create;
+            dl[it] = del;
             bcm[it] = fin && P.bc != SPH_BC_NONE;
             bY[it] = Xp[1];
             bZ[it] = Xp[2];
         }
+        // (C) loads for the duplicates and boundary conditions (pre-BC velocity)
+        float vx[kUpdItems], vy[kUpdItems], vz[kUpdItems];
+        long long sid[kUpdItems];
+        int okey[kUpdItems];
+#pragma unroll
+        for (int it = 0; it < kUpdItems; ++it) {
+            vx[it] = vy[it] = vz[it] = 0.0f;
+            sid[it] = 0;
+            okey[it] = 0;
+            const int pi = pidx[it];
+            if (cr[it] || bcm[it]) {
+                vx[it] = p.vx[pi];
+                vy[it] = p.vy[pi];
+                if (dim == 3) vz[it] = p.vz[pi];
+            }
+            if (cr[it]) sid[it] = p.id[pi];
+            if (carry && (cr[it] || dl[it] || bcm[it])) okey[it] = ws.key[pi];
+        }
+        // (D) stores that do not need the staging slot
+#pragma unroll
+        for (int it = 0; it < kUpdItems; ++it) {
+            const int pi = pidx[it];
+            if (pi < 0) continue;
+            const int k = kk[it];
+            const PortDev &P = s_ports[k];
+            float px = x[it], py = y[it], pz = z[it];
+            if (cr[it]) {
+                // recycle: x <- fl(x - fl(a u)) (Eqs. 2D/3D_Inverse_transformation, R10)
+                px = __fsub_rn(px, P.s[0]);
+                py = __fsub_rn(py, P.s[1]);
+                p.x[pi] = px;
+                p.y[pi] = py;
+                if (dim == 3) {
+                    pz = __fsub_rn(pz, P.s[2]);
+                    p.z[pi] = pz;
+                }
+                atomicAdd(&port_counts[k], 1);
+            }
+            if (nlab[it] != INT_MIN) p.label[pi] = nlab[it];
+            if (dl[it]) {
+                atomicAdd(&port_counts[max_ports + k], 1);
+                ++del_cnt;
+                del_min = pi < del_min ? pi : del_min;
+            }
+            if (cr[it]) continue;                                 // BC and key after staging
+            float nvx = vx[it], nvy = vy[it], nvz = vz[it];
+            if (bcm[it]) {
+                const float u = bc_speed(P, dim, vx[it], vy[it], vz[it], bY[it], bZ[it]);
+                nvx = __fmul_rn(u, P.Q[0]);
+                nvy = __fmul_rn(u, P.Q[1]);
+                p.vx[pi] = nvx;
+                p.vy[pi] = nvy;
+                if (dim == 3) {
+                    nvz = __fmul_rn(u, P.Q[2]);
+                    p.vz[pi] = nvz;
+                }
+            }
+            // key carry-over: the next-build key follows a velocity change or a deletion
+            if (carry && (dl[it] || bcm[it])) {
+                int oob = 0;
+                const int knew = dl[it] ? -1 : carry_key(g, px, py, pz, nvx, nvy, nvz, cdt, carry, oob);
+                carry_set(ws, pi, okey[it], knew);
+            }
+        }
+        // (E) ranks of the tile's CREATEs, staging slots
+        SPH_TRACE(tile, 2);
         unsigned excl[kUpdItems], total;
         striped_scan<kThreads, kUpdItems>(cr, excl, total, s_warp);
-        if (threadIdx.x < 32) {
-            const unsigned pre = tile_prefix(ws.tile_upd, tile, epoch, total);
-            if (threadIdx.x == 0) s_prefix = pre;
+        if (threadIdx.x == 0) {
+            ws.tile_cr[tile] = total;
+            s_u0 = total ? (long long)atomicAdd((unsigned long long *)&ctr->n_stage_raw, (unsigned long long)total) : 0;
         }
-        __syncthreads();
+        if (total) __syncthreads();
+        const long long u0 = s_u0;
+        SPH_TRACE(tile, 3);
+        // (F) the duplicates: bitwise copy of the pre-recycle state, label fluid
+        // (R11); then the boundary condition of the recycled particle
 #pragma unroll
         for (int it = 0; it < kUpdItems; ++it) {
             if (!cr[it]) continue;
-            const long long slot = (long long)s_prefix + excl[it];
+            const int pi = pidx[it];
+            const int k = kk[it];
+            const PortDev &P = s_ports[k];
+            const long long slot = u0 + excl[it];
             if (slot < ws.max_new) {
-                const int pi = pidx[it];
-                // duplicate = bitwise copy of the pre-recycle state, label fluid (R11)
-                ws.sx[slot] = ox[it];
-                ws.sy[slot] = oy[it];
-                ws.svx[slot] = p.vx[pi];
-                ws.svy[slot] = p.vy[pi];
+                ws.sx[slot] = x[it];
+                ws.sy[slot] = y[it];
+                ws.svx[slot] = vx[it];
+                ws.svy[slot] = vy[it];
                 if (dim == 3) {
-                    ws.sz[slot] = oz[it];
-                    ws.svz[slot] = p.vz[pi];
+                    ws.sz[slot] = z[it];
+                    ws.svz[slot] = vz[it];
                 }
                 for (int e = 0; e < p.n_extra; ++e) ws.sextra[e][slot] = p.extra[e][pi];
-                ws.sid[slot] = p.id[pi];
-                ws.sport[slot] = kk[it];
+                ws.sid[slot] = sid[it];
+                ws.sport[slot] = k;
+                ws.stile[slot] = (int)tile;
+                ws.sexcl[slot] = (int)excl[it];
             } else {
                 atomicOr(&ctr->status, kStStaging);
             }
-        }
-        // boundary-condition state of the port's buffer particles, after the duplicates
-        // were staged with the pre-BC state (paper §IV)
-#pragma unroll
-        for (int it = 0; it < kUpdItems; ++it) {
-            if (!bcm[it]) continue;
-            const int pi = pidx[it];
-            const PortDev &P = s_ports[kk[it]];
-            float u;
-            if (P.bc == SPH_BC_PRESSURE) {
-                // v <- (v.u) u (Eq. velocity_correction)
-                u = __fadd_rn(__fmul_rn(p.vx[pi], P.Q[0]), __fmul_rn(p.vy[pi], P.Q[1]));
-                if (dim == 3) u = __fadd_rn(u, __fmul_rn(p.vz[pi], P.Q[2]));
-                // recycled particles: rho = rho0 + p_b / c0^2 (Eq. postulate-density)
-                // (a Windkessel-driven port reads the density of this step from the device)
-                if (cr[it] && P.rho_col >= 0) p.extra[P.rho_col][pi] = P.rho_dev ? ws.drv_rho[kk[it]] : P.rho_b;
-            } else {
-                // v_X' from the profile (Eqs. 2D/3D_velocity_profile), v = Q^T (v_X', 0, 0)
-                u = P.u0;
-                if (P.profile == SPH_PROFILE_PARABOLIC) {
-                    const float t = __fdiv_rn(bY[it], P.R);
-                    u = __fmul_rn(P.u0, __fsub_rn(1.0f, __fmul_rn(t, t)));
-                } else if (P.profile == SPH_PROFILE_PARABOLIC_RADIAL) {
-                    float r2 = __fmul_rn(bY[it], bY[it]);
-                    if (dim == 3) r2 = __fadd_rn(r2, __fmul_rn(bZ[it], bZ[it]));
-                    u = __fmul_rn(P.u0, __fsub_rn(1.0f, __fdiv_rn(r2, P.R2)));
+            const float px = __fsub_rn(x[it], P.s[0]), py = __fsub_rn(y[it], P.s[1]);
+            const float pz = dim == 3 ? __fsub_rn(z[it], P.s[2]) : 0.0f;
+            float nvx = vx[it], nvy = vy[it], nvz = vz[it];
+            if (bcm[it]) {
+                const float u = bc_speed(P, dim, vx[it], vy[it], vz[it], bY[it], bZ[it]);
+                nvx = __fmul_rn(u, P.Q[0]);
+                nvy = __fmul_rn(u, P.Q[1]);
+                p.vx[pi] = nvx;
+                p.vy[pi] = nvy;
+                if (dim == 3) {
+                    nvz = __fmul_rn(u, P.Q[2]);
+                    p.vz[pi] = nvz;
                 }
+                // recycled particles: rho = rho0 + p_b / c0^2 (Eq. postulate-density,
+                // P:557-563); a Windkessel-driven port reads this step's from the device
+                if (P.bc == SPH_BC_PRESSURE && P.rho_col >= 0)
+                    p.extra[P.rho_col][pi] = P.rho_dev ? ws.drv_rho[k] : P.rho_b;
             }
-            p.vx[pi] = __fmul_rn(u, P.Q[0]);
-            p.vy[pi] = __fmul_rn(u, P.Q[1]);
-            if (dim == 3) p.vz[pi] = __fmul_rn(u, P.Q[2]);
-        }
-        // key carry-over: particles whose position or velocity changed here (or that
-        // were deleted) get their next-build key and histogram entry corrected
-        if (carry) {
-#pragma unroll
-            for (int it = 0; it < kUpdItems; ++it) {
-                if (!(cr[it] || dl[it] || bcm[it])) continue;
-                const int pi = pidx[it];
-                carry_fix(g, ws, pi, dl[it], p.x[pi], p.y[pi], dim == 3 ? p.z[pi] : 0.0f, p.vx[pi], p.vy[pi],
-                          dim == 3 ? p.vz[pi] : 0.0f, cdt, carry);
+            if (carry) {
+                int oob = 0;
+                carry_set(ws, pi, okey[it], carry_key(g, px, py, pz, nvx, nvy, nvz, cdt, carry, oob));
             }
         }
-        if (tile == ntiles - 1 && threadIdx.x == 0) ctr->n_stage = (long long)s_prefix + total;
+        SPH_TRACE(tile, 4);
         __syncthreads();
     }
     const int lane = threadIdx.x & 31;
@@ -370,8 +486,59 @@ __global__ void __launch_bounds__(kThreads) k_upd_main(PartDev p, GridDev g, con
             atomicOr(&ctr->status, kStMotion);
         }
     }
+    // the last block to finish: exclusive scan of the tile CREATE counts (the
+    // canonical staging order) and the number created
+    __shared__ bool s_last;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        s_last = atomicAdd(&ctr->done_upd, 1) == (int)gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!s_last) return;
+#ifdef SPHBUF_TRACE
+    if (threadIdx.x == 0) g_trace_k[2] = gtimer();
+#endif
+    __threadfence();
+    const long long nt = ntiles < ws.upd_tiles ? ntiles : ws.upd_tiles;
+    unsigned carry_in = 0;
+    for (long long b0 = 0; b0 < nt; b0 += kThreads) {
+        const long long t = b0 + threadIdx.x;
+        const unsigned c = t < nt ? __ldcg(ws.tile_cr + t) : 0u;
+        unsigned tot;
+        const unsigned ex = block_excl_scan<kThreads>(c, tot, s_warp);
+        if (t < nt) ws.tile_pre[t] = carry_in + ex;
+        carry_in += tot;
+    }
+    if (threadIdx.x == 0) {
+        ctr->n_stage = carry_in;
+        ctr->done_upd = 0;
+    }
+#ifdef SPHBUF_TRACE
+    if (threadIdx.x == 0) g_trace_k[3] = gtimer();
+#endif
 }
 
+
+#ifdef SPHBUF_TRACE
+}  // namespace sphbuf
+extern "C" int sph_trace_read(unsigned long long *host, int max_tiles)
+{
+    const int n = max_tiles < sphbuf::kTraceTiles ? max_tiles : sphbuf::kTraceTiles;
+    return (int)cudaMemcpyFromSymbol(host, sphbuf::g_trace, sizeof(unsigned long long) * 7 * n);
+}
+extern "C" int sph_trace_kernel(unsigned long long *host, int reset)
+{
+    cudaError_t e = cudaMemcpyFromSymbol(host, sphbuf::g_trace_k, sizeof(unsigned long long) * 4);
+    if (reset) {
+        const unsigned long long init[4] = {~0ull, 0ull, 0ull, 0ull};
+        cudaMemcpyToSymbol(sphbuf::g_trace_k, init, sizeof(init));
+        static unsigned long long zero[sphbuf::kTraceTiles][7];
+        cudaMemcpyToSymbol(sphbuf::g_trace, zero, sizeof(zero));
+    }
+    return (int)e;
+}
+namespace sphbuf {
+#endif
 
 // ------------------------------------------------------------------ launchers
 

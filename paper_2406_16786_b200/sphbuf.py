@@ -79,9 +79,10 @@ def lib():
     if _L is not None:
         return _L
     debug = os.environ.get("SPHBUF_DEBUG") == "1"     # the bounds-asserting build (tests only)
-    path = _build.LIB_DEBUG if debug else _build.LIB
+    trace = os.environ.get("SPHBUF_TRACE") == "1"     # tile timeline of the update (tools/upd_trace.py)
+    path = _build.LIB_DEBUG if debug else _build.LIB_TRACE if trace else _build.LIB
     if not os.path.exists(path) or os.environ.get("SPHBUF_REBUILD"):
-        path = _build.build(debug=debug)
+        path = _build.build(debug=debug, trace=trace)
     L = C.CDLL(path)
     vp, i32, i64, f32 = C.c_void_p, C.c_int32, C.c_int64, C.c_float
     P = C.POINTER
