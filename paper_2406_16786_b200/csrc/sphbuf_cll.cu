@@ -233,10 +233,12 @@ __device__ __forceinline__ unsigned long long gtimer2()
     } while (0)
 #endif
 
+template <int kCellItems>
 __global__ void __launch_bounds__(kThreads) k_cell_scan(GridDev g, Workspace ws, int *cell_start, int *cell_end,
                                                         long long *n_out, long long ntiles, const long long *n_src)
 {
     pdl_entry();
+    constexpr int kCellTile = kThreads * kCellItems;
     constexpr int V = kCellItems / 4;
     __shared__ unsigned s_warp[kThreads / 32 + 1];
     __shared__ long long s_tile;
@@ -262,54 +264,35 @@ __global__ void __launch_bounds__(kThreads) k_cell_scan(GridDev g, Workspace ws,
     const long long nc = g.ncells;
     // warp-striped layout: warp w owns cells [tile base + w 32 kCellItems, +32 kCellItems);
     // row v of it is int4 #(32 v + lane), so every load / store instruction of a
-    // warp covers 512 contiguous bytes
+    // warp covers 512 contiguous bytes.  Two passes over the tile: the sums (loads
+    // kRowBatch rows at a time), then, after the look-back, the rows again (L2) for
+    // the cell ranges — a tile of kCellTile cells costs few registers, so at C5 all
+    // tiles are resident in one wave and the look-back never waits on a later one.
+    constexpr int kRowBatch = V < 8 ? V : 8;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const long long wbase = tile * kCellTile + (long long)warp * (32 * kCellItems);
     const bool full = tile * kCellTile + kCellTile <= nc;
-    int4 c[V];
-    // the histogram is read and re-zeroed (the next build's, or the gather's key
-    // carry-over, accumulates into it); the scatter's cursors start from zero
-    if (full) {
-        int4 *pc = reinterpret_cast<int4 *>(ws.cell_count + wbase) + lane;
-        int4 *pk = reinterpret_cast<int4 *>(ws.cursor + wbase) + lane;
+    const int4 *pc = reinterpret_cast<const int4 *>(ws.cell_count + wbase) + lane;
+    auto row = [&](int v) -> int4 {
+        if (full) return __ldcg(pc + 32 * v);
+        int t[4];
 #pragma unroll
-        for (int v = 0; v < V; ++v) c[v] = pc[32 * v];
-#pragma unroll
-        for (int v = 0; v < V; ++v) {
-            pc[32 * v] = make_int4(0, 0, 0, 0);
-            pk[32 * v] = make_int4(0, 0, 0, 0);
+        for (int q = 0; q < 4; ++q) {
+            const long long j = wbase + 4 * (32 * v + lane) + q;
+            t[q] = j < nc ? __ldcg(ws.cell_count + j) : 0;
         }
-    } else {
+        return make_int4(t[0], t[1], t[2], t[3]);
+    };
+    unsigned tsum = 0;
 #pragma unroll
-        for (int v = 0; v < V; ++v) {
-            int t[4];
+    for (int v0 = 0; v0 < V; v0 += kRowBatch) {
+        int4 c[kRowBatch];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const long long j = wbase + 4 * (32 * v + lane) + q;
-                t[q] = j < nc ? ws.cell_count[j] : 0;
-                if (j < nc) {
-                    ws.cell_count[j] = 0;
-                    ws.cursor[j] = 0;
-                }
-            }
-            c[v] = make_int4(t[0], t[1], t[2], t[3]);
-        }
+        for (int b = 0; b < kRowBatch; ++b) c[b] = row(v0 + b);
+#pragma unroll
+        for (int b = 0; b < kRowBatch; ++b) tsum += (unsigned)(c[b].x + c[b].y + c[b].z + c[b].w);
     }
-    // per row: exclusive prefix of this lane's int4 inside the row, and the rows
-    // before it; then the warps of the block, then the tiles (look-back)
-    unsigned rowpre[V], wtot = 0;
-#pragma unroll
-    for (int v = 0; v < V; ++v) {
-        const unsigned sv = (unsigned)(c[v].x + c[v].y + c[v].z + c[v].w);
-        unsigned inc = sv;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const unsigned y = __shfl_up_sync(0xffffffffu, inc, o);
-            if (lane >= o) inc += y;
-        }
-        rowpre[v] = wtot + inc - sv;
-        wtot += __shfl_sync(0xffffffffu, inc, 31);
-    }
+    const unsigned wtot = warp_sum(tsum);
     unsigned total;
     const unsigned wexcl = block_excl_scan<kThreads>(lane == 0 ? wtot : 0u, total, s_warp);
     const unsigned woff = __shfl_sync(0xffffffffu, wexcl, 0);
@@ -321,33 +304,50 @@ __global__ void __launch_bounds__(kThreads) k_cell_scan(GridDev g, Workspace ws,
     __syncthreads();
     SCAN_TRACE(2);
     const unsigned prefix = s_prefix;
-    if (full) {
-        int4 *ps = reinterpret_cast<int4 *>(cell_start + wbase) + lane;
-        int4 *pe = reinterpret_cast<int4 *>(cell_end + wbase) + lane;
+    // second pass: cell ranges; the histogram is re-zeroed (the next build's, or
+    // the gather's key carry-over, accumulates into it), the scatter's cursors too
+    unsigned run = prefix + woff;                    // first slot of this warp's current row
+    constexpr int kWB = 4;
 #pragma unroll
-        for (int v = 0; v < V; ++v) {
-            int run = (int)(prefix + woff + rowpre[v]);
+    for (int v0 = 0; v0 < V; v0 += kWB) {
+        int4 c[kWB];
+#pragma unroll
+        for (int b = 0; b < kWB; ++b) c[b] = row(v0 + b);
+#pragma unroll
+        for (int b = 0; b < kWB; ++b) {
+            const int v = v0 + b;
+            const unsigned sv = (unsigned)(c[b].x + c[b].y + c[b].z + c[b].w);
+            unsigned inc = sv;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned y = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += y;
+            }
+            int r = (int)(run + inc - sv);
+            run += __shfl_sync(0xffffffffu, inc, 31);
             int4 st, en;
-            st.x = run; run += c[v].x; en.x = run;
-            st.y = run; run += c[v].y; en.y = run;
-            st.z = run; run += c[v].z; en.z = run;
-            st.w = run; run += c[v].w; en.w = run;
-            ps[32 * v] = st;
-            pe[32 * v] = en;
-        }
-    } else {
+            st.x = r; r += c[b].x; en.x = r;
+            st.y = r; r += c[b].y; en.y = r;
+            st.z = r; r += c[b].z; en.z = r;
+            st.w = r; r += c[b].w; en.w = r;
+            if (full) {
+                const long long q4 = (wbase >> 2) + 32 * v + lane;
+                reinterpret_cast<int4 *>(cell_start)[q4] = st;
+                reinterpret_cast<int4 *>(cell_end)[q4] = en;
+                reinterpret_cast<int4 *>(ws.cell_count)[q4] = make_int4(0, 0, 0, 0);
+                reinterpret_cast<int4 *>(ws.cursor)[q4] = make_int4(0, 0, 0, 0);
+            } else {
+                const int s4[4] = {st.x, st.y, st.z, st.w}, e4[4] = {en.x, en.y, en.z, en.w};
 #pragma unroll
-        for (int v = 0; v < V; ++v) {
-            int run = (int)(prefix + woff + rowpre[v]);
-            const int cv[4] = {c[v].x, c[v].y, c[v].z, c[v].w};
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const long long j = wbase + 4 * (32 * v + lane) + q;
-                if (j < nc) {
-                    cell_start[j] = run;
-                    cell_end[j] = run + cv[q];
+                for (int q = 0; q < 4; ++q) {
+                    const long long j = wbase + 4 * (32 * v + lane) + q;
+                    if (j < nc) {
+                        cell_start[j] = s4[q];
+                        cell_end[j] = e4[q];
+                        ws.cell_count[j] = 0;
+                        ws.cursor[j] = 0;
+                    }
                 }
-                run += cv[q];
             }
         }
     }
@@ -747,7 +747,10 @@ cudaError_t launch_cll_finish(const PartDev &in, const PartDev &out, const GridD
                               cudaStream_t s, Launch *L)
 {
     const int advect = advect_b ? 1 : 0;
-    const long long ntiles = (g.ncells + kCellTile - 1) / kCellTile;
+    // cells per thread of K2: 32 (many small tiles) unless that takes more than
+    // one wave of resident blocks, then 128
+    const bool big = g.ncells > kScanBigCells;
+    const long long ntiles = (g.ncells + (big ? kCellTileBig : kCellTile) - 1) / (big ? kCellTileBig : kCellTile);
     const long long cap = in.cap;
     if (recv_lo || recv_hi) {
         L->before(s);
@@ -757,8 +760,12 @@ cudaError_t launch_cll_finish(const PartDev &in, const PartDev &out, const GridD
     }
     L->before(s);
     const bool no_key_pass = cc.use && !cc.mig;
-    launch_k(k_cell_scan, dim3((unsigned)(ntiles > 0 ? ntiles : 1)), dim3(kThreads), 0, s, g, ws, cell_start, cell_end,
-             out.n, ntiles, no_key_pass ? (const long long *)in.n : (const long long *)nullptr);
+    if (big)
+        launch_k(k_cell_scan<kCellItemsBig>, dim3((unsigned)ntiles), dim3(kThreads), 0, s, g, ws, cell_start,
+                 cell_end, out.n, ntiles, no_key_pass ? (const long long *)in.n : (const long long *)nullptr);
+    else
+        launch_k(k_cell_scan<kCellItems>, dim3((unsigned)(ntiles > 0 ? ntiles : 1)), dim3(kThreads), 0, s, g, ws,
+                 cell_start, cell_end, out.n, ntiles, no_key_pass ? (const long long *)in.n : (const long long *)nullptr);
     L->after(s, KID_CELL_SCAN);
     {
         // scatter variants for tuning (SPHBUF_SCATTER=<items>:<threads>); default 4 x 256,

@@ -14,8 +14,11 @@ namespace sphbuf {
 
 // ---------------------------------------------------------------- tiling
 constexpr int kThreads = 256;            // block size of the O(N) kernels
-constexpr int kCellItems = 32;           // cells per thread in the cell scan (multiple of 4)
+constexpr int kCellItems = 32;           // cells per thread in the cell scan (multiple of 32) ...
 constexpr int kCellTile = kThreads * kCellItems;
+constexpr int kCellItemsBig = 128;       // ... or this many above kScanBigCells cells (one wave of tiles)
+constexpr int kCellTileBig = kThreads * kCellItemsBig;
+constexpr long long kScanBigCells = 4LL << 20;
 constexpr int kUpdItems = 2;             // candidates per thread in the update
 constexpr int kUpdTile = kThreads * kUpdItems;
 constexpr int kCmpItems = 4;             // particles per thread in the compaction
