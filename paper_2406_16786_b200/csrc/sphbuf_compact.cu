@@ -54,20 +54,23 @@ __global__ void __launch_bounds__(kThreads) k_compact_count(PartDev p, Workspace
         __syncthreads();
         const long long tile = s_tile;
         if (tile >= ntiles) break;
-        // blocked: thread t counts labels [t*32, t*32+32) of the tile, so warp w
-        // covers exactly sub-tile w (1024 labels) of the compaction move
-        const long long base = ibeg + tile * kCntTile + (long long)threadIdx.x * kCntItems;
+        // warp w counts exactly sub-tile w (1024 labels) of the compaction move;
+        // lane l reads int4 #(32 v + l) of it, so each load covers 512 contiguous bytes
+        const long long wb = ibeg + tile * kCntTile + (long long)warp * (32 * kCntItems);
         unsigned c = 0;
-        if (base + kCntItems <= N) {
-            const int4 *q = reinterpret_cast<const int4 *>(p.label + base);
+        if (wb + 32 * kCntItems <= N) {
+            const int4 *q = reinterpret_cast<const int4 *>(p.label + wb) + lane;
 #pragma unroll
             for (int v = 0; v < kCntItems / 4; ++v) {
-                const int4 a = q[v];
+                const int4 a = q[32 * v];
                 c += (a.x <= -2) + (a.y <= -2) + (a.z <= -2) + (a.w <= -2);
             }
         } else {
-            for (int j = 0; j < kCntItems; ++j)
-                if (base + j < N) c += (p.label[base + j] <= -2);
+            for (int v = 0; v < kCntItems / 4; ++v)
+                for (int j = 0; j < 4; ++j) {
+                    const long long i = wb + 4 * (32 * v + lane) + j;
+                    if (i < N) c += (p.label[i] <= -2);
+                }
         }
         c = warp_sum(c);
         if (lane == 0) s_sub[0][warp] = c;
@@ -97,6 +100,7 @@ __global__ void __launch_bounds__(kThreads) k_compact_move(PartDev p, int dim, W
     pdl_entry();
     __shared__ unsigned s_cnt[kCmpItems * kThreads / 32 + 1];
     __shared__ long long s_tile;
+    __shared__ volatile int s_sink;
     Counters *ctr = ws.ctr;
     const long long D = ctr->n_del;
     if (D == 0) return;
@@ -150,14 +154,20 @@ __global__ void __launch_bounds__(kThreads) k_compact_move(PartDev p, int dim, W
                 }
             }
         }
-        if (dep == 0x7f3a5c11 && mine == 77u) ctr->dummy = dep;   // never true in practice; keeps the dependency
+        // every loaded word is consumed here, before the block barrier in the scan:
+        // the loads have returned before "read done" is published (a volatile
+        // shared-memory store of the XOR is an instruction that needs all of them)
+        s_sink = dep;
         unsigned excl[kCmpItems], total;
         striped_scan<kThreads, kCmpItems>(alive, excl, total, s_cnt);   // contains __syncthreads
         const long long start = ibeg + u * kCmpTile;
         const long long dst0 = start - (long long)ws.sub_off[u];
         if (threadIdx.x < 32) {
+            // every load of this sub-tile has returned (its values were consumed
+            // above and the block barrier passed), so a relaxed store suffices: no
+            // fence waiting for the previous sub-tile's stores
             if (threadIdx.x == 0)
-                asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(ws.rd + u), "r"(epoch) : "memory");
+                asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(ws.rd + u), "r"(epoch) : "memory");
             // wait only for the earlier sub-tiles whose input overlaps the output range
             // [dst0, dst0 + alive) (when the shift exceeds a sub-tile these are a few
             // tiles back, claimed long ago); acquire polling (no full fence), the block
