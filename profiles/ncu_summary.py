@@ -45,7 +45,12 @@ def main(rep, launches, prefix):
     lrows = list(csv.DictReader(io.StringIO("\n".join(text[start:]))))
     agg = collections.defaultdict(list)
     for r in lrows:
-        agg[r["Kernel Name"].split("(")[0].replace("void ", "")].append(float(r["Metric Value"]))
+        name = r["Kernel Name"].split("(")[0].replace("void ", "")
+        if name.startswith("sphbuf::"):
+            name = name[len("sphbuf::"):]
+        if not name.startswith("k_"):
+            continue          # input generation etc. (torch), not the library
+        agg[name].append(float(r["Metric Value"]))
     tot = sum(sum(v) for k, v in agg.items() if "register" not in k)
     out = [f"# ncu summary ({prefix.split('/')[-1]})", "",
            "## Launch list (gpu__time_duration.sum, cold-cache and serialised: compare shares)", "",
