@@ -229,7 +229,11 @@ sph_status sph_advect(sph_ctx *ctx, sph_particles *p, float dt, void *stream);
  * cell; tombstones dropped; the SoA of `in` is gathered into `out` (distinct
  * arrays) and out->n_dev receives the live count.  cell_start / cell_end
  * [ncells of this slab]: first / one-past-last position of each cell in `out`.
- * perm_or_null [in capacity]: new position of each input particle, -1 if dropped. */
+ * perm_or_null [in capacity]: new position of each input particle, -1 if dropped.
+ * With registered ports the build also runs the next sph_buffer_update's
+ * prologue (candidate offsets of the port runs in these cell tables, reset of
+ * the per-update counters that sph_status_sync reports as created / deleted);
+ * that update, given the same cell tables, then launches only its main kernel. */
 sph_status sph_cll_build(sph_ctx *ctx, const sph_particles *in, sph_particles *out, int32_t *cell_start,
                          int32_t *cell_end, int32_t *perm_or_null, void *stream);
 

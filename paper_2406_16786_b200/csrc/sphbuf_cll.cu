@@ -18,6 +18,7 @@
 #include <cstring>
 
 #include "sphbuf_common.cuh"
+#include "sphbuf_prologue.cuh"
 
 namespace sphbuf {
 
@@ -387,12 +388,19 @@ namespace sphbuf {
 // arbitrary here, the gather ranks by id).  (Counting the histogram itself back
 // down instead of zeroed cursors saves K2 two stores per cell but costs the
 // scatter and the gather more than it saves: measured.)
+// Blocks beyond `nscat` run the update prologue K5 instead (UpdPro): it needs only
+// the cell tables K2 just wrote, so it overlaps the scatter and the gather.
 template <int kScatterItems, int NT>
-__global__ void __launch_bounds__(NT) k_cll_scatter(Workspace ws, const int *cell_start, int *perm)
+__global__ void __launch_bounds__(NT) k_cll_scatter(Workspace ws, const int *cell_start, int *perm, int nscat,
+                                                    const int *cell_end, int pro_runs, int pro_max_ports)
 {
     pdl_entry();
+    if ((int)blockIdx.x >= nscat) {
+        upd_prologue_body<NT>(ws, pro_runs, cell_start, cell_end, pro_max_ports, (int)gridDim.x - nscat);
+        return;
+    }
     const long long n = ws.ctr->n_in;
-    const long long stride = (long long)gridDim.x * NT * kScatterItems;
+    const long long stride = (long long)nscat * NT * kScatterItems;
     for (long long base = (long long)blockIdx.x * NT * kScatterItems; base < n; base += stride) {
         int key[kScatterItems];
 #pragma unroll
@@ -630,11 +638,15 @@ __global__ void __launch_bounds__(NT, MINB) k_cll_gather(PartDev in, PartDev out
 // ------------------------------------------------------------------ launchers
 
 template <int I, int NT>
-static void scatter_launch(const Workspace &ws, const int *cell_start, int *perm, long long cap, cudaStream_t s)
+static void scatter_launch(const Workspace &ws, const int *cell_start, const int *cell_end, int *perm, long long cap,
+                           const UpdPro &up, cudaStream_t s)
 {
     static int grid = 0;
     if (!grid) grid = occ_grid(k_cll_scatter<I, NT>, NT);
-    launch_k(k_cll_scatter<I, NT>, dim3(cap_grid(grid, cap, NT * I)), dim3(NT), 0, s, ws, cell_start, perm);
+    const int nscat = cap_grid(grid, cap, NT * I);
+    const int npro = up.n_runs > 0 ? (up.n_runs + NT - 1) / NT : 0;
+    launch_k(k_cll_scatter<I, NT>, dim3(nscat + npro), dim3(NT), 0, s, ws, cell_start, perm, nscat, cell_end,
+             up.n_runs, up.max_ports);
 }
 
 // Gather variants (template instances), chosen by SPHBUF_GATHER=<slots>:<min blocks>
@@ -734,17 +746,19 @@ cudaError_t launch_cll_key(const PartDev &in, const GridDev &g, const Workspace 
 }
 
 cudaError_t launch_cll(const PartDev &in, const PartDev &out, const GridDev &g, const Workspace &ws, int *cell_start,
-                       int *cell_end, int *perm, float dt, bool advect, const CllCarry &cc, cudaStream_t s, Launch *L)
+                       int *cell_end, int *perm, float dt, bool advect, const CllCarry &cc, const UpdPro &up,
+                       cudaStream_t s, Launch *L)
 {
     cudaError_t e = launch_cll_key(in, g, ws, dt, advect, nullptr, nullptr, 0, 0, cc, s, L);
     if (e != cudaSuccess) return e;
-    return launch_cll_finish(in, out, g, ws, nullptr, nullptr, 0, 0, cell_start, cell_end, perm, advect, dt, cc, s, L);
+    return launch_cll_finish(in, out, g, ws, nullptr, nullptr, 0, 0, cell_start, cell_end, perm, advect, dt, cc, up, s,
+                             L);
 }
 
 cudaError_t launch_cll_finish(const PartDev &in, const PartDev &out, const GridDev &g, const Workspace &ws,
                               const float *recv_lo, const float *recv_hi, long long maxm, int rec, int *cell_start,
                               int *cell_end, int *perm, bool advect_b, float dt, const CllCarry &cc,
-                              cudaStream_t s, Launch *L)
+                              const UpdPro &up, cudaStream_t s, Launch *L)
 {
     const int advect = advect_b ? 1 : 0;
     // cells per thread of K2: 32 (many small tiles) unless that takes more than
@@ -773,11 +787,11 @@ cudaError_t launch_cll_finish(const PartDev &in, const PartDev &out, const GridD
         static const char *sv = getenv("SPHBUF_SCATTER");
         const char *v = sv ? sv : "";
         L->before(s);
-        if (!strcmp(v, "8:256")) scatter_launch<8, 256>(ws, cell_start, perm, cap, s);
-        else if (!strcmp(v, "2:256")) scatter_launch<2, 256>(ws, cell_start, perm, cap, s);
-        else if (!strcmp(v, "1:256")) scatter_launch<1, 256>(ws, cell_start, perm, cap, s);
-        else if (!strcmp(v, "2:512")) scatter_launch<2, 512>(ws, cell_start, perm, cap, s);
-        else scatter_launch<4, 256>(ws, cell_start, perm, cap, s);
+        if (!strcmp(v, "8:256")) scatter_launch<8, 256>(ws, cell_start, cell_end, perm, cap, up, s);
+        else if (!strcmp(v, "2:256")) scatter_launch<2, 256>(ws, cell_start, cell_end, perm, cap, up, s);
+        else if (!strcmp(v, "1:256")) scatter_launch<1, 256>(ws, cell_start, cell_end, perm, cap, up, s);
+        else if (!strcmp(v, "2:512")) scatter_launch<2, 512>(ws, cell_start, cell_end, perm, cap, up, s);
+        else scatter_launch<4, 256>(ws, cell_start, cell_end, perm, cap, up, s);
         L->after(s, KID_CLL_SCATTER);
     }
     L->before(s);

@@ -88,6 +88,12 @@ struct sph_ctx {
     std::vector<PortHost> ports;
     std::vector<int> runs;   // 3 ints per run: c0, c1, port (ports in registration order)
     std::vector<int> run_base, run_cnt;   // per port: first run and run count in `runs`
+    // the update prologue K5 run inside the last build's scatter: valid for the
+    // run table version and cell tables it saw, consumed by the next update
+    unsigned runs_ver = 0;
+    bool pro_ready = false;
+    unsigned pro_ver = 0;
+    const int32_t *pro_cs = nullptr, *pro_ce = nullptr;
     std::vector<int> run_cap;             // per port: > 0 once movable (device-enumerated slice)
     std::vector<sph_bc> bcs;              // per port: the last BC set
     std::vector<sph_driver> drivers;      // per port: time-dependent driver (kind NONE if none)
@@ -145,12 +151,13 @@ size_t layout(const sph_ctx *c, char *base, Workspace *W)
     w.cell_count = (int *)take(sizeof(int) * ncells);
     w.cursor = (int *)take(sizeof(int) * ncells);
     w.tile_cells = (unsigned long long *)take(8 * cell_tiles);
-    w.tile_runs = (unsigned long long *)take(8 * (kMaxRuns / 1024 + 1));
+    w.tile_runs = (unsigned long long *)take(8 * (kMaxRuns / 256 + 1));
     w.tile_cmp = (unsigned long long *)take(8 * cmp_tiles);
     w.rd = (unsigned *)take(4 * cmp_subs);
     w.runs = (int *)take(sizeof(int) * 3 * kMaxRuns);
     w.drv = (DriverDev *)take(sizeof(DriverDev) * SPH_MAX_PORTS);
     w.drv_rho = (float *)take(sizeof(float) * SPH_MAX_PORTS);
+    w.port_cnt = (int *)take(sizeof(int) * 2 * SPH_MAX_PORTS);
     w.run_off = (long long *)take(sizeof(long long) * (kMaxRuns + 1));
     const size_t zero_end = off;   // everything above must start zeroed
     w.sub_off = (unsigned *)take(4 * cmp_subs);
@@ -477,6 +484,7 @@ sph_status sph_set_workspace(sph_ctx *c, void *d_ws, size_t bytes)
     cudaError_t e = cudaMemset(d_ws, 0, zero_bytes(c));
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     if (e != cudaSuccess) return cuda_fail(c, e, "sph_set_workspace");
+    ++c->runs_ver;
     if (!c->runs.empty()) {
         e = cudaMemcpy(c->W.runs, c->runs.data(), sizeof(int) * c->runs.size(), cudaMemcpyHostToDevice);
         if (e != cudaSuccess) return cuda_fail(c, e, "sph_set_workspace runs");
@@ -598,6 +606,7 @@ sph_status sph_buffer_register(sph_ctx *c, sph_particles *p, const float origin[
     long long hit = 0;
     enumerate_runs(c->grid, Pi, r2, hit);
     const size_t before = c->runs.size();
+    ++c->runs_ver;
     if ((before + r2.size() / 2 * 3) / 3 > (size_t)kMaxRuns) return fail(c, SPH_ERR_ARG, "too many port runs");
     for (size_t i = 0; i < r2.size(); i += 2) {
         c->runs.push_back(r2[i]);
@@ -691,6 +700,7 @@ sph_status sph_port_move(sph_ctx *c, sph_particles *p, int32_t k, const float or
     if (!c->ws) return fail(c, SPH_ERR_STATE, "no workspace set");
     sph_status st = check_particles(c, p);
     if (st != SPH_OK) return st;
+    ++c->runs_ver;   // the port's runs (and maybe the run table layout) change
     const int dim = c->grid.dim;
     PortDev P1 = c->pt.p[k];
     float o1[3], he[3];
@@ -898,6 +908,23 @@ sph_status sph_advect(sph_ctx *c, sph_particles *p, float dt, void *stream)
     return e == cudaSuccess ? SPH_OK : cuda_fail(c, e, "advect");
 }
 
+// The update prologue rides on the build's scatter when ports exist; the next
+// sph_buffer_update skips it if the runs and cell tables are still those.
+static UpdPro pro_plan(sph_ctx *c, const int32_t *cell_start, const int32_t *cell_end)
+{
+    UpdPro up;
+    const int n_runs = (int)(c->runs.size() / 3);
+    c->pro_ready = n_runs > 0;
+    if (n_runs > 0) {
+        up.n_runs = n_runs;
+        up.max_ports = c->pt.max_ports;
+        c->pro_ver = c->runs_ver;
+        c->pro_cs = cell_start;
+        c->pro_ce = cell_end;
+    }
+    return up;
+}
+
 static sph_status cll_build(sph_ctx *c, const sph_particles *in, sph_particles *out, int32_t *cell_start,
                             int32_t *cell_end, int32_t *perm, float dt, bool advect, void *stream)
 {
@@ -911,8 +938,9 @@ static sph_status cll_build(sph_ctx *c, const sph_particles *in, sph_particles *
     if ((reinterpret_cast<size_t>(cell_start) | reinterpret_cast<size_t>(cell_end)) % 16)
         return fail(c, SPH_ERR_ARG, "cell tables must be 16-byte aligned");
     const CllCarry cc = carry_plan(c, in, advect, dt, false);
+    const UpdPro up = pro_plan(c, cell_start, cell_end);
     cudaError_t e = launch_cll(part_dev(in), part_dev(out), c->gd, c->W, cell_start, cell_end, perm, dt, advect, cc,
-                               static_cast<cudaStream_t>(stream), &c->L);
+                               up, static_cast<cudaStream_t>(stream), &c->L);
     if (e != cudaSuccess) return cuda_fail(c, e, "cll_build");
     carry_after_build(c, cc, out);
     return SPH_OK;
@@ -966,9 +994,10 @@ sph_status sph_cll_finish(sph_ctx *c, sph_particles *in, sph_particles *out, con
         return fail(c, SPH_ERR_ARG, "cll_finish needs distinct input and output arrays");
     if ((reinterpret_cast<size_t>(cell_start) | reinterpret_cast<size_t>(cell_end)) % 16)
         return fail(c, SPH_ERR_ARG, "cell tables must be 16-byte aligned");
+    const UpdPro up = pro_plan(c, cell_start, cell_end);
     cudaError_t e = launch_cll_finish(part_dev(in), part_dev(out), c->gd, c->W, recv_lo, recv_hi, c->max_migrate,
                                       sph_migrate_record_floats(c), cell_start, cell_end, perm, c->key_advect,
-                                      c->key_dt, c->key_cc, static_cast<cudaStream_t>(stream), &c->L);
+                                      c->key_dt, c->key_cc, up, static_cast<cudaStream_t>(stream), &c->L);
     if (e != cudaSuccess) return cuda_fail(c, e, "cll_finish");
     carry_after_build(c, c->key_cc, out);
     return SPH_OK;
@@ -982,8 +1011,11 @@ sph_status sph_buffer_update(sph_ctx *c, sph_particles *p, const int32_t *cell_s
     if (st != SPH_OK) return st;
     if (!cell_start || !cell_end || !port_counts) return fail(c, SPH_ERR_ARG, "NULL argument");
     const int n_runs = (int)(c->runs.size() / 3);
+    const bool pro_done = c->pro_ready && c->pro_ver == c->runs_ver && c->pro_cs == cell_start &&
+                          c->pro_ce == cell_end;
+    c->pro_ready = false;
     cudaError_t e = launch_update(part_dev(p), c->gd, c->pt, c->W, n_runs, cell_start, cell_end, port_counts,
-                                  carry_on(c, p), c->carry_dt, static_cast<cudaStream_t>(stream), &c->L);
+                                  carry_on(c, p), c->carry_dt, pro_done, static_cast<cudaStream_t>(stream), &c->L);
     return e == cudaSuccess ? SPH_OK : cuda_fail(c, e, "buffer_update");
 }
 

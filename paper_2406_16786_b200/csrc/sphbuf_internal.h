@@ -151,13 +151,14 @@ struct Workspace {
     int *src;                        // [capacity]: source index of each sorted slot
     unsigned *tile_cr;               // [upd tiles]: CREATEs of each update tile
     unsigned *tile_pre;              // [upd tiles]: their exclusive prefix (canonical staging order)
-    unsigned long long *tile_runs;   // [kMaxRuns / 1024 + 1]: update prologue look-back
+    unsigned long long *tile_runs;   // [kMaxRuns / 256 + 1]: update prologue look-back
     unsigned long long *tile_cmp;    // [cmp count tiles]
     unsigned *sub_off;               // [cmp sub-tiles]: tombstones before each sub-tile
     unsigned *rd;                    // [cmp sub-tiles]: "read done" epoch flags
     int *runs;                       // [kMaxRuns * 3]: c0, c1, port
     DriverDev *drv;                  // [SPH_MAX_PORTS]: Windkessel state
     float *drv_rho;                  // [SPH_MAX_PORTS]: recycled density of driven pressure BCs
+    int *port_cnt;                   // [2 SPH_MAX_PORTS]: this update's created / deleted per port
     long long *run_off;              // [kMaxRuns + 1]
     int *run_base;                   // [kMaxRuns]: first particle index of each run
     int *tile_run;                   // [upd tiles]: run holding the first candidate of each K6 tile
@@ -210,9 +211,16 @@ struct CllCarry {
     bool mig = false;   // with slab migration (leaver list)
     float dt = 0.f;
 };
+// The update prologue (K5) run by extra blocks of the build's scatter: n_runs > 0
+// enables it (sph_buffer_update then launches K6 alone).
+struct UpdPro {
+    int n_runs = 0;
+    int max_ports = 0;
+};
 cudaError_t launch_cll(const PartDev &in, const PartDev &out, const GridDev &g, const Workspace &ws,
                        int *cell_start, int *cell_end, int *perm, float dt, bool advect, const CllCarry &cc,
-                       cudaStream_t s, Launch *L);
+                       const UpdPro &up, cudaStream_t s, Launch *L);
+
 // advect / dt: the advection of the key pass (launch_cll_key) that this build
 // finishes; the gather applies it to the slab's own particles as it moves them.
 cudaError_t launch_cll_key(const PartDev &in, const GridDev &g, const Workspace &ws, float dt, bool advect,
@@ -221,10 +229,10 @@ cudaError_t launch_cll_key(const PartDev &in, const GridDev &g, const Workspace 
 cudaError_t launch_cll_finish(const PartDev &in, const PartDev &out, const GridDev &g, const Workspace &ws,
                               const float *recv_lo, const float *recv_hi, long long maxm, int rec, int *cell_start,
                               int *cell_end, int *perm, bool advect, float dt, const CllCarry &cc,
-                              cudaStream_t s, Launch *L);
+                              const UpdPro &up, cudaStream_t s, Launch *L);
 cudaError_t launch_update(const PartDev &p, const GridDev &g, const PortTable &pt, const Workspace &ws, int n_runs,
                           const int *cell_start, const int *cell_end, int *port_counts, int carry, float cdt,
-                          cudaStream_t s, Launch *L);
+                          bool prologue_done, cudaStream_t s, Launch *L);
 cudaError_t launch_compact(const PartDev &p, const GridDev &g, const PortTable &pt, const Workspace &ws,
                            const int *all_counts, int nranks, int rank, long long *next_id, int *perm, bool defer,
                            int carry, float cdt, cudaStream_t s, Launch *L);

@@ -6,6 +6,7 @@
 #include <cstdint>
 
 #include "sphbuf_common.cuh"
+#include "sphbuf_prologue.cuh"
 
 namespace sphbuf {
 
@@ -54,78 +55,12 @@ __global__ void __launch_bounds__(kThreads) k_register(PartDev p, int dim, PortD
 
 // ------------------------------------------------------------------ a3-a6: buffer update
 
-// K5: candidate count per port run (cell ranges from the current cell list) and
-// their exclusive scan over 1024-run tiles (ticket order, decoupled look-back),
-// so any number of runs is scanned by many blocks at once; resets the
-// per-update counters.  The tile tickets and the epoch are advanced by the last
-// block to finish (done counter), so the kernel needs no other launch.
+// K5 as its own kernel (see sphbuf_prologue.cuh).
 __global__ void __launch_bounds__(1024) k_upd_prologue(Workspace ws, int n_runs, const int *cell_start,
-                                                       const int *cell_end, int *port_counts, int max_ports)
+                                                       const int *cell_end, int max_ports)
 {
     pdl_entry();
-    __shared__ unsigned s_warp[1024 / 32 + 1];
-    __shared__ int s_tile;
-    __shared__ unsigned s_prefix;
-    Counters *ctr = ws.ctr;
-    const int ntiles = (n_runs + 1023) / 1024;
-    const unsigned epoch = ctr->epoch_upd + 1;
-    if (threadIdx.x == 0) s_tile = atomicAdd(&ctr->ticket_runs, 1);
-    __syncthreads();
-    const int tile = s_tile;
-    if (tile == 0) {
-        if (threadIdx.x == 0) {
-            ctr->ticket_upd = 0;
-            ctr->n_stage = 0;
-            ctr->n_stage_raw = 0;
-            ctr->n_del = 0;
-            ctr->i_first = LLONG_MAX;
-        }
-        for (int i = threadIdx.x; i < 2 * max_ports; i += blockDim.x) port_counts[i] = 0;
-    }
-    if (tile < ntiles) {
-        const int r = tile * 1024 + threadIdx.x;
-        unsigned len = 0;
-        int base = 0;
-        // (c1 < c0: an empty slot of a movable port's run slice)
-        if (r < n_runs && ws.runs[3 * r + 1] >= ws.runs[3 * r]) {
-            base = cell_start[ws.runs[3 * r]];
-            len = (unsigned)(cell_end[ws.runs[3 * r + 1]] - base);
-        }
-        unsigned total;
-        const unsigned ex = block_excl_scan<1024>(len, total, s_warp);
-        if (threadIdx.x < 32) {
-            const unsigned pre = tile_prefix(ws.tile_runs, tile, epoch, total);
-            if (threadIdx.x == 0) s_prefix = pre;
-        }
-        __syncthreads();
-        if (r < n_runs) {
-            const long long off = (long long)s_prefix + ex;
-            ws.run_off[r] = off;
-            ws.run_base[r] = base;
-            // the run holding the first candidate of each K6 tile starting inside it
-            for (long long t = (off + kUpdTile - 1) / kUpdTile; t * kUpdTile < off + len && t < ws.upd_tiles; ++t)
-                ws.tile_run[t] = r;
-        }
-        if (tile == ntiles - 1 && threadIdx.x == 0) {
-            const long long carry = (long long)s_prefix + total;
-            ws.run_off[n_runs] = carry;
-            ctr->n_cand = carry;
-            ctr->checked += carry;
-            if ((carry + kUpdTile - 1) / kUpdTile > ws.upd_tiles) ctr->status |= kStCapacity;
-        }
-    }
-    if (ntiles == 0 && tile == 0 && threadIdx.x == 0) {
-        ws.run_off[0] = 0;
-        ctr->n_cand = 0;
-    }
-    if (threadIdx.x == 0) {
-        __threadfence();
-        if (atomicAdd(&ctr->done_runs, 1) == (int)gridDim.x - 1) {
-            ctr->done_runs = 0;
-            ctr->ticket_runs = 0;
-            ctr->epoch_upd = epoch;
-        }
-    }
+    upd_prologue_body<1024>(ws, n_runs, cell_start, cell_end, max_ports, gridDim.x);
 }
 
 #ifdef SPHBUF_TRACE
@@ -381,11 +316,11 @@ __global__ void __launch_bounds__(kThreads) k_upd_main(PartDev p, GridDev g, con
                     pz = __fsub_rn(pz, P.s[2]);
                     p.z[pi] = pz;
                 }
-                atomicAdd(&port_counts[k], 1);
+                atomicAdd(&ws.port_cnt[k], 1);
             }
             if (nlab[it] != INT_MIN) p.label[pi] = nlab[it];
             if (dl[it]) {
-                atomicAdd(&port_counts[max_ports + k], 1);
+                atomicAdd(&ws.port_cnt[max_ports + k], 1);
                 ++del_cnt;
                 del_min = pi < del_min ? pi : del_min;
             }
@@ -513,6 +448,8 @@ __global__ void __launch_bounds__(kThreads) k_upd_main(PartDev p, GridDev g, con
         ctr->n_stage = carry_in;
         ctr->done_upd = 0;
     }
+    // the per-port counts (accumulated in the workspace) to the caller's array
+    for (int i = threadIdx.x; i < 2 * max_ports; i += blockDim.x) port_counts[i] = __ldcg(ws.port_cnt + i);
 #ifdef SPHBUF_TRACE
     if (threadIdx.x == 0) g_trace_k[3] = gtimer();
 #endif
@@ -561,13 +498,14 @@ cudaError_t launch_register(const PartDev &p, const GridDev &g, const PortTable 
 
 cudaError_t launch_update(const PartDev &p, const GridDev &g, const PortTable &pt, const Workspace &ws, int n_runs,
                           const int *cell_start, const int *cell_end, int *port_counts, int carry, float cdt,
-                          cudaStream_t s, Launch *L)
+                          bool prologue_done, cudaStream_t s, Launch *L)
 {
-    L->before(s);
-    const int pro_blocks = n_runs > 0 ? (n_runs + 1023) / 1024 : 1;
-    launch_k(k_upd_prologue, dim3(pro_blocks), dim3(1024), 0, s, ws, n_runs, cell_start, cell_end, port_counts,
-             pt.max_ports);
-    L->after(s, KID_UPD_PROLOGUE);
+    if (!prologue_done) {
+        L->before(s);
+        const int pro_blocks = n_runs > 0 ? (n_runs + 1023) / 1024 : 1;
+        launch_k(k_upd_prologue, dim3(pro_blocks), dim3(1024), 0, s, ws, n_runs, cell_start, cell_end, pt.max_ports);
+        L->after(s, KID_UPD_PROLOGUE);
+    }
     static int grid = 0;
     if (!grid) grid = occ_grid(k_upd_main, kThreads);
     L->before(s);
