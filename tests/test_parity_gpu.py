@@ -262,3 +262,42 @@ def test_perm_outputs():
     assert int((~keep).sum()) == 40
     assert torch.equal(fin["id"][pk[keep].long()], upd["id"][keep])
     assert torch.all(pk[keep][1:] > pk[keep][:-1])
+
+
+def test_port_registered_between_build_and_update():
+    """The build runs the next update's prologue for the ports it knows; a port
+    registered after the build makes the update run its own prologue — the result
+    equals the oracle's with both ports."""
+    w = inputs.make("C2")
+    K = len(w.ports)
+    st = oracle.to_numpy_state(w.state)
+    oracle.register(st, w.grid, w.ports[0], 0)
+    bu = make_updater(w)
+    bu.load(w.state, w.next_id)
+
+    def reg(k):
+        p = w.ports[k]
+        assert sphbuf.sph_buffer_register(bu.ctx, bu.A, p.origin, p.Q, p.half_extents, p.kind, p.layers, bu.dp,
+                                          bu.members[k:k + 1], None) == k
+
+    reg(0)
+    oracle.advect(st, 2, w.dt)
+    oracle.register(st, w.grid, w.ports[1], 1)     # port 1 identified at the advected positions
+    bu.advect(w.dt)
+    bu.cll_build()          # prologue inside the scatter: port 0's runs only
+    reg(1)                  # new runs: the update must not use that prologue
+    bu.update()
+    res = oracle.update(w.grid, w.ports, st)
+    new, perm, nid = oracle.compact(res, 2, K, res.port_counts[None, :], 0, w.next_id)
+    bu.compact()
+    assert (gpu_counts_to_oracle(bu.port_counts, K) == res.port_counts).all()
+    assert_state_equal(bu.state(), new, "after update")
+    # and a second step where the build's prologue applies again
+    oracle.advect(new, 2, w.dt)
+    res2 = oracle.update(w.grid, w.ports, new)
+    new2, _, nid = oracle.compact(res2, 2, K, res2.port_counts[None, :], 0, nid)
+    bu.cll_build(dt=w.dt)
+    bu.update()
+    bu.compact()
+    assert (gpu_counts_to_oracle(bu.port_counts, K) == res2.port_counts).all()
+    assert_state_equal(bu.state(), new2, "second update")
