@@ -94,6 +94,27 @@ __global__ void __launch_bounds__(kThreads) k_compact_count(PartDev p, Workspace
     }
 }
 
+#ifdef SPHBUF_TRACE
+// K7b sub-tile timeline (tools/upd_trace.py --move): ticket, loads + scan done,
+// predecessor wait done, end, block, SM.
+constexpr int kTraceMove = 1 << 17;
+__device__ unsigned long long g_trace_mv[kTraceMove][6];
+__device__ __forceinline__ unsigned long long gtimer3()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define MV_TRACE(slot)                                                                      \
+    do {                                                                                    \
+        if (threadIdx.x == 0 && u < kTraceMove) g_trace_mv[u][slot] = gtimer3();            \
+    } while (0)
+#else
+#define MV_TRACE(slot) \
+    do {               \
+    } while (0)
+#endif
+
 template <bool HasExtra>
 __global__ void __launch_bounds__(kThreads) k_compact_move(PartDev p, int dim, Workspace ws, int *perm, int carry)
 {
@@ -114,6 +135,15 @@ __global__ void __launch_bounds__(kThreads) k_compact_move(PartDev p, int dim, W
         __syncthreads();
         const long long u = s_tile;
         if (u >= nsub) break;
+        MV_TRACE(0);
+#ifdef SPHBUF_TRACE
+        if (threadIdx.x == 0 && u < kTraceMove) {
+            unsigned smid;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+            g_trace_mv[u][4] = blockIdx.x;
+            g_trace_mv[u][5] = smid;
+        }
+#endif
         bool alive[kCmpItems];
         float x[kCmpItems], y[kCmpItems], z[kCmpItems], vx[kCmpItems], vy[kCmpItems], vz[kCmpItems];
         float ex[kCmpItems][SPH_MAX_EXTRA];
@@ -160,6 +190,7 @@ __global__ void __launch_bounds__(kThreads) k_compact_move(PartDev p, int dim, W
         s_sink = dep;
         unsigned excl[kCmpItems], total;
         striped_scan<kThreads, kCmpItems>(alive, excl, total, s_cnt);   // contains __syncthreads
+        MV_TRACE(1);
         const long long start = ibeg + u * kCmpTile;
         const long long dst0 = start - (long long)ws.sub_off[u];
         if (threadIdx.x < 32) {
@@ -186,6 +217,7 @@ __global__ void __launch_bounds__(kThreads) k_compact_move(PartDev p, int dim, W
             __syncwarp();
         }
         __syncthreads();
+        MV_TRACE(2);
 #pragma unroll
         for (int it = 0; it < kCmpItems; ++it) {
             const long long i = start + it * kThreads + threadIdx.x;
@@ -210,9 +242,25 @@ __global__ void __launch_bounds__(kThreads) k_compact_move(PartDev p, int dim, W
             if (carry) ws.key[o] = kc[it];
             if (perm) perm[i] = (int)o;
         }
+        MV_TRACE(3);
         __syncthreads();
     }
 }
+
+#ifdef SPHBUF_TRACE
+}  // namespace sphbuf
+extern "C" int sph_trace_move(unsigned long long *host, int max_tiles, int reset)
+{
+    const int n = max_tiles < sphbuf::kTraceMove ? max_tiles : sphbuf::kTraceMove;
+    cudaError_t e = cudaMemcpyFromSymbol(host, sphbuf::g_trace_mv, sizeof(unsigned long long) * 6 * n);
+    if (reset) {
+        static unsigned long long zero[sphbuf::kTraceMove][6];
+        cudaMemcpyToSymbol(sphbuf::g_trace_mv, zero, sizeof(zero));
+    }
+    return (int)e;
+}
+namespace sphbuf {
+#endif
 
 // Staged particles after the survivors with IDs from the count matrix (reading
 // R14, §8(e)): off(k, r) = next_id + sum_{k'<k} sum_r' C[r'][k'] + sum_{r'<r} C[r'][k];
