@@ -282,8 +282,9 @@ sph_status sph_cll_finish(sph_ctx *ctx, sph_particles *in, sph_particles *out, c
  *   outlet k        (Alg. 2): X'_0 > a/2             -> DELETE
  *   bidirectional k (Alg. 3): label k and X'_0 > a/2 -> CREATE,
  *                                        label k and X'_0 < -a/2 -> DELETE
- * CREATE stages a bitwise copy of the state in canonical order
- * (port, cell, id) and recycles the particle x <- fl(x - fl(a u))
+ * CREATE stages a bitwise copy of the state together with its rank in
+ * the canonical order (port, cell, id) — the compaction appends the staged
+ * particles in that order — and recycles the particle x <- fl(x - fl(a u))
  * (Eqs. 2D/3D_Inverse_transformation).  DELETE writes a tombstone.
  * Outlet and bidirectional ports then relabel their non-deleted candidates on
  * post-recycle positions.
