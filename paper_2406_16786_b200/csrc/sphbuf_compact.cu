@@ -262,6 +262,153 @@ extern "C" int sph_trace_move(unsigned long long *host, int max_tiles, int reset
 namespace sphbuf {
 #endif
 
+// K7b, two sub-tiles per block in flight (no extra columns): the next sub-tile's
+// loads are issued before waiting for the current one's predecessors, so that
+// wait (their load-time variance) overlaps memory work instead of idling the
+// block.  Progress: a block publishes "read done" for a sub-tile as soon as its
+// loads returned and waits only on smaller sub-tiles; the smallest sub-tile any
+// block is storing has all predecessors published.
+struct MoveTile {
+    float x[kCmpItems], y[kCmpItems], z[kCmpItems], vx[kCmpItems], vy[kCmpItems], vz[kCmpItems];
+    long long id[kCmpItems];
+    int lab[kCmpItems], kc[kCmpItems];
+};
+
+__device__ __forceinline__ void move_load(const PartDev &p, int dim, const Workspace &ws, int carry, long long base,
+                                          long long N, MoveTile &t)
+{
+#pragma unroll
+    for (int it = 0; it < kCmpItems; ++it) {
+        const long long i = base + it * kThreads + threadIdx.x;
+        t.lab[it] = -3;
+        t.kc[it] = 0;
+        t.x[it] = t.y[it] = t.z[it] = t.vx[it] = t.vy[it] = t.vz[it] = 0.0f;
+        t.id[it] = 0;
+        if (i < N) {
+            t.lab[it] = p.label[i];
+            t.kc[it] = carry ? ws.key[i] : 0;
+            t.x[it] = p.x[i];
+            t.y[it] = p.y[i];
+            t.vx[it] = p.vx[i];
+            t.vy[it] = p.vy[i];
+            if (dim == 3) {
+                t.z[it] = p.z[i];
+                t.vz[it] = p.vz[i];
+            } else {
+                t.z[it] = t.vz[it] = 0.0f;
+            }
+            t.id[it] = p.id[i];
+        }
+    }
+}
+
+// Consume every loaded word (so the loads have returned), rank the survivors.
+__device__ __forceinline__ void move_rank(const MoveTile &t, unsigned (&excl)[kCmpItems], bool (&alive)[kCmpItems],
+                                          unsigned &total, unsigned *s_cnt, volatile int *s_sink)
+{
+    int dep = 0;
+#pragma unroll
+    for (int it = 0; it < kCmpItems; ++it) {
+        alive[it] = t.lab[it] > -2;
+        dep ^= t.lab[it] ^ t.kc[it] ^ __float_as_int(t.x[it]) ^ __float_as_int(t.y[it]) ^ __float_as_int(t.z[it]) ^
+               __float_as_int(t.vx[it]) ^ __float_as_int(t.vy[it]) ^ __float_as_int(t.vz[it]) ^ (int)t.id[it] ^
+               (int)(t.id[it] >> 32);
+    }
+    *s_sink = dep;
+    striped_scan<kThreads, kCmpItems>(alive, excl, total, s_cnt);   // contains __syncthreads
+}
+
+__global__ void __launch_bounds__(kThreads) k_compact_move2(PartDev p, int dim, Workspace ws, int *perm, int carry)
+{
+    pdl_entry();
+    __shared__ unsigned s_cnt[kCmpItems * kThreads / 32 + 1];
+    __shared__ long long s_tile;
+    __shared__ volatile int s_sink;
+    Counters *ctr = ws.ctr;
+    const long long D = ctr->n_del;
+    if (D == 0) return;
+    const long long N = ctr->cmp_n;
+    const long long ibeg = cmp_begin(ctr->i_first);
+    const unsigned epoch = ctr->epoch_cmp;
+    const long long nsub = (N - ibeg + kCmpTile - 1) / kCmpTile;
+    auto ticket = [&]() -> long long {
+        if (threadIdx.x == 0) s_tile = atomicAdd(&ctr->ticket_cmp2, 1);
+        __syncthreads();
+        const long long t = s_tile;
+        __syncthreads();
+        return t;
+    };
+    auto publish = [&](long long u) {
+        if (threadIdx.x == 0)
+            asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(ws.rd + u), "r"(epoch) : "memory");
+    };
+    MoveTile A, B;
+    unsigned exA[kCmpItems], exB[kCmpItems], totA, totB;
+    bool alA[kCmpItems], alB[kCmpItems];
+    long long u = ticket();
+    if (u >= nsub) return;
+    move_load(p, dim, ws, carry, ibeg + u * kCmpTile, N, A);
+    move_rank(A, exA, alA, totA, s_cnt, &s_sink);
+    publish(u);
+    while (true) {
+        // the next sub-tile's loads go out first ...
+        const long long u2 = ticket();
+        const bool more = u2 < nsub;
+        if (more) move_load(p, dim, ws, carry, ibeg + u2 * kCmpTile, N, B);
+        // ... then wait for the earlier sub-tiles whose input this output overlaps
+        const long long start = ibeg + u * kCmpTile;
+        const long long dst0 = start - (long long)ws.sub_off[u];
+        if (threadIdx.x < 32) {
+            if (totA > 0 && dst0 < start) {
+                const long long vlo = (dst0 - ibeg) / kCmpTile;
+                long long vhi = (dst0 + totA - 1 - ibeg) / kCmpTile;
+                if (vhi > u - 1) vhi = u - 1;
+                for (long long v = vlo + threadIdx.x; v <= vhi; v += 32) {
+                    unsigned f;
+                    do {
+                        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(ws.rd + v) : "memory");
+                    } while (f != epoch);
+                }
+            }
+            __syncwarp();
+        }
+        __syncthreads();
+#pragma unroll
+        for (int it = 0; it < kCmpItems; ++it) {
+            const long long i = start + it * kThreads + threadIdx.x;
+            if (i >= N) continue;
+            if (!alA[it]) {
+                if (perm) perm[i] = -1;
+                continue;
+            }
+            const long long o = dst0 + exA[it];
+            p.x[o] = A.x[it];
+            p.y[o] = A.y[it];
+            p.vx[o] = A.vx[it];
+            p.vy[o] = A.vy[it];
+            if (dim == 3) {
+                p.z[o] = A.z[it];
+                p.vz[o] = A.vz[it];
+            }
+            p.id[o] = A.id[it];
+            p.label[o] = A.lab[it];
+            if (carry) ws.key[o] = A.kc[it];
+            if (perm) perm[i] = (int)o;
+        }
+        if (!more) break;
+        move_rank(B, exB, alB, totB, s_cnt, &s_sink);
+        publish(u2);
+        u = u2;
+        A = B;
+        totA = totB;
+#pragma unroll
+        for (int it = 0; it < kCmpItems; ++it) {
+            exA[it] = exB[it];
+            alA[it] = alB[it];
+        }
+    }
+}
+
 // Staged particles after the survivors with IDs from the count matrix (reading
 // R14, §8(e)): off(k, r) = next_id + sum_{k'<k} sum_r' C[r'][k'] + sum_{r'<r} C[r'][k];
 // identity perm below i_first; then N and next_id.
@@ -380,9 +527,16 @@ cudaError_t launch_compact(const PartDev &p, const GridDev &g, const PortTable &
                  carry);
     } else {
         static int grid = 0;
-        if (!grid) grid = occ_grid(k_compact_move<false>, kThreads);
-        launch_k(k_compact_move<false>, dim3(cap_grid(grid, p.cap, kCmpTile)), dim3(kThreads), 0, s, p, dim, ws, perm,
-                 carry);
+        static const bool one = getenv("SPHBUF_MOVE1") != nullptr;   // A/B: one sub-tile in flight
+        if (one) {
+            if (!grid) grid = occ_grid(k_compact_move<false>, kThreads);
+            launch_k(k_compact_move<false>, dim3(cap_grid(grid, p.cap, kCmpTile)), dim3(kThreads), 0, s, p, dim, ws,
+                     perm, carry);
+        } else {
+            if (!grid) grid = occ_grid(k_compact_move2, kThreads);
+            launch_k(k_compact_move2, dim3(cap_grid(grid, p.cap, kCmpTile)), dim3(kThreads), 0, s, p, dim, ws, perm,
+                     carry);
+        }
     }
     L->after(s, KID_COMPACT);
     L->before(s);
