@@ -2,6 +2,8 @@
 // a7; north star: "removed by a scan-based stream compaction with an
 // ID/permutation remap").  Only the suffix [i_first, N) after the lowest deleted
 // index moves.
+//   K7s k_compact_sort   the update's deleted positions sorted in shared memory
+//                        (when at most kDelList); then K7a needs no label pass;
 //   K7a k_compact_count  labels only: per 8192-element tile the number of
 //                        tombstones, decoupled look-back scan over tiles, and the
 //                        exclusive tombstone count before every 1024-element
@@ -30,6 +32,42 @@ static_assert(kCntSub == kThreads / 32, "one warp per compaction sub-tile");
 // are rewritten onto themselves).
 __device__ __forceinline__ long long cmp_begin(long long i_first) { return (i_first / kCntTile) * kCntTile; }
 
+// K7s: the update's deleted positions sorted (one block, bitonic in shared memory)
+// when there are at most kDelList of them; K7a then finds every sub-tile's
+// tombstone offset by binary search in the sorted list instead of reading the
+// suffix's labels.
+__global__ void __launch_bounds__(1024) k_compact_sort(Workspace ws)
+{
+    pdl_entry();
+    __shared__ int s[kDelList];
+    Counters *ctr = ws.ctr;
+    const long long D = ctr->n_dlist;
+    if (D == 0 || D > kDelList || D != ctr->n_del) {
+        if (threadIdx.x == 0) ctr->dsort_ok = 0;
+        return;
+    }
+    int P = 32;
+    while (P < D) P <<= 1;
+    for (int i = threadIdx.x; i < P; i += 1024) s[i] = i < D ? ws.del_list[i] : INT_MAX;
+    __syncthreads();
+    for (int k = 2; k <= P; k <<= 1)
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < P; i += 1024) {
+                const int l = i ^ j;
+                if (l > i) {
+                    const int a = s[i], b = s[l];
+                    if ((a > b) == ((i & k) == 0)) {
+                        s[i] = b;
+                        s[l] = a;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    for (int i = threadIdx.x; i < D; i += 1024) ws.del_sorted[i] = s[i];
+    if (threadIdx.x == 0) ctr->dsort_ok = 1;
+}
+
 __global__ void __launch_bounds__(kThreads) k_compact_count(PartDev p, Workspace ws, const long long *next_id)
 {
     pdl_entry();
@@ -46,6 +84,22 @@ __global__ void __launch_bounds__(kThreads) k_compact_count(PartDev p, Workspace
     }
     if (D == 0) return;
     const long long ibeg = cmp_begin(ctr->i_first);
+    if (ctr->dsort_ok) {
+        // tombstones before sub-tile u = deleted positions below its start
+        const long long nsub = (N - ibeg + kCmpTile - 1) / kCmpTile;
+        for (long long u = (long long)blockIdx.x * blockDim.x + threadIdx.x; u < nsub;
+             u += (long long)gridDim.x * blockDim.x) {
+            const long long start = ibeg + u * kCmpTile;
+            int lo = 0, hi = (int)D;                   // first sorted position >= start
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (__ldg(ws.del_sorted + mid) < start) lo = mid + 1;
+                else hi = mid;
+            }
+            ws.sub_off[u] = (unsigned)lo;
+        }
+        return;
+    }
     const unsigned epoch = ctr->epoch_cmp;
     const long long ntiles = (N - ibeg + kCntTile - 1) / kCntTile;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -512,6 +566,9 @@ cudaError_t launch_compact(const PartDev &p, const GridDev &g, const PortTable &
         return cudaGetLastError();
     }
     const int dim = g.dim;
+    L->before(s);
+    launch_k(k_compact_sort, dim3(1), dim3(1024), 0, s, ws);
+    L->after(s, KID_COMPACT_SORT);
     {
         static int grid = 0;
         if (!grid) grid = occ_grid(k_compact_count, kThreads);

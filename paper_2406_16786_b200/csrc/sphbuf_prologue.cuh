@@ -33,6 +33,7 @@ __device__ __forceinline__ void upd_prologue_body(const Workspace &ws, int n_run
             ctr->ticket_upd = 0;
             ctr->n_stage = 0;
             ctr->n_stage_raw = 0;
+            ctr->n_dlist = 0;
             ctr->n_del = 0;
             ctr->i_first = LLONG_MAX;
         }

@@ -280,6 +280,21 @@ __global__ void __launch_bounds__(kThreads) k_upd_main(PartDev p, GridDev g, con
             bY[it] = Xp[1];
             bZ[it] = Xp[2];
         }
+        // deleted positions listed (warp-aggregated) for the in-place compaction,
+        // which derives its sub-tile offsets from them instead of a label pass
+#pragma unroll
+        for (int it = 0; it < kUpdItems; ++it) {
+            const unsigned m = __ballot_sync(0xffffffffu, dl[it]);
+            if (!m) continue;
+            const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+            long long b0 = 0;
+            if (lane == leader) b0 = (long long)atomicAdd((unsigned long long *)&ctr->n_dlist, (unsigned long long)__popc(m));
+            b0 = __shfl_sync(0xffffffffu, b0, leader);
+            if (dl[it]) {
+                const long long slot = b0 + __popc(m & lanemask_lt());
+                if (slot < kDelList) ws.del_list[slot] = pidx[it];
+            }
+        }
         // (C) loads for the duplicates and boundary conditions (pre-BC velocity)
         float vx[kUpdItems], vy[kUpdItems], vz[kUpdItems];
         long long sid[kUpdItems];

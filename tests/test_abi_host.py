@@ -31,6 +31,19 @@ def test_library_exports_every_declared_symbol():
     assert sorted(sphbuf.EXPORTS) == syms
 
 
+def test_kernel_id_table_matches_header():
+    """sph_profile_read fills SPH_NKERNELS entries: the binding's array size, the
+    header's constant and the library's kernel-name table must agree."""
+    import re
+    hdr = open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include", "sphbuf.h")).read()
+    n = int(re.search(r"#define SPH_NKERNELS (\d+)", hdr).group(1))
+    assert sphbuf.NKERNELS == n
+    L = sphbuf.lib()
+    names = [L.sph_kernel_name(i).decode() for i in range(n + 1)]
+    assert all(names[:n]) and names[n] == ""
+    assert len(set(names[:n])) == n
+
+
 def test_library_is_sm100a():
     out = os.popen(f"/usr/local/cuda/bin/cuobjdump --list-elf {sphbuf.lib()._name}").read()
     assert "sm_100a" in out
