@@ -66,6 +66,22 @@ __global__ void make_src(int *src, long long n, int shuffle)
     }
 }
 
+// columns carved from one allocation, column k starting k * stagger bytes past a
+// multiple of the column size (stagger < 0: separate cudaMalloc per column)
+static Cols alloc_cols_stag(long long n, long long stagger)
+{
+    const long long col = ((8 * n + (1 << 21) - 1) >> 21) << 21;   // 2 MB-rounded column slot
+    char *base;
+    cudaMalloc(&base, 8 * col + 8 * stagger + 4096);
+    cudaMemset(base, 0, 8 * col + 8 * stagger + 4096);
+    auto at = [&](int k) { return base + k * col + k * stagger; };
+    Cols c;
+    c.x = (float *)at(0); c.y = (float *)at(1); c.z = (float *)at(2);
+    c.vx = (float *)at(3); c.vy = (float *)at(4); c.vz = (float *)at(5);
+    c.id = (long long *)at(6); c.label = (int *)at(7);
+    return c;
+}
+
 static Cols alloc_cols(long long n)
 {
     Cols c;
@@ -125,6 +141,22 @@ int main()
             printf("SoA gather (%s map, 4 slots/thread, 4 blocks/SM): %.3f ms, %.0f GB/s of 80 B/particle\n",
                    shuffle ? "tile-shuffled" : "identity", ms, 80.0 * n / ms / 1e6);
         }
+    }
+    make_src<<<sms * 8, 256>>>(src, n, 0);
+    const long long staggers[] = {0, 256, 1024, 4096, 65536, 1 << 20};
+    for (long long st : staggers) {
+        Cols a2 = alloc_cols_stag(n, st), b2 = alloc_cols_stag(n, st + 128);
+        for (int r = 0; r < 2; ++r) {
+            cudaEventRecord(e0);
+            soa_gather<2><<<sms * 5, 256>>>(a2, b2, src, key, n);
+            cudaEventRecord(e1);
+            cudaEventSynchronize(e1);
+            cudaEventElapsedTime(&ms, e0, e1);
+            printf("one allocation, column stagger %lld B (out +128): identity map %.3f ms, %.0f GB/s\n", st, ms,
+                   80.0 * n / ms / 1e6);
+        }
+        cudaFree(a2.x);
+        cudaFree(b2.x);
     }
     printf("%s\n", cudaGetErrorString(cudaGetLastError()));
     return 0;
