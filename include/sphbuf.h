@@ -334,7 +334,7 @@ int64_t sph_launch_count(const sph_ctx *ctx);
  * totals; sph_profile_read waits for the last event and returns, per kernel id
  * (0 .. SPH_NKERNELS-1, named by sph_kernel_name), the summed milliseconds and
  * the number of launches.  ms, count: host arrays of SPH_NKERNELS. */
-#define SPH_NKERNELS 18
+#define SPH_NKERNELS 17
 sph_status sph_profile(sph_ctx *ctx, int32_t enable);
 sph_status sph_profile_read(sph_ctx *ctx, double *ms, int64_t *count);
 const char *sph_kernel_name(int32_t i);

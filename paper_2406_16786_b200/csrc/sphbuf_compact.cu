@@ -2,9 +2,9 @@
 // a7; north star: "removed by a scan-based stream compaction with an
 // ID/permutation remap").  Only the suffix [i_first, N) after the lowest deleted
 // index moves.
-//   K7s k_compact_sort   the update's deleted positions sorted in shared memory
-//                        (when at most kDelList); then K7a needs no label pass;
-//   K7a k_compact_count  labels only: per 8192-element tile the number of
+//   K7a k_compact_count  from the update's list of deleted positions (when at most
+//                        kDelList): per-range shared-memory counts, no label pass;
+//                        else labels only: per 8192-element tile the number of
 //                        tombstones, decoupled look-back scan over tiles, and the
 //                        exclusive tombstone count before every 1024-element
 //                        sub-tile (sub_off);
@@ -32,43 +32,14 @@ static_assert(kCntSub == kThreads / 32, "one warp per compaction sub-tile");
 // are rewritten onto themselves).
 __device__ __forceinline__ long long cmp_begin(long long i_first) { return (i_first / kCntTile) * kCntTile; }
 
-// K7s: the update's deleted positions sorted (one block, bitonic in shared memory)
-// when there are at most kDelList of them; K7a then finds every sub-tile's
-// tombstone offset by binary search in the sorted list instead of reading the
-// suffix's labels.
-__global__ void __launch_bounds__(1024) k_compact_sort(Workspace ws)
-{
-    pdl_entry();
-    __shared__ int s[kDelList];
-    Counters *ctr = ws.ctr;
-    const long long D = ctr->n_dlist;
-    if (D == 0 || D > kDelList || D != ctr->n_del) {
-        if (threadIdx.x == 0) ctr->dsort_ok = 0;
-        return;
-    }
-    int P = 32;
-    while (P < D) P <<= 1;
-    for (int i = threadIdx.x; i < P; i += 1024) s[i] = i < D ? ws.del_list[i] : INT_MAX;
-    __syncthreads();
-    for (int k = 2; k <= P; k <<= 1)
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            for (int i = threadIdx.x; i < P; i += 1024) {
-                const int l = i ^ j;
-                if (l > i) {
-                    const int a = s[i], b = s[l];
-                    if ((a > b) == ((i & k) == 0)) {
-                        s[i] = b;
-                        s[l] = a;
-                    }
-                }
-            }
-            __syncthreads();
-        }
-    for (int i = threadIdx.x; i < D; i += 1024) ws.del_sorted[i] = s[i];
-    if (threadIdx.x == 0) ctr->dsort_ok = 1;
-}
+// K7a with the update's list of deleted positions (K6; complete when at most
+// kDelList): each block takes a range of kCntRange sub-tiles, counts the listed
+// positions below the range and, in shared memory, per sub-tile inside it, and
+// scans — no pass over the suffix's labels, no sort.  Otherwise the label pass.
+constexpr int kCntRange = 4096;
 
-__global__ void __launch_bounds__(kThreads) k_compact_count(PartDev p, Workspace ws, const long long *next_id)
+__global__ void __launch_bounds__(kThreads) k_compact_count(PartDev p, Workspace ws, const long long *next_id,
+                                                            int dlist_max)
 {
     pdl_entry();
     __shared__ unsigned s_sub[kCntSub][kThreads / 32];
@@ -84,19 +55,43 @@ __global__ void __launch_bounds__(kThreads) k_compact_count(PartDev p, Workspace
     }
     if (D == 0) return;
     const long long ibeg = cmp_begin(ctr->i_first);
-    if (ctr->dsort_ok) {
-        // tombstones before sub-tile u = deleted positions below its start
+    const long long DL = ctr->n_dlist;
+    if (DL == D && D <= dlist_max) {
+        __shared__ unsigned s_c[kCntRange];
+        __shared__ unsigned s_below;
+        __shared__ unsigned s_scan[kThreads / 32 + 1];
         const long long nsub = (N - ibeg + kCmpTile - 1) / kCmpTile;
-        for (long long u = (long long)blockIdx.x * blockDim.x + threadIdx.x; u < nsub;
-             u += (long long)gridDim.x * blockDim.x) {
-            const long long start = ibeg + u * kCmpTile;
-            int lo = 0, hi = (int)D;                   // first sorted position >= start
-            while (lo < hi) {
-                const int mid = (lo + hi) >> 1;
-                if (__ldg(ws.del_sorted + mid) < start) lo = mid + 1;
-                else hi = mid;
+        for (long long u0 = (long long)blockIdx.x * kCntRange; u0 < nsub; u0 += (long long)gridDim.x * kCntRange) {
+            for (int i = threadIdx.x; i < kCntRange; i += blockDim.x) s_c[i] = 0;
+            if (threadIdx.x == 0) s_below = 0;
+            __syncthreads();
+            const long long lo = ibeg + u0 * kCmpTile, hi = lo + (long long)kCntRange * kCmpTile;
+            unsigned below = 0;
+            for (int q = threadIdx.x; q < (int)D; q += blockDim.x) {
+                const long long pos = __ldg(ws.del_list + q);
+                if (pos < lo) ++below;
+                else if (pos < hi) atomicAdd(&s_c[(pos - lo) / kCmpTile], 1u);
             }
-            ws.sub_off[u] = (unsigned)lo;
+            below = warp_sum(below);
+            if ((threadIdx.x & 31) == 0 && below) atomicAdd(&s_below, below);
+            __syncthreads();
+            // exclusive scan of the range's counts, kCntRange / kThreads per thread
+            constexpr int PER = kCntRange / kThreads;
+            unsigned loc[PER], sum = 0;
+#pragma unroll
+            for (int e = 0; e < PER; ++e) {
+                loc[e] = s_c[threadIdx.x * PER + e];
+                sum += loc[e];
+            }
+            unsigned tot;
+            unsigned run = block_excl_scan<kThreads>(sum, tot, s_scan) + s_below;
+#pragma unroll
+            for (int e = 0; e < PER; ++e) {
+                const long long u = u0 + threadIdx.x * PER + e;
+                if (u < nsub) ws.sub_off[u] = run;
+                run += loc[e];
+            }
+            __syncthreads();
         }
         return;
     }
@@ -566,14 +561,18 @@ cudaError_t launch_compact(const PartDev &p, const GridDev &g, const PortTable &
         return cudaGetLastError();
     }
     const int dim = g.dim;
-    L->before(s);
-    launch_k(k_compact_sort, dim3(1), dim3(1024), 0, s, ws);
-    L->after(s, KID_COMPACT_SORT);
+    // SPHBUF_DLIST_MAX=<n> lowers the list size above which the label pass is used
+    // (tests force the fallback with 0)
+    static const int dmax = [] {
+        const char *e = getenv("SPHBUF_DLIST_MAX");
+        const int v = e ? atoi(e) : kDelList;
+        return v < kDelList ? v : kDelList;
+    }();
     {
         static int grid = 0;
         if (!grid) grid = occ_grid(k_compact_count, kThreads);
         L->before(s);
-        launch_k(k_compact_count, dim3(cap_grid(grid, p.cap, kCntTile)), dim3(kThreads), 0, s, p, ws, next_id);
+        launch_k(k_compact_count, dim3(cap_grid(grid, p.cap, kCntTile)), dim3(kThreads), 0, s, p, ws, next_id, dmax);
         L->after(s, KID_COMPACT_COUNT);
     }
     L->before(s);

@@ -159,7 +159,6 @@ size_t layout(const sph_ctx *c, char *base, Workspace *W)
     w.drv_rho = (float *)take(sizeof(float) * SPH_MAX_PORTS);
     w.port_cnt = (int *)take(sizeof(int) * 2 * SPH_MAX_PORTS);
     w.del_list = (int *)take(sizeof(int) * kDelList);
-    w.del_sorted = (int *)take(sizeof(int) * kDelList);
     w.run_off = (long long *)take(sizeof(long long) * (kMaxRuns + 1));
     const size_t zero_end = off;   // everything above must start zeroed
     w.sub_off = (unsigned *)take(4 * cmp_subs);
@@ -1115,7 +1114,7 @@ int64_t sph_launch_count(const sph_ctx *c) { return c ? c->L.count : 0; }
 static const char *kKernelNames[KID_COUNT] = {
     "advect", "register", "cll_key", "cell_scan", "cll_scatter", "cll_gather", "upd_prologue",
     "upd_main", "compact", "compact_append", "mig_pack", "mig_unpack", "compact_count", "cll_rank",
-    "port_move", "port_enum", "drivers", "compact_sort"};
+    "port_move", "port_enum", "drivers"};
 static_assert(KID_COUNT == SPH_NKERNELS, "sphbuf.h SPH_NKERNELS must match the kernel ids");
 
 const char *sph_kernel_name(int32_t i) { return (i >= 0 && i < KID_COUNT) ? kKernelNames[i] : ""; }

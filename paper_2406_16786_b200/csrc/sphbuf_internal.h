@@ -19,7 +19,7 @@ constexpr int kCellTile = kThreads * kCellItems;
 constexpr int kCellItemsBig = 128;       // ... or this many above kScanBigCells cells (one wave of tiles)
 constexpr int kCellTileBig = kThreads * kCellItemsBig;
 constexpr long long kScanBigCells = 4LL << 20;
-constexpr int kDelList = 8192;           // deletions sorted for the in-place compaction's offsets
+constexpr int kDelList = 8192;           // deletions listed for the in-place compaction's offsets
 constexpr int kUpdItems = 2;             // candidates per thread in the update
 constexpr int kUpdTile = kThreads * kUpdItems;
 constexpr int kCmpItems = 4;             // particles per thread in the compaction
@@ -140,7 +140,6 @@ struct Counters {
     int done_app;          // compaction append: finished blocks
     int done_runs;         // update prologue: finished blocks
     int done_upd;          // update: finished blocks (the last one scans the tile counts)
-    int dsort_ok;          // compaction: the deletion list is complete and sorted
     int dummy;
 };
 
@@ -162,7 +161,7 @@ struct Workspace {
     DriverDev *drv;                  // [SPH_MAX_PORTS]: Windkessel state
     float *drv_rho;                  // [SPH_MAX_PORTS]: recycled density of driven pressure BCs
     int *port_cnt;                   // [2 SPH_MAX_PORTS]: this update's created / deleted per port
-    int *del_list, *del_sorted;      // [kDelList]: this update's deleted positions (K6), sorted (K7s)
+    int *del_list;                   // [kDelList]: this update's deleted positions (K6)
     long long *run_off;              // [kMaxRuns + 1]
     int *run_base;                   // [kMaxRuns]: first particle index of each run
     int *tile_run;                   // [upd tiles]: run holding the first candidate of each K6 tile
@@ -182,7 +181,7 @@ struct Workspace {
 enum KernelId {
     KID_ADVECT, KID_REGISTER, KID_CLL_KEY, KID_CELL_SCAN, KID_CLL_SCATTER, KID_CLL_GATHER, KID_UPD_PROLOGUE,
     KID_UPD_MAIN, KID_COMPACT, KID_COMPACT_APPEND, KID_MIG_PACK, KID_MIG_UNPACK, KID_COMPACT_COUNT, KID_CLL_RANK,
-    KID_PORT_MOVE, KID_PORT_ENUM, KID_DRIVERS, KID_COMPACT_SORT, KID_COUNT
+    KID_PORT_MOVE, KID_PORT_ENUM, KID_DRIVERS, KID_COUNT
 };
 
 // Counts launches; when profiling is on, brackets every launch with a pair of

@@ -70,7 +70,7 @@ EXPORTS = ["sph_ctx_create", "sph_ctx_destroy", "sph_last_error", "sph_workspace
            "sph_kernel_name", "sph_advect_cll_build", "sph_compact_deferred", "sph_cll_key", "sph_cll_finish",
            "sph_port_set_bc", "sph_port_move", "sph_port_set_driver", "sph_cll_invalidate",
            "sph_drivers_step", "sph_driver_read"]
-NKERNELS = 18                       # = SPH_NKERNELS in include/sphbuf.h
+NKERNELS = 17                       # = SPH_NKERNELS in include/sphbuf.h
 
 
 def lib():
