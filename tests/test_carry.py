@@ -63,3 +63,24 @@ def test_carry_survives_any_call_sequence():
     bu.cll_build()
     fin = oracle.update(w.grid, [], st)
     assert_state_equal(bu.state(), {c: v[fin.order] for c, v in st.items() if c != "extra"}, "final")
+
+
+@pytest.mark.gpu
+def test_inplace_compaction_label_pass_fallback():
+    """The in-place compaction's offsets come from the update's deletion list when it
+    is complete; with the list disabled (SPHBUF_DLIST_MAX=0, read once per process,
+    hence a subprocess) the label-pass fallback must give the same bit-exact result."""
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    code = ("import sys; sys.path.insert(0, %r); sys.path.insert(0, %r)\n"
+            "from paper_2406_16786_b200 import inputs\n"
+            "from parity_util import lockstep\n"
+            "w = inputs.c4(scale=0.25, nports=4, n_updates=6)\n"
+            "tot, bu = lockstep(w, 6, check_every=1, fused=True, deferred=False)\n"
+            "assert tot[1] > 0\n"
+            "print('ok')\n") % (os.path.dirname(here), here)
+    env = dict(os.environ, SPHBUF_DLIST_MAX="0")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
