@@ -451,12 +451,22 @@ __global__ void __launch_bounds__(kThreads) k_upd_main(PartDev p, GridDev g, con
     __threadfence();
     const long long nt = ntiles < ws.upd_tiles ? ntiles : ws.upd_tiles;
     unsigned carry_in = 0;
-    for (long long b0 = 0; b0 < nt; b0 += kThreads) {
-        const long long t = b0 + threadIdx.x;
-        const unsigned c = t < nt ? __ldcg(ws.tile_cr + t) : 0u;
+    // kPer consecutive tile counts per thread, all loaded before any is used
+    constexpr int kPer = 8;
+    for (long long b0 = 0; b0 < nt; b0 += (long long)kThreads * kPer) {
+        const long long t0 = b0 + (long long)threadIdx.x * kPer;
+        unsigned c[kPer], sum = 0;
+#pragma unroll
+        for (int e = 0; e < kPer; ++e) c[e] = t0 + e < nt ? __ldcg(ws.tile_cr + t0 + e) : 0u;
+#pragma unroll
+        for (int e = 0; e < kPer; ++e) sum += c[e];
         unsigned tot;
-        const unsigned ex = block_excl_scan<kThreads>(c, tot, s_warp);
-        if (t < nt) ws.tile_pre[t] = carry_in + ex;
+        unsigned run = carry_in + block_excl_scan<kThreads>(sum, tot, s_warp);
+#pragma unroll
+        for (int e = 0; e < kPer; ++e) {
+            if (t0 + e < nt) ws.tile_pre[t0 + e] = run;
+            run += c[e];
+        }
         carry_in += tot;
     }
     if (threadIdx.x == 0) {
