@@ -280,12 +280,14 @@ def run_ours(args):
                        "particles_per_gpu": n0, "ports": n_ports, "candidates_per_step": cand,
                        "created_last": created, "deleted_last": deleted, "dim": dim,
                        "parallelism": f"x-slab dp{world}", "l2": "inputs (>=4.6 GB/GPU) larger than L2; no flush",
-                       "compaction": args.compaction, "advection": "fused into the cell-list key pass" if world == 1
-                       else "separate (before migration)",
+                       "compaction": args.compaction,
+                       "advection": "fused into the cell-list build (the gather advects; next keys carried over)",
                        "gen_s": round(tgen, 1)},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak if achieved else None, "traffic": traffic,
-                         "peak_source": peak_src, "alg_bytes_per_launch": bytes_dom, "ms_per_launch": dom_ms},
+                         "peak_source": peak_src, "alg_bytes_per_launch": bytes_dom, "ms_per_launch": dom_ms,
+                         "note": "a no-compute copy with the gather's access pattern (80 B/particle through the "
+                                 "slot map) takes 1.9-2.06 ms at C5 (tools/soa_copy_probe.cu, DESIGN.md section 6)"},
             "kernels": kernels,
             "phases": phases,
             "other_compaction_mode": alt,
