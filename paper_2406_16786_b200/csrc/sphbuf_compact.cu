@@ -154,13 +154,25 @@ __device__ __forceinline__ unsigned long long gtimer3()
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
-#define MV_TRACE(slot)                                                                      \
+#define MV_TRACE(slot) MV_TRACE_U(u, slot)
+#define MV_TRACE_U(uu, slot)                                                                \
     do {                                                                                    \
-        if (threadIdx.x == 0 && u < kTraceMove) g_trace_mv[u][slot] = gtimer3();            \
+        if (threadIdx.x == 0 && (uu) < kTraceMove) {                                       \
+            g_trace_mv[(uu)][slot] = gtimer3();                                             \
+            if ((slot) == 0) {                                                              \
+                unsigned smid_;                                                             \
+                asm volatile("mov.u32 %0, %%smid;" : "=r"(smid_));                          \
+                g_trace_mv[(uu)][4] = blockIdx.x;                                           \
+                g_trace_mv[(uu)][5] = smid_;                                                \
+            }                                                                               \
+        }                                                                                   \
     } while (0)
 #else
 #define MV_TRACE(slot) \
     do {               \
+    } while (0)
+#define MV_TRACE_U(uu, slot) \
+    do {                     \
     } while (0)
 #endif
 
@@ -396,13 +408,16 @@ __global__ void __launch_bounds__(kThreads) k_compact_move2(PartDev p, int dim, 
     bool alA[kCmpItems], alB[kCmpItems];
     long long u = ticket();
     if (u >= nsub) return;
+    MV_TRACE_U(u, 0);
     move_load(p, dim, ws, carry, ibeg + u * kCmpTile, N, A);
     move_rank(A, exA, alA, totA, s_cnt, &s_sink);
     publish(u);
+    MV_TRACE_U(u, 1);
     while (true) {
         // the next sub-tile's loads go out first ...
         const long long u2 = ticket();
         const bool more = u2 < nsub;
+        if (more) MV_TRACE_U(u2, 0);
         if (more) move_load(p, dim, ws, carry, ibeg + u2 * kCmpTile, N, B);
         // ... then wait for the earlier sub-tiles whose input this output overlaps
         const long long start = ibeg + u * kCmpTile;
@@ -422,6 +437,7 @@ __global__ void __launch_bounds__(kThreads) k_compact_move2(PartDev p, int dim, 
             __syncwarp();
         }
         __syncthreads();
+        MV_TRACE_U(u, 2);
 #pragma unroll
         for (int it = 0; it < kCmpItems; ++it) {
             const long long i = start + it * kThreads + threadIdx.x;
@@ -444,9 +460,11 @@ __global__ void __launch_bounds__(kThreads) k_compact_move2(PartDev p, int dim, 
             if (carry) ws.key[o] = A.kc[it];
             if (perm) perm[i] = (int)o;
         }
+        MV_TRACE_U(u, 3);
         if (!more) break;
         move_rank(B, exB, alB, totB, s_cnt, &s_sink);
         publish(u2);
+        MV_TRACE_U(u2, 1);
         u = u2;
         A = B;
         totA = totB;

@@ -39,7 +39,9 @@ def main():
     d = np.diff(r, axis=1)
     print(f"K7b: {len(t)} sub-tiles, span {r[:, 3].max():.1f} us, last start {r[:, 0].max():.1f} us, "
           f"blocks {len(np.unique(t[:, 4]))}")
-    for name, col in zip(["loads+scan", "wait", "stores"], d.T):
+    # K7b two in flight: [0] loads issued, [1] loads returned + ranked + "read done",
+    # [2] predecessors waited for (the block's next sub-tile loading meanwhile), [3] stored
+    for name, col in zip(["loads+rank", "until stores may start", "stores"], d.T):
         print(f"  {name:12s} mean {col.mean():7.2f} us  p50 {np.median(col):7.2f}  p99 {np.percentile(col, 99):7.2f}")
     tot = r[:, 3] - r[:, 0]
     print(f"  per sub-tile mean {tot.mean():.2f} us; sub-tiles per block {len(t) / len(np.unique(t[:, 4])):.1f}")
