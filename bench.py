@@ -307,7 +307,7 @@ def run_e2e(su, w, args, dev, world):
     """The same metric end to end: every step uploads the rank's particle state from
     pinned host memory (H2D), runs the update through the public API, and reads
     the updated state back (D2H) — a host-resident simulation loop.  The read-back
-    of one step and the upload of the next are pipelined per column on two copy
+    of one step and the upload of the next are pipelined per column quarter on two copy
     streams (the two PCIe directions run concurrently): column c goes up again as
     soon as it has come down, and the next step starts once every column is up."""
     bu = su.bu
@@ -323,7 +323,8 @@ def run_e2e(su, w, args, dev, world):
     steps = max(2, min(args.steps, args.e2e_steps))
     stream = torch.cuda.current_stream()
     up, down = torch.cuda.Stream(), torch.cuda.Stream()
-    evs = {c: torch.cuda.Event() for c in names}
+    chunks = 4                                          # per column: a short pipeline tail
+    evs = {(c, k): torch.cuda.Event() for c in names for k in range(chunks)}
     checked0 = bu.stats()["checked_total"]
     h2d = d2h = 0
     per = sum(col(c).element_size() for c in names)
@@ -345,14 +346,19 @@ def run_e2e(su, w, args, dev, world):
         n = int(bu.A.n.item())
         down.wait_stream(stream)
         last = s == steps - 1
+        m = (n + chunks - 1) // chunks
         for c in names:
-            with torch.cuda.stream(down):            # this step's result
-                host[c][:n].copy_(col(c)[:n], non_blocking=True)
-                evs[c].record(down)
-            if not last:
-                with torch.cuda.stream(up):          # the next step's input, column by column
-                    up.wait_event(evs[c])
-                    col(c)[:n].copy_(host[c][:n], non_blocking=True)
+            for k in range(chunks):
+                a, b = k * m, min(n, (k + 1) * m)
+                if a >= b:
+                    continue
+                with torch.cuda.stream(down):        # this step's result
+                    host[c][a:b].copy_(col(c)[a:b], non_blocking=True)
+                    evs[c, k].record(down)
+                if not last:
+                    with torch.cuda.stream(up):      # the next step's input, chunk by chunk
+                        up.wait_event(evs[c, k])
+                        col(c)[a:b].copy_(host[c][a:b], non_blocking=True)
         d2h += n * per + 8
         if not last:
             h2d += n * per
@@ -371,7 +377,7 @@ def run_e2e(su, w, args, dev, world):
     return {"value": checked / (ms / 1e3), "unit": "particles_checked/s", "ms_per_step": ms / steps,
             "steps": steps, "h2d_bytes_per_step": h2d // steps, "d2h_bytes_per_step": d2h // steps,
             "what": "pinned host state -> device, update via BufferUpdater/SlabUpdater, state -> pinned host; "
-                    "read-back and next upload pipelined per column on two copy streams"}
+                    "read-back and next upload pipelined per column quarter on two copy streams"}
 
 
 # ------------------------------------------------------------------ CPU oracle (reference arm / cpu_baseline)
