@@ -53,7 +53,9 @@ typedef enum {
     SPH_ERR_MOTION = -6,           /* (device) a buffer particle found outside its decision region P_k
                                       (it moved more than the one-cell margin in one step; reading R12) */
     SPH_ERR_CUDA = -7,             /* a CUDA runtime call failed (see sph_last_error) */
-    SPH_ERR_STATE = -9             /* call order violated (e.g. no workspace) */
+    SPH_ERR_STATE = -9             /* call order violated: no workspace; sph_buffer_update while the
+                                      previous update is not compacted; sph_compact(_deferred) with
+                                      no update to compact; a build or migration pack in between */
 } sph_status;
 
 /* Port kinds: unidirectional inlet (Alg. 1), unidirectional
@@ -95,7 +97,8 @@ typedef struct {
     int64_t deleted;        /* deleted by the last update (this rank) */
     int64_t checked_total;  /* candidates checked since context creation */
     int64_t out_of_grid;    /* particles clamped into boundary cells, cumulative */
-    int64_t motion_errors;  /* buffer particles beyond 3a/2, cumulative */
+    int64_t motion_errors;  /* buffer particles found among their port's candidates but outside
+                               P_k (reading R12), cumulative */
     int64_t migrated_out;   /* particles packed for neighbour slabs, cumulative */
     int64_t first_deleted;  /* lowest deleted index of the last update (INT64_MAX if none) */
     int32_t status_bits;    /* sticky device error bits: 1 capacity, 2 staging, 4 motion, 8 migration */

@@ -86,10 +86,13 @@ def lib():
         L.orc_windkessel.restype = C.c_double
         L.orc_port_move.argtypes = [C.POINTER(State), C.c_int32, C.POINTER(Port), C.POINTER(Port), C.c_int32]
         L.orc_port_move.restype = C.c_int64
-        L.orc_register.argtypes = [C.POINTER(State), C.POINTER(Grid), C.POINTER(Port), C.c_int32, C.c_int32]
+        L.orc_register.argtypes = [C.POINTER(State), C.POINTER(Grid), C.POINTER(Port), C.c_int32]
         L.orc_register.restype = C.c_int64
         L.orc_update.argtypes = [C.POINTER(Grid), C.POINTER(Port), C.c_int32, C.POINTER(State), C.c_int32,
-                                 C.c_int32, C.POINTER(UpdateOut)]
+                                 C.POINTER(UpdateOut)]
+        L.orc_tie_margin.argtypes = [C.POINTER(State), C.POINTER(Grid), C.POINTER(Port), C.c_int32, C.c_double,
+                                     C.c_void_p]
+        L.orc_tie_margin.restype = C.c_double
         L.orc_update.restype = C.c_int
         L.orc_compact.argtypes = [C.POINTER(State), C.c_void_p, C.POINTER(State), C.c_void_p, C.c_int32,
                                   C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int64, C.POINTER(State),
@@ -287,11 +290,105 @@ def port_move(st: dict, dim: int, port_from, port_to, k: int) -> int:
     return int(lib().orc_port_move(C.byref(r.s), dim, C.byref(A), C.byref(B), k))
 
 
-def register(st: dict, grid, port, k: int, prec: int = 0) -> int:
+# ----------------------------------------------------------------- O7 tie check
+
+_TIE_TAU_DP = None           # None: off; else every register/update certifies margins
+
+
+_TIE_COLLECT = None          # a list: collect the offending ids instead of raising
+
+
+class TieError(AssertionError):
+    """An input violates the north_star tie margin (a particle within 1e-4 dp of a
+    threshold at a decision or relabel point): such an input is invalid.
+    ``ids`` holds the ids of the offending particles."""
+
+    def __init__(self, msg, ids=()):
+        super().__init__(msg)
+        self.ids = list(ids)
+
+
+def enable_tie_check(tau_dp: float | None = 1e-4):
+    """Make every ``register`` and ``update`` certify that no particle is within
+    tau_dp * dp of a threshold face (O7) at the registration point, the decision
+    point (the state passed to ``update``) and the relabel point (its survivors
+    after the update); dp = a / layers of the ports.  None switches it off."""
+    global _TIE_TAU_DP
+    _TIE_TAU_DP = tau_dp
+
+
+class collect_ties:
+    """Context manager: inside, the tie check appends the offending ids to
+    ``self.ids`` instead of raising (used to screen a test's own dynamics)."""
+
+    def __enter__(self):
+        global _TIE_COLLECT, _TIE_TAU_DP
+        self.saved = (_TIE_COLLECT, _TIE_TAU_DP)
+        self.ids = []
+        _TIE_COLLECT = self.ids
+        if _TIE_TAU_DP is None:
+            _TIE_TAU_DP = 1e-4
+        return self
+
+    def __exit__(self, *a):
+        global _TIE_COLLECT, _TIE_TAU_DP
+        _TIE_COLLECT, _TIE_TAU_DP = self.saved
+
+
+class no_tie_check:
+    """Context manager for pins that put particles exactly on a threshold on purpose
+    (strict-inequality checks): the tie check is off inside."""
+
+    def __enter__(self):
+        global _TIE_TAU_DP
+        self.saved, _TIE_TAU_DP = _TIE_TAU_DP, None
+
+    def __exit__(self, *a):
+        global _TIE_TAU_DP
+        _TIE_TAU_DP = self.saved
+
+
+def _port_dp(ports):
+    dps = [2.0 * float(p.half_extents[0]) / p.layers for p in ports if getattr(p, "layers", 0)]
+    return min(dps) if dps else None
+
+
+def _certify(st, grid, ports, what):
+    if _TIE_TAU_DP is None or not ports or len(st["x"]) == 0:
+        return
+    dp = _port_dp(ports)
+    if dp is None:
+        return
+    m, bad = tie_margin(st, grid, ports, _TIE_TAU_DP * dp)
+    if len(bad):
+        ids = st["id"][bad].tolist()
+        if _TIE_COLLECT is not None:
+            _TIE_COLLECT.extend(ids)
+            return
+        raise TieError(f"{what}: {len(bad)} particles within {_TIE_TAU_DP:g} dp of a threshold "
+                       f"(min margin {m / dp:.3g} dp; first ids {ids[:5]})", ids)
+
+
+def register(st: dict, grid, port, k: int) -> int:
+    """O0: Alg. 1 identification / initial relabel of port k (f64 decisions)."""
+    _certify(st, grid, [port], f"registration of port {k}")
     r = _StateRef(st)
     G = cgrid(grid)
     P = cport(port)
-    return int(lib().orc_register(C.byref(r.s), C.byref(G), C.byref(P), k, prec))
+    return int(lib().orc_register(C.byref(r.s), C.byref(G), C.byref(P), k))
+
+
+def tie_margin(st: dict, grid, ports, tau: float):
+    """O7: minimum f64 distance of any particle near a port to a threshold face of
+    InBox_k or P_k (sph_oracle.c orc_tie_margin), and the indices of the particles
+    closer than ``tau``.  Returns (min_margin, flagged_indices)."""
+    n = len(st["x"])
+    flags = np.zeros(max(n, 1), np.uint8)
+    r = _StateRef(st)
+    G = cgrid(grid)
+    P = cports(ports)
+    m = lib().orc_tie_margin(C.byref(r.s), C.byref(G), P, len(ports), float(tau), flags.ctypes.data)
+    return float(m), np.nonzero(flags[:n])[0]
 
 
 @dataclass
@@ -312,9 +409,9 @@ class UpdateResult:
     motion_errors: int
 
 
-def update(grid, ports, st: dict, mode: int = 0, prec: int = 0, cap_stage: int | None = None,
+def update(grid, ports, st: dict, mode: int = 0, cap_stage: int | None = None,
            rho_b: dict | None = None) -> UpdateResult:
-    """O2-O5 on one slab: cell list, decisions, duplicate + recycle, relabel.
+    """O2-O5 on one slab: cell list, f64 decisions, duplicate + recycle, relabel.
     rho_b: {port: recycled density} overriding the pressure BC's (a Windkessel driver)."""
     dim = grid.dim
     n = len(st["x"])
@@ -345,11 +442,15 @@ def update(grid, ports, st: dict, mode: int = 0, prec: int = 0, cap_stage: int |
     P = cports(ports)
     for k, v in (rho_b or {}).items():
         P[k].rho_b = float(v)
-    rc = lib().orc_update(C.byref(G), P, K, C.byref(ri.s), mode, prec, C.byref(o))
+    _certify(st, grid, ports, "decision point")
+    rc = lib().orc_update(C.byref(G), P, K, C.byref(ri.s), mode, C.byref(o))
     if rc != 0:
         raise RuntimeError("oracle staging overflow")
     ns = int(o.n_stage)
     trim = lambda d, m: {k: ([e[:m] for e in v] if k == "extra" else v[:m]) for k, v in d.items()}
+    if _TIE_TAU_DP is not None and K:
+        keep = dport[:n] < 0
+        _certify({c: v[:n][keep] for c, v in srt.items() if c != "extra"}, grid, ports, "relabel point")
     return UpdateResult(order[:n], cstart[:nc], cend[:nc], int(o.out_of_grid), cport_[:n], dport[:n],
                         trim(srt, n), trim(stg, ns), sport[:ns], ssrc[:ns], counts[:2 * K], int(o.checked),
                         int(o.multi_decision), int(o.motion_errors))
@@ -376,11 +477,11 @@ def compact(res: UpdateResult, dim: int, K: int, all_counts: np.ndarray, rank: i
     return st, perm[:n], int(nid.value)
 
 
-def step(st: dict, grid, ports, next_id: int, dt: float | None, mode: int = 0, prec: int = 0):
+def step(st: dict, grid, ports, next_id: int, dt: float | None, mode: int = 0):
     """One single-slab update: (advect) -> O2..O5 -> O6 with a 1-rank count matrix.
     Returns (new_state, UpdateResult, perm, next_id_after).  ``st`` is advected in place."""
     if dt is not None:
         advect(st, grid.dim, dt)
-    res = update(grid, ports, st, mode, prec)
+    res = update(grid, ports, st, mode)
     new, perm, nid = compact(res, grid.dim, len(ports), res.port_counts[None, :], 0, next_id)
     return new, res, perm, nid

@@ -15,17 +15,19 @@
  * ambiguous passage listed in DESIGN.md §3.
  *
  * Arithmetic.  The paper fixes no precision (R16).  State is fp32 (BASELINE
- * configs).  Where floating point decides an integer (a crossing, an in-box
- * test, a cell index) this oracle takes the decision in the kernel's precision
- * with every operation a single IEEE-754 binary32 round-to-nearest operation in
- * a fixed order ("pinned fp32", DESIGN.md §3 "Pinned arithmetic"):
- *     d_j  = fl(x_j - o_j)
- *     X'_r = fl( fl( fl(Q_r0*d_0) + fl(Q_r1*d_1) ) + fl(Q_r2*d_2) )   (3-D)
- *     X'_r = fl( fl(Q_r0*d_0) + fl(Q_r1*d_1) )                          (2-D)
- * This file must be compiled with -ffp-contract=off (no FMA contraction) on an
- * SSE target (FLT_EVAL_METHOD == 0).  A second precision, prec=1, decides in
- * f64 from the same fp32 inputs; it is used by the pins to show the pinned fp32
- * decisions equal the exact-arithmetic decisions away from ties.
+ * configs).  Every DECISION (a crossing, P_k membership, an in-box test) is
+ * taken from the plain definition in f64: the fp32 position
+ * is widened exactly, d = x - o and X' = Q d are formed in double.  The inputs
+ * are tie-screened (north_star: every particle at least 1e-4 dp from every
+ * threshold; orc_tie_margin below is the check), so the exact decision is the
+ * only correct one and the GPU's own-precision decisions must equal it.  Only
+ * the three STATE MUTATIONS are pinned fp32, one IEEE-754 binary32
+ * round-to-nearest operation each in a fixed order, because they produce fp32
+ * state that is compared bit for bit (DESIGN.md §3 "Pinned arithmetic"):
+ * advection x <- fl(x + fl(v dt)), recycling x <- fl(x - fl(a u)) and the cell
+ * index floor(fl(fl(x - lo) * fl(1/cs))); plus the BC velocity and the moving-
+ * port transfer, which write state too.  This file must be compiled with
+ * -ffp-contract=off (no FMA contraction) on an SSE target (FLT_EVAL_METHOD == 0).
  *
  * parity pinned: see tests/test_oracle_pins.py (closed forms, hand cases
  * H1-H6, lattice counts, invariants, brute force vs cell-restricted).
@@ -204,46 +206,86 @@ static void recycle_shift(const orc_port *p, float s[3])
 
 /* ----------------------------------------------------------- predicates */
 
-/* Local-frame test of one particle against one port.  Returns:
+/* Local-frame test of one particle against one port, in f64 (O3).  Returns:
  *   bit0 = x in P_k   (|X'_r| < he_r + m, m = cs: reading R4, the paper's
  *                      "approximately one layer of cells" P:413)
  *   bit1 = InBox_k    (|X'| < a/2 & |Y'| < b/2 (& |Z'| < c/2), strict)
  *   bit2 = X'_0 > a/2   (crossing the buffer-fluid interface / outlet boundary)
- *   bit3 = X'_0 < -a/2  (bidirectional reverse crossing)
- *   bit4 = X'_0 - a > a/2 (moved more than one buffer length; reading R12) */
-static int classify(const orc_port *p, int32_t dim, float cs, float x, float y, float z, int32_t prec)
+ *   bit3 = X'_0 < -a/2  (bidirectional reverse crossing) */
+static int classify(const orc_port *p, int32_t dim, float cs, float x, float y, float z)
 {
     int bits = 0;
-    if (prec == 0) {
-        float X[3];
-        orc_to_local_f32(p, dim, x, y, z, X);
-        int inP = 1, inB = 1;
-        for (int r = 0; r < dim; ++r) {
-            float heP = p->he[r] + cs;
-            if (!(fabsf(X[r]) < heP)) inP = 0;
-            if (!(fabsf(X[r]) < p->he[r])) inB = 0;
-        }
-        if (inP) bits |= 1;
-        if (inB) bits |= 2;
-        if (X[0] > p->he[0]) bits |= 4;
-        if (X[0] < -p->he[0]) bits |= 8;
-        if (X[0] - 2.0f * p->he[0] > p->he[0]) bits |= 16;
-    } else {
-        double X[3];
-        orc_to_local_f64(p, dim, x, y, z, X);
-        int inP = 1, inB = 1;
-        for (int r = 0; r < dim; ++r) {
-            double heP = (double)p->he[r] + (double)cs;
-            if (!(fabs(X[r]) < heP)) inP = 0;
-            if (!(fabs(X[r]) < (double)p->he[r])) inB = 0;
-        }
-        if (inP) bits |= 1;
-        if (inB) bits |= 2;
-        if (X[0] > (double)p->he[0]) bits |= 4;
-        if (X[0] < -(double)p->he[0]) bits |= 8;
-        if (X[0] - 2.0 * (double)p->he[0] > (double)p->he[0]) bits |= 16;
+    double X[3];
+    orc_to_local_f64(p, dim, x, y, z, X);
+    int inP = 1, inB = 1;
+    for (int r = 0; r < dim; ++r) {
+        double heP = (double)p->he[r] + (double)cs;
+        if (!(fabs(X[r]) < heP)) inP = 0;
+        if (!(fabs(X[r]) < (double)p->he[r])) inB = 0;
     }
+    if (inP) bits |= 1;
+    if (inB) bits |= 2;
+    if (X[0] > (double)p->he[0]) bits |= 4;
+    if (X[0] < -(double)p->he[0]) bits |= 8;
     return bits;
+}
+
+/* O7 tie margin (north_star, BASELINE.json: "The generator keeps every particle at
+ * least 1e-4 dp from any threshold, so no decision is a tie").
+ * The thresholds of the method are the faces of InBox_k (|X'_r| = he_r: P:394-395,
+ * X'_0 = +-a/2 is a face of InBox_k) and of the decision
+ * region P_k (|X'_r| = he_r + m, reading R4).  For every particle i and port k
+ * with x_i inside P_k inflated by tau (|X'_r| < he_r + m + tau for every r,
+ * X' in f64), the margin is min over axes r of
+ *     min( | |X'_r| - he_r | , | |X'_r| - (he_r + m) | ),
+ * a conservative stand-in for the distance to the nearest face (it also counts
+ * the planes' extensions inside P_k).  Returns the minimum over all pairs
+ * (HUGE_VAL if no particle is near any port); flags[i] = 1 where some margin of
+ * i is < tau (flags may be NULL).  The caller evaluates it at every decision
+ * point (registration, after each advection) and relabel point (after each
+ * update, on post-recycle positions). */
+double orc_tie_margin(const orc_state *s, const orc_grid *g, const orc_port *ports, int32_t K, double tau,
+                      uint8_t *flags)
+{
+    const int32_t dim = g->dim;
+    const double m = (double)g->cs;
+    double best = HUGE_VAL;
+    /* exact early-out: a particle outside the bounding sphere of P_k inflated by
+     * tau (radius^2 = 1.01 * sum_r (he_r + m + tau)^2) is not near port k */
+    double *R2 = (double *)malloc(sizeof(double) * (size_t)(K > 0 ? K : 1));
+    for (int32_t k = 0; k < K; ++k) {
+        double acc = 0.0;
+        for (int r = 0; r < dim; ++r) {
+            double e = (double)ports[k].he[r] + m + tau;
+            acc += e * e;
+        }
+        R2[k] = 1.01 * acc;
+    }
+    for (int64_t i = 0; i < s->n; ++i) {
+        if (flags) flags[i] = 0;
+        for (int32_t k = 0; k < K; ++k) {
+            const orc_port *p = &ports[k];
+            double e0 = (double)s->x[i] - (double)p->o[0], e1 = (double)s->y[i] - (double)p->o[1];
+            double e2 = dim == 3 ? (double)s->z[i] - (double)p->o[2] : 0.0;
+            if (e0 * e0 + e1 * e1 + e2 * e2 > R2[k]) continue;
+            double X[3];
+            orc_to_local_f64(p, dim, s->x[i], s->y[i], dim == 3 ? s->z[i] : 0.0f, X);
+            int near = 1;
+            for (int r = 0; r < dim; ++r)
+                if (!(fabs(X[r]) < (double)p->he[r] + m + tau)) near = 0;
+            if (!near) continue;
+            for (int r = 0; r < dim; ++r) {
+                double a = fabs(X[r]);
+                double d1 = fabs(a - (double)p->he[r]);
+                double d2 = fabs(a - ((double)p->he[r] + m));
+                double d = d1 < d2 ? d1 : d2;
+                if (d < best) best = d;
+                if (d < tau && flags) flags[i] = 1;
+            }
+        }
+    }
+    free(R2);
+    return best;
 }
 
 /* ------------------------------------------------------------ cell list */
@@ -500,12 +542,12 @@ double orc_windkessel(double P, double Q, double Qprev, double dt, double Rp, do
  * buffer particle of port k.  For outlet and bidirectional ports the same test is
  * the initial relabel (Alg. 2/3 second procedure).
  * Returns the number of particles labelled k afterwards. */
-int64_t orc_register(orc_state *s, const orc_grid *g, const orc_port *p, int32_t k, int32_t prec)
+int64_t orc_register(orc_state *s, const orc_grid *g, const orc_port *p, int32_t k)
 {
     int64_t members = 0;
     for (int64_t i = 0; i < s->n; ++i) {
         if (s->label[i] == -1) {
-            int b = classify(p, g->dim, g->cs, s->x[i], s->y[i], g->dim == 3 ? s->z[i] : 0.0f, prec);
+            int b = classify(p, g->dim, g->cs, s->x[i], s->y[i], g->dim == 3 ? s->z[i] : 0.0f);
             if (b & 2) s->label[i] = k;
         }
         if (s->label[i] == k) ++members;
@@ -548,7 +590,10 @@ typedef struct {
     int32_t *port_counts;  /* [2K]: created_k at [k], deleted_k at [K + k] */
     int64_t checked;       /* particle-port tests performed */
     int64_t multi_decision;/* particles with more than one decision (must be 0) */
-    int64_t motion_errors; /* members of k outside P_k (reading R12; diagnostic) */
+    int64_t motion_errors; /* members of k outside P_k (reading R12; diagnostic): the paper
+                              checks only the local cell-linked lists around the buffer
+                              (P:411-413), so a buffer particle that left that region
+                              can no longer be generated, deleted or relabelled */
 } orc_update_out;
 
 static void copy_row(const orc_state *src, int64_t i, orc_state *dst, int64_t j, int32_t dim)
@@ -566,10 +611,10 @@ static void copy_row(const orc_state *src, int64_t i, orc_state *dst, int64_t j,
 /* One buffer update on one slab.  mode 0 = brute force over every particle and
  * port in the global frame ("through the equation of the threshold line or
  * surface"); mode 1 = only particles in the oracle's own P_k cell set (the
- * paper's local cell-linked lists).  prec 0 = pinned fp32, 1 = f64.
+ * paper's local cell-linked lists).  Decisions in f64 (O3).
  * Returns 0, or -1 if staging overflows. */
 int orc_update(const orc_grid *g, const orc_port *ports, int32_t K, const orc_state *in,
-               int32_t mode, int32_t prec, orc_update_out *out)
+               int32_t mode, orc_update_out *out)
 {
     const int32_t dim = g->dim;
     const int64_t n = in->n;
@@ -625,7 +670,7 @@ int orc_update(const orc_grid *g, const orc_port *ports, int32_t K, const orc_st
             }
             for (int64_t j = jb; j < je; ++j) {
                 ++out->checked;
-                int b = classify(p, dim, g->cs, S->x[j], S->y[j], dim == 3 ? S->z[j] : 0.0f, prec);
+                int b = classify(p, dim, g->cs, S->x[j], S->y[j], dim == 3 ? S->z[j] : 0.0f);
                 int member = (S->label[j] == k);
                 if (member && !(b & 1)) ++out->motion_errors;          /* reading R12 (diagnostic) */
                 if (!(b & 1)) continue;                               /* x not in P_k (R4) */
@@ -703,7 +748,7 @@ int orc_update(const orc_grid *g, const orc_port *ports, int32_t K, const orc_st
             }
             for (int64_t j = jb; j < je; ++j) {
                 if (out->delete_port[j] >= 0) continue;
-                int b = classify(p, dim, g->cs, S->x[j], S->y[j], dim == 3 ? S->z[j] : 0.0f, prec);
+                int b = classify(p, dim, g->cs, S->x[j], S->y[j], dim == 3 ? S->z[j] : 0.0f);
                 if (b & 2) S->label[j] = k;
                 else if (S->label[j] == k) S->label[j] = -1;
             }

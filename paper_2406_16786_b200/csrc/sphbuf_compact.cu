@@ -480,8 +480,9 @@ __global__ void __launch_bounds__(kThreads) k_compact_move2(PartDev p, int dim, 
 // R14, §8(e)): off(k, r) = next_id + sum_{k'<k} sum_r' C[r'][k'] + sum_{r'<r} C[r'][k];
 // identity perm below i_first; then N and next_id.
 // defer: the tombstones stay in place (the next sph_cll_build drops them) and the
-// staged particles go to [N, N + C); launched with one block, so N and next_id
-// can be read directly.
+// staged particles go to [N, N + C).  Many blocks: thread 0 of every block reads
+// N and next_id into shared memory before the block barrier and before it counts
+// the block done, so the last block's update of them cannot race a reader.
 __global__ void __launch_bounds__(kThreads) k_compact_append(PartDev p, GridDev g, int n_ports, int max_ports,
                                                              Workspace ws, const int *all_counts, int nranks,
                                                              int rank, long long *next_id, int *perm, bool defer,
@@ -491,12 +492,14 @@ __global__ void __launch_bounds__(kThreads) k_compact_append(PartDev p, GridDev 
     pdl_entry();
     __shared__ long long s_off[SPH_MAX_PORTS];
     __shared__ long long s_beg[SPH_MAX_PORTS];
-    __shared__ long long s_total;
+    __shared__ long long s_total, s_nid0, s_N;
     Counters *ctr = ws.ctr;
-    // N and next_id before the append: read here by every block (deferred), or
-    // recorded by k_compact_count; the last block to finish writes the new ones
-    const long long nid0 = defer ? *next_id : ctr->cmp_next_id;
+    // N and next_id before the append: read by thread 0 of every block (deferred),
+    // or recorded by k_compact_count; the last block to finish writes the new ones
     if (threadIdx.x == 0) {
+        const long long nid0 = defer ? *(volatile long long *)next_id : ctr->cmp_next_id;
+        s_nid0 = nid0;
+        s_N = defer ? *(volatile long long *)p.n : ctr->cmp_n;
         long long acc = nid0, beg = 0;
         for (int k = 0; k < n_ports; ++k) {
             long long before = 0, all = 0;
@@ -513,7 +516,8 @@ __global__ void __launch_bounds__(kThreads) k_compact_append(PartDev p, GridDev 
         s_total = acc - nid0;
     }
     __syncthreads();
-    const long long N = defer ? *p.n : ctr->cmp_n;
+    const long long nid0 = s_nid0;
+    const long long N = s_N;
     const long long D = defer ? 0 : ctr->n_del;
     long long C = ctr->n_stage;
     if (C > ws.max_new) C = ws.max_new;

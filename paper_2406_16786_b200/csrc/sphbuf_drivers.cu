@@ -72,12 +72,12 @@ __global__ void __launch_bounds__(256) k_drivers(PartDev p, int dim, Workspace w
     ws.drv_rho[E.k] = __double2float_rn(E.rho0 + P / E.c0sq);
 }
 
-cudaError_t launch_drivers(const PartDev &p, const Workspace &ws, const DriverLaunch &D, const int *cell_start,
-                           const int *cell_end, cudaStream_t s, Launch *L)
+cudaError_t launch_drivers(const PartDev &p, int dim, const Workspace &ws, const DriverLaunch &D,
+                           const int *cell_start, const int *cell_end, cudaStream_t s, Launch *L)
 {
     if (D.n <= 0) return cudaSuccess;
     L->before(s);
-    launch_k(k_drivers, dim3(D.n), dim3(256), 0, s, p, p.z ? 3 : 2, ws, D, cell_start, cell_end);
+    launch_k(k_drivers, dim3(D.n), dim3(256), 0, s, p, dim, ws, D, cell_start, cell_end);
     L->after(s, KID_DRIVERS);
     return cudaGetLastError();
 }

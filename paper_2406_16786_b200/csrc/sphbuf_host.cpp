@@ -92,6 +92,9 @@ struct sph_ctx {
     // run table version and cell tables it saw, consumed by the next update
     unsigned runs_ver = 0;
     bool pro_ready = false;
+    // call order: build -> update -> compact; the update's deletion
+    // list and staging area are live until the compaction consumes them
+    bool update_pending = false;
     unsigned pro_ver = 0;
     const int32_t *pro_cs = nullptr, *pro_ce = nullptr;
     std::vector<int> run_cap;             // per port: > 0 once movable (device-enumerated slice)
@@ -879,7 +882,7 @@ sph_status sph_drivers_step(sph_ctx *c, sph_particles *p, double t, double dt, c
             E.dt = dt;
         }
     }
-    cudaError_t e = launch_drivers(part_dev(p), c->W, L, cell_start, cell_end, static_cast<cudaStream_t>(stream),
+    cudaError_t e = launch_drivers(part_dev(p), c->gd.dim, c->W, L, cell_start, cell_end, static_cast<cudaStream_t>(stream),
                                    &c->L);
     return e == cudaSuccess ? SPH_OK : cuda_fail(c, e, "drivers_step");
 }
@@ -930,6 +933,7 @@ static sph_status cll_build(sph_ctx *c, const sph_particles *in, sph_particles *
                             int32_t *cell_end, int32_t *perm, float dt, bool advect, void *stream)
 {
     if (!c) return SPH_ERR_ARG;
+    if (c->update_pending) return fail(c, SPH_ERR_STATE, "cll_build: the last buffer update was not compacted");
     sph_status st = check_particles(c, in);
     if (st == SPH_OK) st = check_particles(c, out);
     if (st != SPH_OK) return st;
@@ -970,6 +974,7 @@ sph_status sph_cll_key(sph_ctx *c, sph_particles *in, float dt, int32_t advect, 
                        void *stream)
 {
     if (!c) return SPH_ERR_ARG;
+    if (c->update_pending) return fail(c, SPH_ERR_STATE, "cll_key: the last buffer update was not compacted");
     sph_status st = check_particles(c, in);
     if (st != SPH_OK) return st;
     if ((send_lo == nullptr) != (send_hi == nullptr)) return fail(c, SPH_ERR_ARG, "give both send buffers or none");
@@ -987,6 +992,7 @@ sph_status sph_cll_finish(sph_ctx *c, sph_particles *in, sph_particles *out, con
                           const float *recv_hi, int32_t *cell_start, int32_t *cell_end, int32_t *perm, void *stream)
 {
     if (!c) return SPH_ERR_ARG;
+    if (c->update_pending) return fail(c, SPH_ERR_STATE, "cll_finish: the last buffer update was not compacted");
     sph_status st = check_particles(c, in);
     if (st == SPH_OK) st = check_particles(c, out);
     if (st != SPH_OK) return st;
@@ -1011,13 +1017,17 @@ sph_status sph_buffer_update(sph_ctx *c, sph_particles *p, const int32_t *cell_s
     sph_status st = check_particles(c, p);
     if (st != SPH_OK) return st;
     if (!cell_start || !cell_end || !port_counts) return fail(c, SPH_ERR_ARG, "NULL argument");
+    if (c->update_pending)
+        return fail(c, SPH_ERR_STATE, "buffer_update: the previous update was not compacted");
     const int n_runs = (int)(c->runs.size() / 3);
     const bool pro_done = c->pro_ready && c->pro_ver == c->runs_ver && c->pro_cs == cell_start &&
                           c->pro_ce == cell_end;
     c->pro_ready = false;
     cudaError_t e = launch_update(part_dev(p), c->gd, c->pt, c->W, n_runs, cell_start, cell_end, port_counts,
                                   carry_on(c, p), c->carry_dt, pro_done, static_cast<cudaStream_t>(stream), &c->L);
-    return e == cudaSuccess ? SPH_OK : cuda_fail(c, e, "buffer_update");
+    if (e != cudaSuccess) return cuda_fail(c, e, "buffer_update");
+    c->update_pending = true;
+    return SPH_OK;
 }
 
 static sph_status compact(sph_ctx *c, sph_particles *p, const int32_t *all_counts, int32_t nranks, int32_t rank,
@@ -1028,6 +1038,7 @@ static sph_status compact(sph_ctx *c, sph_particles *p, const int32_t *all_count
     if (st != SPH_OK) return st;
     if (!all_counts || !next_id_dev || nranks <= 0 || rank < 0 || rank >= nranks)
         return fail(c, SPH_ERR_ARG, "bad count matrix / rank");
+    if (!c->update_pending) return fail(c, SPH_ERR_STATE, "compact: no buffer update to compact");
     int carry = carry_on(c, p);
     if (carry == 2 && !defer) {
         // an in-place compaction renumbers particles behind the leaver list: the
@@ -1038,7 +1049,9 @@ static sph_status compact(sph_ctx *c, sph_particles *p, const int32_t *all_count
     cudaError_t e = launch_compact(part_dev(p), c->gd, c->pt, c->W, all_counts, nranks, rank,
                                    reinterpret_cast<long long *>(next_id_dev), perm, defer, carry, c->carry_dt,
                                    static_cast<cudaStream_t>(stream), &c->L);
-    return e == cudaSuccess ? SPH_OK : cuda_fail(c, e, "compact");
+    if (e != cudaSuccess) return cuda_fail(c, e, "compact");
+    c->update_pending = false;
+    return SPH_OK;
 }
 
 sph_status sph_compact(sph_ctx *c, sph_particles *p, const int32_t *all_counts, int32_t nranks, int32_t rank,
@@ -1061,6 +1074,7 @@ sph_status sph_migrate_pack(sph_ctx *c, sph_particles *p, float *send_lo, float 
     sph_status st = check_particles(c, p);
     if (st != SPH_OK) return st;
     if (!send_lo || !send_hi) return fail(c, SPH_ERR_ARG, "NULL send buffer");
+    if (c->update_pending) return fail(c, SPH_ERR_STATE, "migrate_pack: the last buffer update was not compacted");
     carry_drop(c);
     cudaError_t e = launch_migrate_pack(part_dev(p), c->gd, c->W, send_lo, send_hi, c->max_migrate,
                                         sph_migrate_record_floats(c), static_cast<cudaStream_t>(stream),

@@ -248,8 +248,8 @@ cudaError_t launch_port_move(const PartDev &p, const GridDev &g, const PortDev &
                              long long *moved, const Workspace &ws, int carry, float cdt, cudaStream_t s, Launch *L);
 cudaError_t launch_port_enum(const GridDev &g, const PortEnum &P, float cs, int *runs, int cap, cudaStream_t s,
                              Launch *L);
-cudaError_t launch_drivers(const PartDev &p, const Workspace &ws, const DriverLaunch &D, const int *cell_start,
-                           const int *cell_end, cudaStream_t s, Launch *L);
+cudaError_t launch_drivers(const PartDev &p, int dim, const Workspace &ws, const DriverLaunch &D,
+                           const int *cell_start, const int *cell_end, cudaStream_t s, Launch *L);
 int sm_count();
 
 }  // namespace sphbuf

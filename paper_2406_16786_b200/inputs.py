@@ -136,6 +136,7 @@ class Workload:
     next_id: int
     notes: str = ""
     slab_cells: list = field(default_factory=list)   # per-slab [cx_begin, cx_end) for C5
+    redrawn: int = 0         # particles whose jitter the tie screen re-drew
 
     @property
     def n(self) -> int:
@@ -241,33 +242,242 @@ def _lattice(counts, dp, device, origin=(0.0, 0.0, 0.0), index_offset=0):
     return comps, idx + index_offset
 
 
+# ----------------------------------------------------------------- tie screen
+
+TIE_TAU_DP = 1e-4            # north_star: every particle >= 1e-4 dp from any threshold
+_SCREEN_GUARD = 1.1          # the screen flags at 1.1 tau (the oracle certifies tau, O7)
+
+
+def _local64(xs, port, dim):
+    """f64 local coordinates Q (x - o) of fp32 positions (input validation only)."""
+    d = [xs[j].double() - float(port.origin[j]) for j in range(dim)]
+    out = []
+    for r in range(dim):
+        acc = None
+        for j in range(dim):
+            t = float(port.Q[3 * r + j]) * d[j]
+            acc = t if acc is None else acc + t
+        out.append(acc)
+    return out
+
+
+def _near_faces(X, port, dim, cs, tau):
+    """(inside P_k inflated by tau, some local coordinate within tau of a face value
+    he_r or he_r + m) for f64 local coordinates X."""
+    near = None
+    close = None
+    for r in range(dim):
+        a = X[r].abs()
+        he = float(port.half_extents[r])
+        nr = a < he + cs + tau
+        cr = ((a - he).abs() < tau) | ((a - (he + cs)).abs() < tau)
+        near = nr if near is None else near & nr
+        close = cr if close is None else close | cr
+    return near & close
+
+
+def _tie_flags(x32, v32, ports, dim, cs, dt, n_updates, tau):
+    """Flag the particles (fp32 positions x32, velocities v32: lists of tensors) that
+    come within tau of a threshold face of InBox_k or P_k of any port over the run.
+
+    Kinematic model of the run (no decisions are taken here): each particle's
+    pinned fp32 free flight x <- fl(x + fl(v dt)) (the advection driver); and,
+    every time a trajectory crosses the plane X'_0 = +a/2 of an inlet or
+    bidirectional port forward inside its P_k, an extra trajectory starting from
+    the position shifted back by one buffer length, fl(x - fl(a u)) (a recycled
+    buffer particle), which is followed the same way.  Deletions and
+    labels are ignored, so the set of positions covers every position the
+    particle and its duplicates/recycled copies can take (a superset: more
+    redraws, never a missed tie).  Positions are checked at registration (step 0),
+    after every advection (decision points) and where a recycled copy starts
+    (relabel point)."""
+    dev = x32[0].device
+    n = x32[0].numel()
+    flag = torch.zeros(n, dtype=torch.bool, device=dev)
+    if n == 0 or not ports:
+        return flag
+    dt32 = torch.tensor(dt, dtype=torch.float32, device=dev)
+    slack = 0.05 * cs
+    # preselect (particle, port) pairs whose straight path comes near P_k
+    sel = []
+    xe = [x32[j].double() + float(n_updates) * float(dt) * v32[j].double() for j in range(dim)]
+    for p in ports:
+        X0 = _local64(x32, p, dim)
+        Xe = _local64(xe, p, dim)
+        m = None
+        for r in range(dim):
+            R = float(p.half_extents[r]) + cs + tau + slack
+            mr = (torch.minimum(X0[r], Xe[r]) < R) & (torch.maximum(X0[r], Xe[r]) > -R)
+            m = mr if m is None else m & mr
+        sel.append(m)
+    anyp = torch.zeros(n, dtype=torch.bool, device=dev)
+    for m in sel:
+        anyp |= m
+    org = torch.nonzero(anyp).squeeze(1)                   # origin of every trajectory
+    if org.numel() == 0:
+        return flag
+    pos = [x32[j][org].clone() for j in range(dim)]
+    vel = [v32[j][org].clone() for j in range(dim)]
+    shift = []
+    for p in ports:
+        a = np.float32(2.0) * np.float32(p.half_extents[0])
+        shift.append([float(np.float32(a * np.float32(p.Q[j]))) for j in range(dim)])
+
+    def check(tr_pos, tr_org):
+        for k, p in enumerate(ports):
+            on = sel[k][tr_org]
+            if not bool(on.any()):
+                continue
+            idx = torch.nonzero(on).squeeze(1)
+            X = _local64([c[idx] for c in tr_pos], p, dim)
+            bad = _near_faces(X, p, dim, cs, tau)
+            flag[tr_org[idx[bad]]] = True
+
+    check(pos, org)
+    for _ in range(n_updates):
+        prev = pos
+        pos = [prev[j] + vel[j] * dt32 for j in range(dim)]
+        check(pos, org)
+        new_pos, new_vel, new_org = [], [], []
+        for k, p in enumerate(ports):
+            if p.kind == OUTLET:
+                continue
+            on = torch.nonzero(sel[k][org]).squeeze(1)
+            if on.numel() == 0:
+                continue
+            X = _local64([c[on] for c in pos], p, dim)
+            Xp = _local64([c[on] for c in prev], p, dim)[0]
+            inP = None
+            for r in range(dim):
+                t = X[r].abs() < float(p.half_extents[r]) + cs
+                inP = t if inP is None else inP & t
+            he0 = float(p.half_extents[0])
+            cross = inP & (X[0] > he0) & (Xp <= he0)
+            if not bool(cross.any()):
+                continue
+            ci = on[cross]
+            new_pos.append([pos[j][ci] - torch.tensor(shift[k][j], dtype=torch.float32, device=dev)
+                            for j in range(dim)])
+            new_vel.append([vel[j][ci] for j in range(dim)])
+            new_org.append(org[ci])
+        if new_org:
+            bp = [torch.cat([q[j] for q in new_pos]) for j in range(dim)]
+            bv = [torch.cat([q[j] for q in new_vel]) for j in range(dim)]
+            bo = torch.cat(new_org)
+            check(bp, bo)
+            pos = [torch.cat([pos[j], bp[j]]) for j in range(dim)]
+            vel = [torch.cat([vel[j], bv[j]]) for j in range(dim)]
+            org = torch.cat([org, bo])
+    return flag
+
+
+def _hash_jitter(ids, attempt: int, comp: int, salt: int, dp: float):
+    """Counter-based uniform draw in [-0.1 dp, 0.1 dp) for re-drawn particles
+    (splitmix64 of (salt, id, attempt, component)); identical on every device."""
+    with np.errstate(over="ignore"):
+        z = (ids.astype(np.uint64) * np.uint64(0x9E3779B97F4A7C15)
+             + np.uint64(attempt) * np.uint64(0xD1B54A32D192ED03)
+             + np.uint64(comp) * np.uint64(0x8CB92BA72F3D8DD7)
+             + np.uint64(salt))
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        z = z ^ (z >> np.uint64(31))
+    u = (z >> np.uint64(11)).astype(np.float64) * (1.0 / 9007199254740992.0)
+    return (u * 2.0 - 1.0) * (0.1 * dp)
+
+
+def _screen(base, xyz, vel_fn, ids, ports, dim, dp, cs, dt, n_updates, salt, max_rounds=40):
+    """Tie screen (north_star; SURVEY §8(d) "Tie-screen"): re-draw the jitter (and
+    recompute the velocity) of every particle that comes within 1e-4 dp of a
+    threshold over the run, until none does.  base: lattice sites (f64), xyz:
+    jittered positions (f64, modified in place), vel_fn(xyz_subset, index_subset)
+    -> velocity (f64 list).  Returns (xyz, v, number of re-drawn particles)."""
+    tau = _SCREEN_GUARD * TIE_TAU_DP * dp
+    v = vel_fn(xyz, None)
+    sub = None
+    redrawn = set()
+    ids_np = ids.cpu().numpy()
+    for attempt in range(1, max_rounds + 1):
+        xs = [c if sub is None else c[sub] for c in xyz]
+        vs = [c if sub is None else c[sub] for c in v]
+        bad = _tie_flags([c.float() for c in xs], [c.float() for c in vs], ports, dim, cs, dt, n_updates, tau)
+        idx = torch.nonzero(bad).squeeze(1)
+        if sub is not None:
+            idx = sub[idx]
+        if idx.numel() == 0:
+            return xyz, v, len(redrawn)
+        ii = ids_np[idx.cpu().numpy()]
+        redrawn.update(int(i) for i in ii)
+        for j in range(dim):
+            jit = torch.from_numpy(_hash_jitter(ii, attempt, j, salt, dp)).to(xyz[j].device)
+            xyz[j][idx] = base[j][idx] + jit
+        vn = vel_fn([c[idx] for c in xyz], idx)
+        for j in range(dim):
+            v[j][idx] = vn[j]
+        sub = idx
+    raise RuntimeError("tie screen did not converge")
+
+
+def nudge(w: "Workload", nudges: dict, salt: int = 0x5EED) -> "Workload":
+    """Move the particles whose id is a key of ``nudges`` (id -> attempt) by a
+    counter-based offset of up to +-0.05 dp per component (tests/tiescreen.py:
+    tie screen of a test's own dynamics).  Velocities and every other particle are
+    unchanged.  In place; returns w."""
+    if not nudges:
+        return w
+    st = w.state
+    ids = st["id"].cpu().numpy()
+    want = np.fromiter(nudges.keys(), dtype=np.int64)
+    att = np.fromiter(nudges.values(), dtype=np.int64)
+    pos = np.nonzero(np.isin(ids, want))[0]
+    if pos.size == 0:
+        return w
+    order = {int(i): int(a) for i, a in zip(want, att)}
+    a_of = np.array([order[int(i)] for i in ids[pos]], dtype=np.int64)
+    idx = torch.from_numpy(pos).to(st["x"].device)
+    for j, c in enumerate(("x", "y", "z")[:w.dim]):
+        off = np.empty(pos.size)
+        for a in np.unique(a_of):
+            m = a_of == a
+            off[m] = 0.5 * _hash_jitter(ids[pos[m]], 1000 + int(a), j, salt, w.dp)
+        col = st[c]
+        col[idx] = (col[idx].double() + torch.from_numpy(off).to(col.device)).float()
+    return w
+
+
 # ----------------------------------------------------------------- configs
 
-def c1(device="cpu", dt=0.002, name="C1") -> Workload:
-    """2-D orthogonal channel 2.0x0.4 at dp=0.01 (BASELINE configs[0])."""
+def c1(device="cpu", dt=0.002, name="C1", n_updates=20) -> Workload:
+    """2-D orthogonal channel 2.0x0.4 at dp=0.01 (BASELINE configs[0]).
+    ``n_updates`` only sets the tie screen's horizon (the config is one update;
+    the tests run up to 20)."""
     dim, dp = 2, 0.01
     h = 1.3 * dp
     cs = f32(2 * h)
     g = _gen(SEED_BASE + 1, device)
-    xyz, ids = _lattice((200, 40), dp, device)
+    base, ids = _lattice((200, 40), dp, device)
     n = ids.numel()
-    for j in range(dim):
-        xyz[j] = xyz[j] + _jitter(n, g, device, dp)
-    v = [1.0 + _noise(n, g, device), _noise(n, g, device)]
+    xyz = [base[j] + _jitter(n, g, device, dp) for j in range(dim)]
+    noise = [_noise(n, g, device), _noise(n, g, device)]
     I = (1.0, 0.0, 0.0, 0.0, 1.0, 0.0, 0.0, 0.0, 1.0)
     ports = [_port((0.02, 0.2, 0.0), I, (0.02, 0.2, 0.0), INLET, 4),
              _port((1.98, 0.2, 0.0), I, (0.02, 0.2, 0.0), OUTLET, 4)]
-    v = _project_near_ports(xyz, v, ports[:1], dim, 2 * dp)
+
+    def vel(x, idx):
+        nz = [c if idx is None else c[idx] for c in noise]
+        return _project_near_ports(x, [1.0 + nz[0], nz[1]], ports[:1], dim, 2 * dp)
+    xyz, v, nre = _screen(base, xyz, vel, ids, ports, dim, dp, cs, f32(dt), n_updates, SEED_BASE + 1)
     lo = (f32(-2 * cs), f32(-2 * cs), 0.0)
     ncell = (int(math.ceil(2.0 / cs)) + 4, int(math.ceil(0.4 / cs)) + 4, 1)
     grid = Grid(dim, lo, cs, ncell)
     return Workload(name, dim, dp, h, grid, ports, _pack_state(xyz, v, ids, dim), f32(dt), 1, n,
-                    notes="200x40 lattice; inlet x in (0,0.04), outlet x in (1.96,2.0)")
+                    notes=f"200x40 lattice; inlet x in (0,0.04), outlet x in (1.96,2.0); {nre} re-drawn",
+                    redrawn=nre)
 
 
-def c1e(device="cpu") -> Workload:
+def c1e(device="cpu", n_updates=20) -> Workload:
     """C1 with dt=0.0095: exactly the last lattice layer crosses at each end (R18)."""
-    return c1(device, dt=0.0095, name="C1e")
+    return c1(device, dt=0.0095, name="C1e", n_updates=n_updates)
 
 
 def c2(device="cpu", n_updates=100) -> Workload:
@@ -285,6 +495,7 @@ def c2(device="cpu", n_updates=100) -> Workload:
     th = math.radians(30.0)
     X = math.cos(th) * s - math.sin(th) * w
     Y = math.sin(th) * s + math.cos(th) * w
+    base = [X, Y]
     xyz = [X + _jitter(n, g, device, dp), Y + _jitter(n, g, device, dp)]
     u0 = (math.cos(th), math.sin(th))
     nrm = (math.cos(math.radians(75.0)), math.sin(math.radians(75.0)))
@@ -293,26 +504,33 @@ def c2(device="cpu", n_updates=100) -> Workload:
     p1 = _port((end[0] - 0.004 * nrm[0], end[1] - 0.004 * nrm[1], 0.0), frame_rows_2d(math.radians(255.0)),
                (0.004, 0.2 / c45, 0.0), BIDIRECTIONAL, 4)
     ports = [p0, p1]
-    # velocity: nearest port k, sigma = +1 where Y'_k > 0 else -1 ("sign flipping per region")
-    d0 = (xyz[0] - p0.origin[0]) ** 2 + (xyz[1] - p0.origin[1]) ** 2
-    d1 = (xyz[0] - p1.origin[0]) ** 2 + (xyz[1] - p1.origin[1]) ** 2
-    near1 = d1 < d0
-    v = [torch.zeros(n, dtype=torch.float64, device=device) for _ in range(2)]
-    for k, p in enumerate(ports):
-        sel = near1 if k == 1 else ~near1
-        yl = _local(xyz, p, dim)[1]
-        sig = torch.where(yl > 0, 1.0, -1.0)
-        for j in range(2):
-            v[j] = torch.where(sel, sig * p.Q[j], v[j])
-    v = [v[0] + _noise(n, g, device), v[1] + _noise(n, g, device)]
-    v = _project_near_ports(xyz, v, ports, dim, 2 * dp)
+    noise = [_noise(n, g, device), _noise(n, g, device)]
+
+    def vel(x, idx):
+        # nearest port k, sigma = +1 where Y'_k > 0 else -1 ("sign flipping per region")
+        m = x[0].numel()
+        d0 = (x[0] - p0.origin[0]) ** 2 + (x[1] - p0.origin[1]) ** 2
+        d1 = (x[0] - p1.origin[0]) ** 2 + (x[1] - p1.origin[1]) ** 2
+        near1 = d1 < d0
+        v = [torch.zeros(m, dtype=torch.float64, device=device) for _ in range(2)]
+        for k, p in enumerate(ports):
+            sel = near1 if k == 1 else ~near1
+            yl = _local(x, p, dim)[1]
+            sig = torch.where(yl > 0, 1.0, -1.0)
+            for j in range(2):
+                v[j] = torch.where(sel, sig * p.Q[j], v[j])
+        nz = [c if idx is None else c[idx] for c in noise]
+        v = [v[0] + nz[0], v[1] + nz[1]]
+        return _project_near_ports(x, v, ports, dim, 2 * dp)
+    xyz, v, nre = _screen(base, xyz, vel, ids, ports, dim, dp, cs, f32(0.0005), n_updates, SEED_BASE + 2)
     xs, ys = xyz[0], xyz[1]
     pad = 12
     lo = (f32(float(xs.min()) - pad * cs), f32(float(ys.min()) - pad * cs), 0.0)
     ncell = (int(math.ceil((float(xs.max()) - lo[0]) / cs)) + pad, int(math.ceil((float(ys.max()) - lo[1]) / cs)) + pad, 1)
     grid = Grid(dim, lo, cs, ncell)
     return Workload("C2", dim, dp, h, grid, ports, _pack_state(xyz, v, ids, dim), f32(0.0005), n_updates, n,
-                    notes="30-degree channel, 45-degree slanted end; bidirectional ports at 30 and 255 degrees")
+                    notes=f"30-degree channel, 45-degree slanted end; bidirectional ports at 30 and 255 degrees; "
+                          f"{nre} re-drawn", redrawn=nre)
 
 
 def c3(device="cpu", n_updates=100, scale=1.0) -> Workload:
@@ -323,22 +541,26 @@ def c3(device="cpu", n_updates=100, scale=1.0) -> Workload:
     nx = int(round(400 * scale))
     cs = f32(1.0 / 153.0)
     g = _gen(SEED_BASE + 3, device)
-    xyz, ids = _lattice((nx, 80, 80), dp, device)
+    base, ids = _lattice((nx, 80, 80), dp, device)
     n = ids.numel()
-    for j in range(3):
-        xyz[j] = xyz[j] + _jitter(n, g, device, dp)
-    v = [1.0 + _noise(n, g, device), _noise(n, g, device), _noise(n, g, device)]
+    xyz = [base[j] + _jitter(n, g, device, dp) for j in range(3)]
+    noise = [_noise(n, g, device), _noise(n, g, device), _noise(n, g, device)]
     I = (1.0, 0.0, 0.0, 0.0, 1.0, 0.0, 0.0, 0.0, 1.0)
     ports = [_port((0.005, 0.1, 0.1), I, (0.005, 0.1, 0.1), INLET, 4),
              _port((nx * dp - 0.005, 0.1, 0.1), I, (0.005, 0.1, 0.1), OUTLET, 4)]
-    v = _project_near_ports(xyz, v, ports[:1], dim, 2 * dp)
+
+    def vel(x, idx):
+        nz = [c if idx is None else c[idx] for c in noise]
+        return _project_near_ports(x, [1.0 + nz[0], nz[1], nz[2]], ports[:1], dim, 2 * dp)
+    xyz, v, nre = _screen(base, xyz, vel, ids, ports, dim, dp, cs, f32(0.0002), n_updates, SEED_BASE + 3)
     pad = 4
     lo = (f32(-pad * cs),) * 3
     ncell = (int(math.ceil(L / cs)) + 2 * pad, int(math.ceil(0.2 / cs)) + 2 * pad, int(math.ceil(0.2 / cs)) + 2 * pad)
     grid = Grid(dim, lo, cs, ncell)
     return Workload("C3" if scale == 1.0 else f"C3x{scale:g}", dim, dp, h, grid, ports,
                     _pack_state(xyz, v, ids, dim), f32(0.0002), n_updates, n,
-                    notes=f"{nx}x80x80 lattice duct; inlet x in (0,0.01), outlet at x={nx * dp:g}")
+                    notes=f"{nx}x80x80 lattice duct; inlet x in (0,0.01), outlet at x={nx * dp:g}; {nre} re-drawn",
+                    redrawn=nre)
 
 
 def _draw_ports(rng, nports, box_lo, box_hi, dp, cs, steps, dt, existing, x_margin_lo=True, x_margin_hi=True,
@@ -404,16 +626,19 @@ def _preclear(xyz, ports, dp, cs, steps, dt):
     return keep
 
 
-def _nearest_port_velocity(xyz, ports, n, g, device, dp):
-    best = torch.full((n,), float("inf"), dtype=torch.float64, device=device)
-    v = [torch.zeros(n, dtype=torch.float64, device=device) for _ in range(3)]
+def _nearest_port_velocity(xyz, ports, noise, dp):
+    """v = u of the nearest port origin + noise, axial only near the ports."""
+    m = xyz[0].numel()
+    dev = xyz[0].device
+    best = torch.full((m,), float("inf"), dtype=torch.float64, device=dev)
+    v = [torch.zeros(m, dtype=torch.float64, device=dev) for _ in range(3)]
     for p in ports:
         d2 = sum((xyz[j] - p.origin[j]) ** 2 for j in range(3))
         sel = d2 < best
         best = torch.where(sel, d2, best)
         for j in range(3):
             v[j] = torch.where(sel, torch.full_like(v[j], p.Q[j]), v[j])
-    v = [v[j] + _noise(n, g, device) for j in range(3)]
+    v = [v[j] + noise[j] for j in range(3)]
     return _project_near_ports(xyz, v, ports, 3, 2 * dp)
 
 
@@ -430,22 +655,27 @@ def c4(device="cpu", n_updates=100, scale=1.0, nports=8) -> Workload:
     bc = (0.1 * scale, 0.2 * scale) if scale < 1 else (0.1, 0.2)
     ports, _ = _draw_ports(rng, nports, (0, 0, 0), box, dp, cs, n_updates, dt, [], bc_range=bc)
     g = _gen(SEED_BASE + 4, device)
-    xyz, ids = _lattice(counts, dp, device)
+    base, ids = _lattice(counts, dp, device)
     n0 = ids.numel()
-    for j in range(3):
-        xyz[j] = xyz[j] + _jitter(n0, g, device, dp)
+    xyz = [base[j] + _jitter(n0, g, device, dp) for j in range(3)]
     keep = _preclear(xyz, ports, dp, cs, n_updates, dt)
     xyz = [c[keep] for c in xyz]
+    base = [c[keep] for c in base]
     ids = ids[keep]
     n = ids.numel()
-    v = _nearest_port_velocity(xyz, ports, n, g, device, dp)
+    noise = [_noise(n, g, device) for _ in range(3)]
+
+    def vel(x, idx):
+        return _nearest_port_velocity(x, ports, [c if idx is None else c[idx] for c in noise], dp)
+    xyz, v, nre = _screen(base, xyz, vel, ids, ports, dim, dp, cs, f32(dt), n_updates, SEED_BASE + 4)
     pad = 10
     lo = (f32(-pad * cs),) * 3
     ncell = tuple(int(math.ceil(b / cs)) + 2 * pad for b in box)
     grid = Grid(dim, lo, cs, ncell)
     return Workload("C4" if scale == 1.0 else f"C4x{scale:g}", dim, dp, h, grid, ports,
                     _pack_state(xyz, v, ids, dim), f32(dt), n_updates, n0,
-                    notes=f"{counts} lattice junction, {nports} random ports, pre-cleared")
+                    notes=f"{counts} lattice junction, {nports} random ports, pre-cleared; {nre} re-drawn",
+                    redrawn=nre)
 
 
 C5_SLAB_LEN = 1.6
@@ -497,15 +727,21 @@ def c5(device="cpu", slab=0, nslabs=1, scale=1.0, n_updates=50) -> Workload:
     shaping = [p for r in (slab - 1, slab, slab + 1) if 0 <= r < len(per_slab) for p in per_slab[r]]
     g = _gen(SEED_BASE + 5 + 1000 * slab, device)
     per = counts[0] * counts[1] * counts[2]
-    xyz, ids = _lattice(counts, dp, device, origin=(L * slab, 0.0, 0.0), index_offset=per * slab)
+    base, ids = _lattice(counts, dp, device, origin=(L * slab, 0.0, 0.0), index_offset=per * slab)
     n0 = ids.numel()
-    for j in range(3):
-        xyz[j] = xyz[j] + _jitter(n0, g, device, dp)
+    xyz = [base[j] + _jitter(n0, g, device, dp) for j in range(3)]
     keep = _preclear(xyz, shaping, dp, cs, n_updates, dt)
     xyz = [c[keep] for c in xyz]
+    base = [c[keep] for c in base]
     ids = ids[keep]
     n = ids.numel()
-    v = _nearest_port_velocity(xyz, shaping, n, g, device, dp)
+    noise = [_noise(n, g, device) for _ in range(3)]
+
+    def vel(x, idx):
+        return _nearest_port_velocity(x, shaping, [c if idx is None else c[idx] for c in noise], dp)
+    # screened against the ports of slabs r-1..r+1 whatever nslabs is, so slab r's
+    # content does not depend on the number of GPUs
+    xyz, v, nre = _screen(base, xyz, vel, ids, shaping, dim, dp, cs, f32(dt), n_updates, SEED_BASE + 5 + 1000 * slab)
     pad_x, pad_yz = C5_PAD_X, C5_PAD_YZ
     lo = (f32(-pad_x * cs), f32(-pad_yz * cs), f32(-pad_yz * cs))
     nyz = int(math.ceil(W / cs)) + 2 * pad_yz
@@ -518,8 +754,8 @@ def c5(device="cpu", slab=0, nslabs=1, scale=1.0, n_updates=50) -> Workload:
     grid = Grid(dim, lo, cs, ncell, slabs[slab][0], slabs[slab][1])
     name = "C5" if scale == 1.0 else f"C5x{scale:g}"
     return Workload(name, dim, dp, h, grid, ports, _pack_state(xyz, v, ids, dim), f32(dt), n_updates, C5_NEXT_ID,
-                    notes=f"slab {slab}/{nslabs}, {counts} lattice per slab, 8 ports per slab",
-                    slab_cells=slabs)
+                    notes=f"slab {slab}/{nslabs}, {counts} lattice per slab, 8 ports per slab; {nre} re-drawn",
+                    slab_cells=slabs, redrawn=nre)
 
 
 # ----------------------------------------------------------------- rotating sprinkler (moving ports)

@@ -11,6 +11,11 @@ if ROOT not in sys.path:
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")
     config.addinivalue_line("markers", "slow: long-running case")
+    # every oracle decision in the suite is certified tie-free (north_star: >= 1e-4 dp
+    # from any threshold), so the oracle's f64 decisions are the exact ones the GPU
+    # (fp32) must reproduce bit for bit
+    import oracle
+    oracle.enable_tie_check(1e-4)
 
 
 def pytest_collection_modifyitems(config, items):

@@ -1,5 +1,10 @@
 """Shared helpers for the GPU parity tests: run the CUDA path (through the C ABI)
-and the CPU oracle in lock-step on the same seeded inputs and compare."""
+and the CPU oracle in lock-step on the same seeded inputs and compare.
+
+The oracle decides in f64 from the plain definition; the GPU
+decides in fp32.  They must agree bit for bit because the inputs are tie-screened:
+``certify_margins`` asserts, at every decision and relabel point the oracle sees,
+that no particle is within TIE_TAU_DP * dp of a threshold face (north_star; O7)."""
 import numpy as np
 import torch
 
@@ -7,6 +12,19 @@ import oracle
 from paper_2406_16786_b200 import inputs, sphbuf
 
 MAXP = sphbuf.MAX_PORTS
+TIE_TAU_DP = 1e-4            # north_star (BASELINE.json): >= 1e-4 dp from any threshold
+
+
+def certify_margins(st, grid, ports, dp, what=""):
+    """O7: assert every particle of ``st`` is at least 1e-4 dp from every threshold
+    face of InBox_k / P_k (oracle.tie_margin, f64).  Returns the minimum margin / dp."""
+    if not ports or len(st["x"]) == 0:
+        return float("inf")
+    m, bad = oracle.tie_margin(st, grid, ports, TIE_TAU_DP * dp)
+    assert len(bad) == 0, f"{what}: {len(bad)} particles within 1e-4 dp of a threshold (min {m / dp:.3g} dp)"
+    return m / dp
+
+
 COLS = ("x", "y", "z", "vx", "vy", "vz")
 
 
@@ -44,7 +62,7 @@ def make_updater(w, capacity=None, max_new=None, n_extra=0):
 
 
 def lockstep(w, n_updates, check_cll=True, state=None, next_id=None, capacity=None, max_new=None,
-             check_every=1, fused=False, deferred=False):
+             check_every=1, fused=False, deferred=False, margins=True):
     """deferred: the GPU runs sph_compact_deferred; the tombstones then vanish in the
     next cell-list build, so states are compared in cell-list order (every checked
     step and once more after the last update) instead of post-compaction order."""
@@ -55,6 +73,8 @@ def lockstep(w, n_updates, check_cll=True, state=None, next_id=None, capacity=No
     K = len(w.ports)
     st0 = state if state is not None else w.state
     st = oracle.to_numpy_state(st0)
+    if margins:
+        certify_margins(st, w.grid, w.ports, w.dp, "registration")
     mem_o = [oracle.register(st, w.grid, p, k) for k, p in enumerate(w.ports)]
     bu = make_updater(w, capacity, max_new, n_extra=len(st.get("extra") or []))
     bu.load({k: (v if k == "extra" else torch.as_tensor(v)) for k, v in st0.items()} if state is not None
@@ -67,9 +87,13 @@ def lockstep(w, n_updates, check_cll=True, state=None, next_id=None, capacity=No
     tot = np.zeros(2, np.int64)
     for step in range(n_updates):
         oracle.advect(st, dim, w.dt)
+        if margins:
+            certify_margins(st, w.grid, w.ports, w.dp, f"decision point, update {step}")
         res = oracle.update(w.grid, w.ports, st)
         assert res.multi_decision == 0
         new, perm, nid = oracle.compact(res, dim, K, res.port_counts[None, :], 0, nid)
+        if margins:
+            certify_margins(new, w.grid, w.ports, w.dp, f"relabel point, update {step}")
         if fused:
             bu.cll_build(dt=w.dt)          # sph_advect_cll_build
         else:

@@ -118,18 +118,30 @@ def test_velocity_bc_profile_hand_cases():
     np.testing.assert_allclose([S3["vx"][0], S3["vy"][0], S3["vz"][0]], [0.0, 0.75, 0.0], atol=1e-6)
 
 
-def bc_workloads():
-    """C2 with pressure BCs (density column) on both bidirectional ports; a C3 duct
-    with a radial velocity profile at the inlet and a pressure BC at the outlet."""
+def _bc_w2():
     w2 = inputs.make("C2")
     bcp = BC(BC_PRESSURE, rho0=1000.0, c0=10.0, p_b=5.0, rho_column=0)
     w2.ports = with_bc(w2.ports, [bcp, bcp])
     w2.state["extra"] = [torch.full((w2.n,), 1000.0)]
+    return w2
+
+
+def _bc_w3():
     w3 = inputs.c3(scale=0.25, n_updates=30)
     w3.ports = with_bc(w3.ports, [BC(BC_VELOCITY, profile=PROFILE_PARABOLIC_RADIAL, u0=1.0, radius=0.1),
                                   BC(BC_PRESSURE, rho0=1.0, c0=10.0, p_b=0.0, rho_column=0)])
     w3.state["extra"] = [torch.ones(w3.n)]
-    return [(w2, 20), (w3, 30)]
+    return w3
+
+
+def bc_workloads():
+    """C2 with pressure BCs (density column) on both bidirectional ports; a C3 duct
+    with a radial velocity profile at the inlet and a pressure BC at the outlet.
+    The BCs change the buffer particles' velocities, so both are tie-screened on
+    their own dynamics (tests/tiescreen.py)."""
+    from tiescreen import screened, static_dry_run
+    return [(screened("bc-C2", _bc_w2, static_dry_run(20)), 20),
+            (screened("bc-C3", _bc_w3, static_dry_run(30)), 30)]
 
 
 @pytest.mark.gpu

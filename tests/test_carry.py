@@ -32,7 +32,11 @@ def test_carry_survives_any_call_sequence():
     """Fused builds (carry made and used), a change of dt (carried keys cleared), a
     standalone advection + plain build, deferred and in-place compactions mixed:
     the state after every update equals the oracle's."""
-    w = inputs.make("C2")
+    from tiescreen import screened, static_dry_run
+    plan = ["fused", "fused", "dt2", "fused", "split", "fused", "fused", "split", "dt2", "dt2", "fused"]
+    w0 = inputs.make("C2")
+    dts = [w0.dt * (0.5 if mode == "dt2" else 1.0) for mode in plan]
+    w = screened("carry-C2", lambda: inputs.make("C2"), static_dry_run(len(plan), dts))
     K = len(w.ports)
     st = oracle.to_numpy_state(w.state)
     for k, p in enumerate(w.ports):
@@ -41,7 +45,6 @@ def test_carry_survives_any_call_sequence():
     bu.load(w.state, w.next_id)
     bu.register_ports()
     nid = w.next_id
-    plan = ["fused", "fused", "dt2", "fused", "split", "fused", "fused", "split", "dt2", "dt2", "fused"]
     for n, mode in enumerate(plan):
         dt = w.dt * (0.5 if mode == "dt2" else 1.0)
         oracle.advect(st, w.dim, dt)

@@ -92,9 +92,7 @@ def test_port_flux_by_hand():
     assert abs(oracle.port_flux(st, 2, rot, 1) / 2 ** 32 - 2.0) < 1e-6
 
 
-def duct_with_drivers(scale=0.25, n_updates=40):
-    """C3 duct: Fourier plug inlet (Table I), Windkessel outlet (Table II descending
-    aorta), pressure BC with a density column."""
+def _duct_with_drivers(scale, n_updates, nudges):
     w = inputs.c3(scale=scale, n_updates=n_updates)
     inlet, outlet = w.ports
     dp = w.dp
@@ -106,7 +104,42 @@ def duct_with_drivers(scale=0.25, n_updates=40):
                     BC(BC_PRESSURE, rho0=1060.0, c0=40.0, p_b=0.0, rho_column=0),
                     Driver(DRIVER_WINDKESSEL, Rp=Rp, C=Cc, Rd=Rd, P0=1.0e4, volume=dp ** 3))]
     w.state["extra"] = [torch.full((w.n,), 1060.0)]
-    return w
+    return inputs.nudge(w, nudges)
+
+
+_SCREENED = {}
+
+
+def duct_with_drivers(scale=0.15, n_updates=40):
+    """C3 duct: Fourier plug inlet (Table I), Windkessel outlet (Table II descending
+    aorta), pressure BC with a density column.  The driven inlet speed changes the
+    buffer particles' motion, so the input is tie-screened on this test's own
+    dynamics (tests/tiescreen.py)."""
+    from tiescreen import screen
+    key = (scale, n_updates)
+    if key not in _SCREENED:
+        def dry_run(w, lin):
+            st = oracle.to_numpy_state(w.state)
+            for k, p in enumerate(w.ports):
+                oracle.register(st, w.grid, p, k)
+            drv = _OracleDrivers(w)
+            nid = w.next_id
+            for n in range(n_updates):
+                oracle.advect(st, 3, w.dt)
+                ports, rho, Q = drv.step(st, (n + 1) * w.dt)
+                res = oracle.update(w.grid, ports, st, rho_b=rho)
+                new, perm, nid = oracle.compact(res, 3, 2, res.port_counts[None, :], 0, nid)
+                lin.record(res, new)
+                st = new
+        nudges = {}
+
+        def make(nd):
+            nudges.clear()
+            nudges.update(nd)
+            return _duct_with_drivers(scale, n_updates, nd)
+        screen(make, dry_run)
+        _SCREENED[key] = dict(nudges)
+    return _duct_with_drivers(scale, n_updates, _SCREENED[key])
 
 
 class _OracleDrivers:

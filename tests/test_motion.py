@@ -26,6 +26,49 @@ from paper_2406_16786_b200 import inputs
 from paper_2406_16786_b200.inputs import INLET, Port, f32, frame_rows_2d
 
 from parity_util import assert_state_equal, gpu_counts_to_oracle, make_updater
+from tiescreen import screen
+
+_SCREENED = {}
+
+
+def _moving_dry_run(pose_fn, n_steps):
+    """The oracle sequence of a moving-port run (advect, update, compact, move every
+    port to its next pose) for the tie screen (tests/tiescreen.py)."""
+    def run(w, lin):
+        K = len(w.ports)
+        st = oracle.to_numpy_state(w.state)
+        for k, p in enumerate(w.ports):
+            oracle.register(st, w.grid, p, k)
+        ports = list(w.ports)
+        nid = w.next_id
+        for step in range(n_steps):
+            oracle.advect(st, w.dim, w.dt)
+            res = oracle.update(w.grid, ports, st)
+            new, perm, nid = oracle.compact(res, w.dim, K, res.port_counts[None, :], 0, nid)
+            lin.record(res, new)
+            for k, (o, Q) in pose_fn(w, step).items():
+                nxt = Port(o, Q, ports[k].half_extents, ports[k].kind, ports[k].layers, ports[k].bc)
+                oracle.port_move(new, w.dim, ports[k], nxt, k)
+                ports[k] = nxt
+            st = new
+    return run
+
+
+def screened(name, device="cpu", n_steps=200):
+    """C6 / C7 tie-screened on their own moving-port dynamics over n_steps."""
+    key = (name, device, n_steps)
+    pose = (lambda w, s: dict(enumerate(_sprinkler_poses(w, s)))) if name == "C6" else \
+        (lambda w, s: {0: _c7_pose(w, s)})
+    if key not in _SCREENED:
+        got = {}
+
+        def make(nd):
+            got.clear()
+            got.update(nd)
+            return inputs.nudge(inputs.make(name, device=device), nd)
+        screen(make, _moving_dry_run(pose, n_steps))
+        _SCREENED[key] = dict(got)
+    return inputs.nudge(inputs.make(name, device=device), _SCREENED[key])
 
 
 def _one(st_pts, vel, labels):
@@ -110,7 +153,7 @@ def test_sprinkler_oracle_invariants():
     member counts stay 32, brute force = cell-restricted decisions at the current
     pose, every duplicate lies just past its nozzle's interface (a/2 < X'_0 <
     a/2 + |v| dt) in the pose of its step, and every emitted particle stays fluid."""
-    w = inputs.make("C6")
+    w = screened("C6", n_steps=100)
     K = len(w.ports)
     st = oracle.to_numpy_state(w.state)
     for k, p in enumerate(w.ports):
@@ -147,7 +190,7 @@ def test_sprinkler_oracle_invariants():
 def test_sprinkler_gpu_parity(n_steps=200):
     """Lock-step GPU (sph_port_move through the C ABI) vs oracle, 200 updates,
     bit-exact state after every update."""
-    w = inputs.make("C6", device="cuda")
+    w = screened("C6", device="cuda", n_steps=n_steps)
     K = len(w.ports)
     st = oracle.to_numpy_state(w.state)
     for k, p in enumerate(w.ports):
@@ -194,7 +237,7 @@ def test_rotating_port_3d_oracle_invariants():
     """3-D port turning about (1,1,1) (C7), 60 updates on the oracle: inlet member
     count constant, brute force = cell-restricted decisions at every pose, no
     particle with two decisions, no motion error."""
-    w = inputs.make("C7")
+    w = screened("C7", n_steps=60)
     K = len(w.ports)
     st = oracle.to_numpy_state(w.state)
     m0 = [oracle.register(st, w.grid, p, k) for k, p in enumerate(w.ports)]
@@ -219,7 +262,7 @@ def test_rotating_port_3d_oracle_invariants():
 def test_rotating_port_3d_gpu_parity(n_steps=100):
     """C7 on the GPU (3-D K9 move, 3-D K10 enumeration) vs the oracle, 100 updates,
     bit-exact; the in-place compaction every update."""
-    w = inputs.make("C7", device="cuda")
+    w = screened("C7", device="cuda", n_steps=n_steps)
     K = len(w.ports)
     st = oracle.to_numpy_state(w.state)
     for k, p in enumerate(w.ports):

@@ -248,7 +248,8 @@ def test_strict_inequalities_at_faces():
     neither in the box nor crossing."""
     p = mkport((0.5, 0.25, 0), np.eye(3), (0.25, 0.125, 0), OUTLET)     # exact binary fractions
     st = mkstate([[0.75, 0.25], [0.5, 0.375], [0.5, 0.25]], 2)
-    res, new, perm, nid = run1(GRID2, [p], st)
+    with oracle.no_tie_check():          # exact ties on purpose: the definition's strictness
+        res, new, perm, nid = run1(GRID2, [p], st)
     assert list(res.port_counts) == [0, 0]
     lab = dict(zip(new["id"].tolist(), new["label"].tolist()))
     assert lab == {0: -1, 1: -1, 2: 0}
@@ -291,7 +292,8 @@ def test_C3_inlet_members_lattice_count():
 
 # ----------------------------------------------------------- invariants (§8(c) O7)
 
-def _check_step(grid, ports, st, next_id, dt):
+
+def _check_step(grid, ports, st, next_id, dt, dp):
     """One update with every O7 self-check; returns (new_state, next_id)."""
     dim = grid.dim
     K = len(ports)
@@ -336,17 +338,10 @@ def _check_step(grid, ports, st, next_id, dt):
         xl = oracle.to_local(p, dim, [res.sorted[c][j] for c in ("x", "y", "z")[:dim]], prec=1)
         assert abs(xl[0]) < p.half_extents[0]
         np.testing.assert_allclose(xl[1:dim], xl_old[1:dim], atol=2e-6)
-    # f64 decisions agree with pinned fp32 away from ties
-    res64 = oracle.update(grid, ports, st, mode=0, prec=1)
-    diff = np.nonzero((res64.create_port != res.create_port) | (res64.delete_port != res.delete_port))[0]
-    for j in diff:
-        near = False
-        for p in ports:
-            xl = oracle.to_local(p, dim, [res.sorted[c][j] for c in ("x", "y", "z")[:dim]], prec=1)
-            faces = [abs(abs(xl[r]) - p.half_extents[r]) for r in range(dim)]
-            faces += [abs(abs(xl[r]) - p.half_extents[r] - grid.cs) for r in range(dim)]
-            near |= min(faces) < 1e-6
-        assert near, "f64 and fp32 decisions differ away from a face"
+    # the input is valid: no particle within 1e-4 dp of a threshold at the decision
+    # point (north_star; O7), so the f64 decisions above are the exact ones
+    m, bad = oracle.tie_margin(st, grid, ports, 1e-4 * dp)
+    assert len(bad) == 0, f"tie: min margin {m}"
     # ledger
     new, perm, nid = oracle.compact(res, dim, K, res.port_counts[None, :], 0, next_id)
     C_ = int(res.port_counts[:K].sum())
@@ -360,8 +355,7 @@ def _check_step(grid, ports, st, next_id, dt):
     for k, p in enumerate(ports):
         if p.kind == INLET:
             assert np.sum(new["label"] == k) == np.sum(before["label"] == k)
-    # outlet / bidirectional membership == brute-force in-box scan, numpy f64,
-    # ignoring particles within 1e-6 of a face (there fp32 and f64 may differ)
+    # outlet / bidirectional membership == brute-force in-box scan, numpy f64
     old_mask = new["id"] < next_id
     P = np.stack([new[c][old_mask].astype(np.float64) for c in ("x", "y", "z")[:dim]], 1)
     for k, p in enumerate(ports):
@@ -371,9 +365,8 @@ def _check_step(grid, ports, st, next_id, dt):
         XL = (P - np.asarray(p.origin[:dim], np.float64)) @ Qm.T
         he = np.asarray(p.half_extents[:dim], np.float64)
         inb = np.all(np.abs(XL) < he, axis=1)
-        tie = np.any(np.abs(np.abs(XL) - he) < 1e-6, axis=1)
         lab = new["label"][old_mask] == k
-        assert np.all((lab == inb) | tie)
+        assert np.all(lab == inb)
     return new, nid, res
 
 
@@ -382,7 +375,7 @@ def test_invariants_C1e():
     st = oracle.to_numpy_state(w.state)
     for k, p in enumerate(w.ports):
         oracle.register(st, w.grid, p, k)
-    _check_step(w.grid, w.ports, st, w.next_id, w.dt)
+    _check_step(w.grid, w.ports, st, w.next_id, w.dt, w.dp)
 
 
 @pytest.mark.slow
@@ -394,7 +387,7 @@ def test_invariants_C2_bidirectional_steps():
     nid = w.next_id
     tot = np.zeros(4, int)
     for _ in range(6):
-        st, nid, res = _check_step(w.grid, w.ports, st, nid, w.dt)
+        st, nid, res = _check_step(w.grid, w.ports, st, nid, w.dt, w.dp)
         tot += res.port_counts
     assert tot[:2].sum() > 0 and tot[2:].sum() > 0      # both generation and deletion happen
 
@@ -407,7 +400,7 @@ def test_invariants_3d_junction_small():
     nid = w.next_id
     tot = np.zeros(8, int)
     for _ in range(3):
-        st, nid, res = _check_step(w.grid, w.ports, st, nid, w.dt)
+        st, nid, res = _check_step(w.grid, w.ports, st, nid, w.dt, w.dp)
         tot += res.port_counts
     assert tot[:4].sum() > 0 and tot[4:].sum() > 0
 
@@ -468,3 +461,62 @@ def test_ids_independent_of_slab_split():
     order_cat = np.argsort(cat["id"])
     for k in ref:
         np.testing.assert_array_equal(ref[k][order_ref], cat[k][order_cat])
+
+
+# ----------------------------------------------------------- tie screen (north_star, O7)
+
+def _certified_run(w, steps):
+    """Run the oracle over ``steps`` updates and return the minimum tie margin / dp
+    over every decision point (registration, after each advection) and relabel point
+    (after each update).  No oracle code shapes the input: the generator screens
+    with its own kinematic model (inputs._tie_flags); this is the independent check."""
+    tau = 1e-4 * w.dp
+    st = oracle.to_numpy_state(w.state)
+    K = len(w.ports)
+    mins = []
+    m, bad = oracle.tie_margin(st, w.grid, w.ports, tau)
+    assert len(bad) == 0
+    mins.append(m)
+    for k, p in enumerate(w.ports):
+        oracle.register(st, w.grid, p, k)
+    nid = w.next_id
+    for s in range(steps):
+        oracle.advect(st, w.dim, w.dt)
+        m, bad = oracle.tie_margin(st, w.grid, w.ports, tau)
+        assert len(bad) == 0, f"{w.name} update {s}: {len(bad)} ties at the decision point"
+        mins.append(m)
+        res = oracle.update(w.grid, w.ports, st)
+        assert res.multi_decision == 0
+        st, perm, nid = oracle.compact(res, w.dim, K, res.port_counts[None, :], 0, nid)
+        m, bad = oracle.tie_margin(st, w.grid, w.ports, tau)
+        assert len(bad) == 0, f"{w.name} update {s}: {len(bad)} ties at the relabel point"
+        mins.append(m)
+    return min(mins) / w.dp
+
+
+@pytest.mark.parametrize("name,make,steps", [
+    ("C1e", lambda: inputs.c1e(n_updates=20), 20),
+    ("C2", lambda: inputs.c2(), 100),
+    ("C3x0.1", lambda: inputs.c3(scale=0.1, n_updates=100), 100),
+    ("C4x0.25", lambda: inputs.c4(scale=0.25, nports=4, n_updates=10), 10),
+    ("C5x0.3 slab 1/2", lambda: inputs.c5(scale=0.3, slab=1, nslabs=2, n_updates=6), 6),
+])
+def test_tie_screen_margin_certified(name, make, steps):
+    """north_star: "The generator keeps every particle at least 1e-4 dp from any
+    threshold, so no decision is a tie."  Certified by the oracle (f64) over the
+    whole horizon the generator screened, on the configs the GPU tests run."""
+    w = make()
+    m = _certified_run(w, steps)
+    assert m >= 1e-4, (name, m)
+
+
+def test_tie_screen_redraws_only_flagged_particles():
+    """The screen re-draws a few particles and leaves every other one bitwise as the
+    unscreened recipe draws it (same seeded streams)."""
+    w = inputs.c3(scale=0.1, n_updates=100)
+    w0 = inputs.c3(scale=0.1, n_updates=0)         # horizon 0: only the registration point
+    assert 0 < w.redrawn < 0.01 * w.n
+    diff = (w.state["x"] != w0.state["x"]) | (w.state["y"] != w0.state["y"]) | (w.state["z"] != w0.state["z"])
+    assert int(diff.sum()) <= w.redrawn
+    lat = (w.state["id"] // 6400).double() * 0.0025 + 0.00125       # x lattice site of each id
+    assert float((w.state["x"].double() - lat).abs().max()) <= 0.1 * 0.0025 * (1 + 1e-6)
