@@ -53,6 +53,8 @@ typedef enum {
     SPH_ERR_MOTION = -6,           /* (device) a buffer particle found outside its decision region P_k
                                       (it moved more than the one-cell margin in one step; reading R12) */
     SPH_ERR_CUDA = -7,             /* a CUDA runtime call failed (see sph_last_error) */
+    SPH_ERR_NCCL = -8,             /* an NCCL call failed or NCCL could not be loaded (see sph_last_error);
+                                      asynchronous NCCL errors are reported by sph_status_sync */
     SPH_ERR_STATE = -9             /* call order violated: no workspace; sph_buffer_update while the
                                       previous update is not compacted; sph_compact(_deferred) with
                                       no update to compact; a build or migration pack in between */
@@ -325,8 +327,71 @@ int32_t sph_migrate_record_floats(const sph_ctx *ctx);
 sph_status sph_migrate_pack(sph_ctx *ctx, sph_particles *p, float *send_lo, float *send_hi, void *stream);
 sph_status sph_migrate_unpack(sph_ctx *ctx, sph_particles *p, const float *recv, void *stream);
 
+/* Multi-GPU x-slab decomposition: one process per GPU, each rank
+ * a context whose grid slab [cx_begin, cx_end) is its share of the x cell
+ * columns.  The decomposition shards naturally because the buffers are spatially
+ * local: the candidates lie in "the nearby local cell-linked lists".
+ * Per update two exchanges, both enqueued on the caller's stream (no host
+ * synchronisation, so a P-rank update can be captured in one CUDA graph):
+ *   neighbour migration   particles whose cell left the slab go to rank r-1 / r+1
+ *                         (they move less than one cell per update);
+ *   count allgather       every rank's per-port created / deleted counts -> the
+ *                         count matrix sph_compact turns into IDs identical for
+ *                         every number of GPUs (reading R14).
+ * The library owns its communicator: NCCL (libnccl.so.2, loaded with dlopen at
+ * the first call; in a torch process this is torch's NCCL) over NVLink /
+ * NVSwitch, or an in-process loopback group for tests.  Migration messages are
+ * fixed-size (4 header words + max_migrate records, sph_ctx_create), so no count
+ * has to reach the host: size max_migrate to the expected migrants per face with
+ * headroom; overflow is reported as SPH_ERR_CAPACITY by sph_status_sync.  The
+ * migration buffers live in the workspace (sph_workspace_bytes includes them
+ * when max_migrate > 0). */
+#define SPH_COMM_ID_BYTES 128
+
+/* Rank 0: a fresh NCCL unique id (SPH_COMM_ID_BYTES bytes) for the caller to
+ * broadcast to every rank (e.g. torch.distributed.broadcast). */
+sph_status sph_comm_unique_id(void *id_out);
+
+/* Collective over the nranks processes: create this rank's NCCL communicator
+ * from the broadcast id.  Needs the workspace set and, for nranks > 1,
+ * max_migrate > 0.  Blocks until every rank has joined.  SPH_ERR_NCCL on
+ * failure; SPH_ERR_STATE if the context already has a communicator. */
+sph_status sph_comm_init(sph_ctx *ctx, const void *nccl_unique_id, int32_t nranks, int32_t rank);
+
+/* Tests: the contexts ctxs[0..nranks) of this process (one device, rank r =
+ * ctxs[r]) form a loopback group: the exchanges below become device copies on
+ * the caller's stream.  Phase-ordered use only (every rank's pack before any
+ * exchange, every update before any allgather); sph_migrate and
+ * sph_migrate_cll_build are refused (SPH_ERR_STATE). */
+sph_status sph_comm_init_loopback(sph_ctx *const *ctxs, int32_t nranks);
+
+/* all_counts [nranks][2 max_ports] (device int32) <- every rank's port_counts
+ * [2 max_ports] (as written by sph_buffer_update): ncclAllGather on `stream`.
+ * Without a communicator (one rank) a device copy. */
+sph_status sph_allgather_counts(sph_ctx *ctx, const int32_t *port_counts, int32_t *all_counts, void *stream);
+
+/* Neighbour exchange of the library's migration buffers: send lo -> rank r-1,
+ * send hi -> rank r+1 and the matching receives, in one NCCL group
+ * (ncclGroupStart / ncclSend / ncclRecv / ncclGroupEnd). */
+sph_status sph_migrate_exchange(sph_ctx *ctx, void *stream);
+
+/* Standalone migration (between an advection and a plain sph_cll_build):
+ * pack the particles whose cell left the slab (tombstoned), exchange, append
+ * the received ones.  No-op on one rank. */
+sph_status sph_migrate(sph_ctx *ctx, sph_particles *p, void *stream);
+
+/* The build with the migration fused into its key pass — the per-update call of
+ * a rank: sph_cll_key (advection when advect != 0; leavers packed into the
+ * library's buffers), sph_migrate_exchange, sph_cll_finish (arrivals appended,
+ * then scan, scatter, gather).  With a communicator, sph_cll_key and
+ * sph_cll_finish given NULL buffers use the library's buffers too (the split
+ * form, required by a loopback group). */
+sph_status sph_migrate_cll_build(sph_ctx *ctx, sph_particles *in, sph_particles *out, float dt, int32_t advect,
+                                 int32_t *cell_start, int32_t *cell_end, int32_t *perm_or_null, void *stream);
+
 /* The only synchronising call: waits for `stream`, returns the statistics and
- * the first sticky device error (SPH_ERR_CAPACITY / SPH_ERR_MOTION) if any. */
+ * the first sticky device error (SPH_ERR_CAPACITY / SPH_ERR_MOTION) if any, or
+ * an asynchronous NCCL error (SPH_ERR_NCCL). */
 sph_status sph_status_sync(sph_ctx *ctx, const sph_particles *p, void *stream, sph_stats *out);
 
 /* Number of kernels this context has launched (for the bench's launch count). */

@@ -13,7 +13,7 @@ LIB = os.path.join(HERE, "libsphbuf.so")
 LIB_DEBUG = os.path.join(HERE, "libsphbuf_debug.so")   # -DSPHBUF_DEBUG: device bounds asserts
 LIB_TRACE = os.path.join(HERE, "libsphbuf_trace.so")   # -DSPHBUF_TRACE: per-tile timestamps of the update (tools/)
 SOURCES = ["sphbuf_cll.cu", "sphbuf_update.cu", "sphbuf_compact.cu", "sphbuf_migrate.cu", "sphbuf_motion.cu",
-           "sphbuf_drivers.cu", "sphbuf_host.cpp"]
+           "sphbuf_drivers.cu", "sphbuf_host.cpp", "sphbuf_comm.cpp"]
 DEPS = SOURCES + ["sphbuf_internal.h", "sphbuf_common.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "--fmad=false",
@@ -37,7 +37,8 @@ def build(force: bool = False, verbose: bool = False, debug: bool = False, trace
         return lib
     tmp = lib + f".tmp{os.getpid()}"
     extra = ["-DSPHBUF_DEBUG"] if debug else ["-DSPHBUF_TRACE"] if trace else []
-    cmd = [NVCC, *FLAGS, *extra, "-I", INCLUDE, "-I", CSRC, *[os.path.join(CSRC, s) for s in SOURCES], "-o", tmp]
+    cmd = [NVCC, *FLAGS, *extra, "-I", INCLUDE, "-I", CSRC, *[os.path.join(CSRC, s) for s in SOURCES], "-o", tmp,
+           "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)

@@ -119,7 +119,19 @@ struct sph_ctx {
     const float *carry_x = nullptr;
     const int64_t *carry_id = nullptr;
     CllCarry key_cc{};
+    // multi-GPU (§8(e)): the library's communicator (sph_comm_init / _loopback)
+    Comm *comm = nullptr;
+    const int32_t *last_port_counts = nullptr;   // the last update's counts (loopback allgather source)
 };
+
+namespace {
+// In-process loopback group: contexts of one process on one device exchange
+// through device copies on the caller's stream (tests; no kernel waits on another).
+struct LoopGroup {
+    std::vector<sph_ctx *> m;
+    int live = 0;
+};
+}  // namespace
 
 namespace {
 
@@ -183,6 +195,10 @@ size_t layout(const sph_ctx *c, char *base, Workspace *W)
         w.svz = (float *)take(4 * mn);
     }
     for (int e = 0; e < c->n_extra; ++e) w.sextra[e] = (float *)take(4 * mn);
+    if (c->max_migrate > 0) {
+        const long long mig = 4 + c->max_migrate * (long long)(2 * c->grid.dim + c->n_extra + 3);
+        for (int b = 0; b < 4; ++b) w.mig[b] = (float *)take(4 * mig);
+    }
     w.sid = (long long *)take(8 * mn);
     w.sport = (int *)take(4 * mn);
     w.stile = (int *)take(4 * mn);
@@ -422,7 +438,19 @@ sph_status sph_ctx_create(const sph_grid *grid, float h, int64_t capacity, int32
     return SPH_OK;
 }
 
-void sph_ctx_destroy(sph_ctx *c) { delete c; }
+void sph_ctx_destroy(sph_ctx *c)
+{
+    if (!c) return;
+    if (c->comm) {
+        if (c->comm->kind == Comm::LOOPBACK) {
+            LoopGroup *g = static_cast<LoopGroup *>(c->comm->loop);
+            g->m[c->comm->rank] = nullptr;
+            if (--g->live == 0) delete g;
+        }
+        comm_destroy(c->comm);
+    }
+    delete c;
+}
 
 const char *sph_last_error(const sph_ctx *c) { return c ? c->err.c_str() : "null context"; }
 
@@ -978,6 +1006,10 @@ sph_status sph_cll_key(sph_ctx *c, sph_particles *in, float dt, int32_t advect, 
     sph_status st = check_particles(c, in);
     if (st != SPH_OK) return st;
     if ((send_lo == nullptr) != (send_hi == nullptr)) return fail(c, SPH_ERR_ARG, "give both send buffers or none");
+    if (!send_lo && c->comm && c->comm->nranks > 1) {     // the library's own migration buffers
+        send_lo = c->W.mig[0];
+        send_hi = c->W.mig[1];
+    }
     c->key_advect = advect != 0;
     c->key_dt = dt;
     c->key_cc = carry_plan(c, in, advect != 0, dt, send_lo != nullptr);
@@ -1001,6 +1033,10 @@ sph_status sph_cll_finish(sph_ctx *c, sph_particles *in, sph_particles *out, con
         return fail(c, SPH_ERR_ARG, "cll_finish needs distinct input and output arrays");
     if ((reinterpret_cast<size_t>(cell_start) | reinterpret_cast<size_t>(cell_end)) % 16)
         return fail(c, SPH_ERR_ARG, "cell tables must be 16-byte aligned");
+    if (!recv_lo && !recv_hi && c->comm && c->comm->nranks > 1) {   // the library's own migration buffers
+        if (c->comm->rank > 0) recv_lo = c->W.mig[2];
+        if (c->comm->rank < c->comm->nranks - 1) recv_hi = c->W.mig[3];
+    }
     const UpdPro up = pro_plan(c, cell_start, cell_end);
     cudaError_t e = launch_cll_finish(part_dev(in), part_dev(out), c->gd, c->W, recv_lo, recv_hi, c->max_migrate,
                                       sph_migrate_record_floats(c), cell_start, cell_end, perm, c->key_advect,
@@ -1027,6 +1063,7 @@ sph_status sph_buffer_update(sph_ctx *c, sph_particles *p, const int32_t *cell_s
                                   carry_on(c, p), c->carry_dt, pro_done, static_cast<cudaStream_t>(stream), &c->L);
     if (e != cudaSuccess) return cuda_fail(c, e, "buffer_update");
     c->update_pending = true;
+    c->last_port_counts = port_counts;
     return SPH_OK;
 }
 
@@ -1119,8 +1156,139 @@ sph_status sph_status_sync(sph_ctx *c, const sph_particles *p, void *stream, sph
     out->n_ports = c->pt.n;
     if (h.status & (kStCapacity | kStStaging | kStMigrate))
         return fail(c, SPH_ERR_CAPACITY, "device capacity / staging / migration buffer overflow");
-    if (h.status & kStMotion) return fail(c, SPH_ERR_MOTION, "a buffer particle moved more than a buffer length");
+    if (h.status & kStMotion)
+        return fail(c, SPH_ERR_MOTION, "a buffer particle was found outside its decision region P_k");
+    if (c->comm) {
+        std::string m;
+        if (comm_async_error(c->comm, &m) != 0) return fail(c, SPH_ERR_NCCL, m);
+    }
     return SPH_OK;
+}
+
+// =============================================================================== multi-GPU (§8(e))
+
+sph_status sph_comm_unique_id(void *id_out)
+{
+    if (!id_out) return SPH_ERR_ARG;
+    std::string m;
+    return comm_unique_id(id_out, &m) == 0 ? SPH_OK : SPH_ERR_NCCL;
+}
+
+static sph_status comm_precheck(sph_ctx *c, int32_t nranks, int32_t rank)
+{
+    if (nranks < 1 || rank < 0 || rank >= nranks) return fail(c, SPH_ERR_ARG, "comm: bad rank / nranks");
+    if (c->comm) return fail(c, SPH_ERR_STATE, "comm: already initialised");
+    if (!c->ws) return fail(c, SPH_ERR_STATE, "comm: set the workspace first (it holds the migration buffers)");
+    if (nranks > 1 && c->max_migrate <= 0) return fail(c, SPH_ERR_ARG, "comm: nranks > 1 needs max_migrate > 0");
+    return SPH_OK;
+}
+
+sph_status sph_comm_init(sph_ctx *c, const void *nccl_unique_id, int32_t nranks, int32_t rank)
+{
+    if (!c || !nccl_unique_id) return SPH_ERR_ARG;
+    sph_status st = comm_precheck(c, nranks, rank);
+    if (st != SPH_OK) return st;
+    std::string m;
+    Comm *cm = comm_nccl(nccl_unique_id, nranks, rank, &m);
+    if (!cm) return fail(c, SPH_ERR_NCCL, m);
+    c->comm = cm;
+    return SPH_OK;
+}
+
+sph_status sph_comm_init_loopback(sph_ctx *const *ctxs, int32_t nranks)
+{
+    if (!ctxs || nranks < 1) return SPH_ERR_ARG;
+    for (int r = 0; r < nranks; ++r) {
+        if (!ctxs[r]) return SPH_ERR_ARG;
+        sph_status st = comm_precheck(ctxs[r], nranks, r);
+        if (st != SPH_OK) return st;
+        if (ctxs[r]->max_migrate != ctxs[0]->max_migrate || ctxs[r]->n_extra != ctxs[0]->n_extra ||
+            ctxs[r]->max_ports != ctxs[0]->max_ports || ctxs[r]->grid.dim != ctxs[0]->grid.dim)
+            return fail(ctxs[r], SPH_ERR_ARG, "loopback: members differ in max_migrate / n_extra / max_ports / dim");
+    }
+    LoopGroup *g = new LoopGroup();
+    g->m.assign(ctxs, ctxs + nranks);
+    g->live = nranks;
+    for (int r = 0; r < nranks; ++r) {
+        Comm *cm = new Comm();
+        cm->kind = Comm::LOOPBACK;
+        cm->nranks = nranks;
+        cm->rank = r;
+        cm->loop = g;
+        ctxs[r]->comm = cm;
+    }
+    return SPH_OK;
+}
+
+sph_status sph_allgather_counts(sph_ctx *c, const int32_t *port_counts, int32_t *all_counts, void *stream)
+{
+    if (!c || !port_counts || !all_counts) return SPH_ERR_ARG;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const size_t cnt = 2 * (size_t)c->max_ports;
+    if (!c->comm || (c->comm->nranks == 1 && c->comm->kind == Comm::LOOPBACK)) {
+        cudaError_t e = cudaMemcpyAsync(all_counts, port_counts, cnt * sizeof(int32_t), cudaMemcpyDeviceToDevice, s);
+        return e == cudaSuccess ? SPH_OK : cuda_fail(c, e, "allgather_counts");
+    }
+    std::vector<const int32_t *> loop;
+    if (c->comm->kind == Comm::LOOPBACK) {
+        LoopGroup *g = static_cast<LoopGroup *>(c->comm->loop);
+        for (sph_ctx *m : g->m) loop.push_back(m ? m->last_port_counts : nullptr);
+    }
+    std::string m;
+    if (comm_allgather_i32(c->comm, port_counts, all_counts, cnt, s, loop, &m) != 0)
+        return fail(c, SPH_ERR_NCCL, "allgather_counts: " + m);
+    return SPH_OK;
+}
+
+sph_status sph_migrate_exchange(sph_ctx *c, void *stream)
+{
+    if (!c) return SPH_ERR_ARG;
+    if (!c->comm) return fail(c, SPH_ERR_STATE, "migrate_exchange: no communicator (sph_comm_init)");
+    if (c->comm->nranks == 1) return SPH_OK;
+    const size_t cnt = 4 + (size_t)c->max_migrate * (size_t)sph_migrate_record_floats(c);
+    const float *lo_peer = nullptr, *hi_peer = nullptr;
+    if (c->comm->kind == Comm::LOOPBACK) {
+        LoopGroup *g = static_cast<LoopGroup *>(c->comm->loop);
+        const int r = c->comm->rank;
+        if ((r > 0 && !g->m[r - 1]) || (r < c->comm->nranks - 1 && !g->m[r + 1]))
+            return fail(c, SPH_ERR_STATE, "migrate_exchange: a loopback neighbour was destroyed");
+        if (r > 0) lo_peer = g->m[r - 1]->W.mig[1];
+        if (r < c->comm->nranks - 1) hi_peer = g->m[r + 1]->W.mig[0];
+    }
+    std::string m;
+    if (comm_neighbour_exchange(c->comm, c->W.mig[0], c->W.mig[1], c->W.mig[2], c->W.mig[3], cnt,
+                                static_cast<cudaStream_t>(stream), lo_peer, hi_peer, &m) != 0)
+        return fail(c, SPH_ERR_NCCL, "migrate_exchange: " + m);
+    return SPH_OK;
+}
+
+sph_status sph_migrate(sph_ctx *c, sph_particles *p, void *stream)
+{
+    if (!c) return SPH_ERR_ARG;
+    if (!c->comm) return fail(c, SPH_ERR_STATE, "migrate: no communicator (sph_comm_init)");
+    if (c->comm->nranks == 1) return SPH_OK;
+    if (c->comm->kind == Comm::LOOPBACK)
+        return fail(c, SPH_ERR_STATE, "migrate: a loopback group needs the split calls "
+                                      "(sph_migrate_pack, sph_migrate_exchange, sph_migrate_unpack), phase by phase");
+    sph_status st = sph_migrate_pack(c, p, c->W.mig[0], c->W.mig[1], stream);
+    if (st == SPH_OK) st = sph_migrate_exchange(c, stream);
+    if (st == SPH_OK && c->comm->rank > 0) st = sph_migrate_unpack(c, p, c->W.mig[2], stream);
+    if (st == SPH_OK && c->comm->rank < c->comm->nranks - 1) st = sph_migrate_unpack(c, p, c->W.mig[3], stream);
+    return st;
+}
+
+sph_status sph_migrate_cll_build(sph_ctx *c, sph_particles *in, sph_particles *out, float dt, int32_t advect,
+                                 int32_t *cell_start, int32_t *cell_end, int32_t *perm_or_null, void *stream)
+{
+    if (!c) return SPH_ERR_ARG;
+    if (!c->comm) return fail(c, SPH_ERR_STATE, "migrate_cll_build: no communicator (sph_comm_init)");
+    if (c->comm->kind == Comm::LOOPBACK && c->comm->nranks > 1)
+        return fail(c, SPH_ERR_STATE, "migrate_cll_build: a loopback group needs the split calls "
+                                      "(sph_cll_key, sph_migrate_exchange, sph_cll_finish), phase by phase");
+    sph_status st = sph_cll_key(c, in, dt, advect, nullptr, nullptr, stream);
+    if (st == SPH_OK) st = sph_migrate_exchange(c, stream);
+    if (st == SPH_OK) st = sph_cll_finish(c, in, out, nullptr, nullptr, cell_start, cell_end, perm_or_null, stream);
+    return st;
 }
 
 int64_t sph_launch_count(const sph_ctx *c) { return c ? c->L.count : 0; }

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -171,11 +172,35 @@ struct Workspace {
     int *sport;                      // port of each staged particle
     int *stile, *sexcl;              // update tile of each staged particle and its rank inside the tile:
                                      // canonical slot = tile_pre[stile] + sexcl
+    float *mig[4];                   // library-owned migration buffers: send lo, send hi, recv lo, recv hi
+                                     // (4 header words + max_migrate records each; max_migrate > 0)
     long long max_new;
     long long max_leave;
     long long upd_tiles;
     long long cmp_tiles;
 };
+
+// ---------------------------------------------------------------- communicator (sphbuf_comm.cpp)
+// The library's communicator of the x-slab decomposition: NCCL (loaded with
+// dlopen) or an in-process loopback group (contexts on one device; device copies).
+struct Comm {
+    enum Kind { NCCL, LOOPBACK } kind = NCCL;
+    void *nccl = nullptr;     // ncclComm_t
+    int nranks = 1, rank = 0;
+    void *loop = nullptr;     // LOOPBACK: the group (owned by sphbuf_host.cpp)
+};
+int comm_unique_id(void *out, std::string *err);
+Comm *comm_nccl(const void *id, int nranks, int rank, std::string *err);
+void comm_destroy(Comm *c);
+// recv [nranks][count] <- every rank's send [count]; loop_send: the members' send buffers (LOOPBACK)
+int comm_allgather_i32(Comm *c, const int32_t *send, int32_t *recv, size_t count, cudaStream_t s,
+                       const std::vector<const int32_t *> &loop_send, std::string *err);
+// send_lo -> rank-1 (its recv_hi), send_hi -> rank+1 (its recv_lo); count floats each way;
+// loop_lo_peer / loop_hi_peer: rank-1's send_hi and rank+1's send_lo (LOOPBACK)
+int comm_neighbour_exchange(Comm *c, const float *send_lo, const float *send_hi, float *recv_lo, float *recv_hi,
+                            size_t count, cudaStream_t s, const float *loop_lo_peer, const float *loop_hi_peer,
+                            std::string *err);
+int comm_async_error(Comm *c, std::string *err);
 
 // ---------------------------------------------------------------- launch bookkeeping
 enum KernelId {

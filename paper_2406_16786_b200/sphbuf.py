@@ -24,7 +24,8 @@ INLET, OUTLET, BIDIRECTIONAL = 0, 1, 2
 
 STATUS = {0: "SPH_OK", -1: "SPH_ERR_ARG", -2: "SPH_ERR_NOT_ORTHONORMAL", -3: "SPH_ERR_OVERLAP",
           -4: "SPH_ERR_OUT_OF_GRID", -5: "SPH_ERR_CAPACITY", -6: "SPH_ERR_MOTION", -7: "SPH_ERR_CUDA",
-          -9: "SPH_ERR_STATE"}
+          -8: "SPH_ERR_NCCL", -9: "SPH_ERR_STATE"}
+COMM_ID_BYTES = 128                 # = SPH_COMM_ID_BYTES
 
 
 class SphError(RuntimeError):
@@ -69,7 +70,8 @@ EXPORTS = ["sph_ctx_create", "sph_ctx_destroy", "sph_last_error", "sph_workspace
            "sph_launch_count", "sph_port_cells", "sph_frame_from_axis", "sph_profile", "sph_profile_read",
            "sph_kernel_name", "sph_advect_cll_build", "sph_compact_deferred", "sph_cll_key", "sph_cll_finish",
            "sph_port_set_bc", "sph_port_move", "sph_port_set_driver", "sph_cll_invalidate",
-           "sph_drivers_step", "sph_driver_read"]
+           "sph_drivers_step", "sph_driver_read", "sph_comm_unique_id", "sph_comm_init", "sph_comm_init_loopback",
+           "sph_allgather_counts", "sph_migrate_exchange", "sph_migrate", "sph_migrate_cll_build"]
 NKERNELS = 17                       # = SPH_NKERNELS in include/sphbuf.h
 
 
@@ -133,6 +135,16 @@ def lib():
     L.sph_profile_read.argtypes = [vp, vp, vp]
     L.sph_kernel_name.argtypes = [i32]
     L.sph_kernel_name.restype = C.c_char_p
+    L.sph_comm_unique_id.argtypes = [vp]
+    L.sph_comm_init.argtypes = [vp, vp, i32, i32]
+    L.sph_comm_init_loopback.argtypes = [vp, i32]
+    L.sph_allgather_counts.argtypes = [vp, vp, vp, vp]
+    L.sph_migrate_exchange.argtypes = [vp, vp]
+    L.sph_migrate.argtypes = [vp, P(sph_particles), vp]
+    L.sph_migrate_cll_build.argtypes = [vp, P(sph_particles), P(sph_particles), f32, i32, vp, vp, vp, vp]
+    for name in ("sph_comm_unique_id", "sph_comm_init", "sph_comm_init_loopback", "sph_allgather_counts",
+                 "sph_migrate_exchange", "sph_migrate", "sph_migrate_cll_build"):
+        getattr(L, name).restype = C.c_int
     for name in ("sph_profile", "sph_profile_read","sph_ctx_create", "sph_set_workspace", "sph_port_check", "sph_buffer_register", "sph_advect",
                  "sph_cll_build", "sph_buffer_update", "sph_compact", "sph_migrate_pack", "sph_migrate_unpack",
                  "sph_status_sync", "sph_port_cells", "sph_frame_from_axis"):
@@ -311,6 +323,41 @@ def sph_migrate_pack(ctx, parts, send_lo, send_hi, stream=None):
 
 def sph_migrate_unpack(ctx, parts, recv, stream=None):
     _check(lib().sph_migrate_unpack(ctx.h, C.byref(parts.abi), _ptr(recv), _stream(stream)), ctx.h)
+
+
+def sph_comm_unique_id() -> bytes:
+    buf = (C.c_ubyte * COMM_ID_BYTES)()
+    _check(lib().sph_comm_unique_id(buf))
+    return bytes(buf)
+
+
+def sph_comm_init(ctx, unique_id: bytes, nranks, rank):
+    buf = (C.c_ubyte * COMM_ID_BYTES).from_buffer_copy(unique_id)
+    _check(lib().sph_comm_init(ctx.h, buf, int(nranks), int(rank)), ctx.h)
+
+
+def sph_comm_init_loopback(ctxs):
+    arr = (C.c_void_p * len(ctxs))(*[c.h.value for c in ctxs])
+    rc = lib().sph_comm_init_loopback(arr, len(ctxs))
+    _check(rc, ctxs[0].h if rc else None)
+
+
+def sph_allgather_counts(ctx, port_counts, all_counts, stream=None):
+    _check(lib().sph_allgather_counts(ctx.h, _ptr(port_counts), _ptr(all_counts), _stream(stream)), ctx.h)
+
+
+def sph_migrate_exchange(ctx, stream=None):
+    _check(lib().sph_migrate_exchange(ctx.h, _stream(stream)), ctx.h)
+
+
+def sph_migrate(ctx, parts, stream=None):
+    _check(lib().sph_migrate(ctx.h, C.byref(parts.abi), _stream(stream)), ctx.h)
+
+
+def sph_migrate_cll_build(ctx, pin, pout, dt, cell_start, cell_end, perm=None, stream=None):
+    _check(lib().sph_migrate_cll_build(ctx.h, C.byref(pin.abi), C.byref(pout.abi), float(dt or 0.0),
+                                       0 if dt is None else 1, _ptr(cell_start), _ptr(cell_end), _ptr(perm),
+                                       _stream(stream)), ctx.h)
 
 
 def sph_status_sync(ctx, parts=None, stream=None, check=True) -> dict:

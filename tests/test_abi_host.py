@@ -150,3 +150,24 @@ def test_workspace_bytes_scale():
     w, ctx = ctx_c1()
     b = sphbuf.sph_workspace_bytes(ctx)
     assert b > 16384 * 12
+
+
+def test_comm_host_checks_without_gpu():
+    """The multi-GPU calls validate on the host before touching NCCL or the device:
+    bad rank / nranks -> SPH_ERR_ARG; no workspace yet (it holds the migration
+    buffers) -> SPH_ERR_STATE; an exchange without a communicator -> SPH_ERR_STATE;
+    the NCCL unique id (rank 0's bootstrap) is 128 bytes and fresh per call."""
+    import ctypes as C
+    w = inputs.make("C1")
+    ctx = sphbuf.Context(w.grid, w.h, 16384, 64, 1024, max_migrate=256)
+    L = sphbuf.lib()
+    uid = (C.c_ubyte * sphbuf.COMM_ID_BYTES)()
+    assert L.sph_comm_init(ctx.h, uid, 2, 2) == -1
+    assert L.sph_comm_init(ctx.h, uid, 0, 0) == -1
+    assert L.sph_comm_init(ctx.h, uid, 2, 0) == -9
+    arr = (C.c_void_p * 1)(ctx.h.value)
+    assert L.sph_comm_init_loopback(arr, 1) == -9
+    assert L.sph_migrate_exchange(ctx.h, None) == -9
+    assert L.sph_allgather_counts(ctx.h, None, None, None) == -1
+    a, b = sphbuf.sph_comm_unique_id(), sphbuf.sph_comm_unique_id()
+    assert len(a) == len(b) == 128 and a != b

@@ -1,12 +1,18 @@
 """Multi-rank x-slab decomposition.
 
-* CPU, world size 2, gloo: the product's ``dist.Comm`` (neighbour exchange of
-  fixed-size migration buffers, count allgather) drives a per-rank oracle
-  update; the union of the ranks' states must equal the single-process oracle
-  (same IDs, same columns) after every update.
-* GPU (one device): ``dist.LoopbackGroup`` runs P slabs of the CUDA path in one
-  process (device copies stand in for NCCL); the union must equal the
-  single-process oracle bit-exactly.
+* CPU, world size 2, gloo: the decomposition's host logic — neighbour exchange
+  of fixed-size migration buffers in the library's record layout, count
+  allgather, the ID offset rule — drives a per-rank oracle update; the union of
+  the ranks' states must equal the single-process oracle (same IDs, same
+  columns) after every update.  Rank 0's NCCL unique id reaches every rank
+  through ``dist.broadcast_unique_id`` (the library's bootstrap).
+* GPU (one device): the library's loopback communicator runs P slabs of the
+  CUDA path in one process (``dist.LoopbackGroup``: device copies stand in for
+  NCCL; the same buffers, calls and host logic); the union must equal the
+  single-process oracle bit-exactly — C4 cut into slabs, the C5 weak-scaling
+  workload generated slab by slab (P = 2, 4; straddling ports; both compaction
+  modes), and a P-rank step captured in one CUDA graph.  The library's NCCL
+  communicator runs at world size 1 (two ranks cannot share a GPU under NCCL).
 """
 import os
 import socket
@@ -19,7 +25,7 @@ import torch.multiprocessing as mp
 
 import oracle
 from paper_2406_16786_b200 import inputs
-from paper_2406_16786_b200.dist import Comm, id_offsets
+from paper_2406_16786_b200.dist import broadcast_unique_id, id_offsets
 
 COLS = ("x", "y", "z", "vx", "vy", "vz")
 
@@ -91,10 +97,36 @@ def _world():
     return w, st, cuts
 
 
+class _HostExchange:
+    """The exchange pattern of the library's communicator (sphbuf_comm.cpp) over
+    torch.distributed on CPU: send lo -> rank-1, send hi -> rank+1 (fixed-size
+    buffers, count in the header); allgather of the count vectors."""
+
+    def __init__(self, rank, world):
+        self.rank, self.world = rank, world
+
+    def exchange(self, send_lo, send_hi, recv_lo, recv_hi):
+        ops = []
+        if self.rank > 0:
+            ops.append(dist.P2POp(dist.isend, send_lo, self.rank - 1))
+            ops.append(dist.P2POp(dist.irecv, recv_lo, self.rank - 1))
+        if self.rank < self.world - 1:
+            ops.append(dist.P2POp(dist.isend, send_hi, self.rank + 1))
+            ops.append(dist.P2POp(dist.irecv, recv_hi, self.rank + 1))
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+
+    def allgather_counts(self, counts, out):
+        dist.all_gather_into_tensor(out.view(-1), counts)
+
+
 def _rank_main(rank, world, port, steps, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    comm = Comm(rank, world)
+    uid = broadcast_unique_id(rank)          # the library's NCCL bootstrap (ncclGetUniqueId runs on CPU)
+    assert isinstance(uid, bytes) and len(uid) == 128
+    comm = _HostExchange(rank, world)
     w, st_all, cuts = _world()
     K = len(w.ports)
     g = w.grid.slab(cuts[rank], cuts[rank + 1])
@@ -132,7 +164,7 @@ def _rank_main(rank, world, port, steps, q):
                 assert new_ids.min() <= offs[k] <= new_ids.max()
         nid = nid2
         out.append({k: v.copy() for k, v in st.items()})
-    q.put((rank, out, nid, migrated[0]))
+    q.put((rank, out, nid, migrated[0], uid))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -147,10 +179,13 @@ def test_gloo_two_ranks_match_single_process():
         p.start()
     got = dict()
     received = 0
+    uids = set()
     for _ in range(2):
-        r, out, nid, mig = q.get(timeout=600)
+        r, out, nid, mig, uid = q.get(timeout=600)
         got[r] = (out, nid)
         received += mig
+        uids.add(uid)
+    assert len(uids) == 1, "every rank must receive rank 0's unique id"
     assert received > 0, "no particle crossed the slab face: the exchange was not exercised"
     for p in procs:
         p.join(timeout=120)
@@ -207,7 +242,7 @@ def test_loopback_slabs_match_oracle(P, deferred):
     their keys over with migration (leaver lists); tombstones left
     by the deferred compaction are not part of the state compared."""
     from paper_2406_16786_b200.dist import LoopbackGroup, SlabUpdater
-    w = inputs.c4(scale=0.5, nports=8, n_updates=6)
+    w = inputs.c4(scale=0.5, nports=8, n_updates=8)
     st = oracle.to_numpy_state(w.state)
     ncx = w.grid.ncell[0]
     cuts = [int(round(i * ncx / P)) for i in range(P + 1)]
@@ -216,7 +251,7 @@ def test_loopback_slabs_match_oracle(P, deferred):
     for r in range(P):
         ws = inputs.Workload(w.name, 3, w.dp, w.h, w.grid.slab(cuts[r], cuts[r + 1]), w.ports,
                              {k: torch.from_numpy(v) for k, v in parts[r].items()}, w.dt, w.n_updates, w.next_id)
-        su = SlabUpdater(ws, r, P, inputs.capacity_for(ws, 0.2), max_migrate=1 << 16, comm=None, deferred=deferred)
+        su = SlabUpdater(ws, r, P, inputs.capacity_for(ws, 0.2), max_migrate=1 << 16, deferred=deferred)
         su.load(ws.state, w.next_id)
         slabs.append(su)
     grp = LoopbackGroup(slabs)
@@ -240,3 +275,141 @@ def test_loopback_slabs_match_oracle(P, deferred):
             assert int(su.bu.next_id.item()) == nid
         assert sum(su.bu.stats()["migrated_out"] for su in slabs) >= 0
     assert sum(su.bu.stats()["migrated_out"] for su in slabs) > 0
+
+
+def _c5_union(P, n_updates):
+    """The C5 weak-scaling workload at a CPU-sized scale, generated slab by slab
+    (c5(slab=r, nslabs=P)); returns the slabs and the single-domain problem."""
+    slabs = [inputs.c5(scale=0.3, slab=r, nslabs=P, n_updates=n_updates) for r in range(P)]
+    w0 = slabs[0]
+    grid = inputs.Grid(3, w0.grid.lo, w0.grid.cs, w0.grid.ncell)
+    st = {k: torch.cat([w.state[k] for w in slabs]) for k in w0.state}
+    return slabs, inputs.Workload("C5x0.3-union", 3, w0.dp, w0.h, grid, w0.ports, st, w0.dt, n_updates,
+                                  w0.next_id)
+
+
+@pytest.mark.gpu
+@pytest.mark.slow
+@pytest.mark.parametrize("P", [2, 4])
+def test_loopback_c5_multislab_both_compaction_modes(P):
+    """BASELINE configs[4] (C5) as the driver's scaling run would cut it: slab r
+    generated by c5(slab=r, nslabs=P) (ports straddling slab faces), P ranks of
+    the CUDA path through the library's loopback communicator, 10 updates, in-
+    place and deferred compaction side by side; the union of the ranks equals
+    the single-process oracle bit-exactly after every update."""
+    from paper_2406_16786_b200.dist import LoopbackGroup, SlabUpdater, expected_migrants
+    n_updates = 10
+    slabs, whole = _c5_union(P, n_updates)
+    # some port straddles a slab face (its P_k crosses x = 1.6 r * scale)
+    faces = [whole.grid.lo[0] + whole.grid.cs * b for (b, e) in slabs[0].slab_cells[1:]]
+    straddle = 0
+    for p in whole.ports:
+        ext = sum(abs(p.Q[3 * r]) * (p.half_extents[r] + whole.grid.cs) for r in range(3))
+        straddle += any(p.origin[0] - ext < f < p.origin[0] + ext for f in faces)
+    assert straddle > 0
+    st = oracle.to_numpy_state(whole.state)
+    for k, p in enumerate(whole.ports):
+        oracle.register(st, whole.grid, p, k)
+    groups = {}
+    for deferred in (False, True):
+        us = []
+        for r, w in enumerate(slabs):
+            mm = max(4096, 3 * expected_migrants(w.state, w.grid, w.dt))
+            su = SlabUpdater(w, r, P, inputs.capacity_for(w, 0.1), max_migrate=mm, deferred=deferred)
+            su.load(w.state, w.next_id)
+            us.append(su)
+        groups[deferred] = (LoopbackGroup(us), us)
+    nid = whole.next_id
+    for s in range(n_updates):
+        st, res, perm, nid = oracle.step(st, whole.grid, whole.ports, nid, whole.dt)
+        ref = by_id(st)
+        for deferred, (grp, us) in groups.items():
+            grp.step(whole.dt)
+            union = None
+            for su in us:
+                g = {k: v.numpy() for k, v in su.bu.state().items()}
+                live = g["label"] > -2
+                g = {k: v[live] for k, v in g.items()}
+                union = g if union is None else cat(union, g)
+            union = by_id(union)
+            for k in ref:
+                np.testing.assert_array_equal(union[k], ref[k], err_msg=f"P={P} deferred={deferred} step {s} {k}")
+            for su in us:
+                assert int(su.bu.next_id.item()) == nid
+    for deferred, (grp, us) in groups.items():
+        assert sum(su.bu.stats()["migrated_out"] for su in us) > 0
+
+
+@pytest.mark.gpu
+def test_loopback_step_captured_in_one_cuda_graph():
+    """A P = 2 step (key pass + pack, exchange, finish + update, count allgather,
+    compaction on both ranks) captured in one CUDA graph and replayed: the union
+    equals the oracle after 2 warm-up + 3 x 2 replayed updates."""
+    from paper_2406_16786_b200.dist import LoopbackGroup, SlabUpdater
+    w = inputs.c4(scale=0.5, nports=8, n_updates=8)
+    st = oracle.to_numpy_state(w.state)
+    ncx = w.grid.ncell[0]
+    cuts = [0, ncx // 2, ncx]
+    parts = split(st, w.grid, cuts)
+    us = []
+    for r in range(2):
+        ws = inputs.Workload(w.name, 3, w.dp, w.h, w.grid.slab(cuts[r], cuts[r + 1]), w.ports,
+                             {k: torch.from_numpy(v) for k, v in parts[r].items()}, w.dt, w.n_updates, w.next_id)
+        su = SlabUpdater(ws, r, 2, inputs.capacity_for(ws, 0.2), max_migrate=1 << 15, deferred=True)
+        su.load(ws.state, w.next_id)
+        us.append(su)
+    grp = LoopbackGroup(us)
+    g = grp.capture(w.dt)
+    for _ in range(3):
+        g.replay()
+    for k, p in enumerate(w.ports):
+        oracle.register(st, w.grid, p, k)
+    nid = w.next_id
+    for _ in range(8):
+        st, res, perm, nid = oracle.step(st, w.grid, w.ports, nid, w.dt)
+    union = None
+    for su in us:
+        gg = {k: v.numpy() for k, v in su.bu.state().items()}
+        live = gg["label"] > -2
+        gg = {k: v[live] for k, v in gg.items()}
+        union = gg if union is None else cat(union, gg)
+    union, ref = by_id(union), by_id(st)
+    for k in ref:
+        np.testing.assert_array_equal(union[k], ref[k], err_msg=k)
+    assert int(us[0].bu.next_id.item()) == int(us[1].bu.next_id.item()) == nid
+
+
+@pytest.mark.gpu
+def test_nccl_communicator_single_rank():
+    """The library's own NCCL communicator (sph_comm_init from a unique id that
+    torch.distributed broadcast): at world size 1 the fused migrate + build and
+    the ncclAllGather of the counts run through NCCL, bit-exact with the oracle."""
+    from paper_2406_16786_b200 import sphbuf
+    from paper_2406_16786_b200.dist import SlabUpdater
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(free_port()))
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        uid = broadcast_unique_id(0)
+        w = inputs.make("C2")
+        su = SlabUpdater(w, 0, 1, inputs.capacity_for(w), max_migrate=1024)
+        su.init_nccl(uid)
+        with pytest.raises(sphbuf.SphError) as e:
+            su.init_nccl(uid)
+        assert e.value.code == -9
+        su.load(w.state, w.next_id)
+        st = oracle.to_numpy_state(w.state)
+        for k, p in enumerate(w.ports):
+            oracle.register(st, w.grid, p, k)
+        nid = w.next_id
+        for s in range(5):
+            st, res, perm, nid = oracle.step(st, w.grid, w.ports, nid, w.dt)
+            su.step(w.dt)
+            assert su.all_counts[0].cpu().tolist()[:2] == res.port_counts[:2].tolist()
+        su.bu.cll_build()          # drops the tombstones a deferred compaction would leave
+        got = by_id({k: v.numpy() for k, v in su.bu.state().items()})
+        ref = by_id(st)
+        for k in ref:
+            np.testing.assert_array_equal(got[k], ref[k], err_msg=k)
+        assert su.bu.stats()["n"] == len(st["x"])
+    finally:
+        dist.destroy_process_group()

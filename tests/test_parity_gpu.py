@@ -301,3 +301,32 @@ def test_port_registered_between_build_and_update():
     bu.compact()
     assert (gpu_counts_to_oracle(bu.port_counts, K) == res2.port_counts).all()
     assert_state_equal(bu.state(), new2, "second update")
+
+
+def test_call_order_is_enforced():
+    """SURVEY §8(b) call order build -> update -> compact: the update's deletion
+    list and staging area are live until the compaction consumes them, so a
+    compaction without an update, a second update, or a build in between is
+    refused with SPH_ERR_STATE (nothing enqueued) and the state stays correct."""
+    w = inputs.make("C1e")
+    bu = make_updater(w)
+    bu.load(w.state, w.next_id)
+    bu.register_ports()
+    with pytest.raises(sphbuf.SphError) as e:
+        bu.compact()
+    assert e.value.code == -9
+    bu.cll_build(dt=w.dt)
+    bu.update()
+    for bad in (lambda: bu.update(), lambda: bu.cll_build(), lambda: bu.cll_build(dt=w.dt)):
+        with pytest.raises(sphbuf.SphError) as e:
+            bad()
+        assert e.value.code == -9
+    bu.compact()
+    with pytest.raises(sphbuf.SphError) as e:
+        bu.compact(deferred=True)
+    assert e.value.code == -9
+    st = oracle.to_numpy_state(w.state)
+    for k, p in enumerate(w.ports):
+        oracle.register(st, w.grid, p, k)
+    new, res, perm, nid = oracle.step(st, w.grid, w.ports, w.next_id, w.dt)
+    assert_state_equal(bu.state(), new, "after refused calls")

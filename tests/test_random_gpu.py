@@ -275,7 +275,7 @@ def test_random_slabs_lockstep(seed, P):
         part["extra"] = [torch.from_numpy(c[sel].copy()) for c in st["extra"]]
         ws = inputs.Workload(w.name, w.dim, w.dp, w.h, w.grid.slab(cuts[r], cuts[r + 1]), w.ports, part, w.dt,
                              w.n_updates, w.next_id)
-        su = SlabUpdater(ws, r, P, inputs.capacity_for(ws, 0.3) + 4096, max_migrate=1 << 15, comm=None,
+        su = SlabUpdater(ws, r, P, inputs.capacity_for(ws, 0.3) + 4096, max_migrate=1 << 15,
                          deferred=mode["deferred"], n_extra=1)
         su.load(ws.state, w.next_id)
         slabs.append(su)
