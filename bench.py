@@ -4,12 +4,22 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C5|C4|C3|C2]
 
 A step is one update of the whole hot path on one
-batch of synthetic particles: advect (driver) -> [migrate, N>1] -> sph_cll_build
--> sph_buffer_update -> [count allgather, N>1] -> sph_compact.  Default workload:
+batch of synthetic particles: advect (driver, fused into the build) -> [migrate,
+N>1: sph_migrate_cll_build] -> sph_cll_build -> sph_buffer_update -> [count
+allgather, N>1: sph_allgather_counts] -> sph_compact.  Default workload:
 C5 (BASELINE configs[4]): 128M particles per GPU in x-slabs, 8 ports per slab,
 weak scaling; inputs (4.6 GB per GPU) are far larger than L2, so no flush is
 needed between steps.  value = candidate particles checked per second summed
 over ranks (the metric's "buffer-update particles checked/sec").
+
+--gpus N without torchrun (WORLD_SIZE unset) re-launches itself under
+torch.distributed.run with N ranks on 127.0.0.1.
+
+Timing: the headline (value, ms_per_step) is K steps with the library's
+per-kernel profiling OFF (programmatic dependent launch overlaps the kernels);
+a second pass of min(K, 10) steps records CUDA events between the phases
+(t_cll, t_comm, t_update, t_compact: median and p90) and around every kernel
+(the per-kernel split and the roofline of the dominant kernel).
 
 --impl reference times the CPU oracle (the "reference arm"; test
 infrastructure, oracle/) on a bounded sample of the same workload.
@@ -35,7 +45,7 @@ import torch
 import torch.distributed as dist
 
 from paper_2406_16786_b200 import inputs, sphbuf
-from paper_2406_16786_b200.dist import Comm, SlabUpdater
+from paper_2406_16786_b200.dist import SlabUpdater, broadcast_unique_id, expected_migrants
 
 PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FALLBACK_HBM = 6650.0
@@ -134,25 +144,116 @@ def algorithmic_bytes(kernel, dim, n, ncells, cand, created, deleted, moved):
     }.get(kernel)
 
 
+def _pct(xs, q):
+    xs = sorted(xs)
+    if not xs:
+        return None
+    k = min(len(xs) - 1, max(0, int(math.ceil(q * len(xs))) - 1))
+    return xs[k]
+
+
+class PhaseTimer:
+    """CUDA events between the phases of one step on the launching stream, and
+    NVTX ranges around them (the breakdown pass; the headline pass has none)."""
+
+    def __init__(self):
+        self.steps = []
+
+    def step(self, su, dt, world):
+        bu = su.bu
+        s = torch.cuda.current_stream()
+        ev = []
+
+        def mark(name=None):
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(s)
+            ev.append((name, e))
+
+        nv = torch.cuda.nvtx
+        mark()
+        if su.has_comm and world > 1:
+            nv.range_push("cll_key+pack")
+            sphbuf.sph_cll_key(bu.ctx, bu.A, dt)
+            nv.range_pop()
+            mark("cll")
+            nv.range_push("comm: neighbour exchange")
+            sphbuf.sph_migrate_exchange(bu.ctx)
+            nv.range_pop()
+            mark("comm")
+            nv.range_push("cll_finish")
+            sphbuf.sph_cll_finish(bu.ctx, bu.A, bu.B, bu.cell_start, bu.cell_end)
+            bu.A, bu.B = bu.B, bu.A
+            nv.range_pop()
+            mark("cll")
+            nv.range_push("buffer_update")
+            bu.update()
+            nv.range_pop()
+            mark("update")
+            nv.range_push("comm: count allgather")
+            sphbuf.sph_allgather_counts(bu.ctx, bu.port_counts, su.all_counts)
+            nv.range_pop()
+            mark("comm")
+            nv.range_push("compact")
+            bu.compact(su.all_counts, world, su.rank, deferred=su.deferred)
+            nv.range_pop()
+            mark("compact")
+        else:
+            nv.range_push("cll_build (advection fused)")
+            bu.cll_build(dt=dt)
+            nv.range_pop()
+            mark("cll")
+            nv.range_push("buffer_update")
+            bu.update()
+            nv.range_pop()
+            mark("update")
+            nv.range_push("compact")
+            bu.compact(deferred=su.deferred)
+            nv.range_pop()
+            mark("compact")
+        self.steps.append(ev)
+
+    def summary(self):
+        """{phase: {median, p90}} in ms over the steps (synchronises)."""
+        torch.cuda.synchronize()
+        per = {"cll": [], "comm": [], "update": [], "compact": [], "step": []}
+        for ev in self.steps:
+            acc = dict.fromkeys(per, 0.0)
+            for (_, a), (name, b) in zip(ev[:-1], ev[1:]):
+                acc[name] += a.elapsed_time(b)
+            acc["step"] = ev[0][1].elapsed_time(ev[-1][1])
+            for k in per:
+                per[k].append(acc[k])
+        return {f"t_{k}": {"median_ms": round(statistics.median(v), 5), "p90_ms": round(_pct(v, 0.9), 5)}
+                for k, v in per.items() if v}
+
+
 def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world != args.gpus:
-        if world == 1 and args.gpus > 1:
-            raise SystemExit("--gpus N>1 must be launched with torch.distributed.run")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    uid = None
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
+        uid = broadcast_unique_id(rank)          # the library creates and owns its ncclComm_t
     tgen = time.time()
     w = make_workload(args.config, rank, world, dev, args.scale)
     torch.cuda.synchronize()
     tgen = time.time() - tgen
     cap = inputs.capacity_for(w, 0.05)
     max_new = max(65536, w.n // 200)
-    su = SlabUpdater(w, rank, world, cap, max_migrate=1 << 18, max_new=max_new, comm=Comm(rank, world), device=dev,
+    max_mig = 0
+    if world > 1:
+        # fixed-size messages (no host sync): 3x the particles that change cell column
+        # in one step on the busier rank, at least 4096
+        est = torch.tensor([float(expected_migrants(w.state, w.grid, w.dt))], device=dev)
+        dist.all_reduce(est, op=dist.ReduceOp.MAX)
+        max_mig = max(4096, int(3 * float(est.item())))
+    su = SlabUpdater(w, rank, world, cap, max_migrate=max_mig, max_new=max_new, device=dev,
                      deferred=(args.compaction == "deferred"))
+    if world > 1:
+        su.init_nccl(uid)
     su.load(w.state, w.next_id)
     n0 = w.n
     del w.state
@@ -165,11 +266,20 @@ def run_ours(args):
             dist.barrier()
         torch.cuda.synchronize()
 
-    def timed(steps, sample_clocks):
+    def reduce(ms, count):
+        t = torch.tensor([ms, float(count)], dtype=torch.float64, device=dev)
+        if world > 1:
+            tmax = t.clone()
+            dist.all_reduce(tmax[:1], op=dist.ReduceOp.MAX)
+            tsum = t.clone()
+            dist.all_reduce(tsum[1:], op=dist.ReduceOp.SUM)
+            return float(tmax[0]), float(tsum[1])
+        return ms, float(count)
+
+    def headline(steps, sample_clocks):
         """Exactly `steps` steps between barrier + synchronize on both sides, CUDA
-        events on the launching stream, max over ranks; per-kernel event times."""
+        events on the launching stream, max over ranks; no per-kernel events."""
         s0 = bu.stats()
-        sphbuf.sph_profile(bu.ctx, True)
         l0 = bu.launches()
         clocks = ClockSampler(local) if sample_clocks else None
         if clocks:
@@ -184,50 +294,80 @@ def run_ours(args):
         barrier()
         clk = clocks.stop() if clocks else None
         ms = e0.elapsed_time(e1)
-        prof = sphbuf.sph_profile_read(bu.ctx)
-        sphbuf.sph_profile(bu.ctx, False)
         s1 = bu.stats()
         checked = s1["checked_total"] - s0["checked_total"]
-        t = torch.tensor([ms, float(checked)], dtype=torch.float64, device=dev)
-        if world > 1:
-            tmax = t.clone()
-            dist.all_reduce(tmax[:1], op=dist.ReduceOp.MAX)
-            tsum = t.clone()
-            dist.all_reduce(tsum[1:], op=dist.ReduceOp.SUM)
-            ms, checked_all = float(tmax[0]), float(tsum[1])
-        else:
-            checked_all = float(checked)
-        return ms, checked_all, checked, bu.launches() - l0, prof, clk, s1
+        ms_max, checked_all = reduce(ms, checked)
+        return ms_max, checked_all, checked, bu.launches() - l0, clk, s1
 
-    for _ in range(args.warmup):
-        su.step(w.dt)
-    ms_max, checked_all, checked, launches, prof, clk, s = timed(args.steps, True)
-    value = checked_all / (ms_max / 1e3)
-    # the other compaction mode, same state and harness (reported beside the headline)
-    su.deferred = not su.deferred
+    def breakdown(steps):
+        """Phase events + per-kernel events (sph_profile) over `steps` steps."""
+        pt = PhaseTimer()
+        sphbuf.sph_profile(bu.ctx, True)
+        barrier()
+        for _ in range(steps):
+            pt.step(su, w.dt, world)
+        barrier()
+        prof = sphbuf.sph_profile_read(bu.ctx)
+        sphbuf.sph_profile(bu.ctx, False)
+        return pt.summary(), {k: v for k, v in prof.items() if v[1] > 0}, bu.stats()
+
+    modes = [args.compaction, "inplace" if args.compaction == "deferred" else "deferred"]
+    res = {}
+    for mi, mode in enumerate(modes):
+        su.deferred = mode == "deferred"
+        for _ in range(args.warmup if mi == 0 else 3):
+            su.step(w.dt)
+        ms_max, checked_all, checked, launches, clk, s = headline(args.steps, mi == 0)
+        phases, prof, sb = breakdown(min(args.steps, 10))
+        res[mode] = dict(ms=ms_max, checked_all=checked_all, checked=checked, launches=launches, clk=clk, s=s,
+                         phases=phases, prof=prof, sb=sb)
+    su.deferred = modes[0] == "deferred"
     for _ in range(2):
         su.step(w.dt)
-    ams, achk, _, _, aprof, _, _ = timed(args.steps, False)
-    su.deferred = not su.deferred
-    alt = {"compaction": "inplace" if args.compaction == "deferred" else "deferred",
-           "ms_per_step": ams / args.steps, "value": achk / (ams / 1e3),
-           "kernels_ms": {k: round(v[0] / v[1], 4) for k, v in aprof.items() if v[1] > 0}}
-    for _ in range(2):
-        su.step(w.dt)
 
-    # roofline of the dominant kernel (live CUDA-event times of the timed region)
     dim = bu.dim
-    n = s["n"]
+    S = 8 * dim + 12
     ncells = w.grid.ncells_local
-    per_kernel = {k: v for k, v in prof.items() if v[1] > 0}
-    dom = max(per_kernel, key=lambda k: per_kernel[k][0])
-    dom_ms = per_kernel[dom][0] / per_kernel[dom][1]
-    cand = checked / max(1, args.steps)
-    created = s["created"]
-    deleted = s["deleted"]
-    moved = max(0, n + deleted - created - s["first_deleted"]) if deleted else 0
-    bytes_dom = algorithmic_bytes(dom, dim, n, ncells, cand, created, deleted, moved)
     peak, peak_src = hbm_peak()
+
+    def mode_report(mode):
+        r = res[mode]
+        s, prof = r["sb"], r["prof"]
+        n = s["n"]
+        cand = r["checked"] / max(1, args.steps)
+        created, deleted = s["created"], s["deleted"]
+        moved = max(0, n + deleted - created - s["first_deleted"]) if deleted else 0
+        kms = {k: v[0] / v[1] for k, v in prof.items()}
+        t_upd = kms.get("upd_prologue", 0) + kms.get("upd_main", 0)
+        t_cmp = kms.get("compact_count", 0) + kms.get("compact", 0) + kms.get("compact_append", 0)
+        t_cll = sum(kms.get(k, 0) for k in ("cll_key", "cell_scan", "cll_scatter", "cll_gather", "advect",
+                                            "mig_pack", "mig_unpack"))
+        b_upd = cand * (4 * dim + 4) + created * (2 * S + 4 * dim)
+        b_cmp = (2 * S * moved - S * deleted + S * created) if mode == "inplace" else S * created
+        b_cll = n * (2 * S + 32)
+        frac = lambda b, t: b / (t / 1e3) / 1e9 / peak if t else None
+        return {
+            "ms_per_step": r["ms"] / args.steps, "value": r["checked_all"] / (r["ms"] / 1e3),
+            "phases": r["phases"],
+            "update_compact": {"alg_bytes": b_upd + b_cmp, "kernel_ms": t_upd + t_cmp,
+                               "frac": frac(b_upd + b_cmp, t_upd + t_cmp),
+                               "what": "SURVEY 8(d) headline: (B_update + B_compact) / (t_update + t_compact); "
+                                       "kernel times from the breakdown pass"},
+            "cll_build": {"alg_bytes": b_cll, "kernel_ms": t_cll, "frac": frac(b_cll, t_cll),
+                          "what": "2S + 32 B per particle (SURVEY 8(d))"},
+            "kernels_ms": {k: round(v, 4) for k, v in kms.items()},
+            "cand": cand, "created": created, "deleted": deleted, "moved": moved, "n": n,
+        }
+
+    rep = {m: mode_report(m) for m in modes}
+    main_r = res[modes[0]]
+    R = rep[modes[0]]
+    value = R["value"]
+    step_ms = R["ms_per_step"]
+    prof = main_r["prof"]
+    dom = max(prof, key=lambda k: prof[k][0])
+    dom_ms = prof[dom][0] / prof[dom][1]
+    bytes_dom = algorithmic_bytes(dom, dim, R["n"], ncells, R["cand"], R["created"], R["deleted"], R["moved"])
     achieved = bytes_dom / (dom_ms / 1e3) / 1e9 if bytes_dom else None
     traffic = None
     tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -236,24 +376,8 @@ def run_ours(args):
             traffic = json.load(open(tf)).get(args.config, {}).get(dom)
         except Exception:
             traffic = None
-    step_ms = ms_max / args.steps
-    kernels = {k: {"ms_per_launch": round(v[0] / v[1], 4), "share": round(v[0] / sum(x[0] for x in per_kernel.values()), 4)}
-               for k, v in per_kernel.items()}
-    # SURVEY §8(d) phase budgets: update+compaction bytes vs their time, and the cell-list
-    # build at 2S + 32 B per particle (plain counting sort), each against the HBM peak
-    S = 8 * dim + 12
-    kms = {k: v[0] / v[1] for k, v in per_kernel.items()}
-    t_upd = kms.get("upd_prologue", 0) + kms.get("upd_main", 0)
-    t_cmp = kms.get("compact_count", 0) + kms.get("compact", 0) + kms.get("compact_append", 0)
-    t_cll = sum(kms.get(k, 0) for k in ("cll_key", "cell_scan", "cll_scatter", "cll_gather", "advect"))
-    b_upd = cand * (4 * dim + 4) + created * (2 * S + 4 * dim)
-    b_cmp = (2 * S * moved - S * deleted + S * created) if args.compaction == "inplace" else S * created
-    b_cll = n * (2 * S + 32)
-    phases = {"update_compact_ms": t_upd + t_cmp, "update_compact_alg_bytes": b_upd + b_cmp,
-              "update_compact_frac": (b_upd + b_cmp) / ((t_upd + t_cmp) / 1e3) / 1e9 / peak if t_upd + t_cmp else None,
-              "cll_ms": t_cll, "cll_alg_bytes": b_cll,
-              "cll_frac": b_cll / (t_cll / 1e3) / 1e9 / peak if t_cll else None,
-              "note": "update+compact is latency-bound at C5 size (~12 MB of candidate work); see DESIGN.md §6"}
+    tot = sum(v[0] for v in prof.values())
+    kernels = {k: {"ms_per_launch": round(v[0] / v[1], 4), "share": round(v[0] / tot, 4)} for k, v in prof.items()}
 
     # e2e: same metric through the public API with host-resident particles
     e2e = None
@@ -275,24 +399,31 @@ def run_ours(args):
             "value": value, "unit": "particles_checked/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": step_ms, "us_per_step": step_ms * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic (seeded lattice + jitter, BASELINE config shapes)",
+            "data": "synthetic (seeded lattice + jitter, tie-screened, BASELINE config shapes)",
             "config": {"workload": f"{args.config}" + (f" scale {args.scale}" if args.scale != 1 else ""),
-                       "particles_per_gpu": n0, "ports": n_ports, "candidates_per_step": cand,
-                       "created_last": created, "deleted_last": deleted, "dim": dim,
+                       "particles_per_gpu": n0, "ports": n_ports, "candidates_per_step": R["cand"],
+                       "created_last": R["created"], "deleted_last": R["deleted"], "dim": dim,
                        "parallelism": f"x-slab dp{world}", "l2": "inputs (>=4.6 GB/GPU) larger than L2; no flush",
-                       "compaction": args.compaction,
+                       "compaction": modes[0], "max_migrate": max_mig,
                        "advection": "fused into the cell-list build (the gather advects; next keys carried over)",
+                       "timing": "headline with per-kernel profiling off; phases/kernels from a second pass",
                        "gen_s": round(tgen, 1)},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak if achieved else None, "traffic": traffic,
                          "peak_source": peak_src, "alg_bytes_per_launch": bytes_dom, "ms_per_launch": dom_ms,
+                         "update_compact_8d": {m: {"frac": rep[m]["update_compact"]["frac"],
+                                                   "alg_bytes": rep[m]["update_compact"]["alg_bytes"],
+                                                   "kernel_ms": rep[m]["update_compact"]["kernel_ms"]}
+                                               for m in modes},
+                         "cll_build_8d": {m: rep[m]["cll_build"]["frac"] for m in modes},
                          "note": "a no-compute copy with the gather's access pattern (80 B/particle through the "
                                  "slot map) takes 1.9-2.06 ms at C5 (tools/soa_copy_probe.cu, DESIGN.md section 6)"},
             "kernels": kernels,
-            "phases": phases,
-            "other_compaction_mode": alt,
-            "gpu_launches": launches,
-            "clocks": clk,
+            "phases": {m: rep[m]["phases"] for m in modes},
+            "modes": {m: {k: rep[m][k] for k in ("ms_per_step", "value", "update_compact", "cll_build",
+                                                  "kernels_ms")} for m in modes},
+            "gpu_launches": main_r["launches"],
+            "clocks": main_r["clk"],
             "e2e": e2e,
             "cpu_baseline": cpu,
             "configs_us_per_update": sweep,
@@ -439,27 +570,61 @@ def oracle_sample(args, dev):
     return w, st
 
 
-def oracle_step_timed(w, st, nid):
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def oracle_step_timed(w, st, nid, mode, threads):
+    """One oracle update (O2-O6: cell list, decisions, apply, relabel, compaction),
+    wall-clock timed; mode 1 = cell-restricted (the paper's local cell-linked lists,
+    the CPU form of the method), 0 = brute force over every particle and port.
+    Returns (state, next_id, seconds, candidates, t_cll, t_decide); candidates =
+    particles in the cells intersecting each P_k (the metric's unit of work)."""
     import oracle
+    oracle.set_threads(threads)
     oracle.advect(st, w.dim, w.dt)
     t0 = time.perf_counter()
-    res = oracle.update(w.grid, w.ports, st, mode=0)
+    res = oracle.update(w.grid, w.ports, st, mode=mode)
     new, perm, nid = oracle.compact(res, w.dim, len(w.ports), res.port_counts[None, :], 0, nid)
     dt = time.perf_counter() - t0
-    # the method's candidates in this sample (cells intersecting P_k), the metric's unit of work
-    cand = 0
-    for p in w.ports:
-        m = oracle.port_cells(w.grid, p).astype(bool)
-        cand += int((res.cell_end - res.cell_start)[m].sum())
-    return new, nid, dt, cand
+    if mode == 1:
+        cand = res.checked
+    else:
+        cand = 0
+        for p in w.ports:
+            m = oracle.port_cells(w.grid, p).astype(bool)
+            cand += int((res.cell_end - res.cell_start)[m].sum())
+    return new, nid, dt, cand, res.t_cll, res.t_decide
 
 
 def cpu_baseline(args, dev):
+    """The oracle as it stands, on this host's cores, on a bounded sample: cell-
+    restricted with every core (the headline value), cell-restricted on one core,
+    and brute force with every core."""
+    import oracle
     w, st = oracle_sample(args, dev)
-    new, nid, dt, cand = oracle_step_timed(w, st, w.next_id)
-    return {"value": cand / dt, "unit": "particles_checked/s", "cores": 1, "kind": "oracle",
-            "sample": f"one oracle update (brute force O2-O6, decide+apply+compact) of {args.config} at scale "
-                      f"{args.cpu_scale * args.scale} ({w.n} particles, {len(w.ports)} ports), {dt:.2f} s"}
+    T = os.cpu_count() or 1
+    runs = []
+    for mode, threads in ((1, T), (1, 1), (0, T)):
+        s2 = {k: (v.copy() if not isinstance(v, list) else [c.copy() for c in v]) for k, v in st.items()}
+        _, _, dt, cand, tc, td = oracle_step_timed(w, s2, w.next_id, mode, threads)
+        runs.append({"mode": "cell-restricted" if mode == 1 else "brute force", "threads": threads,
+                     "s_per_update": round(dt, 3), "s_cell_list": round(tc, 3), "s_decide_apply": round(td, 3),
+                     "value": cand / dt, "candidates": cand})
+    oracle.set_threads(T)
+    head = runs[0]
+    return {"value": head["value"], "unit": "particles_checked/s", "cores": T, "kind": "oracle",
+            "cpu_model": cpu_model(), "mode": head["mode"],
+            "sample": f"one oracle update (O2-O6: cell list, f64 decisions, apply, relabel, compaction) of "
+                      f"{args.config} at scale {args.cpu_scale * args.scale} ({w.n} particles, {len(w.ports)} ports); "
+                      f"OpenMP on the independent per-particle loops only",
+            "runs": runs}
 
 
 def run_reference(args):
@@ -469,26 +634,53 @@ def run_reference(args):
         return
     dev = torch.device("cuda", 0) if torch.cuda.is_available() else torch.device("cpu")
     w, st = oracle_sample(args, dev)
+    T = os.cpu_count() or 1
     nid = w.next_id
     for _ in range(args.warmup):
-        st, nid, _, _ = oracle_step_timed(w, st, nid)
+        st, nid, _, _, _, _ = oracle_step_timed(w, st, nid, 1, T)
     tot, cand = 0.0, 0
     for _ in range(args.steps):
-        st, nid, dt, c = oracle_step_timed(w, st, nid)
+        st, nid, dt, c, _, _ = oracle_step_timed(w, st, nid, 1, T)
         tot += dt
         cand += c
     v = cand / tot
     line = {"impl": "reference", "metric": "buffer-update particles checked/sec & us/step; % of B200 HBM peak; "
             "1/2/4/8 GPU", "value": v, "unit": "particles_checked/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": tot / args.steps * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64 decisions, f32 state", "data": "synthetic",
             "config": {"workload": f"{args.config} sample at scale {args.cpu_scale * args.scale}",
                        "particles": w.n, "ports": len(w.ports)},
-            "cpu_baseline": {"value": v, "unit": "particles_checked/s", "cores": 1, "kind": "oracle",
-                             "sample": f"{args.steps} oracle updates of {args.config} at scale "
+            "cpu_baseline": {"value": v, "unit": "particles_checked/s", "cores": T, "kind": "oracle",
+                             "cpu_model": cpu_model(), "mode": "cell-restricted",
+                             "sample": f"{args.steps} oracle updates (O2-O6) of {args.config} at scale "
                                        f"{args.cpu_scale * args.scale} ({w.n} particles)"},
             "e2e": {"value": v, "unit": "particles_checked/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def spawn(args) -> int:
+    """--gpus N without torchrun: re-launch this script under torch.distributed.run
+    (one rank per GPU, rendezvous on 127.0.0.1) and return its exit code."""
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def spawn_check(args):
+    """(CPU) the rank layout a spawned run sees: one JSON line per rank."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    dist.init_process_group("gloo")
+    t = torch.tensor([rank + 1])
+    dist.all_reduce(t)
+    print(json.dumps({"rank": rank, "world": world, "local_rank": int(os.environ.get("LOCAL_RANK", "0")),
+                      "sum_ranks_plus_1": int(t.item())}), flush=True)
+    dist.destroy_process_group()
 
 
 def main():
@@ -507,10 +699,15 @@ def main():
     ap.add_argument("--compaction", default="deferred", choices=["inplace", "deferred"],
                     help="sph_compact (in-place stable compaction each update) or sph_compact_deferred "
                          "(removal fused into the next cell-list build)")
+    ap.add_argument("--spawn-check", action="store_true", help="(CPU test) print each spawned rank's layout")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
-    if args.impl == "reference":
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn(args))
+    if args.spawn_check:
+        spawn_check(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)

@@ -20,7 +20,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "sph_oracle.c")
 _SO = os.path.join(_HERE, "_build", "liboracle.so")
-CFLAGS = ["-O2", "-std=c99", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared", "-Wall"]
+CFLAGS = ["-O2", "-std=c99", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared", "-Wall", "-fopenmp"]
 
 
 def build(force: bool = False) -> str:
@@ -55,7 +55,8 @@ class UpdateOut(C.Structure):
                 ("out_of_grid", C.c_int64), ("create_port", C.c_void_p), ("delete_port", C.c_void_p),
                 ("sorted", State), ("staged", State), ("stage_port", C.c_void_p), ("stage_src", C.c_void_p),
                 ("cap_stage", C.c_int64), ("n_stage", C.c_int64), ("port_counts", C.c_void_p),
-                ("checked", C.c_int64), ("multi_decision", C.c_int64), ("motion_errors", C.c_int64)]
+                ("checked", C.c_int64), ("multi_decision", C.c_int64), ("motion_errors", C.c_int64),
+                ("t_cll", C.c_double), ("t_decide", C.c_double)]
 
 
 _lib = None
@@ -65,6 +66,8 @@ def lib():
     global _lib
     if _lib is None:
         L = C.CDLL(build())
+        L.orc_set_threads.argtypes = [C.c_int32]
+        L.orc_set_threads.restype = C.c_int32
         L.orc_frame_2d.argtypes = [C.c_double, C.c_void_p]
         L.orc_frame_3d.argtypes = [C.c_void_p, C.c_void_p]
         L.orc_frame_3d.restype = C.c_int
@@ -205,6 +208,12 @@ def cports(ports):
 
 
 # ----------------------------------------------------------------- API
+
+def set_threads(n: int = 0) -> int:
+    """Threads of the oracle's independent per-particle loops (0: OpenMP default);
+    results do not depend on it.  Returns the count in use."""
+    return int(lib().orc_set_threads(int(n)))
+
 
 def frame_2d(theta: float) -> np.ndarray:
     Q = np.zeros(9)
@@ -407,6 +416,8 @@ class UpdateResult:
     checked: int
     multi_decision: int
     motion_errors: int
+    t_cll: float = 0.0          # seconds in O2 (cell list)
+    t_decide: float = 0.0       # seconds in O3-O5b (decide, apply, relabel, BC)
 
 
 def update(grid, ports, st: dict, mode: int = 0, cap_stage: int | None = None,
@@ -453,7 +464,7 @@ def update(grid, ports, st: dict, mode: int = 0, cap_stage: int | None = None,
         _certify({c: v[:n][keep] for c, v in srt.items() if c != "extra"}, grid, ports, "relabel point")
     return UpdateResult(order[:n], cstart[:nc], cend[:nc], int(o.out_of_grid), cport_[:n], dport[:n],
                         trim(srt, n), trim(stg, ns), sport[:ns], ssrc[:ns], counts[:2 * K], int(o.checked),
-                        int(o.multi_decision), int(o.motion_errors))
+                        int(o.multi_decision), int(o.motion_errors), float(o.t_cll), float(o.t_decide))
 
 
 def compact(res: UpdateResult, dim: int, K: int, all_counts: np.ndarray, rank: int, next_id: int):

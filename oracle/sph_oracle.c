@@ -29,11 +29,22 @@
  * port transfer, which write state too.  This file must be compiled with
  * -ffp-contract=off (no FMA contraction) on an SSE target (FLT_EVAL_METHOD == 0).
  *
+ * Threads.  Compiled with -fopenmp: the per-particle loops whose iterations are
+ * independent (advection, identification, the O3 decisions, the O5 relabel, the
+ * BC state, the O7 margins) are split across threads; the order-defining steps
+ * (the O2 sort, the O4 canonical walk, the O6 compaction) stay sequential, so
+ * every result is the same for any thread count (orc_set_threads).
+ *
  * parity pinned: see tests/test_oracle_pins.py (closed forms, hand cases
  * H1-H6, lattice counts, invariants, brute force vs cell-restricted).
  */
+#define _POSIX_C_SOURCE 199309L
 #include <math.h>
 #include <stdint.h>
+#include <time.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 #include <stdlib.h>
 #include <string.h>
 
@@ -77,6 +88,18 @@ typedef struct {
 } orc_state;
 
 enum { ORC_INLET = 0, ORC_OUTLET = 1, ORC_BIDIR = 2 };
+
+/* Threads of the parallel loops (<= 0: the OpenMP default).  Returns the count in use. */
+int32_t orc_set_threads(int32_t n)
+{
+#ifdef _OPENMP
+    if (n > 0) omp_set_num_threads(n);
+    return omp_get_max_threads();
+#else
+    (void)n;
+    return 1;
+#endif
+}
 
 /* ------------------------------------------------------------ frames (§III.A) */
 
@@ -261,6 +284,7 @@ double orc_tie_margin(const orc_state *s, const orc_grid *g, const orc_port *por
         }
         R2[k] = 1.01 * acc;
     }
+#pragma omp parallel for schedule(static) reduction(min : best)
     for (int64_t i = 0; i < s->n; ++i) {
         if (flags) flags[i] = 0;
         for (int32_t k = 0; k < K; ++k) {
@@ -402,6 +426,7 @@ int64_t orc_port_cells(const orc_grid *g, const orc_port *p, uint8_t *mask)
 /* Driver step (not part of the method): x <- fl(x + fl(v dt)) per component. */
 void orc_advect(orc_state *s, int32_t dim, float dt)
 {
+#pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < s->n; ++i) {
         float dx = s->vx[i] * dt;
         s->x[i] = s->x[i] + dx;
@@ -545,6 +570,7 @@ double orc_windkessel(double P, double Q, double Qprev, double dt, double Rp, do
 int64_t orc_register(orc_state *s, const orc_grid *g, const orc_port *p, int32_t k)
 {
     int64_t members = 0;
+#pragma omp parallel for schedule(static) reduction(+ : members)
     for (int64_t i = 0; i < s->n; ++i) {
         if (s->label[i] == -1) {
             int b = classify(p, g->dim, g->cs, s->x[i], s->y[i], g->dim == 3 ? s->z[i] : 0.0f);
@@ -594,7 +620,16 @@ typedef struct {
                               checks only the local cell-linked lists around the buffer
                               (P:411-413), so a buffer particle that left that region
                               can no longer be generated, deleted or relabelled */
+    double t_cll;          /* seconds in O2 (cell list: keys, sort, tables, reorder) */
+    double t_decide;       /* seconds in O3-O5b (decisions, apply, relabel, BC state) */
 } orc_update_out;
+
+static double now_s(void)
+{
+    struct timespec t;
+    clock_gettime(CLOCK_MONOTONIC, &t);
+    return (double)t.tv_sec + 1e-9 * (double)t.tv_nsec;
+}
 
 static void copy_row(const orc_state *src, int64_t i, orc_state *dst, int64_t j, int32_t dim)
 {
@@ -606,6 +641,39 @@ static void copy_row(const orc_state *src, int64_t i, orc_state *dst, int64_t j,
     for (int e = 0; e < src->n_extra; ++e) dst->extra[e][j] = src->extra[e][i];
     dst->id[j] = src->id[i];
     dst->label[j] = src->label[i];
+}
+
+/* The particle ranges [rb[q], re[q]) that port k checks: the whole array in
+ * fixed chunks (mode 0, brute force) or the ranges of the cells of the oracle's
+ * own P_k cell set (mode 1).  Returns their number; *rb, *re malloc'ed. */
+static int64_t port_ranges(const orc_grid *g, const orc_port *p, int32_t mode, int64_t n, const int32_t *cell_start,
+                           const int32_t *cell_end, int64_t **rb, int64_t **re)
+{
+    const int64_t chunk = 65536;
+    if (mode == 0) {
+        int64_t nr = (n + chunk - 1) / chunk;
+        *rb = (int64_t *)malloc(sizeof(int64_t) * (size_t)(nr > 0 ? nr : 1));
+        *re = (int64_t *)malloc(sizeof(int64_t) * (size_t)(nr > 0 ? nr : 1));
+        for (int64_t q = 0; q < nr; ++q) {
+            (*rb)[q] = q * chunk;
+            (*re)[q] = (q + 1) * chunk < n ? (q + 1) * chunk : n;
+        }
+        return nr;
+    }
+    const int64_t nc = orc_ncells(g);
+    uint8_t *mask = (uint8_t *)calloc((size_t)(nc > 0 ? nc : 1), 1);
+    int64_t nr = orc_port_cells(g, p, mask);
+    *rb = (int64_t *)malloc(sizeof(int64_t) * (size_t)(nr > 0 ? nr : 1));
+    *re = (int64_t *)malloc(sizeof(int64_t) * (size_t)(nr > 0 ? nr : 1));
+    int64_t q = 0;
+    for (int64_t c = 0; c < nc; ++c)
+        if (mask[c]) {
+            (*rb)[q] = cell_start[c];
+            (*re)[q] = cell_end[c];
+            ++q;
+        }
+    free(mask);
+    return q;
 }
 
 /* One buffer update on one slab.  mode 0 = brute force over every particle and
@@ -620,6 +688,7 @@ int orc_update(const orc_grid *g, const orc_port *ports, int32_t K, const orc_st
     const int64_t n = in->n;
     const int64_t nc = orc_ncells(g);
 
+    const double t0 = now_s();
     /* O2: cell-linked list -- cell of each particle, then order by (cell, id). */
     key_t3 *keys = (key_t3 *)malloc(sizeof(key_t3) * (size_t)(n > 0 ? n : 1));
     out->out_of_grid = 0;
@@ -648,31 +717,27 @@ int orc_update(const orc_grid *g, const orc_port *ports, int32_t K, const orc_st
     }
     free(keys);
 
+    const double t1 = now_s();
+    out->t_cll = t1 - t0;
     /* O3: decisions (Alg. 1, Alg. 2, Alg. 3). */
     for (int64_t j = 0; j < n; ++j) { out->create_port[j] = -1; out->delete_port[j] = -1; }
     int32_t *ndec = (int32_t *)calloc((size_t)(n > 0 ? n : 1), sizeof(int32_t));
-    uint8_t *mask = NULL;
     out->checked = 0;
     out->multi_decision = 0;
     out->motion_errors = 0;
     for (int32_t k = 0; k < K; ++k) {
         const orc_port *p = &ports[k];
-        int64_t jb = 0, je = n;
-        if (mode == 1) {
-            mask = (uint8_t *)calloc((size_t)(nc > 0 ? nc : 1), 1);
-            orc_port_cells(g, p, mask);
-        }
-        for (int64_t c = 0; c < (mode == 1 ? nc : 1); ++c) {
-            if (mode == 1) {
-                if (!mask[c]) continue;
-                jb = out->cell_start[c];
-                je = out->cell_end[c];
-            }
-            for (int64_t j = jb; j < je; ++j) {
-                ++out->checked;
+        int64_t *rb, *re;
+        const int64_t nr = port_ranges(g, p, mode, n, out->cell_start, out->cell_end, &rb, &re);
+        int64_t checked = 0, motion = 0, multi = 0;
+        /* each particle lies in one range of port k: the iterations are independent */
+#pragma omp parallel for schedule(dynamic, 8) reduction(+ : checked, motion, multi)
+        for (int64_t q = 0; q < nr; ++q) {
+            for (int64_t j = rb[q]; j < re[q]; ++j) {
+                ++checked;
                 int b = classify(p, dim, g->cs, S->x[j], S->y[j], dim == 3 ? S->z[j] : 0.0f);
                 int member = (S->label[j] == k);
-                if (member && !(b & 1)) ++out->motion_errors;          /* reading R12 (diagnostic) */
+                if (member && !(b & 1)) ++motion;                     /* reading R12 (diagnostic) */
                 if (!(b & 1)) continue;                               /* x not in P_k (R4) */
                 int create = 0, del = 0;
                 if (p->kind == ORC_INLET) {
@@ -687,14 +752,17 @@ int orc_update(const orc_grid *g, const orc_port *ports, int32_t K, const orc_st
                     del = member && (b & 8);
                 }
                 if (create || del) {
-                    if (ndec[j]++ > 0) { ++out->multi_decision; continue; }
+                    if (ndec[j]++ > 0) { ++multi; continue; }
                     if (create) out->create_port[j] = k;
                     if (del) out->delete_port[j] = k;
                 }
             }
         }
-        free(mask);
-        mask = NULL;
+        out->checked += checked;
+        out->motion_errors += motion;
+        out->multi_decision += multi;
+        free(rb);
+        free(re);
     }
     free(ndec);
 
@@ -735,26 +803,19 @@ int orc_update(const orc_grid *g, const orc_port *ports, int32_t K, const orc_st
     for (int32_t k = 0; k < K; ++k) {
         const orc_port *p = &ports[k];
         if (p->kind == ORC_INLET) continue;
-        int64_t jb = 0, je = n;
-        if (mode == 1) {
-            mask = (uint8_t *)calloc((size_t)(nc > 0 ? nc : 1), 1);
-            orc_port_cells(g, p, mask);
-        }
-        for (int64_t c = 0; c < (mode == 1 ? nc : 1); ++c) {
-            if (mode == 1) {
-                if (!mask[c]) continue;
-                jb = out->cell_start[c];
-                je = out->cell_end[c];
-            }
-            for (int64_t j = jb; j < je; ++j) {
+        int64_t *rb, *re;
+        const int64_t nr = port_ranges(g, p, mode, n, out->cell_start, out->cell_end, &rb, &re);
+#pragma omp parallel for schedule(dynamic, 8)
+        for (int64_t q = 0; q < nr; ++q) {
+            for (int64_t j = rb[q]; j < re[q]; ++j) {
                 if (out->delete_port[j] >= 0) continue;
                 int b = classify(p, dim, g->cs, S->x[j], S->y[j], dim == 3 ? S->z[j] : 0.0f);
                 if (b & 2) S->label[j] = k;
                 else if (S->label[j] == k) S->label[j] = -1;
             }
         }
-        free(mask);
-        mask = NULL;
+        free(rb);
+        free(re);
     }
 
     /* O5b: boundary-condition state of every buffer particle of port k after the
@@ -771,6 +832,7 @@ int orc_update(const orc_grid *g, const orc_port *ports, int32_t K, const orc_st
     for (int32_t k = 0; k < K; ++k) {
         const orc_port *p = &ports[k];
         if (p->bc == 0) continue;
+#pragma omp parallel for schedule(static)
         for (int64_t j = 0; j < n; ++j) {
             if (out->delete_port[j] >= 0 || S->label[j] != k) continue;
             float u;
@@ -808,6 +870,7 @@ int orc_update(const orc_grid *g, const orc_port *ports, int32_t K, const orc_st
             if (dim == 3) S->vz[j] = u * p->Q[2];
         }
     }
+    out->t_decide = now_s() - t1;
     return 0;
 }
 

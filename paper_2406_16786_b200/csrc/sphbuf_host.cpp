@@ -11,7 +11,19 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "sphbuf_internal.h"
+
+// NVTX range around each enqueueing ABI call (SURVEY §5 "NVTX ranges per phase"):
+// host-side push/pop, free when no tool is attached.
+namespace {
+struct NvtxRange {
+    explicit NvtxRange(const char *n) { nvtxRangePushA(n); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+}  // namespace
+#define SPH_NVTX(name) NvtxRange nvtx_range_(name)
 
 using namespace sphbuf;
 
@@ -606,6 +618,7 @@ sph_status sph_buffer_register(sph_ctx *c, sph_particles *p, const float origin[
                                const float he[3], int32_t kind, int32_t layers, float dp, int32_t *port_id_out,
                                int64_t *members_out_dev, void *stream)
 {
+    SPH_NVTX("sph_buffer_register");
     if (!c) return SPH_ERR_ARG;
     sph_status st = sph_port_check(c, origin, Q, he, kind, layers, dp);
     if (st != SPH_OK) return st;
@@ -726,6 +739,7 @@ static cudaError_t enumerate_slice(sph_ctx *c, int k, const float o[3], const fl
 sph_status sph_port_move(sph_ctx *c, sph_particles *p, int32_t k, const float origin[3], const float Q[9],
                          const int32_t *cell_start, const int32_t *cell_end, void *stream)
 {
+    SPH_NVTX("sph_port_move");
     if (!c) return SPH_ERR_ARG;
     if (!origin || !Q || !cell_start || !cell_end) return fail(c, SPH_ERR_ARG, "NULL argument");
     if (k < 0 || k >= c->pt.n) return fail(c, SPH_ERR_ARG, "unknown port");
@@ -879,6 +893,7 @@ static double fourier_speed(const sph_driver &d, double t)
 sph_status sph_drivers_step(sph_ctx *c, sph_particles *p, double t, double dt, const int32_t *cell_start,
                             const int32_t *cell_end, void *stream)
 {
+    SPH_NVTX("sph_drivers_step");
     if (!c) return SPH_ERR_ARG;
     if (!cell_start || !cell_end) return fail(c, SPH_ERR_ARG, "NULL cell table");
     if (!(dt > 0.0)) return fail(c, SPH_ERR_ARG, "dt <= 0");
@@ -932,6 +947,7 @@ sph_status sph_driver_read(sph_ctx *c, int32_t k, double out[3], void *stream)
 
 sph_status sph_advect(sph_ctx *c, sph_particles *p, float dt, void *stream)
 {
+    SPH_NVTX("sph_advect");
     if (!c) return SPH_ERR_ARG;
     sph_status st = check_particles(c, p);
     if (st != SPH_OK) return st;
@@ -960,6 +976,7 @@ static UpdPro pro_plan(sph_ctx *c, const int32_t *cell_start, const int32_t *cel
 static sph_status cll_build(sph_ctx *c, const sph_particles *in, sph_particles *out, int32_t *cell_start,
                             int32_t *cell_end, int32_t *perm, float dt, bool advect, void *stream)
 {
+    SPH_NVTX("sph_cll_build");
     if (!c) return SPH_ERR_ARG;
     if (c->update_pending) return fail(c, SPH_ERR_STATE, "cll_build: the last buffer update was not compacted");
     sph_status st = check_particles(c, in);
@@ -1001,6 +1018,7 @@ sph_status sph_cll_invalidate(sph_ctx *c)
 sph_status sph_cll_key(sph_ctx *c, sph_particles *in, float dt, int32_t advect, float *send_lo, float *send_hi,
                        void *stream)
 {
+    SPH_NVTX("sph_cll_key");
     if (!c) return SPH_ERR_ARG;
     if (c->update_pending) return fail(c, SPH_ERR_STATE, "cll_key: the last buffer update was not compacted");
     sph_status st = check_particles(c, in);
@@ -1023,6 +1041,7 @@ sph_status sph_cll_key(sph_ctx *c, sph_particles *in, float dt, int32_t advect, 
 sph_status sph_cll_finish(sph_ctx *c, sph_particles *in, sph_particles *out, const float *recv_lo,
                           const float *recv_hi, int32_t *cell_start, int32_t *cell_end, int32_t *perm, void *stream)
 {
+    SPH_NVTX("sph_cll_finish");
     if (!c) return SPH_ERR_ARG;
     if (c->update_pending) return fail(c, SPH_ERR_STATE, "cll_finish: the last buffer update was not compacted");
     sph_status st = check_particles(c, in);
@@ -1049,6 +1068,7 @@ sph_status sph_cll_finish(sph_ctx *c, sph_particles *in, sph_particles *out, con
 sph_status sph_buffer_update(sph_ctx *c, sph_particles *p, const int32_t *cell_start, const int32_t *cell_end,
                              int32_t *port_counts, void *stream)
 {
+    SPH_NVTX("sph_buffer_update");
     if (!c) return SPH_ERR_ARG;
     sph_status st = check_particles(c, p);
     if (st != SPH_OK) return st;
@@ -1070,6 +1090,7 @@ sph_status sph_buffer_update(sph_ctx *c, sph_particles *p, const int32_t *cell_s
 static sph_status compact(sph_ctx *c, sph_particles *p, const int32_t *all_counts, int32_t nranks, int32_t rank,
                           int64_t *next_id_dev, int32_t *perm, bool defer, void *stream)
 {
+    SPH_NVTX("sph_compact");
     if (!c) return SPH_ERR_ARG;
     sph_status st = check_particles(c, p);
     if (st != SPH_OK) return st;
@@ -1107,6 +1128,7 @@ int32_t sph_migrate_record_floats(const sph_ctx *c) { return c ? 2 * c->grid.dim
 
 sph_status sph_migrate_pack(sph_ctx *c, sph_particles *p, float *send_lo, float *send_hi, void *stream)
 {
+    SPH_NVTX("sph_migrate_pack");
     if (!c) return SPH_ERR_ARG;
     sph_status st = check_particles(c, p);
     if (st != SPH_OK) return st;
@@ -1121,6 +1143,7 @@ sph_status sph_migrate_pack(sph_ctx *c, sph_particles *p, float *send_lo, float 
 
 sph_status sph_migrate_unpack(sph_ctx *c, sph_particles *p, const float *recv, void *stream)
 {
+    SPH_NVTX("sph_migrate_unpack");
     if (!c) return SPH_ERR_ARG;
     sph_status st = check_particles(c, p);
     if (st != SPH_OK) return st;
@@ -1222,6 +1245,7 @@ sph_status sph_comm_init_loopback(sph_ctx *const *ctxs, int32_t nranks)
 
 sph_status sph_allgather_counts(sph_ctx *c, const int32_t *port_counts, int32_t *all_counts, void *stream)
 {
+    SPH_NVTX("sph_allgather_counts");
     if (!c || !port_counts || !all_counts) return SPH_ERR_ARG;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const size_t cnt = 2 * (size_t)c->max_ports;
@@ -1242,6 +1266,7 @@ sph_status sph_allgather_counts(sph_ctx *c, const int32_t *port_counts, int32_t 
 
 sph_status sph_migrate_exchange(sph_ctx *c, void *stream)
 {
+    SPH_NVTX("sph_migrate_exchange");
     if (!c) return SPH_ERR_ARG;
     if (!c->comm) return fail(c, SPH_ERR_STATE, "migrate_exchange: no communicator (sph_comm_init)");
     if (c->comm->nranks == 1) return SPH_OK;

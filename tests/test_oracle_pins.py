@@ -7,6 +7,8 @@ them.  None of these expected values is produced by the oracle itself.
 """
 import math
 
+import os
+
 import numpy as np
 import pytest
 
@@ -520,3 +522,27 @@ def test_tie_screen_redraws_only_flagged_particles():
     assert int(diff.sum()) <= w.redrawn
     lat = (w.state["id"] // 6400).double() * 0.0025 + 0.00125       # x lattice site of each id
     assert float((w.state["x"].double() - lat).abs().max()) <= 0.1 * 0.0025 * (1 + 1e-6)
+
+
+def test_oracle_results_do_not_depend_on_threads():
+    """The oracle's parallel loops are the independent per-particle ones; one
+    thread and all threads give identical updates (both modes)."""
+    w = inputs.make("C2")
+    outs = []
+    for t in (1, 0):
+        oracle.set_threads(t if t else (os.cpu_count() or 1))
+        st = oracle.to_numpy_state(w.state)
+        for k, p in enumerate(w.ports):
+            oracle.register(st, w.grid, p, k)
+        for mode in (0, 1):
+            s2 = oracle.to_numpy_state(st)
+            oracle.advect(s2, 2, w.dt)
+            res = oracle.update(w.grid, w.ports, s2, mode=mode)
+            outs.append((t, mode, res))
+    oracle.set_threads(os.cpu_count() or 1)
+    ref = outs[0][2]
+    for t, mode, res in outs[1:]:
+        np.testing.assert_array_equal(res.create_port, ref.create_port)
+        np.testing.assert_array_equal(res.delete_port, ref.delete_port)
+        for c in ref.sorted:
+            np.testing.assert_array_equal(res.sorted[c], ref.sorted[c])
