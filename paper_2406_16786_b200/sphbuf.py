@@ -339,7 +339,9 @@ def sph_comm_init(ctx, unique_id: bytes, nranks, rank):
 def sph_comm_init_loopback(ctxs):
     arr = (C.c_void_p * len(ctxs))(*[c.h.value for c in ctxs])
     rc = lib().sph_comm_init_loopback(arr, len(ctxs))
-    _check(rc, ctxs[0].h if rc else None)
+    if rc:
+        msgs = [m for m in (c.last_error for c in ctxs) if m]
+        raise SphError(rc, "; ".join(msgs))
 
 
 def sph_allgather_counts(ctx, port_counts, all_counts, stream=None):

@@ -311,10 +311,11 @@ def test_loopback_c5_multislab_both_compaction_modes(P):
     for k, p in enumerate(whole.ports):
         oracle.register(st, whole.grid, p, k)
     groups = {}
+    # one message size for every rank (sender and receiver must agree)
+    mm = max(4096, 3 * max(expected_migrants(w.state, w.grid, w.dt) for w in slabs))
     for deferred in (False, True):
         us = []
         for r, w in enumerate(slabs):
-            mm = max(4096, 3 * expected_migrants(w.state, w.grid, w.dt))
             su = SlabUpdater(w, r, P, inputs.capacity_for(w, 0.1), max_migrate=mm, deferred=deferred)
             su.load(w.state, w.next_id)
             us.append(su)
