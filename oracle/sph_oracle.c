@@ -689,19 +689,21 @@ int orc_update(const orc_grid *g, const orc_port *ports, int32_t K, const orc_st
     const int64_t nc = orc_ncells(g);
 
     const double t0 = now_s();
-    /* O2: cell-linked list -- cell of each particle, then order by (cell, id). */
+    /* O2: cell-linked list -- cell of each particle, then order by
+     * (cell, id): a counting sort by cell (histogram, exclusive prefix = the cell
+     * tables, placement), then each cell's particles sorted by id. */
+    int64_t *cell = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n > 0 ? n : 1));
     key_t3 *keys = (key_t3 *)malloc(sizeof(key_t3) * (size_t)(n > 0 ? n : 1));
-    out->out_of_grid = 0;
+    int64_t oob_total = 0;
+#pragma omp parallel for schedule(static) reduction(+ : oob_total)
     for (int64_t i = 0; i < n; ++i) {
         int32_t oob = 0;
-        keys[i].cell = orc_cell_of(g, in->x[i], in->y[i], dim == 3 ? in->z[i] : 0.0f, &oob);
-        keys[i].id = in->id[i];
-        keys[i].idx = i;
-        out->out_of_grid += oob;
+        cell[i] = orc_cell_of(g, in->x[i], in->y[i], dim == 3 ? in->z[i] : 0.0f, &oob);
+        oob_total += oob;
     }
-    qsort(keys, (size_t)n, sizeof(key_t3), cmp_key);
+    out->out_of_grid = oob_total;
     for (int64_t c = 0; c < nc; ++c) { out->cell_start[c] = 0; out->cell_end[c] = 0; }
-    for (int64_t j = 0; j < n; ++j) out->cell_end[keys[j].cell] += 1;     /* counts */
+    for (int64_t i = 0; i < n; ++i) out->cell_end[cell[i]] += 1;          /* counts */
     int64_t run = 0;
     for (int64_t c = 0; c < nc; ++c) {
         int64_t cnt = out->cell_end[c];
@@ -709,8 +711,39 @@ int orc_update(const orc_grid *g, const orc_port *ports, int32_t K, const orc_st
         run += cnt;
         out->cell_end[c] = (int32_t)run;
     }
+    {
+        int32_t *cursor = (int32_t *)malloc(sizeof(int32_t) * (size_t)(nc > 0 ? nc : 1));
+        for (int64_t c = 0; c < nc; ++c) cursor[c] = out->cell_start[c];
+        for (int64_t i = 0; i < n; ++i) {
+            const int64_t j = cursor[cell[i]]++;
+            keys[j].cell = cell[i];
+            keys[j].id = in->id[i];
+            keys[j].idx = i;
+        }
+        free(cursor);
+    }
+    free(cell);
+    /* each cell by id (cells are independent) */
+#pragma omp parallel for schedule(dynamic, 4096)
+    for (int64_t c = 0; c < nc; ++c) {
+        const int64_t b = out->cell_start[c], e = out->cell_end[c];
+        if (e - b > 32) {
+            qsort(keys + b, (size_t)(e - b), sizeof(key_t3), cmp_key);
+            continue;
+        }
+        for (int64_t u = b + 1; u < e; ++u) {          /* insertion sort */
+            key_t3 t = keys[u];
+            int64_t v = u;
+            while (v > b && keys[v - 1].id > t.id) {
+                keys[v] = keys[v - 1];
+                --v;
+            }
+            keys[v] = t;
+        }
+    }
     orc_state *S = &out->sorted;
     S->n = n;
+#pragma omp parallel for schedule(static)
     for (int64_t j = 0; j < n; ++j) {
         out->order[j] = keys[j].idx;
         copy_row(in, keys[j].idx, S, j, dim);

@@ -4,6 +4,7 @@
 // the candidates of the port cell runs (arXiv 2406.16786 §III).
 #include <climits>
 #include <cstdint>
+#include <cstdlib>
 
 #include "sphbuf_common.cuh"
 #include "sphbuf_prologue.cuh"
@@ -122,7 +123,7 @@ __device__ __forceinline__ float bc_speed(const PortDev &P, int dim, float vx, f
 // dependent memory round trips.
 __global__ void __launch_bounds__(kThreads) k_upd_main(PartDev p, GridDev g, const __grid_constant__ PortTable pt,
                                                        Workspace ws, int n_runs, const int *cell_start,
-                                                       int *port_counts, int carry, float cdt)
+                                                       int *port_counts, int carry, float cdt, int tile_runs_max)
 {
     const int dim = g.dim;
     pdl_entry();
@@ -177,7 +178,7 @@ __global__ void __launch_bounds__(kThreads) k_upd_main(PartDev p, GridDev g, con
         const int r0 = ws.tile_run[tile];
         const int r1 = tile + 1 < ntiles ? ws.tile_run[tile + 1] : n_runs - 1;
         const int nr = r1 - r0 + 1;
-        const bool staged = nr <= kTileRuns;
+        const bool staged = nr <= tile_runs_max;   // (tests lower it: SPHBUF_TILE_RUNS)
         if (staged) {
             for (int i = threadIdx.x; i < nr; i += blockDim.x) {
                 s_roff[i] = (int)(ws.run_off[r0 + i] - t0);
@@ -533,9 +534,16 @@ cudaError_t launch_update(const PartDev &p, const GridDev &g, const PortTable &p
     }
     static int grid = 0;
     if (!grid) grid = occ_grid(k_upd_main, kThreads);
+    // SPHBUF_TILE_RUNS=<n> lowers the number of runs a tile stages in shared memory
+    // (tests force the global-search path with 0)
+    static const int trmax = [] {
+        const char *e = getenv("SPHBUF_TILE_RUNS");
+        const int v = e ? atoi(e) : kTileRuns;
+        return v < kTileRuns ? (v < 0 ? 0 : v) : kTileRuns;
+    }();
     L->before(s);
     launch_k(k_upd_main, dim3(cap_grid(grid, ws.upd_tiles, 1)), dim3(kThreads), 0, s, p, g, pt, ws, n_runs, cell_start,
-             port_counts, carry, cdt);
+             port_counts, carry, cdt, trmax);
     L->after(s, KID_UPD_MAIN);
     return cudaGetLastError();
 }

@@ -87,3 +87,31 @@ def test_inplace_compaction_label_pass_fallback():
     env = dict(os.environ, SPHBUF_DLIST_MAX="0")
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
+
+
+@pytest.mark.gpu
+def test_update_global_run_search_path():
+    """K6 stages a tile's port runs in shared memory when they fit (kTileRuns);
+    otherwise it binary-searches the runs in global memory.  SPHBUF_TILE_RUNS=0
+    (read once per process, hence a subprocess) forces the global path for every
+    tile: bit-exact with the oracle on C2 (bidirectional), a 3-D junction with
+    in-place compaction and moving random ports."""
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    code = ("import sys; sys.path.insert(0, %r); sys.path.insert(0, %r)\n"
+            "import oracle; oracle.enable_tie_check(1e-4)\n"
+            "from paper_2406_16786_b200 import inputs\n"
+            "from parity_util import lockstep\n"
+            "tot, bu = lockstep(inputs.make('C2'), 12, check_every=3, fused=True, deferred=True)\n"
+            "assert tot[0] > 0 and tot[1] > 0\n"
+            "w = inputs.c4(scale=0.25, nports=4, n_updates=6)\n"
+            "tot, bu = lockstep(w, 6, check_every=1, fused=True, deferred=False)\n"
+            "assert tot.sum() > 0\n"
+            "import test_random_gpu as tr\n"
+            "tr.test_random_moving_ports_lockstep(3)\n"
+            "print('ok')\n") % (os.path.dirname(here), here)
+    env = dict(os.environ, SPHBUF_TILE_RUNS="0")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]

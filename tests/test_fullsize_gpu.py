@@ -26,20 +26,25 @@ def test_C3_full_duct_inplace_compaction():
     assert tot[0] > 0 and tot[1] > 0
 
 
-def test_C4_full_junction_two_updates():
+def test_C4_full_junction_20_updates():
+    """BASELINE configs[3] at full size: 20 updates, every state compared at updates
+    0, 10 and 19 (every update's counts and the oracle's tie certification run)."""
     w = inputs.c4(device="cuda", n_updates=100)
     assert w.n > 60_000_000
-    tot, bu = lockstep(w, 2, check_every=1, fused=True, deferred=True)
+    tot, bu = lockstep(w, 20, check_every=10, fused=True, deferred=True)
     assert tot[0] > 0 and tot[1] > 0
     del bu
     torch.cuda.empty_cache()
 
 
-def test_C5_full_slab_two_updates():
-    """(the second build uses the keys the first build's gather carried over)"""
+def test_C5_full_slab_50_updates_sampled():
+    """BASELINE configs[4] at full size for its whole 50-update run, in the bench's
+    launch configuration (fused advection, key carry-over, deferred compaction):
+    state, cell tables and counts compared bit-exactly every 10 updates and after
+    the last; the tie margin certified at every decision and relabel point."""
     w = inputs.c5(device="cuda", slab=0, nslabs=1)
     assert w.n > 120_000_000
-    tot, bu = lockstep(w, 2, check_every=1, fused=True, deferred=True)
+    tot, bu = lockstep(w, 50, check_every=10, fused=True, deferred=True)
     assert tot[0] > 0 and tot[1] > 0
     del bu
     torch.cuda.empty_cache()
