@@ -20,6 +20,7 @@
 #include <cstdint>
 
 #include "sphbuf_common.cuh"
+#include "sphbuf_tma.cuh"
 
 namespace sphbuf {
 
@@ -476,6 +477,178 @@ __global__ void __launch_bounds__(kThreads) k_compact_move2(PartDev p, int dim, 
     }
 }
 
+// K7b with the copy engine (no extra columns, no perm; the default in-place move):
+// sub-tiles move through shared memory by 1-D bulk copies.  Per sub-tile: one
+// thread arms an mbarrier and issues one cp.async.bulk per column (x, y, (z), vx,
+// vy, (vz), label, carried key, id) into an input stage; the block ranks the
+// survivors (striped scan of the labels), publishes "read done" (the bulk copy
+// completed: every byte of the input has left global memory), waits for the few
+// earlier sub-tiles its output range overlaps (as k_compact_move2), packs the
+// survivors into an output stage laid out with the same 16-byte phase as their
+// destination [dst0, dst0 + alive), and one thread issues a bulk store per column
+// for the 16-byte aligned middle; the ragged ends (< 16 bytes per column) are
+// stored by the threads that hold them.  Two input stages: the next sub-tile's
+// copies are in flight while this one is ranked, waited for and stored.
+constexpr int kTmaStage = kCmpTile + 4;     // elements per column per stage (+ room for the 16-byte phase)
+struct alignas(16) TmaStage {
+    float c[6][kTmaStage];                   // x, y, z, vx, vy, vz
+    int lab[kTmaStage];
+    int key[kTmaStage];
+    long long id[kTmaStage];
+};
+constexpr size_t kTmaSmem = 3 * sizeof(TmaStage);
+
+__global__ void __launch_bounds__(kThreads, 1) k_compact_move_tma(PartDev p, int dim, Workspace ws, int carry)
+{
+    pdl_entry();
+    extern __shared__ __align__(128) unsigned char dsm[];
+    TmaStage *stage = reinterpret_cast<TmaStage *>(dsm);    // [0], [1]: input; [2]: output
+    __shared__ __align__(8) uint64_t s_bar[2];
+    __shared__ unsigned s_cnt[kCmpItems * kThreads / 32 + 1];
+    __shared__ long long s_tile;
+    Counters *ctr = ws.ctr;
+    const long long D = ctr->n_del;
+    if (D == 0) return;
+    const long long N = ctr->cmp_n;
+    const long long ibeg = cmp_begin(ctr->i_first);
+    const unsigned epoch = ctr->epoch_cmp;
+    const long long nsub = (N - ibeg + kCmpTile - 1) / kCmpTile;
+    const int ncf = dim == 3 ? 6 : 4;                       // float columns in use
+    float *gcol[6] = {p.x, p.y, p.vx, p.vy, p.z, p.vz};     // (2-D: the first four)
+    const int scol[6] = {0, 1, 3, 4, 2, 5};                 // their index in TmaStage::c
+    if (threadIdx.x == 0) {
+        mbar_init(&s_bar[0], 1);
+        mbar_init(&s_bar[1], 1);
+        fence_mbar_init();
+    }
+    auto ticket = [&]() -> long long {
+        if (threadIdx.x == 0) s_tile = atomicAdd(&ctr->ticket_cmp2, 1);
+        __syncthreads();
+        const long long t = s_tile;
+        __syncthreads();
+        return t;
+    };
+    // thread 0: bulk copies of sub-tile u into input stage b (16-byte multiples; the
+    // last sub-tile's ragged remainder is loaded by the threads after the wait)
+    auto issue = [&](long long u, int b) {
+        const long long start = ibeg + u * kCmpTile;
+        const long long cnt = N - start < kCmpTile ? N - start : kCmpTile;
+        const uint32_t n4 = (uint32_t)(cnt & ~3LL), n8 = (uint32_t)(cnt & ~1LL);
+        const uint32_t bytes = (uint32_t)(ncf + 1 + (carry ? 1 : 0)) * n4 * 4u + n8 * 8u;
+        TmaStage &S = stage[b];
+        mbar_arrive_expect_tx(&s_bar[b], bytes);
+        if (n4) {
+            for (int c = 0; c < ncf; ++c) bulk_g2s(S.c[scol[c]], gcol[c] + start, n4 * 4u, &s_bar[b]);
+            bulk_g2s(S.lab, p.label + start, n4 * 4u, &s_bar[b]);
+            if (carry) bulk_g2s(S.key, ws.key + start, n4 * 4u, &s_bar[b]);
+        }
+        if (n8) bulk_g2s(S.id, p.id + start, n8 * 8u, &s_bar[b]);
+    };
+    long long u = ticket();
+    if (u >= nsub) return;
+    int b = 0;
+    uint32_t ph0 = 0, ph1 = 0;
+    if (threadIdx.x == 0) issue(u, 0);
+    while (true) {
+        const long long u2 = ticket();
+        const bool more = u2 < nsub;
+        if (more && threadIdx.x == 0) issue(u2, b ^ 1);
+        mbar_wait(&s_bar[b], b ? ph1 : ph0);
+        if (b) ph1 ^= 1u;
+        else ph0 ^= 1u;
+        TmaStage &S = stage[b];
+        TmaStage &O = stage[2];
+        const long long start = ibeg + u * kCmpTile;
+        const int cnt = (int)(N - start < kCmpTile ? N - start : kCmpTile);
+        const int n4 = cnt & ~3, n8 = cnt & ~1;
+        // ragged remainder of the last sub-tile (< 4 elements)
+        for (int e = n4 + (int)threadIdx.x; e < cnt; e += kThreads) {
+            for (int c = 0; c < ncf; ++c) S.c[scol[c]][e] = gcol[c][start + e];
+            S.lab[e] = p.label[start + e];
+            if (carry) S.key[e] = ws.key[start + e];
+        }
+        for (int e = n8 + (int)threadIdx.x; e < cnt; e += kThreads) S.id[e] = p.id[start + e];
+        if (cnt < kCmpTile) __syncthreads();                 // (uniform) the remainder is read by other threads
+        bool alive[kCmpItems];
+        unsigned excl[kCmpItems], total;
+#pragma unroll
+        for (int it = 0; it < kCmpItems; ++it) {
+            const int e = it * kThreads + threadIdx.x;
+            alive[it] = e < cnt && S.lab[e] > -2;
+        }
+        striped_scan<kThreads, kCmpItems>(alive, excl, total, s_cnt);   // contains __syncthreads
+        const long long dst0 = start - (long long)ws.sub_off[u];
+        if (threadIdx.x < 32) {
+            // every input byte of u has left global memory (bulk copy complete, ragged
+            // loads consumed before the scan's barrier)
+            if (threadIdx.x == 0)
+                asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(ws.rd + u), "r"(epoch) : "memory");
+            if (total > 0 && dst0 < start) {
+                const long long vlo = (dst0 - ibeg) / kCmpTile;
+                long long vhi = (dst0 + total - 1 - ibeg) / kCmpTile;
+                if (vhi > u - 1) vhi = u - 1;
+                for (long long v = vlo + threadIdx.x; v <= vhi; v += 32) {
+                    unsigned f;
+                    do {
+                        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(ws.rd + v) : "memory");
+                    } while (f != epoch);
+                }
+            }
+            __syncwarp();
+            if (threadIdx.x == 0) bulk_wait_read_all();     // the output stage is free again
+        }
+        __syncthreads();
+        // survivors into the output stage, 16-byte phase of the destination kept;
+        // the ragged ends of each column go straight to global memory
+        const long long end = dst0 + total;
+        const long long a4 = (dst0 + 3) & ~3LL, e4 = end & ~3LL;
+        const long long a8 = (dst0 + 1) & ~1LL, e8 = end & ~1LL;
+        const long long base4 = dst0 & ~3LL, base8 = dst0 & ~1LL;
+        const bool mid4 = e4 > a4, mid8 = e8 > a8;
+#pragma unroll
+        for (int it = 0; it < kCmpItems; ++it) {
+            if (!alive[it]) continue;
+            const int e = it * kThreads + threadIdx.x;
+            const long long o = dst0 + excl[it];
+            const int s4 = (int)(o - base4), s8 = (int)(o - base8);
+            const bool dir4 = !mid4 || o < a4 || o >= e4, dir8 = !mid8 || o < a8 || o >= e8;
+            for (int c = 0; c < ncf; ++c) {
+                const float v = S.c[scol[c]][e];
+                if (dir4) gcol[c][o] = v;
+                else O.c[scol[c]][s4] = v;
+            }
+            const int lv = S.lab[e];
+            if (dir4) p.label[o] = lv;
+            else O.lab[s4] = lv;
+            if (carry) {
+                const int kv = S.key[e];
+                if (dir4) ws.key[o] = kv;
+                else O.key[s4] = kv;
+            }
+            const long long iv = S.id[e];
+            if (dir8) p.id[o] = iv;
+            else O.id[s8] = iv;
+        }
+        fence_async_smem();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            if (mid4) {
+                const int s = (int)(a4 - base4);
+                const uint32_t bytes = (uint32_t)(e4 - a4) * 4u;
+                for (int c = 0; c < ncf; ++c) bulk_s2g(gcol[c] + a4, O.c[scol[c]] + s, bytes);
+                bulk_s2g(p.label + a4, O.lab + s, bytes);
+                if (carry) bulk_s2g(ws.key + a4, O.key + s, bytes);
+            }
+            if (mid8) bulk_s2g(p.id + a8, O.id + (int)(a8 - base8), (uint32_t)(e8 - a8) * 8u);
+            bulk_commit();
+        }
+        if (!more) break;
+        u = u2;
+        b ^= 1;
+    }
+    if (threadIdx.x == 0) bulk_wait_all();
+}
+
 // Staged particles after the survivors with IDs from the count matrix (reading
 // R14, §8(e)): off(k, r) = next_id + sum_{k'<k} sum_r' C[r'][k'] + sum_{r'<r} C[r'][k];
 // identity perm below i_first; then N and next_id.
@@ -606,7 +779,26 @@ cudaError_t launch_compact(const PartDev &p, const GridDev &g, const PortTable &
     } else {
         static int grid = 0;
         static const bool one = getenv("SPHBUF_MOVE1") != nullptr;   // A/B: one sub-tile in flight
-        if (one) {
+        // the copy-engine move (default); SPHBUF_MOVE_TMA=0 selects the register move
+        static const bool tma = [] {
+            const char *e = getenv("SPHBUF_MOVE_TMA");
+            return !(e && e[0] == '0');
+        }();
+        const bool aligned = ((reinterpret_cast<size_t>(p.x) | reinterpret_cast<size_t>(p.y) |
+                               reinterpret_cast<size_t>(p.vx) | reinterpret_cast<size_t>(p.vy) |
+                               reinterpret_cast<size_t>(p.label) | reinterpret_cast<size_t>(p.id) |
+                               reinterpret_cast<size_t>(ws.key) |
+                               (dim == 3 ? reinterpret_cast<size_t>(p.z) | reinterpret_cast<size_t>(p.vz) : 0)) &
+                              15) == 0;
+        if (tma && aligned && !perm && !one) {
+            static bool attr = false;
+            if (!attr) {
+                cudaFuncSetAttribute(k_compact_move_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem);
+                attr = true;
+            }
+            launch_k(k_compact_move_tma, dim3(cap_grid(sm_count_cached(), p.cap, kCmpTile)), dim3(kThreads),
+                     kTmaSmem, s, p, dim, ws, carry);
+        } else if (one) {
             if (!grid) grid = occ_grid(k_compact_move<false>, kThreads);
             launch_k(k_compact_move<false>, dim3(cap_grid(grid, p.cap, kCmpTile)), dim3(kThreads), 0, s, p, dim, ws,
                      perm, carry);

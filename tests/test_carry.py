@@ -115,3 +115,28 @@ def test_update_global_run_search_path():
     env = dict(os.environ, SPHBUF_TILE_RUNS="0")
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
+
+
+@pytest.mark.gpu
+def test_inplace_compaction_register_move_path():
+    """The in-place move runs on the copy engine (k_compact_move_tma, bulk copies
+    through shared memory) by default; SPHBUF_MOVE_TMA=0 selects the register move
+    (k_compact_move2): both bit-exact with the oracle (3-D junction, carried keys;
+    C2 in 2-D)."""
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    code = ("import sys; sys.path.insert(0, %r); sys.path.insert(0, %r)\n"
+            "import oracle; oracle.enable_tie_check(1e-4)\n"
+            "from paper_2406_16786_b200 import inputs\n"
+            "from parity_util import lockstep\n"
+            "w = inputs.c4(scale=0.25, nports=4, n_updates=6)\n"
+            "tot, bu = lockstep(w, 6, check_every=1, fused=True, deferred=False)\n"
+            "assert tot[1] > 0\n"
+            "tot, bu = lockstep(inputs.make('C2'), 8, check_every=1, fused=False, deferred=False)\n"
+            "assert tot[1] > 0\n"
+            "print('ok')\n") % (os.path.dirname(here), here)
+    env = dict(os.environ, SPHBUF_MOVE_TMA="0")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
