@@ -477,35 +477,42 @@ __global__ void __launch_bounds__(kThreads) k_compact_move2(PartDev p, int dim, 
     }
 }
 
-// K7b with the copy engine (no extra columns, no perm; the default in-place move):
-// sub-tiles move through shared memory by 1-D bulk copies.  Per sub-tile: one
-// thread arms an mbarrier and issues one cp.async.bulk per column (x, y, (z), vx,
-// vy, (vz), label, carried key, id) into an input stage; the block ranks the
-// survivors (striped scan of the labels), publishes "read done" (the bulk copy
-// completed: every byte of the input has left global memory), waits for the few
-// earlier sub-tiles its output range overlaps (as k_compact_move2), packs the
-// survivors into an output stage laid out with the same 16-byte phase as their
-// destination [dst0, dst0 + alive), and one thread issues a bulk store per column
-// for the 16-byte aligned middle; the ragged ends (< 16 bytes per column) are
-// stored by the threads that hold them.  Two input stages: the next sub-tile's
-// copies are in flight while this one is ranked, waited for and stored.
+// K7b on the copy engine (no extra columns, no perm; the default in-place move),
+// warp-specialised.  Warp 0 is the producer: one lane takes sub-tile tickets,
+// waits for a free stage, arms the stage's "full" mbarrier and issues one
+// cp.async.bulk per column (x, y, (z), vx, vy, (vz), label, carried key, id) into
+// it, and publishes "read done" for every sub-tile as soon as its copy completed
+// (every input byte has left global memory), in ticket order.  Warp 1 checks the
+// dependencies ahead of the consumers: for each issued sub-tile it waits for the
+// "read done" of the earlier sub-tiles whose input the sub-tile's output range
+// can overlap (outputs move down by at most D), then arrives on the stage's
+// "ready" mbarrier — so no global-memory poll is on the consumers' path.  Warps
+// 2..9 consume the stages in order: rank the survivors (striped scan of the
+// labels), compact them inside the stage, shifted to the 16-byte phase of their
+// destination [dst0, dst0 + alive), and one lane issues a bulk store per column
+// for the aligned middle (the ragged ends, < 16 bytes per column, are stored by
+// the threads that hold them); the stage returns to the producer once that store
+// has read it.  kTmaStages stages: up to kTmaStages - 2 copies in flight per SM.
 constexpr int kTmaStage = kCmpTile + 4;     // elements per column per stage (+ room for the 16-byte phase)
+constexpr int kTmaStages = 5;
 struct alignas(16) TmaStage {
     float c[6][kTmaStage];                   // x, y, z, vx, vy, vz
     int lab[kTmaStage];
     int key[kTmaStage];
     long long id[kTmaStage];
 };
-constexpr size_t kTmaSmem = 3 * sizeof(TmaStage);
+constexpr size_t kTmaSmem = kTmaStages * sizeof(TmaStage);
+constexpr int kTmaThreads = kThreads + 64;   // 8 consumer warps + the producer and the dependency warp
 
-__global__ void __launch_bounds__(kThreads, 1) k_compact_move_tma(PartDev p, int dim, Workspace ws, int carry)
+__global__ void __launch_bounds__(kTmaThreads, 1) k_compact_move_tma(PartDev p, int dim, Workspace ws, int carry)
 {
     pdl_entry();
     extern __shared__ __align__(128) unsigned char dsm[];
-    TmaStage *stage = reinterpret_cast<TmaStage *>(dsm);    // [0], [1]: input; [2]: output
-    __shared__ __align__(8) uint64_t s_bar[2];
+    TmaStage *stage = reinterpret_cast<TmaStage *>(dsm);
+    __shared__ __align__(8) uint64_t s_full[kTmaStages], s_empty[kTmaStages], s_ready[kTmaStages];
+    __shared__ long long s_tile[kTmaStages];
+    __shared__ volatile long long s_issued;
     __shared__ unsigned s_cnt[kCmpItems * kThreads / 32 + 1];
-    __shared__ long long s_tile;
     Counters *ctr = ws.ctr;
     const long long D = ctr->n_del;
     if (D == 0) return;
@@ -514,139 +521,211 @@ __global__ void __launch_bounds__(kThreads, 1) k_compact_move_tma(PartDev p, int
     const unsigned epoch = ctr->epoch_cmp;
     const long long nsub = (N - ibeg + kCmpTile - 1) / kCmpTile;
     const int ncf = dim == 3 ? 6 : 4;                       // float columns in use
-    float *gcol[6] = {p.x, p.y, p.vx, p.vy, p.z, p.vz};     // (2-D: the first four)
-    const int scol[6] = {0, 1, 3, 4, 2, 5};                 // their index in TmaStage::c
     if (threadIdx.x == 0) {
-        mbar_init(&s_bar[0], 1);
-        mbar_init(&s_bar[1], 1);
+        for (int s = 0; s < kTmaStages; ++s) {
+            mbar_init(&s_full[s], 1);
+            mbar_init(&s_empty[s], 1);
+            mbar_init(&s_ready[s], 1);
+        }
         fence_mbar_init();
+        s_issued = 0;
     }
-    auto ticket = [&]() -> long long {
-        if (threadIdx.x == 0) s_tile = atomicAdd(&ctr->ticket_cmp2, 1);
-        __syncthreads();
-        const long long t = s_tile;
-        __syncthreads();
-        return t;
-    };
-    // thread 0: bulk copies of sub-tile u into input stage b (16-byte multiples; the
-    // last sub-tile's ragged remainder is loaded by the threads after the wait)
-    auto issue = [&](long long u, int b) {
-        const long long start = ibeg + u * kCmpTile;
-        const long long cnt = N - start < kCmpTile ? N - start : kCmpTile;
-        const uint32_t n4 = (uint32_t)(cnt & ~3LL), n8 = (uint32_t)(cnt & ~1LL);
-        const uint32_t bytes = (uint32_t)(ncf + 1 + (carry ? 1 : 0)) * n4 * 4u + n8 * 8u;
-        TmaStage &S = stage[b];
-        mbar_arrive_expect_tx(&s_bar[b], bytes);
-        if (n4) {
-            for (int c = 0; c < ncf; ++c) bulk_g2s(S.c[scol[c]], gcol[c] + start, n4 * 4u, &s_bar[b]);
-            bulk_g2s(S.lab, p.label + start, n4 * 4u, &s_bar[b]);
-            if (carry) bulk_g2s(S.key, ws.key + start, n4 * 4u, &s_bar[b]);
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        // ---------------------------------------------------------------- producer
+        if (threadIdx.x != 0) return;
+        float *gcol[6] = {p.x, p.y, p.vx, p.vy, p.z, p.vz};
+        const int scol[6] = {0, 1, 3, 4, 2, 5};
+        long long issued = 0, published = 0;
+        long long tiles[kTmaStages];
+        bool done = false;
+        while (!done || published < issued) {
+            // publish every completed copy, in order
+            while (published < issued) {
+                const int s = (int)(published % kTmaStages);
+                if (!mbar_test(&s_full[s], (uint32_t)((published / kTmaStages) & 1))) break;
+                asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(ws.rd + tiles[s]), "r"(epoch) : "memory");
+                ++published;
+            }
+            if (done) continue;
+            // the next stage, once its previous sub-tile has been stored
+            const int s = (int)(issued % kTmaStages);
+            if (issued >= kTmaStages && !mbar_test(&s_empty[s], (uint32_t)(((issued / kTmaStages) - 1) & 1)))
+                continue;
+            const long long u = atomicAdd(&ctr->ticket_cmp2, 1);
+            s_tile[s] = u;
+            if (u >= nsub) {
+                mbar_arrive(&s_full[s]);                   // consumers see the end
+                __threadfence_block();
+                s_issued = issued + 1;                     // (the dependency warp sees the end too)
+                done = true;
+                continue;
+            }
+            const long long start = ibeg + u * kCmpTile;
+            const long long cnt = N - start < kCmpTile ? N - start : kCmpTile;
+            const uint32_t n4 = (uint32_t)(cnt & ~3LL), n8 = (uint32_t)(cnt & ~1LL);
+            const uint32_t bytes = (uint32_t)(ncf + 1 + (carry ? 1 : 0)) * n4 * 4u + n8 * 8u;
+            TmaStage &S = stage[s];
+            mbar_arrive_expect_tx(&s_full[s], bytes);
+            if (n4) {
+                for (int c = 0; c < ncf; ++c) bulk_g2s(S.c[scol[c]], gcol[c] + start, n4 * 4u, &s_full[s]);
+                bulk_g2s(S.lab, p.label + start, n4 * 4u, &s_full[s]);
+                if (carry) bulk_g2s(S.key, ws.key + start, n4 * 4u, &s_full[s]);
+            }
+            if (n8) bulk_g2s(S.id, p.id + start, n8 * 8u, &s_full[s]);
+            tiles[s] = u;
+            ++issued;
+            __threadfence_block();
+            s_issued = issued;
         }
-        if (n8) bulk_g2s(S.id, p.id + start, n8 * 8u, &s_bar[b]);
-    };
-    long long u = ticket();
-    if (u >= nsub) return;
-    int b = 0;
-    uint32_t ph0 = 0, ph1 = 0;
-    if (threadIdx.x == 0) issue(u, 0);
-    while (true) {
-        const long long u2 = ticket();
-        const bool more = u2 < nsub;
-        if (more && threadIdx.x == 0) issue(u2, b ^ 1);
-        mbar_wait(&s_bar[b], b ? ph1 : ph0);
-        if (b) ph1 ^= 1u;
-        else ph0 ^= 1u;
-        TmaStage &S = stage[b];
-        TmaStage &O = stage[2];
-        const long long start = ibeg + u * kCmpTile;
-        const int cnt = (int)(N - start < kCmpTile ? N - start : kCmpTile);
-        const int n4 = cnt & ~3, n8 = cnt & ~1;
-        // ragged remainder of the last sub-tile (< 4 elements)
-        for (int e = n4 + (int)threadIdx.x; e < cnt; e += kThreads) {
-            for (int c = 0; c < ncf; ++c) S.c[scol[c]][e] = gcol[c][start + e];
-            S.lab[e] = p.label[start + e];
-            if (carry) S.key[e] = ws.key[start + e];
-        }
-        for (int e = n8 + (int)threadIdx.x; e < cnt; e += kThreads) S.id[e] = p.id[start + e];
-        if (cnt < kCmpTile) __syncthreads();                 // (uniform) the remainder is read by other threads
-        bool alive[kCmpItems];
-        unsigned excl[kCmpItems], total;
-#pragma unroll
-        for (int it = 0; it < kCmpItems; ++it) {
-            const int e = it * kThreads + threadIdx.x;
-            alive[it] = e < cnt && S.lab[e] > -2;
-        }
-        striped_scan<kThreads, kCmpItems>(alive, excl, total, s_cnt);   // contains __syncthreads
-        const long long dst0 = start - (long long)ws.sub_off[u];
-        if (threadIdx.x < 32) {
-            // every input byte of u has left global memory (bulk copy complete, ragged
-            // loads consumed before the scan's barrier)
-            if (threadIdx.x == 0)
-                asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(ws.rd + u), "r"(epoch) : "memory");
-            if (total > 0 && dst0 < start) {
+        return;
+    }
+    if (threadIdx.x < 64) {
+        // ---------------------------------------------------------- dependency warp
+        const int lane = threadIdx.x & 31;
+        for (long long it = 0;; ++it) {
+            while (s_issued <= it) {
+            }
+            __threadfence_block();
+            const int s = (int)(it % kTmaStages);
+            const long long u = s_tile[s];
+            if (u >= nsub) break;
+            const long long start = ibeg + u * kCmpTile;
+            const long long cnt = N - start < kCmpTile ? N - start : kCmpTile;
+            const long long dst0 = start - (long long)ws.sub_off[u];
+            if (dst0 < start) {
+                // the output is at most [dst0, dst0 + cnt): wait for the earlier
+                // sub-tiles whose input it can overlap
                 const long long vlo = (dst0 - ibeg) / kCmpTile;
-                long long vhi = (dst0 + total - 1 - ibeg) / kCmpTile;
+                long long vhi = (dst0 + cnt - 1 - ibeg) / kCmpTile;
                 if (vhi > u - 1) vhi = u - 1;
-                for (long long v = vlo + threadIdx.x; v <= vhi; v += 32) {
+                for (long long w = vlo + lane; w <= vhi; w += 32) {
                     unsigned f;
                     do {
-                        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(ws.rd + v) : "memory");
+                        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(ws.rd + w) : "memory");
                     } while (f != epoch);
                 }
             }
             __syncwarp();
-            if (threadIdx.x == 0) bulk_wait_read_all();     // the output stage is free again
+            if (lane == 0) mbar_arrive(&s_ready[s]);
         }
-        __syncthreads();
-        // survivors into the output stage, 16-byte phase of the destination kept;
-        // the ragged ends of each column go straight to global memory
+        return;
+    }
+    // -------------------------------------------------------------------- consumers
+    const int ct = threadIdx.x - 64, lane = ct & 31, cw = ct >> 5;
+    constexpr int NW = kThreads / 32;
+    float *gcol[6] = {p.x, p.y, p.vx, p.vy, p.z, p.vz};
+    const int scol[6] = {0, 1, 3, 4, 2, 5};
+    int prev = -1;                                           // stage whose store is still reading
+    for (long long it = 0;; ++it) {
+        const int s = (int)(it % kTmaStages);
+        mbar_wait(&s_full[s], (uint32_t)((it / kTmaStages) & 1));
+        const long long u = s_tile[s];
+        if (u >= nsub) break;
+        TmaStage &S = stage[s];
+        const long long start = ibeg + u * kCmpTile;
+        const int cnt = (int)(N - start < kCmpTile ? N - start : kCmpTile);
+        const int n4 = cnt & ~3, n8 = cnt & ~1;
+        // ragged remainder of the last sub-tile (< 4 elements): loaded here
+        if (cnt < kCmpTile) {
+            for (int e = n4 + ct; e < cnt; e += kThreads) {
+                for (int c = 0; c < ncf; ++c) S.c[scol[c]][e] = gcol[c][start + e];
+                S.lab[e] = p.label[start + e];
+                if (carry) S.key[e] = ws.key[start + e];
+            }
+            for (int e = n8 + ct; e < cnt; e += kThreads) S.id[e] = p.id[start + e];
+            named_bar(1, kThreads);
+        }
+        // my elements into registers, survivors ranked (striped order: element it * NT + ct)
+        float v[kCmpItems][6];
+        int lb[kCmpItems], kv[kCmpItems];
+        long long idv[kCmpItems];
+        bool alive[kCmpItems];
+        unsigned bal[kCmpItems];
+#pragma unroll
+        for (int q = 0; q < kCmpItems; ++q) {
+            const int e = q * kThreads + ct;
+            alive[q] = false;
+            if (e < cnt) {
+#pragma unroll
+                for (int c = 0; c < 6; ++c) v[q][c] = c < ncf ? S.c[scol[c]][e] : 0.0f;
+                lb[q] = S.lab[e];
+                kv[q] = carry ? S.key[e] : 0;
+                idv[q] = S.id[e];
+                alive[q] = lb[q] > -2;
+            }
+            bal[q] = __ballot_sync(0xffffffffu, alive[q]);
+            if (lane == 0) s_cnt[q * NW + cw] = __popc(bal[q]);
+        }
+        named_bar(1, kThreads);
+        unsigned excl[kCmpItems], run = 0;
+        const unsigned lt = lanemask_lt();
+#pragma unroll
+        for (int q = 0; q < kCmpItems; ++q) {
+#pragma unroll
+            for (int w = 0; w < NW; ++w) {
+                const unsigned c = s_cnt[q * NW + w];
+                if (w == cw) excl[q] = run + __popc(bal[q] & lt);
+                run += c;
+            }
+        }
+        const unsigned total = run;
+        const long long dst0 = start - (long long)ws.sub_off[u];
+        mbar_wait(&s_ready[s], (uint32_t)((it / kTmaStages) & 1));   // predecessors have read their input
+        // survivors back into the stage at the destination's 16-byte phase; ragged ends direct
         const long long end = dst0 + total;
         const long long a4 = (dst0 + 3) & ~3LL, e4 = end & ~3LL;
         const long long a8 = (dst0 + 1) & ~1LL, e8 = end & ~1LL;
         const long long base4 = dst0 & ~3LL, base8 = dst0 & ~1LL;
         const bool mid4 = e4 > a4, mid8 = e8 > a8;
 #pragma unroll
-        for (int it = 0; it < kCmpItems; ++it) {
-            if (!alive[it]) continue;
-            const int e = it * kThreads + threadIdx.x;
-            const long long o = dst0 + excl[it];
+        for (int q = 0; q < kCmpItems; ++q) {
+            if (!alive[q]) continue;
+            const long long o = dst0 + excl[q];
             const int s4 = (int)(o - base4), s8 = (int)(o - base8);
             const bool dir4 = !mid4 || o < a4 || o >= e4, dir8 = !mid8 || o < a8 || o >= e8;
-            for (int c = 0; c < ncf; ++c) {
-                const float v = S.c[scol[c]][e];
-                if (dir4) gcol[c][o] = v;
-                else O.c[scol[c]][s4] = v;
+#pragma unroll
+            for (int c = 0; c < 6; ++c) {
+                if (c >= ncf) break;
+                if (dir4) gcol[c][o] = v[q][c];
+                else S.c[scol[c]][s4] = v[q][c];
             }
-            const int lv = S.lab[e];
-            if (dir4) p.label[o] = lv;
-            else O.lab[s4] = lv;
+            if (dir4) p.label[o] = lb[q];
+            else S.lab[s4] = lb[q];
             if (carry) {
-                const int kv = S.key[e];
-                if (dir4) ws.key[o] = kv;
-                else O.key[s4] = kv;
+                if (dir4) ws.key[o] = kv[q];
+                else S.key[s4] = kv[q];
             }
-            const long long iv = S.id[e];
-            if (dir8) p.id[o] = iv;
-            else O.id[s8] = iv;
+            if (dir8) p.id[o] = idv[q];
+            else S.id[s8] = idv[q];
         }
         fence_async_smem();
-        __syncthreads();
-        if (threadIdx.x == 0) {
+        named_bar(1, kThreads);
+        if (ct == 0) {
             if (mid4) {
-                const int s = (int)(a4 - base4);
+                const int o4 = (int)(a4 - base4);
                 const uint32_t bytes = (uint32_t)(e4 - a4) * 4u;
-                for (int c = 0; c < ncf; ++c) bulk_s2g(gcol[c] + a4, O.c[scol[c]] + s, bytes);
-                bulk_s2g(p.label + a4, O.lab + s, bytes);
-                if (carry) bulk_s2g(ws.key + a4, O.key + s, bytes);
+                for (int c = 0; c < ncf; ++c) bulk_s2g(gcol[c] + a4, S.c[scol[c]] + o4, bytes);
+                bulk_s2g(p.label + a4, S.lab + o4, bytes);
+                if (carry) bulk_s2g(ws.key + a4, S.key + o4, bytes);
             }
-            if (mid8) bulk_s2g(p.id + a8, O.id + (int)(a8 - base8), (uint32_t)(e8 - a8) * 8u);
+            if (mid8) bulk_s2g(p.id + a8, S.id + (int)(a8 - base8), (uint32_t)(e8 - a8) * 8u);
             bulk_commit();
+            // the previous stage's store has read its data: back to the producer
+            if (prev >= 0) {
+                bulk_wait_read_but_one();
+                mbar_arrive(&s_empty[prev]);
+            }
         }
-        if (!more) break;
-        u = u2;
-        b ^= 1;
+        prev = s;
     }
-    if (threadIdx.x == 0) bulk_wait_all();
+    if (ct == 0) {
+        if (prev >= 0) {
+            bulk_wait_read_all();
+            mbar_arrive(&s_empty[prev]);
+        }
+        bulk_wait_all();
+    }
 }
 
 // Staged particles after the survivors with IDs from the count matrix (reading
@@ -796,7 +875,7 @@ cudaError_t launch_compact(const PartDev &p, const GridDev &g, const PortTable &
                 cudaFuncSetAttribute(k_compact_move_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem);
                 attr = true;
             }
-            launch_k(k_compact_move_tma, dim3(cap_grid(sm_count_cached(), p.cap, kCmpTile)), dim3(kThreads),
+            launch_k(k_compact_move_tma, dim3(cap_grid(sm_count_cached(), p.cap, kCmpTile)), dim3(kTmaThreads),
                      kTmaSmem, s, p, dim, ws, carry);
         } else if (one) {
             if (!grid) grid = occ_grid(k_compact_move<false>, kThreads);
