@@ -171,3 +171,18 @@ def test_comm_host_checks_without_gpu():
     assert L.sph_allgather_counts(ctx.h, None, None, None) == -1
     a, b = sphbuf.sph_comm_unique_id(), sphbuf.sph_comm_unique_id()
     assert len(a) == len(b) == 128 and a != b
+
+
+def test_no_contracted_fma_in_the_library():
+    """The pinned arithmetic is never contracted to FMA: in the
+    sm_100a SASS every FFMA/DFMA belongs to an IEEE-754 division sequence
+    (div.rn: MUFU.RCP + Newton-Raphson, or its slow-path subroutine)."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sphbuf.lib()
+    r = subprocess.run([sys.executable, os.path.join(root, "tools", "sass_summary.py"), "test"], capture_output=True,
+                       text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "whole library: **0**" in r.stdout
+    os.remove(os.path.join(root, "profiles", "test_sass.md"))
