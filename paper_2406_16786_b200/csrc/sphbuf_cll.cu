@@ -17,6 +17,8 @@
 #include <cstdlib>
 #include <cstring>
 
+#include <cooperative_groups.h>
+
 #include "sphbuf_common.cuh"
 #include "sphbuf_prologue.cuh"
 
@@ -365,6 +367,185 @@ __global__ void __launch_bounds__(kThreads) k_cell_scan(GridDev g, Workspace ws,
         }
     }
     SCAN_TRACE(3);
+}
+
+// K2 for small grids (at most kClusterScanCells cells, C1-C3): one thread-block
+// cluster scans the whole histogram.  CTA r of the cluster takes a fixed range of
+// 32 warps x V rows x 128 cells in the warp-striped layout of k_cell_scan (row v
+// of a warp's segment is int4 #(32 v + lane): every load / store instruction of a
+// warp covers 512 contiguous bytes; all V rows of a pass are loaded before they
+// are summed); the CTA totals are exchanged through distributed shared memory
+// (each CTA reads the totals of the CTAs before it) — two cluster barriers
+// instead of a look-back chain over tens of tiles, the latency that dominated K2
+// at C2 / C3 in round 1 (~19 us).
+constexpr int kClusterScanThreads = 1024;
+constexpr int kClusterScanMaxV = 16;
+constexpr long long kClusterScanCells = 16LL * kClusterScanThreads * 4 * kClusterScanMaxV;   // 1M (16 CTAs)
+
+template <int V>
+__global__ void __launch_bounds__(kClusterScanThreads) k_cell_scan_cluster(GridDev g, Workspace ws, int *cell_start,
+                                                                           int *cell_end, long long *n_out,
+                                                                           const long long *n_src)
+{
+    pdl_entry();
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    constexpr int NW = kClusterScanThreads / 32;
+    constexpr int WCELLS = 32 * 4 * V;
+    __shared__ unsigned s_warp[NW + 1];
+    __shared__ unsigned s_total;
+    Counters *ctr = ws.ctr;
+    const int r = (int)cl.block_rank(), R = (int)cl.num_blocks();
+    const long long nc = g.ncells;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const long long wbase = ((long long)r * NW + warp) * WCELLS;
+    const bool full = wbase + WCELLS <= nc;
+    if (n_src && r == 0 && threadIdx.x == 0) {
+        ctr->n_in = *n_src;
+        ctr->mig_base = *n_src;
+    }
+    const int4 *pc = reinterpret_cast<const int4 *>(ws.cell_count + wbase) + lane;
+    auto row = [&](int v) -> int4 {
+        if (full) return __ldcg(pc + 32 * v);
+        int t[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const long long j = wbase + 4 * (32 * v + lane) + q;
+            t[q] = j < nc ? __ldcg(ws.cell_count + j) : 0;
+        }
+        return make_int4(t[0], t[1], t[2], t[3]);
+    };
+    unsigned tsum = 0;
+    {
+        int4 c[V];
+#pragma unroll
+        for (int v = 0; v < V; ++v) c[v] = row(v);
+#pragma unroll
+        for (int v = 0; v < V; ++v) tsum += (unsigned)(c[v].x + c[v].y + c[v].z + c[v].w);
+    }
+    const unsigned wtot = warp_sum(tsum);
+    unsigned total;
+    const unsigned wexcl = block_excl_scan<kClusterScanThreads>(lane == 0 ? wtot : 0u, total, s_warp);
+    const unsigned woff = __shfl_sync(0xffffffffu, wexcl, 0);
+    if (threadIdx.x == 0) s_total = total;
+    cl.sync();
+    unsigned pre = 0;
+    for (int q = 0; q < r; ++q) pre += *cl.map_shared_rank(&s_total, q);
+    unsigned run = pre + woff;                       // first slot of this warp's current row
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+        const int4 c = row(v);
+        const unsigned sv = (unsigned)(c.x + c.y + c.z + c.w);
+        unsigned inc = sv;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+        }
+        int rr = (int)(run + inc - sv);
+        run += __shfl_sync(0xffffffffu, inc, 31);
+        int4 st, en;
+        st.x = rr; rr += c.x; en.x = rr;
+        st.y = rr; rr += c.y; en.y = rr;
+        st.z = rr; rr += c.z; en.z = rr;
+        st.w = rr; rr += c.w; en.w = rr;
+        if (full) {
+            const long long q4 = (wbase >> 2) + 32 * v + lane;
+            reinterpret_cast<int4 *>(cell_start)[q4] = st;
+            reinterpret_cast<int4 *>(cell_end)[q4] = en;
+            reinterpret_cast<int4 *>(ws.cell_count)[q4] = make_int4(0, 0, 0, 0);
+            reinterpret_cast<int4 *>(ws.cursor)[q4] = make_int4(0, 0, 0, 0);
+        } else {
+            const int s4[4] = {st.x, st.y, st.z, st.w}, e4[4] = {en.x, en.y, en.z, en.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const long long j = wbase + 4 * (32 * v + lane) + q;
+                if (j < nc) {
+                    cell_start[j] = s4[q];
+                    cell_end[j] = e4[q];
+                    ws.cell_count[j] = 0;
+                    ws.cursor[j] = 0;
+                }
+            }
+        }
+    }
+    if (r == R - 1 && threadIdx.x == 0) {
+        *n_out = (long long)(pre + total);
+        ctr->n_leave = 0;   // the leaver list of the next build starts here
+    }
+    cl.sync();              // no CTA leaves while another still reads its total
+}
+
+template <int V>
+static cudaError_t cluster_scan_launch(int csize, const GridDev &g, const Workspace &ws, int *cs, int *ce,
+                                       long long *n_out, const long long *n_src, cudaStream_t s)
+{
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_cell_scan_cluster<V>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        cudaGetLastError();
+        attr = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(csize);
+    cfg.blockDim = dim3(kClusterScanThreads);
+    cfg.stream = s;
+    cudaLaunchAttribute a[2];
+    a[0].id = cudaLaunchAttributeClusterDimension;
+    a[0].val.clusterDim.x = csize;
+    a[0].val.clusterDim.y = 1;
+    a[0].val.clusterDim.z = 1;
+    a[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    a[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = a;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
+    return cudaLaunchKernelEx(&cfg, k_cell_scan_cluster<V>, g, ws, cs, ce, n_out, n_src);
+}
+
+// Cluster size of the small-grid scan: 16 CTAs where the device allows it
+// (non-portable size), else the portable 8; 0 = off (SPHBUF_CLUSTER_SCAN=0).
+static int cluster_scan_size()
+{
+    static int size = -1;
+    if (size >= 0) return size;
+    const char *e = getenv("SPHBUF_CLUSTER_SCAN");
+    if (e && e[0] == '0') return size = 0;
+    size = 8;
+    if (cudaFuncSetAttribute(k_cell_scan_cluster<kClusterScanMaxV>, cudaFuncAttributeNonPortableClusterSizeAllowed,
+                             1) == cudaSuccess) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(16);
+        cfg.blockDim = dim3(kClusterScanThreads);
+        cudaLaunchAttribute a[1];
+        a[0].id = cudaLaunchAttributeClusterDimension;
+        a[0].val.clusterDim.x = 16;
+        a[0].val.clusterDim.y = 1;
+        a[0].val.clusterDim.z = 1;
+        cfg.attrs = a;
+        cfg.numAttrs = 1;
+        int n = 0;
+        if (cudaOccupancyMaxActiveClusters(&n, k_cell_scan_cluster<kClusterScanMaxV>, &cfg) == cudaSuccess && n >= 1)
+            size = 16;
+    }
+    cudaGetLastError();
+    return size;
+}
+
+// Launch the cluster scan if the grid is small enough; false: use the look-back scan.
+static bool launch_cluster_scan(const GridDev &g, const Workspace &ws, int *cs, int *ce, long long *n_out,
+                                const long long *n_src, cudaStream_t s)
+{
+    const int csize = cluster_scan_size();
+    if (csize == 0) return false;
+    const long long per_v = (long long)csize * kClusterScanThreads * 4;   // cells per row across the cluster
+    const long long v = (g.ncells + per_v - 1) / per_v;
+    if (v > kClusterScanMaxV) return false;
+    if (v <= 1) cluster_scan_launch<1>(csize, g, ws, cs, ce, n_out, n_src, s);
+    else if (v <= 2) cluster_scan_launch<2>(csize, g, ws, cs, ce, n_out, n_src, s);
+    else if (v <= 4) cluster_scan_launch<4>(csize, g, ws, cs, ce, n_out, n_src, s);
+    else if (v <= 8) cluster_scan_launch<8>(csize, g, ws, cs, ce, n_out, n_src, s);
+    else cluster_scan_launch<16>(csize, g, ws, cs, ce, n_out, n_src, s);
+    return true;
 }
 
 #ifdef SPHBUF_TRACE
@@ -774,7 +955,9 @@ cudaError_t launch_cll_finish(const PartDev &in, const PartDev &out, const GridD
     }
     L->before(s);
     const bool no_key_pass = cc.use && !cc.mig;
-    if (big)
+    if (launch_cluster_scan(g, ws, cell_start, cell_end, out.n,
+                            no_key_pass ? (const long long *)in.n : (const long long *)nullptr, s)) {
+    } else if (big)
         launch_k(k_cell_scan<kCellItemsBig>, dim3((unsigned)ntiles), dim3(kThreads), 0, s, g, ws, cell_start,
                  cell_end, out.n, ntiles, no_key_pass ? (const long long *)in.n : (const long long *)nullptr);
     else
