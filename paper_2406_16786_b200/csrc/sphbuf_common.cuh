@@ -291,23 +291,28 @@ __device__ __forceinline__ bool in_box(const float X[3], const float he[3], int 
 // Pinned advection (the driver step): x <- fl(x + fl(v dt)).
 __device__ __forceinline__ float advect1(float x, float v, float dt) { return __fadd_rn(x, __fmul_rn(v, dt)); }
 
-// Pinned cell index along one axis: floor(fl(fl(x - lo) * inv_cs)), clamped
-// (branch-free: min/max of the floored value; oob is set when clamping changed it).
+// Pinned cell index along one axis: floor(fl(fl(x - lo) * inv_cs)), clamped to
+// [lo_c, hi_c) (branch-free integer min/max of the floored value, which the
+// float -> int conversion saturates outside the int range; oob is set when the
+// clamp changed it).
 __device__ __forceinline__ int cell_axis(float x, float lo, float inv, int lo_c, int hi_c, int &oob)
 {
     const float t = __fmul_rn(__fsub_rn(x, lo), inv);
-    const float f = floorf(t);
-    const float c = fminf(fmaxf(f, (float)lo_c), (float)(hi_c - 1));
+    const int f = __float2int_rz(floorf(t));
+    const int c = min(max(f, lo_c), hi_c - 1);
     oob |= (c != f);
-    return (int)c;
+    return c;
 }
 
+// DIM: 2 or 3 when known at compile time, 0 to read g.dim.
+template <int DIM = 0>
 __device__ __forceinline__ int cell_of(const GridDev &g, float x, float y, float z, int &oob)
 {
     const int cx = cell_axis(x, g.lo[0], g.inv_cs, g.cx_begin, g.cx_end, oob);
     const int cy = cell_axis(y, g.lo[1], g.inv_cs, 0, g.ncell[1], oob);
     int cz = 0;
-    if (g.dim == 3) cz = cell_axis(z, g.lo[2], g.inv_cs, 0, g.ncell[2], oob);
+    if (DIM == 3 || (DIM == 0 && g.dim == 3)) cz = cell_axis(z, g.lo[2], g.inv_cs, 0, g.ncell[2], oob);
+    if (DIM == 2) return (cx - g.cx_begin) * g.ny + cy;
     return ((cx - g.cx_begin) * g.ny + cy) * g.nz + cz;
 }
 
@@ -318,16 +323,18 @@ __device__ __forceinline__ int cell_of(const GridDev &g, float x, float y, float
 constexpr int kLeaver = -2;
 constexpr int kPacked = -3;
 
+template <int DIM = 0>
 __device__ __forceinline__ int carry_key(const GridDev &g, float x, float y, float z, float vx, float vy, float vz,
                                          float cdt, int carry, int &oob)
 {
-    const float xa = advect1(x, vx, cdt), ya = advect1(y, vy, cdt), za = g.dim == 3 ? advect1(z, vz, cdt) : 0.0f;
+    const bool d3 = DIM == 3 || (DIM == 0 && g.dim == 3);
+    const float xa = advect1(x, vx, cdt), ya = advect1(y, vy, cdt), za = d3 ? advect1(z, vz, cdt) : 0.0f;
     if (carry == 2) {
         int o2 = 0;
         const int cxr = cell_axis(xa, g.lo[0], g.inv_cs, 0, g.ncell[0], o2);
         if (cxr < g.cx_begin || cxr >= g.cx_end) return kLeaver;
     }
-    return cell_of(g, xa, ya, za, oob);
+    return cell_of<DIM>(g, xa, ya, za, oob);
 }
 
 __device__ __forceinline__ void leaver_append(const Workspace &ws, long long i)
