@@ -689,35 +689,37 @@ __global__ void __launch_bounds__(NT, MINB) k_cll_gather(PartDev in, PartDev out
     static_assert(2 * kHalo <= NT, "one halo slot per thread");
     __shared__ long long s_id[kHalo + T + kHalo];
     __shared__ __align__(16) unsigned s_lo[kHalo + T + kHalo];
-    const long long n = *out.n;
+    // slot indices are int32 (capacity < 2^31, checked by sph_ctx_create): 32-bit
+    // index arithmetic throughout
+    const int n = (int)*out.n;
     const int dim = DIM ? DIM : g.dim;
     const int carry = CARRY >= 0 ? CARRY : carry_rt;
     const bool has_perm = PERM >= 0 ? PERM == 1 : perm != nullptr;
     // sources below mig_base are this slab's own particles (advected here when the
     // build fused the advection); received migrants were advected by their sender
-    const long long adv_lim = advect ? ws.ctr->mig_base : 0;
-    const long long stride = (long long)gridDim.x * T;
+    const int adv_lim = advect ? (int)ws.ctr->mig_base : 0;
+    const int stride = (int)gridDim.x * T;
     int oob_next = 0;
     // PF: the slot -> source map of the next tile is loaded while this tile's
     // columns are in flight (one dependent DRAM round trip less per tile)
     int nsrc[ITEMS], nhsrc = 0;
-    auto load_map = [&](long long jb, int (&sv)[ITEMS], int &hs) {
+    auto load_map = [&](int jb, int (&sv)[ITEMS], int &hs) {
 #pragma unroll
         for (int it = 0; it < ITEMS; ++it) {
-            const long long j = jb + it * NT + threadIdx.x;
+            const int j = jb + it * NT + (int)threadIdx.x;
             sv[it] = j < n ? ws.src[j] : -1;
         }
-        const long long jh = threadIdx.x < kHalo ? jb - kHalo + threadIdx.x : jb + T + (threadIdx.x - kHalo);
+        const int jh = threadIdx.x < kHalo ? jb - kHalo + (int)threadIdx.x : jb + T + ((int)threadIdx.x - kHalo);
         hs = (threadIdx.x < 2 * kHalo && jh >= 0 && jh < n) ? ws.src[jh] : -1;
     };
-    if (PF) load_map((long long)blockIdx.x * T, nsrc, nhsrc);
-    auto tile = [&](long long j0, auto full_tag) {
+    if (PF) load_map((int)blockIdx.x * T, nsrc, nhsrc);
+    auto tile = [&](int j0, auto full_tag) {
         constexpr bool Full = decltype(full_tag)::value;      // every slot of the tile is below n
         int src[ITEMS], cb[ITEMS], ce[ITEMS], lab[ITEMS];
         float x[ITEMS], y[ITEMS], z[ITEMS], vx[ITEMS], vy[ITEMS], vz[ITEMS];
         long long id[ITEMS];
         // halo ids (threads 0 .. 2 kHalo - 1): two dependent loads, issued first
-        const long long jh = threadIdx.x < kHalo ? j0 - kHalo + threadIdx.x : j0 + T + (threadIdx.x - kHalo);
+        const int jh = threadIdx.x < kHalo ? j0 - kHalo + (int)threadIdx.x : j0 + T + ((int)threadIdx.x - kHalo);
         const bool hv = threadIdx.x < 2 * kHalo && jh >= 0 && jh < n;
         int hsrc;
         if (PF) {
@@ -728,7 +730,7 @@ __global__ void __launch_bounds__(NT, MINB) k_cll_gather(PartDev in, PartDev out
             hsrc = hv ? ws.src[jh] : 0;
 #pragma unroll
             for (int it = 0; it < ITEMS; ++it) {
-                const long long j = j0 + it * NT + threadIdx.x;
+                const int j = j0 + it * NT + (int)threadIdx.x;
                 src[it] = (Full || j < n) ? ws.src[j] : -1;
             }
         }
@@ -749,7 +751,7 @@ __global__ void __launch_bounds__(NT, MINB) k_cll_gather(PartDev in, PartDev out
             id[it] = in.id[s];
             lab[it] = in.label[s];
         }
-        if (PF) load_map(j0 + stride, nsrc, nhsrc);
+        if (PF && j0 < n - stride) load_map(j0 + stride, nsrc, nhsrc);   // (no int overflow past n)
         bool wide = hv && (hid >> 32) != 0;
         if (threadIdx.x < 2 * kHalo) {
             const int hq = threadIdx.x < kHalo ? threadIdx.x : T + threadIdx.x;
@@ -775,9 +777,9 @@ __global__ void __launch_bounds__(NT, MINB) k_cll_gather(PartDev in, PartDev out
         // 32-bit compares when no id of the window needs its high word
         const bool narrow = !__syncthreads_or(wide);
         // slot indices fit in int32 (cell tables are int32); staged window [w0, w1)
-        const int t0 = (int)j0;
+        const int t0 = j0;
         const int w0 = t0 - kHalo > 0 ? t0 - kHalo : 0;
-        const int w1 = (long long)t0 + T + kHalo < n ? t0 + T + kHalo : (int)n;
+        const int w1 = t0 + T + kHalo < n ? t0 + T + kHalo : n;
         const long long *sid = s_id + (w0 - (t0 - kHalo));
         const unsigned *slo = s_lo + (w0 - (t0 - kHalo));
         int kn[ITEMS];
@@ -818,7 +820,7 @@ __global__ void __launch_bounds__(NT, MINB) k_cll_gather(PartDev in, PartDev out
         }
         __syncthreads();
     };
-    for (long long j0 = (long long)blockIdx.x * T; j0 < n; j0 += stride) tile(j0, std::false_type{});
+    for (int j0 = (int)blockIdx.x * T; j0 < n; j0 = j0 < n - stride ? j0 + stride : n) tile(j0, std::false_type{});
     if (carry) {
         const unsigned o = warp_sum((unsigned)oob_next);
         if ((threadIdx.x & 31) == 0 && o) atomicAdd((unsigned long long *)&ws.ctr->out_of_grid, (unsigned long long)o);
@@ -873,6 +875,21 @@ static void gather_variant(const char *v, const PartDev &in, const PartDev &out,
     // 128- / 512-thread blocks and cp.async / warp-chunk designs;
     // the 3-D, carried-key, no-perm build (the bench's) compiled for its case
     if (!HasExtra && g.dim == 3 && !perm && carry == 1 && !getenv("SPHBUF_GATHER_GENERIC")) {
+        static const char *sv = getenv("SPHBUF_GATHER_SPEC");
+        const char *v = sv ? sv : "";
+#define SPH_GS(name, I, M)                                                                                       \
+    if (!strcmp(v, name)) {                                                                                      \
+        static int grid = 0;                                                                                     \
+        if (!grid) grid = occ_grid(k_cll_gather<false, I, M, kThreads, true, 3, 1, 0>, kThreads);                \
+        launch_k(k_cll_gather<false, I, M, kThreads, true, 3, 1, 0>, dim3(cap_grid(grid, cap, kThreads * I)),    \
+                 dim3(kThreads), 0, s, in, out, g, ws, cs, ce, perm, advect, dt, carry, cdt);                     \
+        return;                                                                                                  \
+    }
+        SPH_GS("2:6", 2, 6)
+        SPH_GS("2:4", 2, 4)
+        SPH_GS("3:4", 3, 4)
+        SPH_GS("3:3", 3, 3)
+#undef SPH_GS
         static int grid = 0;
         if (!grid) grid = occ_grid(k_cll_gather<false, 2, 5, kThreads, true, 3, 1, 0>, kThreads);
         launch_k(k_cll_gather<false, 2, 5, kThreads, true, 3, 1, 0>, dim3(cap_grid(grid, cap, kThreads * 2)),
