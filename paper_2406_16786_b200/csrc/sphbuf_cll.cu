@@ -646,17 +646,25 @@ __device__ __forceinline__ int rank_in_cell(const PartDev &in, const Workspace &
             const unsigned *sc = slo - w0;
             const unsigned m32 = (unsigned)me;
             const int q0 = cb & ~1, q1 = (ce + 1) & ~1;
-            unsigned ge = 0;
+            if (q1 == q0) return 0;
+            // the padding slots (cb - 1 when cb is odd, ce when ce is odd) are
+            // replaced by ~0 in the first / last pair, so they count as >= me
+            uint2 f = *reinterpret_cast<const uint2 *>(sc + q0);
+            if (cb & 1) f.x = 0xffffffffu;
+            if (q1 - q0 == 2 && (ce & 1)) f.y = 0xffffffffu;
+            unsigned ge = add_ge(add_ge(0u, f.x, m32), f.y, m32);
+            if (q1 - q0 > 2) {
 #pragma unroll 2
-            for (int q = q0; q < q1; q += 2) {
-                const uint2 v = *reinterpret_cast<const uint2 *>(sc + q);
-                ge = add_ge(ge, v.x, m32);
-                ge = add_ge(ge, v.y, m32);
+                for (int q = q0 + 2; q < q1 - 2; q += 2) {
+                    const uint2 v = *reinterpret_cast<const uint2 *>(sc + q);
+                    ge = add_ge(ge, v.x, m32);
+                    ge = add_ge(ge, v.y, m32);
+                }
+                uint2 l = *reinterpret_cast<const uint2 *>(sc + q1 - 2);
+                if (ce & 1) l.y = 0xffffffffu;
+                ge = add_ge(add_ge(ge, l.x, m32), l.y, m32);
             }
-            r = (q1 - q0) - (int)ge;
-            if (cb & 1) r -= (sc[cb - 1] < m32);
-            if (ce & 1) r -= (sc[ce] < m32);
-            return r;
+            return (q1 - q0) - (int)ge;
         }
         const long long *sc = sid - w0;
 #pragma unroll 4
