@@ -470,6 +470,7 @@ __global__ void __launch_bounds__(kClusterScanThreads) k_cell_scan_cluster(GridD
             }
         }
     }
+    SPH_CHECK(run <= pre + total);
     if (r == R - 1 && threadIdx.x == 0) {
         *n_out = (long long)(pre + total);
         ctr->n_leave = 0;   // the leaver list of the next build starts here

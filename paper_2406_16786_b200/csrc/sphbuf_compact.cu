@@ -684,6 +684,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_compact_move_tma(PartDev p, 
         for (int q = 0; q < kCmpItems; ++q) {
             if (!alive[q]) continue;
             const long long o = dst0 + excl[q];
+            SPH_CHECK(o >= ibeg - (long long)D && o < start + kCmpTile && o < p.cap);
 #pragma unroll
             for (int c = 0; c < 6; ++c) {
                 if (c >= ncf) break;

@@ -1,8 +1,10 @@
 """Small driver for compute-sanitizer runs (memcheck / racecheck / synccheck /
 initcheck, one tool per invocation): a few updates of C1e, C2 and a small 3-D
-junction through the C ABI, in both compaction modes, plus the moving-port and
-port-driver lock-step tests on a few updates, each checked bit-exactly against
-the oracle.
+junction through the C ABI, in both compaction modes, plus the moving-port,
+port-driver and loopback-slab lock-step tests on a few updates, each checked
+bit-exactly against the oracle.  compute-sanitizer is closed on the GPU pool, so
+tests/test_debug_build.py runs this under the bounds-asserting debug build
+(SPHBUF_DEBUG=1) instead.
 
     compute-sanitizer --tool memcheck python tests/sanitize_run.py
 """
@@ -28,6 +30,8 @@ def main():
     test_sprinkler_gpu_parity(n_steps=12)          # moving ports (K9, K10)
     test_rotating_port_3d_gpu_parity(n_steps=4)
     test_drivers_gpu_parity(n_updates=4)           # port drivers (K11)
+    from test_dist import test_loopback_slabs_match_oracle
+    test_loopback_slabs_match_oracle(2, True)      # loopback communicator, migration, carried keys
     print("sanitize_run: all lock-step checks passed")
 
 
