@@ -680,12 +680,13 @@ def c4(device="cpu", n_updates=100, scale=1.0, nports=8) -> Workload:
 
 C5_SLAB_LEN = 1.6
 C5_CELLS_PER_SLAB = 307
-# empty cells around the C5 box on every side: particles leave it at most
-# 1.2 m/s x 0.0005 s = 0.115 cells per update, so 12 cells cover ~100 updates
-# (the bench runs ~80 per invocation at its driver settings) before any reaches
-# the clamped boundary cells
-C5_PAD_X = 12
-C5_PAD_YZ = 12
+# empty cells around the C5 box: particles leave it at most 1.2 m/s x 0.0005 s =
+# 0.115 cells per update, so 10 cells cover ~87 updates (the bench runs ~80 per
+# invocation at its driver settings) before any reaches the clamped boundary
+# cells; along x the last slab's ports may straddle its outer face (x has no
+# margin at slab faces), so x keeps room for a whole port (34 cells = 0.18 m)
+C5_PAD_X = 34
+C5_PAD_YZ = 10
 C5_NEXT_ID = 1 << 40
 
 
@@ -719,6 +720,22 @@ def c5_ports(nslabs: int, scale=1.0, n_updates=50):
     return per_slab
 
 
+def c5_grid(nslabs: int, scale=1.0):
+    """The global C5 grid of an nslabs-slab problem (x-major cells, 307 per slab at
+    scale 1, empty padding around the box) and each slab's [cx_begin, cx_end)."""
+    dp, h, cs, L, W, counts, cells_per_slab = c5_geometry(scale)
+    pad_x, pad_yz = C5_PAD_X, C5_PAD_YZ
+    lo = (f32(-pad_x * cs), f32(-pad_yz * cs), f32(-pad_yz * cs))
+    nyz = int(math.ceil(W / cs)) + 2 * pad_yz
+    ncell = (cells_per_slab * nslabs + 2 * pad_x, nyz, nyz)
+    slabs = []
+    for r in range(nslabs):
+        b = 0 if r == 0 else pad_x + cells_per_slab * r
+        e = ncell[0] if r == nslabs - 1 else pad_x + cells_per_slab * (r + 1)
+        slabs.append((b, e))
+    return Grid(3, lo, cs, ncell), slabs
+
+
 def c5(device="cpu", slab=0, nslabs=1, scale=1.0, n_updates=50) -> Workload:
     """3-D weak-scaling junction: slab r = [1.6r, 1.6(r+1)) x [0,0.8]^2 at dp=0.002
     (800x400x400 = 128M lattice sites per slab at scale 1).  Returns slab ``slab``
@@ -746,15 +763,8 @@ def c5(device="cpu", slab=0, nslabs=1, scale=1.0, n_updates=50) -> Workload:
     # screened against the ports of slabs r-1..r+1 whatever nslabs is, so slab r's
     # content does not depend on the number of GPUs
     xyz, v, nre = _screen(base, xyz, vel, ids, shaping, dim, dp, cs, f32(dt), n_updates, SEED_BASE + 5 + 1000 * slab)
-    pad_x, pad_yz = C5_PAD_X, C5_PAD_YZ
-    lo = (f32(-pad_x * cs), f32(-pad_yz * cs), f32(-pad_yz * cs))
-    nyz = int(math.ceil(W / cs)) + 2 * pad_yz
-    ncell = (cells_per_slab * nslabs + 2 * pad_x, nyz, nyz)
-    slabs = []
-    for r in range(nslabs):
-        b = 0 if r == 0 else pad_x + cells_per_slab * r
-        e = ncell[0] if r == nslabs - 1 else pad_x + cells_per_slab * (r + 1)
-        slabs.append((b, e))
+    g0, slabs = c5_grid(nslabs, scale)
+    lo, ncell = g0.lo, g0.ncell
     grid = Grid(dim, lo, cs, ncell, slabs[slab][0], slabs[slab][1])
     name = "C5" if scale == 1.0 else f"C5x{scale:g}"
     return Workload(name, dim, dp, h, grid, ports, _pack_state(xyz, v, ids, dim), f32(dt), n_updates, C5_NEXT_ID,

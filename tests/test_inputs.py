@@ -111,3 +111,16 @@ def test_lineage_maps_duplicates_to_their_original():
         assert o < w.next_id
         assert st["label"][st["id"] == o][0] == 0          # the source is an inlet buffer particle
     assert lin.original(3) == 3
+
+
+def test_c5_ports_fit_the_grid_at_every_gpu_count():
+    """Every C5 port's decision region P_k lies strictly inside the grid for 1, 2, 4
+    and 8 slabs at full scale (the registration check, sph_port_check), so the
+    grid's padding leaves room for the ports that straddle the outer slab face."""
+    from paper_2406_16786_b200 import sphbuf
+    dp = inputs.c5_geometry()[0]
+    for P in (1, 2, 4, 8):
+        g, slabs = inputs.c5_grid(P)
+        ctx = sphbuf.Context(g, 1.3 * dp, 1024, 64, 16)
+        for p in [q for r in inputs.c5_ports(P)[:P] for q in r]:
+            assert sphbuf.sph_port_check(ctx, p.origin, p.Q, p.half_extents, p.kind, p.layers, dp) == 0, (P, p)
