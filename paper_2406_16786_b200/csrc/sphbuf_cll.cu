@@ -623,21 +623,6 @@ __global__ void __launch_bounds__(NT) k_cll_scatter(Workspace ws, const int *cel
 
 constexpr int kHalo = 64;   // slots staged on either side of a gather tile
 
-// A global load the compiler cannot merge with an earlier one of the same
-// address (cached in L1): re-reading a value instead of keeping it in a register.
-__device__ __forceinline__ float ld_ca(const float *p)
-{
-    float v;
-    asm volatile("ld.global.ca.f32 %0, [%1];" : "=f"(v) : "l"(p));
-    return v;
-}
-__device__ __forceinline__ int ld_ca(const int *p)
-{
-    int v;
-    asm volatile("ld.global.ca.s32 %0, [%1];" : "=r"(v) : "l"(p));
-    return v;
-}
-
 // acc + [a >= m] (unsigned): the carry of a - m, two instructions per element.
 __device__ __forceinline__ unsigned add_ge(unsigned acc, unsigned a, unsigned m)
 {
@@ -703,7 +688,7 @@ __device__ __forceinline__ int rank_in_cell(const PartDev &in, const Workspace &
 // nullptr) for the default variant (0 / -1 / -1: read at run time); a tile whose
 // slots are all below n runs a body with no per-slot validity checks.
 template <bool HasExtra, int ITEMS, int MINB, int NT = kThreads, bool PF = false, int DIM = 0, int CARRY = -1,
-          int PERM = -1, bool RL = false>
+          int PERM = -1>
 __global__ void __launch_bounds__(NT, MINB) k_cll_gather(PartDev in, PartDev out, GridDev g, Workspace ws,
                                                                const int *cell_start, const int *cell_end, int *perm,
                                                                int advect, float dt, int carry_rt, float cdt)
@@ -739,7 +724,7 @@ __global__ void __launch_bounds__(NT, MINB) k_cll_gather(PartDev in, PartDev out
     if (PF) load_map((int)blockIdx.x * T, nsrc, nhsrc);
     auto tile = [&](int j0, auto full_tag) {
         constexpr bool Full = decltype(full_tag)::value;      // every slot of the tile is below n
-        int src[ITEMS], cb[ITEMS], ce[ITEMS], lab[ITEMS], kn_early[ITEMS];
+        int src[ITEMS], cb[ITEMS], ce[ITEMS], lab[ITEMS];
         float x[ITEMS], y[ITEMS], z[ITEMS], vx[ITEMS], vy[ITEMS], vz[ITEMS];
         long long id[ITEMS];
         // halo ids (threads 0 .. 2 kHalo - 1): two dependent loads, issued first
@@ -797,14 +782,6 @@ __global__ void __launch_bounds__(NT, MINB) k_cll_gather(PartDev in, PartDev out
             s_id[kHalo + it * NT + threadIdx.x] = id[it];
             s_lo[kHalo + it * NT + threadIdx.x] = (unsigned)id[it];
             wide |= (id[it] >> 32) != 0;
-            if (RL && carry) {
-                // RL: the next key now, so the velocities and the label need not
-                // stay in registers across the ranking (they are read again, from
-                // L1, for the stores)
-                int oobn = 0;
-                kn_early[it] = carry_key<DIM>(g, x[it], y[it], z[it], vx[it], vy[it], vz[it], cdt, carry, oobn);
-                oob_next += oobn;
-            }
         }
         // 32-bit compares when no id of the window needs its high word
         const bool narrow = !__syncthreads_or(wide);
@@ -825,23 +802,13 @@ __global__ void __launch_bounds__(NT, MINB) k_cll_gather(PartDev in, PartDev out
                 // key carry-over: the next build's key of the particle now at d (its
                 // position advected again by cdt), so that build needs no key pass;
                 // with slab migration a particle about to leave the slab is listed
-                if (RL) {
-                    kn[it] = kn_early[it];
-                } else {
-                    int oobn = 0;
-                    kn[it] = carry_key<DIM>(g, x[it], y[it], z[it], vx[it], vy[it], vz[it], cdt, carry, oobn);
-                    oob_next += oobn;
-                }
+                int oobn = 0;
+                kn[it] = carry_key<DIM>(g, x[it], y[it], z[it], vx[it], vy[it], vz[it], cdt, carry, oobn);
+                oob_next += oobn;
                 ws.key[d] = kn[it];
                 if (kn[it] == kLeaver) leaver_append(ws, d);
             }
             SPH_CHECK(d >= cb[it] && d < ce[it] && ce[it] <= n && src[it] < in.cap);
-            if (RL) {
-                vx[it] = ld_ca(in.vx + src[it]);
-                vy[it] = ld_ca(in.vy + src[it]);
-                if (dim == 3) vz[it] = ld_ca(in.vz + src[it]);
-                lab[it] = ld_ca(in.label + src[it]);
-            }
             out.x[d] = x[it];
             out.y[d] = y[it];
             out.vx[d] = vx[it];
@@ -932,17 +899,7 @@ static void gather_variant(const char *v, const PartDev &in, const PartDev &out,
         SPH_GS("3:4", 3, 4)
         SPH_GS("3:3", 3, 3)
 #undef SPH_GS
-#define SPH_GR(name, I, M)                                                                                       \
-    if (!strcmp(v, name)) {                                                                                      \
-        static int grid = 0;                                                                                     \
-        if (!grid) grid = occ_grid(k_cll_gather<false, I, M, kThreads, true, 3, 1, 0, true>, kThreads);          \
-        launch_k(k_cll_gather<false, I, M, kThreads, true, 3, 1, 0, true>, dim3(cap_grid(grid, cap, kThreads * I)), \
-                 dim3(kThreads), 0, s, in, out, g, ws, cs, ce, perm, advect, dt, carry, cdt);                     \
-        return;                                                                                                  \
-    }
-        SPH_GR("rl2:5", 2, 5)
-        SPH_GR("rl2:6", 2, 6)
-#undef SPH_GR
+
         static int grid = 0;
         if (!grid) grid = occ_grid(k_cll_gather<false, 2, 5, kThreads, true, 3, 1, 0>, kThreads);
         launch_k(k_cll_gather<false, 2, 5, kThreads, true, 3, 1, 0>, dim3(cap_grid(grid, cap, kThreads * 2)),
