@@ -454,7 +454,7 @@ def run_e2e(su, w, args, dev, world):
     steps = max(2, min(args.steps, args.e2e_steps))
     stream = torch.cuda.current_stream()
     up, down = torch.cuda.Stream(), torch.cuda.Stream()
-    chunks = 4                                          # per column: a short pipeline tail
+    chunks = int(os.environ.get("SPH_E2E_CHUNKS", "4"))    # per column: a short pipeline tail
     evs = {(c, k): torch.cuda.Event() for c in names for k in range(chunks)}
     checked0 = bu.stats()["checked_total"]
     h2d = d2h = 0
