@@ -245,9 +245,9 @@ def run_ours(args):
     max_new = max(65536, w.n // 200)
     max_mig = 0
     if world > 1:
-        # fixed-size messages (no host sync): 3x the particles that change cell column
-        # in one step on the busier rank, at least 4096
-        est = torch.tensor([float(expected_migrants(w.state, w.grid, w.dt))], device=dev)
+        # fixed-size messages (no host sync): 3x the expected steady-state migrants per
+        # face and step on the busiest rank, at least 4096
+        est = torch.tensor([float(expected_migrants(w.state, w.grid, w.dt, w.dp))], device=dev)
         dist.all_reduce(est, op=dist.ReduceOp.MAX)
         max_mig = max(4096, int(3 * float(est.item())))
     su = SlabUpdater(w, rank, world, cap, max_migrate=max_mig, max_new=max_new, device=dev,

@@ -23,6 +23,8 @@ host logic), phase by phase so no kernel waits on another.
 """
 from __future__ import annotations
 
+import math
+
 import torch
 
 from . import sphbuf
@@ -48,15 +50,24 @@ def broadcast_unique_id(rank: int, group=None) -> bytes:
     return obj[0]
 
 
-def expected_migrants(state, grid, dt: float) -> int:
-    """Particles of ``state`` whose cell x-index changes in one advection (an
-    estimate of the per-face migration traffic used to size the messages)."""
+def expected_migrants(state, grid, dt: float, dp: float) -> int:
+    """Expected particles per step that one migration sends across one interior
+    face of the slab [cx_begin, cx_end) of ``grid`` in steady flow: the outward
+    flux sum_i max(+-v_x, 0) dt / dp over the particles within one spacing dp of
+    the face (the larger of the two faces; 0 for a slab without interior faces).
+    Used to size the fixed migration messages (with headroom by the caller)."""
     x = state["x"].double()
-    x1 = x + dt * state["vx"].double()
-    inv = 1.0 / float(grid.cs)
-    c0 = torch.floor((x - grid.lo[0]) * inv)
-    c1 = torch.floor((x1 - grid.lo[0]) * inv)
-    return int((c0 != c1).sum())
+    vx = state["vx"].double()
+    best = 0.0
+    if grid.cx_begin > 0:
+        f = grid.lo[0] + grid.cx_begin * float(grid.cs)
+        near = (x >= f) & (x < f + dp)
+        best = max(best, float((torch.clamp(-vx[near], min=0.0) * (dt / dp)).sum()))
+    if grid.cx_end < grid.ncell[0]:
+        f = grid.lo[0] + grid.cx_end * float(grid.cs)
+        near = (x < f) & (x >= f - dp)
+        best = max(best, float((torch.clamp(vx[near], min=0.0) * (dt / dp)).sum()))
+    return int(math.ceil(best))
 
 
 class SlabUpdater:

@@ -312,7 +312,7 @@ def test_loopback_c5_multislab_both_compaction_modes(P):
         oracle.register(st, whole.grid, p, k)
     groups = {}
     # one message size for every rank (sender and receiver must agree)
-    mm = max(4096, 3 * max(expected_migrants(w.state, w.grid, w.dt) for w in slabs))
+    mm = max(4096, 3 * max(expected_migrants(w.state, w.grid, w.dt, w.dp) for w in slabs))
     for deferred in (False, True):
         us = []
         for r, w in enumerate(slabs):

@@ -124,3 +124,16 @@ def test_c5_ports_fit_the_grid_at_every_gpu_count():
         ctx = sphbuf.Context(g, 1.3 * dp, 1024, 64, 16)
         for p in [q for r in inputs.c5_ports(P)[:P] for q in r]:
             assert sphbuf.sph_port_check(ctx, p.origin, p.Q, p.half_extents, p.kind, p.layers, dp) == 0, (P, p)
+
+
+def test_expected_migrants_is_the_face_flux():
+    """dist.expected_migrants: sum of max(+-v_x, 0) dt / dp over the particles within
+    one spacing of each interior slab face (the larger face), 0 without one."""
+    from paper_2406_16786_b200.dist import expected_migrants
+    g = inputs.Grid(3, (0.0, 0.0, 0.0), 0.01, (100, 10, 10), 40, 60)     # faces at x = 0.4 and 0.6
+    x = torch.tensor([0.4005, 0.4005, 0.5, 0.5995, 0.5995, 0.5995], dtype=torch.float32)
+    vx = torch.tensor([-2.0, 1.0, -5.0, 1.0, 1.0, -1.0], dtype=torch.float32)
+    st = {"x": x, "vx": vx}
+    # lower face: |-2| * dt/dp = 2 * 0.001/0.001 = 2; upper face: (1 + 1) = 2 -> max 2
+    assert expected_migrants(st, g, 0.001, 0.001) == 2
+    assert expected_migrants(st, inputs.Grid(3, (0.0, 0.0, 0.0), 0.01, (100, 10, 10)), 0.001, 0.001) == 0
