@@ -545,9 +545,17 @@ def sweep_configs(dev, names=("C1", "C1e", "C2", "C3", "C4"), replays=50):
         e1.record(stream)
         torch.cuda.synchronize()
         us_stream = e0.elapsed_time(e1) * 1e3 / replays
+        # per-kernel split from a separate profiled pass (an event pair per kernel)
+        sphbuf.sph_profile(bu.ctx, True)
+        for _ in range(10):
+            bu.step(dt_of(name), deferred=True)
+        prof = sphbuf.sph_profile_read(bu.ctx)
+        sphbuf.sph_profile(bu.ctx, False)
+        kern = {k: round(ms * 1e3 / cnt, 2) for k, (ms, cnt) in prof.items() if cnt}
         out[name] = {"particles": n0, "us_per_update_graph": round(us_graph, 2),
                      "us_per_update_stream": round(us_stream, 2), "candidates_per_update": round(cand, 1),
-                     "particles_checked_per_s": cand / (us_graph * 1e-6) if us_graph else None}
+                     "particles_checked_per_s": cand / (us_graph * 1e-6) if us_graph else None,
+                     "kernels_us_profiled": kern}
         del bu, g
         torch.cuda.empty_cache()
     return out

@@ -83,7 +83,9 @@ def lib():
     debug = os.environ.get("SPHBUF_DEBUG") == "1"     # the bounds-asserting build (tests only)
     trace = os.environ.get("SPHBUF_TRACE") == "1"     # tile timeline of the update (tools/upd_trace.py)
     path = _build.LIB_DEBUG if debug else _build.LIB_TRACE if trace else _build.LIB
-    if not os.path.exists(path) or os.environ.get("SPHBUF_REBUILD"):
+    if os.environ.get("SPHBUF_LIB"):                  # another build of the same sources (A/B timing)
+        path = os.environ["SPHBUF_LIB"]
+    elif not os.path.exists(path) or os.environ.get("SPHBUF_REBUILD"):
         path = _build.build(debug=debug, trace=trace)
     L = C.CDLL(path)
     vp, i32, i64, f32 = C.c_void_p, C.c_int32, C.c_int64, C.c_float
