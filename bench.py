@@ -686,8 +686,13 @@ def spawn_check(args):
     dist.init_process_group("gloo")
     t = torch.tensor([rank + 1])
     dist.all_reduce(t)
-    print(json.dumps({"rank": rank, "world": world, "local_rank": int(os.environ.get("LOCAL_RANK", "0")),
-                      "sum_ranks_plus_1": int(t.item())}), flush=True)
+    line = json.dumps({"rank": rank, "world": world, "local_rank": int(os.environ.get("LOCAL_RANK", "0")),
+                       "sum_ranks_plus_1": int(t.item())}) + "\n"
+    for r in range(world):              # one rank at a time: the ranks share one stdout pipe
+        if r == rank:
+            sys.stdout.write(line)
+            sys.stdout.flush()
+        dist.barrier()
     dist.destroy_process_group()
 
 
