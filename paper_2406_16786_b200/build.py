@@ -14,7 +14,7 @@ LIB_DEBUG = os.path.join(HERE, "libsphbuf_debug.so")   # -DSPHBUF_DEBUG: device 
 LIB_TRACE = os.path.join(HERE, "libsphbuf_trace.so")   # -DSPHBUF_TRACE: per-tile timestamps of the update (tools/)
 SOURCES = ["sphbuf_cll.cu", "sphbuf_update.cu", "sphbuf_compact.cu", "sphbuf_migrate.cu", "sphbuf_motion.cu",
            "sphbuf_drivers.cu", "sphbuf_host.cpp", "sphbuf_comm.cpp"]
-DEPS = SOURCES + ["sphbuf_internal.h", "sphbuf_common.cuh"]
+DEPS = SOURCES + ["sphbuf_internal.h", "sphbuf_common.cuh", "sphbuf_tma.cuh", "sphbuf_prologue.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "--fmad=false",
          "-Xcompiler", "-fPIC,-ffp-contract=off", "-shared", "-Xptxas", "-v"]

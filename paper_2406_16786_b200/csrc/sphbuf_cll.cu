@@ -22,6 +22,7 @@
 
 #include "sphbuf_common.cuh"
 #include "sphbuf_prologue.cuh"
+#include "sphbuf_tma.cuh"
 
 namespace sphbuf {
 
@@ -836,6 +837,415 @@ __global__ void __launch_bounds__(NT, MINB) k_cll_gather(PartDev in, PartDev out
     }
 }
 
+// K4 on the copy engine (opt-in, SPHBUF_GATHER_TMA=1: correct and bit-identical,
+// but slower than k_cll_gather on C5 — 3.2 vs 2.1 ms, DESIGN.md §6 — because the
+// stages' shared memory leaves one block of <= 32 warps per SM for a per-tile
+// dependency chain that k_cll_gather hides behind 40).  The sources of a tile of T slots lie
+// mostly in one window of the input (a particle that keeps its cell, or moves to
+// the next cell along z, lands near where it was; measured on C5: ~90% of the
+// sources inside [j0 + drift - 64, j0 + T + drift + 64), drift = the median of
+// (source - slot) over 32 samples of the tile's slot map, tools/map_window_stats.py).
+// One producer warp per block estimates each tile's drift and brings that window
+// of every column into one of S shared-memory stages with cp.async.bulk, running
+// up to S tiles ahead.  The consumer warps (G groups of T/2 threads, 2 slots
+// each, taking the block's tiles in turn) fetch the other sources (cell changers
+// in x and y) of their NEXT tile into the stage's far area with cp.async, as soon
+// as its window is known; the stage's mbarrier completes when both the window
+// copies and those far copies have landed, so a tile finds every source in shared
+// memory and no DRAM round trip is left on the consumers' path.  The rest — the
+// advection, the cell range, the rank by id among the cell's slots, the stores,
+// the carried-over key — is K4's, unchanged, with a named barrier per group
+// instead of the block barrier.  Results are bit-identical to k_cll_gather (the
+// same values reach the same arithmetic).
+template <int DIM, int T, int G, int S>
+struct GtmaCfg {
+    static constexpr int NCG = T / 2;                       // consumer threads per group, 2 slots each
+    static constexpr int NT = G * NCG + 32;                 // + the producer warp
+    static constexpr int H = 64;                            // window margin (elements) on either side
+    static constexpr int W = T + 2 * H;                     // elements copied per column
+    static constexpr int WP = W + 8;                        // column stride in a stage (16-byte multiple)
+    static constexpr int FC = T / 4;                        // far-area entries per stage (overflow: plain loads)
+    static constexpr int NF = 2 * DIM;                      // fp32 columns
+    static constexpr int BPE = 4 * NF + 8 + 4;              // bytes per element (floats, id, label)
+    static constexpr size_t win_bytes = (size_t)WP * BPE;
+    static constexpr size_t stage_bytes = win_bytes + (size_t)FC * BPE;
+    static constexpr int RW = T + 2 * kHalo;                // ranking window (slots)
+    static constexpr size_t rank_bytes = (size_t)RW * 12;   // ids + their low words
+    static constexpr size_t smem = S * stage_bytes + (size_t)G * 2 * rank_bytes;
+    static_assert(W % 4 == 0 && (WP * 4) % 16 == 0 && (FC * 4) % 16 == 0 && stage_bytes % 16 == 0 &&
+                      rank_bytes % 16 == 0, "alignment");
+    static_assert(2 * kHalo <= NCG && NCG % 32 == 0 && S >= 3 * G, "shape: far copies two group tiles ahead");
+};
+
+// Group-wide OR over a named barrier (bar.red): also the group's barrier.
+__device__ __forceinline__ bool named_bar_or(int id, int n, bool p)
+{
+    int r;
+    asm volatile(
+        "{\n\t.reg .pred pi, po;\n\t"
+        "setp.ne.s32 pi, %1, 0;\n\t"
+        "bar.red.or.pred po, %2, %3, pi;\n\t"
+        "selp.s32 %0, 1, 0, po;\n}"
+        : "=r"(r)
+        : "r"((int)p), "r"(id), "r"(n)
+        : "memory");
+    return r != 0;
+}
+
+template <int BYTES>
+__device__ __forceinline__ void cp_async_g2s(void *dst, const void *src)
+{
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(smem_u32(dst)), "l"(src), "n"(BYTES) : "memory");
+}
+
+// The mbarrier's pending count drops when this thread's earlier cp.async copies land.
+__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t *bar)
+{
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void st_release_cta(unsigned long long *p, unsigned long long v)
+{
+    asm volatile("st.release.cta.shared::cta.u64 [%0], %1;" ::"r"(smem_u32(p)), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ unsigned long long ld_acquire_cta(const unsigned long long *p)
+{
+    unsigned long long v;
+    asm volatile("ld.acquire.cta.shared::cta.u64 %0, [%1];" : "=l"(v) : "r"(smem_u32(p)) : "memory");
+    return v;
+}
+
+template <int DIM, int T, int G, int S, int CARRY>
+__global__ void __launch_bounds__(GtmaCfg<DIM, T, G, S>::NT, 1)
+    k_cll_gather_tma(PartDev in, PartDev out, GridDev g, Workspace ws, const int *cell_start, const int *cell_end,
+                     int advect, float dt, float cdt)
+{
+    using C = GtmaCfg<DIM, T, G, S>;
+    constexpr int NCG = C::NCG;
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ uint64_t full[S], empty[S];
+    __shared__ unsigned long long s_win[S];   // (tile sequence << 32) | window start, published by the producer
+    __shared__ int s_fcnt[S];                 // far-area entries taken in each stage
+    pdl_entry();
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 1 + NCG);     // the producer's expect_tx + one cp.async arrival per consumer
+            mbar_init(&empty[s], NCG / 32);
+            s_win[s] = ~0ull;
+            s_fcnt[s] = 0;
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const int n = (int)*out.n;
+    const int capf = (int)(in.cap & ~3LL);                  // windows stay inside the columns' capacity
+    const int ntiles = (n + T - 1) / T;
+    const int nk = (int)blockIdx.x < ntiles ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+    const int lane = threadIdx.x & 31;
+    // stage s: window columns [id][f0..f_{NF-1}][label] (WP each), then the far area (FC each)
+    auto win_id = [&](int s) { return reinterpret_cast<long long *>(smem + s * C::stage_bytes); };
+    auto win_f = [&](int s, int c) {
+        return reinterpret_cast<float *>(smem + s * C::stage_bytes + C::WP * 8 + c * C::WP * 4);
+    };
+    auto win_lab = [&](int s) {
+        return reinterpret_cast<int *>(smem + s * C::stage_bytes + C::WP * (8 + 4 * C::NF));
+    };
+    auto far_id = [&](int s) { return reinterpret_cast<long long *>(smem + s * C::stage_bytes + C::win_bytes); };
+    auto far_f = [&](int s, int c) {
+        return reinterpret_cast<float *>(smem + s * C::stage_bytes + C::win_bytes + C::FC * 8 + c * C::FC * 4);
+    };
+    auto far_lab = [&](int s) {
+        return reinterpret_cast<int *>(smem + s * C::stage_bytes + C::win_bytes + C::FC * (8 + 4 * C::NF));
+    };
+    if ((int)threadIdx.x >= G * NCG) {
+        // ---- producer warp.  The 32 map samples of tile k are loaded D tiles ahead
+        // (a register ring, static indices through the unrolled inner loop).
+        constexpr int D = 4;
+        int pre[D];
+        auto sample = [&](int k) {
+            const int js = ((int)blockIdx.x + k * (int)gridDim.x) * T + lane * (T / 32);
+            return (k < nk && js < n) ? ws.src[js] - js : 0;
+        };
+#pragma unroll
+        for (int u = 0; u < D; ++u) pre[u] = sample(u);
+        for (int k0 = 0; k0 < nk; k0 += D)
+#pragma unroll
+            for (int u = 0; u < D; ++u) {
+                const int k = k0 + u;
+                if (k >= nk) break;
+                const int s = k % S;
+                const int j0 = ((int)blockIdx.x + k * (int)gridDim.x) * T;
+                // drift: the median of (source - slot) over the 32 samples
+                const int dl = pre[u];
+                pre[u] = sample(k + D);
+                int below = 0, eq = 0;
+#pragma unroll 8
+                for (int l = 0; l < 32; ++l) {
+                    const int o = __shfl_sync(0xffffffffu, dl, l);
+                    below += o < dl;
+                    eq += (o == dl) & (l < lane);
+                }
+                const unsigned med = __ballot_sync(0xffffffffu, below + eq == 16);
+                const int drift = __shfl_sync(0xffffffffu, dl, __ffs(med) - 1);
+                long long a = (long long)j0 - C::H + drift;
+                if (a > capf - C::W) a = capf - C::W;
+                if (a < 0) a = 0;
+                const int a4 = (int)a & ~3;
+                const int b4 = a4 + C::W < capf ? a4 + C::W : capf;
+                if (lane == 0) {
+                    if (k >= S) mbar_wait(&empty[s], ((k / S) - 1) & 1);
+                    const unsigned ne = (unsigned)(b4 - a4);
+                    mbar_arrive_expect_tx(&full[s], ne * (unsigned)C::BPE);
+                    if (ne) {
+                        bulk_g2s(win_id(s), in.id + a4, ne * 8u, &full[s]);
+                        bulk_g2s(win_f(s, 0), in.x + a4, ne * 4u, &full[s]);
+                        bulk_g2s(win_f(s, 1), in.y + a4, ne * 4u, &full[s]);
+                        if (DIM == 3) {
+                            bulk_g2s(win_f(s, 2), in.z + a4, ne * 4u, &full[s]);
+                            bulk_g2s(win_f(s, 3), in.vx + a4, ne * 4u, &full[s]);
+                            bulk_g2s(win_f(s, 4), in.vy + a4, ne * 4u, &full[s]);
+                            bulk_g2s(win_f(s, 5), in.vz + a4, ne * 4u, &full[s]);
+                        } else {
+                            bulk_g2s(win_f(s, 2), in.vx + a4, ne * 4u, &full[s]);
+                            bulk_g2s(win_f(s, 3), in.vy + a4, ne * 4u, &full[s]);
+                        }
+                        bulk_g2s(win_lab(s), in.label + a4, ne * 4u, &full[s]);
+                    }
+                    st_release_cta(&s_win[s], ((unsigned long long)k << 32) | (unsigned)a4);
+                }
+                __syncwarp();
+            }
+        return;
+    }
+    // ---- consumers: group gi takes the block's tiles gi, gi + G, ...
+    const int gi = (int)threadIdx.x / NCG, tg = (int)threadIdx.x % NCG;
+    const int carry = CARRY;
+    const int adv_lim = advect ? (int)ws.ctr->mig_base : 0;
+    int oob_next = 0;
+    auto tile_j0 = [&](int k) { return ((int)blockIdx.x + k * (int)gridDim.x) * T; };
+    // slot map of a tile: this thread's two slots and (threads < 2 kHalo) one halo slot
+    auto load_map = [&](int k, int (&sv)[3]) {
+        const int jb = tile_j0(k);
+#pragma unroll
+        for (int it = 0; it < 2; ++it) {
+            const int j = jb + it * NCG + tg;
+            sv[it] = (k < nk && j < n) ? ws.src[j] : -1;
+        }
+        const int jh = tg < kHalo ? jb - kHalo + tg : jb + T + (tg - kHalo);
+        sv[2] = (k < nk && tg < 2 * kHalo && jh >= 0 && jh < n) ? ws.src[jh] : -1;
+    };
+    // far prefetch of tile k (its window published): sources outside the window go
+    // to the stage's far area by cp.async; fi = far index, -1 window (or none), -2
+    // far area full (loaded at the tile); then this thread's arrival on full[s]
+    auto prefetch = [&](int k, const int (&sv)[3], int (&fi)[3]) {
+        const int s = k % S;
+        unsigned long long w;
+        while (true) {
+            w = ld_acquire_cta(&s_win[s]);
+            if ((unsigned)(w >> 32) == (unsigned)k) break;
+        }
+        const int a4 = (int)(unsigned)w;
+        const int b4 = a4 + C::W < capf ? a4 + C::W : capf;
+        bool far[3];
+#pragma unroll
+        for (int it = 0; it < 3; ++it) far[it] = sv[it] >= 0 && !(sv[it] >= a4 && sv[it] < b4);
+        const unsigned m0 = __ballot_sync(0xffffffffu, far[0]), m1 = __ballot_sync(0xffffffffu, far[1]),
+                       m2 = __ballot_sync(0xffffffffu, far[2]);
+        const int tot = __popc(m0) + __popc(m1) + __popc(m2);
+        int base = 0;
+        if (lane == 0 && tot) base = atomicAdd(&s_fcnt[s], tot);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        const unsigned lt = lanemask_lt();
+        const int off[3] = {__popc(m0 & lt), __popc(m0) + __popc(m1 & lt), __popc(m0) + __popc(m1) + __popc(m2 & lt)};
+#pragma unroll
+        for (int it = 0; it < 3; ++it) {
+            fi[it] = -1;
+            if (!far[it]) continue;
+            const int e = base + off[it];
+            if (e >= C::FC) {
+                fi[it] = -2;
+                continue;
+            }
+            fi[it] = e;
+            const int q = sv[it];
+            cp_async_g2s<8>(far_id(s) + e, in.id + q);
+            if (it == 2) continue;                                // halo slots: the id only
+            cp_async_g2s<4>(far_f(s, 0) + e, in.x + q);
+            cp_async_g2s<4>(far_f(s, 1) + e, in.y + q);
+            if (DIM == 3) {
+                cp_async_g2s<4>(far_f(s, 2) + e, in.z + q);
+                cp_async_g2s<4>(far_f(s, 3) + e, in.vx + q);
+                cp_async_g2s<4>(far_f(s, 4) + e, in.vy + q);
+                cp_async_g2s<4>(far_f(s, 5) + e, in.vz + q);
+            } else {
+                cp_async_g2s<4>(far_f(s, 2) + e, in.vx + q);
+                cp_async_g2s<4>(far_f(s, 3) + e, in.vy + q);
+            }
+            cp_async_g2s<4>(far_lab(s) + e, in.label + q);
+        }
+        cp_async_arrive_noinc(&full[s]);
+        return a4;
+    };
+    // this group's tiles k (being processed), k + G (far copies in flight), k + 2G
+    // (map loaded): the far copies of k + 2G are issued at the end of tile k
+    int cur[3], nxt[3], nn[3], fi[3], nfi[3];
+    int a_cur = 0, a_nxt = 0;
+    if (gi < nk) {
+        load_map(gi, cur);
+        load_map(gi + G, nxt);
+        load_map(gi + 2 * G, nn);
+        a_cur = prefetch(gi, cur, fi);
+        if (gi + G < nk) a_nxt = prefetch(gi + G, nxt, nfi);
+    }
+    int par = 0;
+    for (int k = gi; k < nk; k += G, par ^= 1) {
+        const int s = k % S;
+        const int j0 = tile_j0(k);
+        const int src[2] = {cur[0], cur[1]};
+        const int hsrc = cur[2];
+        const int fic[3] = {fi[0], fi[1], fi[2]};
+        const int a4 = a_cur;
+        float x[2], y[2], z[2], vx[2], vy[2], vz[2];
+        long long id[2];
+        int lab[2];
+        long long hid = 0;
+        mbar_wait(&full[s], (k / S) & 1);
+        if (tg == 0) s_fcnt[s] = 0;                               // (all of this tile's far slots are taken)
+#pragma unroll
+        for (int it = 0; it < 2; ++it) {
+            const int q = src[it];
+            z[it] = vz[it] = 0.0f;
+            if (q < 0) continue;
+            if (fic[it] == -1) {
+                const int r = q - a4;
+                x[it] = win_f(s, 0)[r];
+                y[it] = win_f(s, 1)[r];
+                if (DIM == 3) {
+                    z[it] = win_f(s, 2)[r];
+                    vx[it] = win_f(s, 3)[r];
+                    vy[it] = win_f(s, 4)[r];
+                    vz[it] = win_f(s, 5)[r];
+                } else {
+                    vx[it] = win_f(s, 2)[r];
+                    vy[it] = win_f(s, 3)[r];
+                }
+                id[it] = win_id(s)[r];
+                lab[it] = win_lab(s)[r];
+            } else if (fic[it] >= 0) {
+                const int e = fic[it];
+                x[it] = far_f(s, 0)[e];
+                y[it] = far_f(s, 1)[e];
+                if (DIM == 3) {
+                    z[it] = far_f(s, 2)[e];
+                    vx[it] = far_f(s, 3)[e];
+                    vy[it] = far_f(s, 4)[e];
+                    vz[it] = far_f(s, 5)[e];
+                } else {
+                    vx[it] = far_f(s, 2)[e];
+                    vy[it] = far_f(s, 3)[e];
+                }
+                id[it] = far_id(s)[e];
+                lab[it] = far_lab(s)[e];
+            } else {
+                x[it] = in.x[q];
+                y[it] = in.y[q];
+                vx[it] = in.vx[q];
+                vy[it] = in.vy[q];
+                if (DIM == 3) {
+                    z[it] = in.z[q];
+                    vz[it] = in.vz[q];
+                }
+                id[it] = in.id[q];
+                lab[it] = in.label[q];
+            }
+        }
+        if (hsrc >= 0) hid = fic[2] == -1 ? win_id(s)[hsrc - a4] : fic[2] >= 0 ? far_id(s)[fic[2]] : in.id[hsrc];
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);                // the stage goes back to the producer
+        // ---- K4's body: advection, cell range, rank by id, stores, carried key
+        unsigned char *rb = smem + S * C::stage_bytes + (size_t)(gi * 2 + par) * C::rank_bytes;
+        long long *s_id = reinterpret_cast<long long *>(rb);
+        unsigned *s_lo = reinterpret_cast<unsigned *>(rb + C::RW * 8);
+        bool wide = hsrc >= 0 && (hid >> 32) != 0;
+        if (tg < 2 * kHalo) {
+            const int hq = tg < kHalo ? tg : T + tg;
+            s_id[hq] = hid;
+            s_lo[hq] = (unsigned)hid;
+        }
+        int cb[2], ce[2];
+#pragma unroll
+        for (int it = 0; it < 2; ++it) {
+            cb[it] = ce[it] = 0;
+            if (src[it] < 0) continue;
+            if (src[it] < adv_lim) {
+                x[it] = advect1(x[it], vx[it], dt);
+                y[it] = advect1(y[it], vy[it], dt);
+                if (DIM == 3) z[it] = advect1(z[it], vz[it], dt);
+            }
+            int oob = 0;
+            const int key = cell_of<DIM>(g, x[it], y[it], z[it], oob);
+            cb[it] = __ldg(cell_start + key);
+            ce[it] = __ldg(cell_end + key);
+            s_id[kHalo + it * NCG + tg] = id[it];
+            s_lo[kHalo + it * NCG + tg] = (unsigned)id[it];
+            wide |= (id[it] >> 32) != 0;
+        }
+        const bool narrow = !named_bar_or(1 + gi, NCG, wide);
+        const int w0 = j0 - kHalo > 0 ? j0 - kHalo : 0;
+        const int w1 = j0 + T + kHalo < n ? j0 + T + kHalo : n;
+        const long long *sid = s_id + (w0 - (j0 - kHalo));
+        const unsigned *slo = s_lo + (w0 - (j0 - kHalo));
+        int kn[2];
+#pragma unroll
+        for (int it = 0; it < 2; ++it) {
+            kn[it] = -1;
+            if (src[it] < 0) continue;
+            const long long me = id[it];
+            const int d = cb[it] + rank_in_cell(in, ws, sid, slo, narrow, w0, w1, cb[it], ce[it], me);
+            if (carry) {
+                int oobn = 0;
+                kn[it] = carry_key<DIM>(g, x[it], y[it], z[it], vx[it], vy[it], vz[it], cdt, carry, oobn);
+                oob_next += oobn;
+                ws.key[d] = kn[it];
+                if (kn[it] == kLeaver) leaver_append(ws, d);
+            }
+            SPH_CHECK(d >= cb[it] && d < ce[it] && ce[it] <= n && src[it] < in.cap);
+            out.x[d] = x[it];
+            out.y[d] = y[it];
+            out.vx[d] = vx[it];
+            out.vy[d] = vy[it];
+            if (DIM == 3) {
+                out.z[d] = z[it];
+                out.vz[d] = vz[it];
+            }
+            out.id[d] = me;
+            out.label[d] = lab[it];
+        }
+        if (carry) {
+#pragma unroll
+            for (int it = 0; it < 2; ++it) hist_count_runs(ws.cell_count, kn[it]);   // next histogram
+        }
+        // rotate: k + G becomes current; the far copies of k + 2G go out now
+        int a2 = 0, f2[3] = {-1, -1, -1};
+        if (k + 2 * G < nk) a2 = prefetch(k + 2 * G, nn, f2);
+#pragma unroll
+        for (int it = 0; it < 3; ++it) {
+            cur[it] = nxt[it];
+            fi[it] = nfi[it];
+            nxt[it] = nn[it];
+            nfi[it] = f2[it];
+        }
+        a_cur = a_nxt;
+        a_nxt = a2;
+        if (k + 3 * G < nk) load_map(k + 3 * G, nn);
+    }
+    if (carry) {
+        const unsigned o = warp_sum((unsigned)oob_next);
+        if (lane == 0 && o) atomicAdd((unsigned long long *)&ws.ctr->out_of_grid, (unsigned long long)o);
+    }
+}
+
 // ------------------------------------------------------------------ launchers
 
 template <int I, int NT>
@@ -861,6 +1271,70 @@ static void gather_fused(const PartDev &in, const PartDev &out, const GridDev &g
     if (!grid) grid = occ_grid(k_cll_gather<HasExtra, ITEMS, MINB, NT, PF>, NT);
     launch_k(k_cll_gather<HasExtra, ITEMS, MINB, NT, PF>, dim3(cap_grid(grid, cap, NT * ITEMS)), dim3(NT), 0, s, in, out, g, ws, cs, ce,
              perm, advect, dt, carry, cdt);
+}
+
+template <int DIM, int T, int G, int S, int CARRY>
+static void gather_tma_launch(const PartDev &in, const PartDev &out, const GridDev &g, const Workspace &ws,
+                              const int *cs, const int *ce, int advect, float dt, float cdt, long long cap,
+                              cudaStream_t s)
+{
+    using C = GtmaCfg<DIM, T, G, S>;
+    static bool init = false;
+    if (!init) {
+        cudaFuncSetAttribute(k_cll_gather_tma<DIM, T, G, S, CARRY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)C::smem);
+        init = true;
+    }
+    launch_k(k_cll_gather_tma<DIM, T, G, S, CARRY>, dim3(cap_grid(sm_count_cached(), cap, T)), dim3(C::NT), C::smem,
+             s, in, out, g, ws, cs, ce, advect, dt, cdt);
+}
+
+template <int T, int G, int S>
+static void gather_tma_dispatch(const PartDev &in, const PartDev &out, const GridDev &g, const Workspace &ws,
+                                const int *cs, const int *ce, int advect, float dt, int carry, float cdt,
+                                long long cap, cudaStream_t s)
+{
+    if (g.dim == 3) {
+        if (carry == 1) gather_tma_launch<3, T, G, S, 1>(in, out, g, ws, cs, ce, advect, dt, cdt, cap, s);
+        else if (carry == 2) gather_tma_launch<3, T, G, S, 2>(in, out, g, ws, cs, ce, advect, dt, cdt, cap, s);
+        else gather_tma_launch<3, T, G, S, 0>(in, out, g, ws, cs, ce, advect, dt, cdt, cap, s);
+    } else {
+        if (carry == 1) gather_tma_launch<2, T, G, S, 1>(in, out, g, ws, cs, ce, advect, dt, cdt, cap, s);
+        else if (carry == 2) gather_tma_launch<2, T, G, S, 2>(in, out, g, ws, cs, ce, advect, dt, cdt, cap, s);
+        else gather_tma_launch<2, T, G, S, 0>(in, out, g, ws, cs, ce, advect, dt, cdt, cap, s);
+    }
+}
+
+// The copy-engine gather (opt-in: measured slower than k_cll_gather on C5, DESIGN.md
+// §6) applies to builds without extra columns or a perm output whose columns are
+// 16-byte aligned (cp.async.bulk); SPHBUF_GATHER_TMA=1 selects it, =<T>:<G>:<S> a
+// tuning variant (3-D, carried keys).
+static bool try_gather_tma(const PartDev &in, const PartDev &out, const GridDev &g, const Workspace &ws,
+                           const int *cs, const int *ce, int *perm, int advect, float dt, int carry, float cdt,
+                           long long cap, cudaStream_t s)
+{
+    static const char *v = getenv("SPHBUF_GATHER_TMA");
+    if (!v || !*v || !strcmp(v, "0")) return false;
+    if (in.n_extra > 0 || perm) return false;
+    auto al = [](const void *p) { return ((uintptr_t)p & 15) == 0; };
+    if (!al(in.x) || !al(in.y) || !al(in.vx) || !al(in.vy) || !al(in.id) || !al(in.label)) return false;
+    if (g.dim == 3 && (!al(in.z) || !al(in.vz))) return false;
+    if (strcmp(v, "1") && g.dim == 3 && carry == 1) {
+#define SPH_GT(name, T, G, S)                                                                   \
+    if (!strcmp(v, name)) {                                                                     \
+        gather_tma_launch<3, T, G, S, 1>(in, out, g, ws, cs, ce, advect, dt, cdt, cap, s);      \
+        return true;                                                                            \
+    }
+        SPH_GT("1024:1:3", 1024, 1, 3)
+        SPH_GT("512:2:6", 512, 2, 6)
+        SPH_GT("512:1:3", 512, 1, 3)
+        SPH_GT("512:1:4", 512, 1, 4)
+        SPH_GT("256:3:9", 256, 3, 9)
+        SPH_GT("256:2:6", 256, 2, 6)
+#undef SPH_GT
+    }
+    gather_tma_dispatch<512, 2, 6>(in, out, g, ws, cs, ce, advect, dt, carry, cdt, cap, s);
+    return true;
 }
 
 template <bool HasExtra>
@@ -918,6 +1392,7 @@ static void launch_gather(const PartDev &in, const PartDev &out, const GridDev &
         v = getenv("SPHBUF_GATHER");
         if (!v) v = "";
     }
+    if (!*v && try_gather_tma(in, out, g, ws, cs, ce, perm, advect, dt, carry, cdt, cap, s)) return;
     if (in.n_extra > 0) gather_variant<true>(v, in, out, g, ws, cs, ce, perm, advect, dt, carry, cdt, cap, s);
     else gather_variant<false>(v, in, out, g, ws, cs, ce, perm, advect, dt, carry, cdt, cap, s);
 }

@@ -140,3 +140,32 @@ def test_inplace_compaction_register_move_path():
     env = dict(os.environ, SPHBUF_MOVE_TMA="0")
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
+
+
+@pytest.mark.gpu
+def test_copy_engine_gather_path():
+    """The opt-in copy-engine gather (k_cll_gather_tma, SPHBUF_GATHER_TMA=1: window
+    of every column by cp.async.bulk, far sources by cp.async into the stage) is
+    bit-exact with the oracle: C2 (2-D, carried keys), a 3-D junction with in-place
+    compaction, the duct with the advection outside the build (no carry), and the
+    junction cut into 2 slabs (carried keys with migration)."""
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    code = ("import sys; sys.path.insert(0, %r); sys.path.insert(0, %r)\n"
+            "import oracle; oracle.enable_tie_check(1e-4)\n"
+            "from paper_2406_16786_b200 import inputs\n"
+            "from parity_util import lockstep\n"
+            "tot, bu = lockstep(inputs.make('C2'), 10, check_every=2, fused=True, deferred=True)\n"
+            "assert tot[0] > 0 and tot[1] > 0\n"
+            "w = inputs.c4(scale=0.25, nports=4, n_updates=6)\n"
+            "tot, bu = lockstep(w, 6, check_every=1, fused=True, deferred=False)\n"
+            "assert tot.sum() > 0\n"
+            "tot, bu = lockstep(inputs.c3(scale=0.5), 4, check_every=2, fused=False, deferred=True)\n"
+            "import test_dist as td\n"
+            "td.test_loopback_slabs_match_oracle(2, True)\n"
+            "print('ok')\n") % (os.path.dirname(here), here)
+    env = dict(os.environ, SPHBUF_GATHER_TMA="1")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]

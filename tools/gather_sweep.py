@@ -1,5 +1,6 @@
 #!/usr/bin/env python
-"""Tuning sweep of the cell-list gather variants (SPHBUF_GATHER=<kind>:<slots>:<min blocks>).
+"""Tuning sweep of the cell-list gather variants (SPHBUF_GATHER=<kind>:<slots>:<min blocks>, or any
+NAME=value such as SPHBUF_GATHER_TMA=<tile>:<groups>:<stages>).
 
     python tools/gather_sweep.py [--config C5] [--steps 8] [variant ...]
 
@@ -62,7 +63,8 @@ def main():
     variants = args or VARIANTS
     res = {}
     for v in variants:
-        env = dict(os.environ, SPHBUF_GATHER=v)
+        # "NAME=value" sets that variable (e.g. SPHBUF_GATHER_TMA=512:2:4), else SPHBUF_GATHER
+        env = dict(os.environ, **({v.split("=", 1)[0]: v.split("=", 1)[1]} if "=" in v else {"SPHBUF_GATHER": v}))
         r = subprocess.run([sys.executable, __file__, "--child", "--config", config, "--steps", str(steps)], env=env,
                            capture_output=True, text=True, timeout=600)
         line = [l for l in r.stdout.splitlines() if l.startswith("{")]

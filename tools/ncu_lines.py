@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Aggregate an ncu source page (sass,cuda) by CUDA source line.
 
-    python tools/ncu_lines.py <report.ncu-rep> <kernel regex> [top]
+    python tools/ncu_lines.py <report.ncu-rep> <kernel regex> [top] [--stall]   (--stall: sort by stall samples)
 """
 import collections
 import csv
@@ -13,6 +13,7 @@ import sys
 def main():
     rep, kern = sys.argv[1], sys.argv[2]
     top = int(sys.argv[3]) if len(sys.argv) > 3 else 30
+    by_stall = "--stall" in sys.argv
     out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "-k", f"regex:{kern}", "--print-source",
                           "sass,cuda"], capture_output=True, text=True).stdout
     lines = out.splitlines()
@@ -24,7 +25,7 @@ def main():
     agg = collections.defaultdict(lambda: [0, 0, ""])
     seen = set()
     for r in rows[1:]:
-        if len(r) != len(h):
+        if len(r) != len(h) or not r[0].strip():
             continue
         key = (r[0], r[2])
         if key in seen:
@@ -41,7 +42,7 @@ def main():
     te = sum(a[0] for a in agg.values()) or 1
     ts = sum(a[1] for a in agg.values()) or 1
     print(f"total warp instructions {te}, stall samples {ts}")
-    for ln, (e, s, src) in sorted(agg.items(), key=lambda kv: -kv[1][0])[:top]:
+    for ln, (e, s, src) in sorted(agg.items(), key=lambda kv: -kv[1][1 if by_stall else 0])[:top]:
         print(f"{ln:>5} inst {e / te:6.1%} stall {s / ts:6.1%}  {src}")
 
 
