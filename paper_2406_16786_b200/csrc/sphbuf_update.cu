@@ -5,6 +5,7 @@
 #include <climits>
 #include <cstdint>
 #include <cstdlib>
+#include <cstring>
 
 #include "sphbuf_common.cuh"
 #include "sphbuf_prologue.cuh"
@@ -121,7 +122,11 @@ __device__ __forceinline__ float bc_speed(const PortDev &P, int dim, float vx, f
 // particle is tile_pre[tile] + rank (read by the compaction).  Per tile, every
 // load is issued before the stores it does not depend on, so a tile costs few
 // dependent memory round trips.
-__global__ void __launch_bounds__(kThreads) k_upd_main(PartDev p, GridDev g, const __grid_constant__ PortTable pt,
+// MINB: resident blocks per SM the registers are bounded for (tiles in one wave);
+// SPEC: the velocity, id and carried key of every candidate are loaded with its
+// position (one dependent round trip less for the tiles with creations or BC).
+template <int MINB, bool SPEC>
+__global__ void __launch_bounds__(kThreads, MINB) k_upd_main(PartDev p, GridDev g, const __grid_constant__ PortTable pt,
                                                        Workspace ws, int n_runs, const int *cell_start,
                                                        int *port_counts, int carry, float cdt, int tile_runs_max)
 {
@@ -191,10 +196,16 @@ __global__ void __launch_bounds__(kThreads) k_upd_main(PartDev p, GridDev g, con
         // (A) candidate -> particle, loads of what the decisions need
         int pidx[kUpdItems], kk[kUpdItems], lab[kUpdItems];
         float x[kUpdItems], y[kUpdItems], z[kUpdItems];
+        float vx[kUpdItems], vy[kUpdItems], vz[kUpdItems];
+        long long sid[kUpdItems];
+        int okey[kUpdItems];
 #pragma unroll
         for (int it = 0; it < kUpdItems; ++it) {
             pidx[it] = -1;
             kk[it] = 0;
+            vx[it] = vy[it] = vz[it] = 0.0f;
+            sid[it] = 0;
+            okey[it] = 0;
             const int rel = it * kThreads + threadIdx.x;
             const long long gc = t0 + rel;
             if (gc >= n_cand) continue;
@@ -227,6 +238,13 @@ __global__ void __launch_bounds__(kThreads) k_upd_main(PartDev p, GridDev g, con
             y[it] = p.y[pi];
             z[it] = dim == 3 ? p.z[pi] : 0.0f;
             lab[it] = p.label[pi];
+            if (SPEC) {
+                vx[it] = p.vx[pi];
+                vy[it] = p.vy[pi];
+                if (dim == 3) vz[it] = p.vz[pi];
+                sid[it] = p.id[pi];
+                if (carry) okey[it] = ws.key[pi];
+            }
         }
         // (B) decisions, pure arithmetic
         bool cr[kUpdItems], dl[kUpdItems], bcm[kUpdItems];
@@ -297,14 +315,9 @@ __global__ void __launch_bounds__(kThreads) k_upd_main(PartDev p, GridDev g, con
             }
         }
         // (C) loads for the duplicates and boundary conditions (pre-BC velocity)
-        float vx[kUpdItems], vy[kUpdItems], vz[kUpdItems];
-        long long sid[kUpdItems];
-        int okey[kUpdItems];
 #pragma unroll
         for (int it = 0; it < kUpdItems; ++it) {
-            vx[it] = vy[it] = vz[it] = 0.0f;
-            sid[it] = 0;
-            okey[it] = 0;
+            if (SPEC) break;
             const int pi = pidx[it];
             if (cr[it] || bcm[it]) {
                 vx[it] = p.vx[pi];
@@ -532,8 +545,6 @@ cudaError_t launch_update(const PartDev &p, const GridDev &g, const PortTable &p
         launch_k(k_upd_prologue, dim3(pro_blocks), dim3(1024), 0, s, ws, n_runs, cell_start, cell_end, pt.max_ports);
         L->after(s, KID_UPD_PROLOGUE);
     }
-    static int grid = 0;
-    if (!grid) grid = occ_grid(k_upd_main, kThreads);
     // SPHBUF_TILE_RUNS=<n> lowers the number of runs a tile stages in shared memory
     // (tests force the global-search path with 0)
     static const int trmax = [] {
@@ -541,9 +552,31 @@ cudaError_t launch_update(const PartDev &p, const GridDev &g, const PortTable &p
         const int v = e ? atoi(e) : kTileRuns;
         return v < kTileRuns ? (v < 0 ? 0 : v) : kTileRuns;
     }();
+    // SPHBUF_UPD=<min blocks per SM>:<speculative loads 0/1> for tuning runs
+    static const char *uv = getenv("SPHBUF_UPD");
+    const char *v = uv ? uv : "";
     L->before(s);
-    launch_k(k_upd_main, dim3(cap_grid(grid, ws.upd_tiles, 1)), dim3(kThreads), 0, s, p, g, pt, ws, n_runs, cell_start,
-             port_counts, carry, cdt, trmax);
+#define SPH_UPD(name, M, SP)                                                                                      \
+    if (!strcmp(v, name)) {                                                                                       \
+        static int grid = 0;                                                                                      \
+        if (!grid) grid = occ_grid(k_upd_main<M, SP>, kThreads);                                                 \
+        launch_k(k_upd_main<M, SP>, dim3(cap_grid(grid, ws.upd_tiles, 1)), dim3(kThreads), 0, s, p, g, pt, ws,   \
+                 n_runs, cell_start, port_counts, carry, cdt, trmax);                                             \
+        L->after(s, KID_UPD_MAIN);                                                                                \
+        return cudaGetLastError();                                                                                \
+    }
+    SPH_UPD("3:0", 3, false)
+    SPH_UPD("4:1", 4, true)
+    SPH_UPD("5:0", 5, false)
+    SPH_UPD("5:1", 5, true)
+    SPH_UPD("6:0", 6, false)
+    SPH_UPD("6:1", 6, true)
+    SPH_UPD("8:1", 8, true)
+#undef SPH_UPD
+    static int grid = 0;
+    if (!grid) grid = occ_grid(k_upd_main<4, false>, kThreads);
+    launch_k(k_upd_main<4, false>, dim3(cap_grid(grid, ws.upd_tiles, 1)), dim3(kThreads), 0, s, p, g, pt, ws, n_runs,
+             cell_start, port_counts, carry, cdt, trmax);
     L->after(s, KID_UPD_MAIN);
     return cudaGetLastError();
 }

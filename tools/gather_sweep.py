@@ -76,7 +76,7 @@ def main():
         ms = d["ms"]
         cll = sum(ms.get(k, 0) for k in ("cll_key", "cell_scan", "cll_scatter", "cll_gather"))
         print(f"{v or 'default':12s} gather {ms.get('cll_gather', 0):.4f} ms  cll {cll:.4f} ms  n {d['n']}  "
-              f"hash {d['hash']}", flush=True)
+              f"hash {d['hash']}  " + " ".join(f"{k} {1e3 * t:.1f}us" for k, t in sorted(ms.items())), flush=True)
     hs = {d["hash"] for d in res.values()}
     print("checksums agree" if len(hs) == 1 else f"CHECKSUM MISMATCH {hs}")
 
