@@ -781,9 +781,14 @@ __global__ void __launch_bounds__(kThreads) k_compact_append(PartDev p, GridDev 
         const long long ibeg = D ? cmp_begin(ctr->i_first) : N;
         for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < ibeg; i += stride) perm[i] = (int)i;
     }
-    if (threadIdx.x == 0) {
+    // completion among the blocks that had work (all of them with a perm output;
+    // else the first ceil(C / blockDim) — a small append does not wait for the
+    // whole grid's atomics); with no work at all, block 0 writes N and next_id
+    const long long per = blockDim.x;
+    const int working = perm ? (int)gridDim.x : (int)((C + per - 1) / per < gridDim.x ? (C + per - 1) / per : gridDim.x);
+    if (threadIdx.x == 0 && ((int)blockIdx.x < working || (working == 0 && blockIdx.x == 0))) {
         __threadfence();
-        if (atomicAdd(&ctr->done_app, 1) == (int)gridDim.x - 1) {
+        if (working == 0 || atomicAdd(&ctr->done_app, 1) == working - 1) {
             ctr->done_app = 0;
             *p.n = dst0 + C;
             *next_id = nid0 + s_total;

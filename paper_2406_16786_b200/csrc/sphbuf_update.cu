@@ -144,16 +144,22 @@ __global__ void __launch_bounds__(kThreads, MINB) k_upd_main(PartDev p, GridDev 
         atomicMax(&g_trace_k[1], t);
     }
 #endif
-    long long next_ticket = 0;
-    if (threadIdx.x == 0) next_ticket = atomicAdd(&ctr->ticket_upd, 1);
+    // a block's first tile is its index; further tiles come from the ticket counter
+    // (offset by the grid); a block with no tile leaves at once and takes no part
+    // in the completion count below (small configurations launch far more blocks
+    // than they have tiles)
+    const long long n_cand = ctr->n_cand;
+    const long long ntiles_all = (n_cand + kUpdTile - 1) / kUpdTile;
+    const long long nt_run = ntiles_all < ws.upd_tiles ? ntiles_all : ws.upd_tiles;
+    if ((long long)blockIdx.x >= nt_run && !(blockIdx.x == 0 && nt_run == 0)) return;
+    long long next_ticket = blockIdx.x;
     {
         const int words = pt.n * (int)(sizeof(PortDev) / 4);
         const unsigned *src = reinterpret_cast<const unsigned *>(pt.p);
         unsigned *dst = reinterpret_cast<unsigned *>(s_ports);
         for (int w = threadIdx.x; w < words; w += blockDim.x) dst[w] = src[w];
     }
-    const long long n_cand = ctr->n_cand;
-    const long long ntiles = (n_cand + kUpdTile - 1) / kUpdTile;
+    const long long ntiles = ntiles_all;
     const int max_ports = pt.max_ports;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         ctr->epoch_cmp += 1;  // consumed by the compaction that follows
@@ -161,6 +167,7 @@ __global__ void __launch_bounds__(kThreads, MINB) k_upd_main(PartDev p, GridDev 
         ctr->ticket_cmp2 = 0;
     }
     long long del_cnt = 0, del_min = LLONG_MAX, motion = 0;
+    int my_tiles = 0;
     while (true) {
         if (threadIdx.x == 0) s_tile = next_ticket;
         __syncthreads();
@@ -176,7 +183,8 @@ __global__ void __launch_bounds__(kThreads, MINB) k_upd_main(PartDev p, GridDev 
         }
 #endif
         // the ticket of this block's next tile, taken now (off the critical path)
-        if (threadIdx.x == 0) next_ticket = atomicAdd(&ctr->ticket_upd, 1);
+        if (threadIdx.x == 0) next_ticket = (long long)gridDim.x + atomicAdd(&ctr->ticket_upd, 1);
+        ++my_tiles;
         // the tile's runs [r0, r1] (K5's tile_run) staged in shared memory: offsets
         // relative to the tile, first particle index, port
         const long long t0 = tile * kUpdTile;
@@ -450,12 +458,13 @@ __global__ void __launch_bounds__(kThreads, MINB) k_upd_main(PartDev p, GridDev 
             atomicOr(&ctr->status, kStMotion);
         }
     }
-    // the last block to finish: exclusive scan of the tile CREATE counts (the
-    // canonical staging order) and the number created
+    // the block that completes the last tile: exclusive scan of the tile CREATE
+    // counts (the canonical staging order) and the number created (with no tile
+    // at all, block 0)
     __shared__ bool s_last;
     if (threadIdx.x == 0) {
         __threadfence();
-        s_last = atomicAdd(&ctr->done_upd, 1) == (int)gridDim.x - 1;
+        s_last = nt_run == 0 || atomicAdd(&ctr->done_upd, my_tiles) + my_tiles == (int)nt_run;
     }
     __syncthreads();
     if (!s_last) return;
