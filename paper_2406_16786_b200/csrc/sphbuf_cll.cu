@@ -305,6 +305,11 @@ __global__ void __launch_bounds__(kThreads) k_cell_scan(GridDev g, Workspace ws,
     if (threadIdx.x < 32) {
         unsigned pre = tile_prefix(ws.tile_cells, tile, epoch, total);
         if (threadIdx.x == 0) s_prefix = pre;
+    } else if (full) {
+        // while warp 0 looks back, the other warps clear the tile's scatter cursors
+        // (they do not depend on the prefix)
+        int4 *cz = reinterpret_cast<int4 *>(ws.cursor + tile * kCellTile);
+        for (int q = (int)threadIdx.x - 32; q < kCellTile / 4; q += kThreads - 32) cz[q] = make_int4(0, 0, 0, 0);
     }
     __syncthreads();
     SCAN_TRACE(2);
@@ -340,7 +345,6 @@ __global__ void __launch_bounds__(kThreads) k_cell_scan(GridDev g, Workspace ws,
                 reinterpret_cast<int4 *>(cell_start)[q4] = st;
                 reinterpret_cast<int4 *>(cell_end)[q4] = en;
                 reinterpret_cast<int4 *>(ws.cell_count)[q4] = make_int4(0, 0, 0, 0);
-                reinterpret_cast<int4 *>(ws.cursor)[q4] = make_int4(0, 0, 0, 0);
             } else {
                 const int s4[4] = {st.x, st.y, st.z, st.w}, e4[4] = {en.x, en.y, en.z, en.w};
 #pragma unroll
