@@ -596,23 +596,23 @@ __global__ void __launch_bounds__(NT) k_cll_scatter(Workspace ws, const int *cel
             const long long i = base + it * NT + threadIdx.x;
             key[it] = i < n ? ws.key[i] : -1;
         }
-        // run heads of all items first, then all their atomics in flight together
+        // lanes with equal keys grouped (match.any: a cell changer between two pieces
+        // of a stayer run does not split the run's atomic), one cursor atomic per
+        // distinct key of the warp, all items' atomics in flight together; the
+        // lanes of a group take consecutive slots in lane order
         const int lane = threadIdx.x & 31;
-        const unsigned le = lanemask_lt() | (1u << lane);
-        int b[kScatterItems], hl[kScatterItems];
+        const unsigned lt = lanemask_lt();
+        int b[kScatterItems], hl[kScatterItems], rl[kScatterItems];
 #pragma unroll
         for (int it = 0; it < kScatterItems; ++it) {
-            const int prev = __shfl_up_sync(0xffffffffu, key[it], 1);
-            const bool head = (lane == 0) || (key[it] != prev);
-            const unsigned heads = __ballot_sync(0xffffffffu, head);
-            const unsigned above = heads & ~le;
-            const int next = above ? __ffs(above) - 1 : 32;
-            hl[it] = 31 - __clz(heads & le);
-            b[it] = (head && key[it] >= 0) ? atomicAdd(&ws.cursor[key[it]], next - lane) : 0;
+            const unsigned grp = __match_any_sync(0xffffffffu, key[it]);
+            hl[it] = __ffs(grp) - 1;
+            rl[it] = __popc(grp & lt);
+            b[it] = (hl[it] == lane && key[it] >= 0) ? atomicAdd(&ws.cursor[key[it]], __popc(grp)) : 0;
         }
 #pragma unroll
         for (int it = 0; it < kScatterItems; ++it) {
-            const int rk = __shfl_sync(0xffffffffu, b[it], hl[it]) + lane - hl[it];
+            const int rk = __shfl_sync(0xffffffffu, b[it], hl[it]) + rl[it];
             const long long i = base + it * NT + threadIdx.x;
             if (i >= n) continue;
             if (key[it] >= 0) {
