@@ -123,7 +123,7 @@ __global__ void __launch_bounds__(kThreads) k_cll_key(PartDev in, GridDev g, Wor
         }
 #pragma unroll
         for (int it = 0; it < kKeyItems; ++it) {
-            hist_count_runs(ws.cell_count, key[it]);     // one atomic per run of equal keys
+            hist_count_match(ws.cell_count, key[it]);    // one atomic per distinct key of the warp
             const long long i = base + it * kThreads + threadIdx.x;
             if (i < n) ws.key[i] = key[it];
         }
@@ -830,7 +830,7 @@ __global__ void __launch_bounds__(NT, MINB) k_cll_gather(PartDev in, PartDev out
         }
         if (carry) {
 #pragma unroll
-            for (int it = 0; it < ITEMS; ++it) hist_count_runs(ws.cell_count, kn[it]);   // next histogram
+            for (int it = 0; it < ITEMS; ++it) hist_count_match(ws.cell_count, kn[it]);   // next histogram
         }
         __syncthreads();
     };

@@ -168,6 +168,14 @@ __device__ __forceinline__ void hist_count_runs(int *cnt, int key)
     if (head && key >= 0) atomicAdd(&cnt[key], next - lane);
 }
 
+// The same count with lanes grouped by equal key (match.any): one atomic per
+// distinct key of the warp, however the equal keys are interleaved.
+__device__ __forceinline__ void hist_count_match(int *cnt, int key)
+{
+    const unsigned grp = __match_any_sync(0xffffffffu, key);
+    if (key >= 0 && (int)(__ffs(grp) - 1) == (int)(threadIdx.x & 31)) atomicAdd(&cnt[key], __popc(grp));
+}
+
 // Block-wide exclusive scan of one unsigned per thread (NT threads).
 template <int NT>
 __device__ __forceinline__ unsigned block_excl_scan(unsigned v, unsigned &total, unsigned *s_warp)
