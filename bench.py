@@ -353,6 +353,11 @@ def run_ours(args):
                                "frac": frac(b_upd + b_cmp, t_upd + t_cmp),
                                "what": "SURVEY 8(d) headline: (B_update + B_compact) / (t_update + t_compact); "
                                        "kernel times from the breakdown pass"},
+            # the in-place move also carries each moved particle's next-build key (4 B
+            # read + 4 B written), the price of the key pass the next build skips
+            "compact_move_with_keys": ({"bytes": 2 * (S + 4) * moved, "kernel_ms": kms.get("compact", 0),
+                                        "frac": frac(2 * (S + 4) * moved, kms.get("compact", 0))}
+                                       if mode == "inplace" and kms.get("compact") else None),
             "cll_build": {"alg_bytes": b_cll, "kernel_ms": t_cll, "frac": frac(b_cll, t_cll),
                           "what": "2S + 32 B per particle (SURVEY 8(d))"},
             "kernels_ms": {k: round(v, 4) for k, v in kms.items()},
@@ -417,12 +422,14 @@ def run_ours(args):
                                                    "kernel_ms": rep[m]["update_compact"]["kernel_ms"]}
                                                for m in modes},
                          "cll_build_8d": {m: rep[m]["cll_build"]["frac"] for m in modes},
-                         "note": "a no-compute copy with the gather's access pattern (80 B/particle through the "
-                                 "slot map) takes 1.9-2.06 ms at C5 (tools/soa_copy_probe.cu, DESIGN.md section 6)"},
+                         "inplace_move_with_keys": rep["inplace"]["compact_move_with_keys"] if "inplace" in rep else None,
+                         "note": "the gather is at the floor of its access pattern: the same loads and stores through "
+                                 "the real C5 slot map with no arithmetic take 2.66-2.69 ms (tools/gather_tma_probe.cu, "
+                                 "DESIGN.md section 6)"},
             "kernels": kernels,
             "phases": {m: rep[m]["phases"] for m in modes},
             "modes": {m: {k: rep[m][k] for k in ("ms_per_step", "value", "update_compact", "cll_build",
-                                                  "kernels_ms")} for m in modes},
+                                                  "compact_move_with_keys", "kernels_ms")} for m in modes},
             "gpu_launches": main_r["launches"],
             "clocks": main_r["clk"],
             "e2e": e2e,
