@@ -374,13 +374,17 @@ def run_ours(args):
     dom_ms = prof[dom][0] / prof[dom][1]
     bytes_dom = algorithmic_bytes(dom, dim, R["n"], ncells, R["cand"], R["created"], R["deleted"], R["moved"])
     achieved = bytes_dom / (dom_ms / 1e3) / 1e9 if bytes_dom else None
-    traffic = None
+    traffic, ncu_k = None, None
     tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tf):
         try:
-            traffic = json.load(open(tf)).get(args.config, {}).get(dom)
+            tj = json.load(open(tf))
+            traffic = tj.get(args.config, {}).get(dom)
+            # the ncu counters the north star names (DRAM rate, L2 hit rate, warp
+            # efficiency of the ballot / scan code) for the dominant kernel and K6
+            ncu_k = {k: v for k, v in tj.get(args.config + "_ncu", {}).items() if k in (dom, "upd_main")} or None
         except Exception:
-            traffic = None
+            traffic, ncu_k = None, None
     tot = sum(v[0] for v in prof.values())
     kernels = {k: {"ms_per_launch": round(v[0] / v[1], 4), "share": round(v[0] / tot, 4)} for k, v in prof.items()}
 
@@ -422,6 +426,8 @@ def run_ours(args):
                                                    "kernel_ms": rep[m]["update_compact"]["kernel_ms"]}
                                                for m in modes},
                          "cll_build_8d": {m: rep[m]["cll_build"]["frac"] for m in modes},
+                         "frac_of_spec_8tbs": achieved / 8000.0 if achieved else None,
+                         "ncu": ncu_k,
                          "inplace_move_with_keys": rep["inplace"]["compact_move_with_keys"] if "inplace" in rep else None,
                          "note": "the gather is at the floor of its access pattern: the same loads and stores through "
                                  "the real C5 slot map with no arithmetic take 2.66-2.69 ms (tools/gather_tma_probe.cu, "
