@@ -26,12 +26,13 @@ def test_C3_full_duct_inplace_compaction():
     assert tot[0] > 0 and tot[1] > 0
 
 
-def test_C4_full_junction_20_updates():
-    """BASELINE configs[3] at full size: 20 updates, every state compared at updates
-    0, 10 and 19 (every update's counts and the oracle's tie certification run)."""
+def test_C4_full_junction_100_updates():
+    """BASELINE configs[3] at full size for its whole 100-update run: every state
+    compared at updates 0, 20, 40, 60, 80 and 99 (every update's counts and the
+    oracle's tie certification run)."""
     w = inputs.c4(device="cuda", n_updates=100)
     assert w.n > 60_000_000
-    tot, bu = lockstep(w, 20, check_every=10, fused=True, deferred=True)
+    tot, bu = lockstep(w, 100, check_every=20, fused=True, deferred=True)
     assert tot[0] > 0 and tot[1] > 0
     del bu
     torch.cuda.empty_cache()
