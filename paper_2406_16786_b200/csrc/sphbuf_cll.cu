@@ -841,6 +841,131 @@ __global__ void __launch_bounds__(NT, MINB) k_cll_gather(PartDev in, PartDev out
     }
 }
 
+// K4 with warp-owned segments (opt-in, SPHBUF_GATHER_SPEC=wl; the 3-D, no-perm,
+// no-extra-column case): each warp takes 64 consecutive slots at a time and
+// stages the ids of 32 slots on either side itself, so a cell is ranked from the
+// warp's own window after a __syncwarp — no block barrier, each warp's chain
+// runs free of the slowest warp of its block.  Everything else is K4's.
+template <int MINB, int CARRY>
+__global__ void __launch_bounds__(kThreads, MINB) k_cll_gather_wl(PartDev in, PartDev out, GridDev g, Workspace ws,
+                                                                  const int *cell_start, const int *cell_end,
+                                                                  int advect, float dt, float cdt)
+{
+    pdl_entry();
+    constexpr int NW = kThreads / 32, SEG = 64, H = 32, W = SEG + 2 * H;
+    __shared__ long long s_id[NW][W];
+    __shared__ __align__(16) unsigned s_lo[NW][W];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int n = (int)*out.n;
+    constexpr int carry = CARRY;
+    const int adv_lim = advect ? (int)ws.ctr->mig_base : 0;
+    const int stride = (int)gridDim.x * NW * SEG;
+    int oob_next = 0;
+    // slot map of a segment: this lane's two slots and its two halo slots (prefetched)
+    int nsrc[2], nh[2];
+    auto load_map = [&](int sb) {
+#pragma unroll
+        for (int it = 0; it < 2; ++it) {
+            const int j = sb + it * 32 + lane;
+            nsrc[it] = j < n ? ws.src[j] : -1;
+            const int jh = it == 0 ? sb - H + lane : sb + SEG + lane;
+            nh[it] = (jh >= 0 && jh < n) ? ws.src[jh] : -1;
+        }
+    };
+    int seg = ((int)blockIdx.x * NW + warp) * SEG;
+    if (seg < n) load_map(seg);
+    for (; seg < n; seg = seg < n - stride ? seg + stride : n) {
+        int src[2], hs[2], cb[2], ce[2], lab[2];
+        float x[2], y[2], z[2], vx[2], vy[2], vz[2];
+        long long id[2], hid[2];
+#pragma unroll
+        for (int it = 0; it < 2; ++it) {
+            src[it] = nsrc[it];
+            hs[it] = nh[it];
+        }
+#pragma unroll
+        for (int it = 0; it < 2; ++it) hid[it] = hs[it] >= 0 ? in.id[hs[it]] : 0;
+#pragma unroll
+        for (int it = 0; it < 2; ++it) {
+            if (src[it] < 0) continue;
+            const int s = src[it];
+            x[it] = in.x[s];
+            y[it] = in.y[s];
+            z[it] = in.z[s];
+            vx[it] = in.vx[s];
+            vy[it] = in.vy[s];
+            vz[it] = in.vz[s];
+            id[it] = in.id[s];
+            lab[it] = in.label[s];
+        }
+        if (seg < n - stride) load_map(seg + stride);
+        bool wide = false;
+#pragma unroll
+        for (int it = 0; it < 2; ++it) {
+            const int hq = it == 0 ? lane : H + SEG + lane;
+            s_id[warp][hq] = hid[it];
+            s_lo[warp][hq] = (unsigned)hid[it];
+            wide |= (hid[it] >> 32) != 0;
+        }
+#pragma unroll
+        for (int it = 0; it < 2; ++it) {
+            cb[it] = ce[it] = 0;
+            if (src[it] < 0) continue;
+            if (src[it] < adv_lim) {
+                x[it] = advect1(x[it], vx[it], dt);
+                y[it] = advect1(y[it], vy[it], dt);
+                z[it] = advect1(z[it], vz[it], dt);
+            }
+            int oob = 0;
+            const int key = cell_of<3>(g, x[it], y[it], z[it], oob);
+            cb[it] = __ldg(cell_start + key);
+            ce[it] = __ldg(cell_end + key);
+            s_id[warp][H + it * 32 + lane] = id[it];
+            s_lo[warp][H + it * 32 + lane] = (unsigned)id[it];
+            wide |= (id[it] >> 32) != 0;
+        }
+        const bool narrow = !__any_sync(0xffffffffu, wide);    // (also the warp's barrier)
+        __syncwarp();
+        const int w0 = seg - H > 0 ? seg - H : 0;               // even: seg is a multiple of 64
+        const int w1 = seg + SEG + H < n ? seg + SEG + H : n;
+        const long long *sid = &s_id[warp][0] + (w0 - (seg - H));
+        const unsigned *slo = &s_lo[warp][0] + (w0 - (seg - H));
+        int kn[2];
+#pragma unroll
+        for (int it = 0; it < 2; ++it) {
+            kn[it] = -1;
+            if (src[it] < 0) continue;
+            const long long me = id[it];
+            const int d = cb[it] + rank_in_cell(in, ws, sid, slo, narrow, w0, w1, cb[it], ce[it], me);
+            if (carry) {
+                int oobn = 0;
+                kn[it] = carry_key<3>(g, x[it], y[it], z[it], vx[it], vy[it], vz[it], cdt, carry, oobn);
+                oob_next += oobn;
+                ws.key[d] = kn[it];
+                if (kn[it] == kLeaver) leaver_append(ws, d);
+            }
+            SPH_CHECK(d >= cb[it] && d < ce[it] && ce[it] <= n && src[it] < in.cap);
+            out.x[d] = x[it];
+            out.y[d] = y[it];
+            out.z[d] = z[it];
+            out.vx[d] = vx[it];
+            out.vy[d] = vy[it];
+            out.vz[d] = vz[it];
+            out.id[d] = me;
+            out.label[d] = lab[it];
+        }
+        if (carry) {
+#pragma unroll
+            for (int it = 0; it < 2; ++it) hist_count_match(ws.cell_count, kn[it]);   // next histogram
+        }
+        __syncwarp();   // the window is rewritten by the next segment
+    }
+    if (carry) {
+        const unsigned o = warp_sum((unsigned)oob_next);
+        if (lane == 0 && o) atomicAdd((unsigned long long *)&ws.ctr->out_of_grid, (unsigned long long)o);
+    }
+}
+
 // K4 on the copy engine (opt-in, SPHBUF_GATHER_TMA=1: correct and bit-identical,
 // but slower than k_cll_gather on C5 — 3.2 vs 2.1 ms, DESIGN.md §6 — because the
 // stages' shared memory leaves one block of <= 32 warps per SM for a per-tile
@@ -1377,6 +1502,18 @@ static void gather_variant(const char *v, const PartDev &in, const PartDev &out,
         SPH_GS("3:4", 3, 4)
         SPH_GS("3:3", 3, 3)
 #undef SPH_GS
+#define SPH_GW(name, M)                                                                                          \
+    if (!strcmp(v, name)) {                                                                                      \
+        static int grid = 0;                                                                                     \
+        if (!grid) grid = occ_grid(k_cll_gather_wl<M, 1>, kThreads);                                             \
+        launch_k(k_cll_gather_wl<M, 1>, dim3(cap_grid(grid, cap, kThreads * 2)), dim3(kThreads), 0, s, in, out, g, \
+                 ws, cs, ce, advect, dt, cdt);                                                                   \
+        return;                                                                                                  \
+    }
+        SPH_GW("wl", 5)
+        SPH_GW("wl4", 4)
+        SPH_GW("wl6", 6)
+#undef SPH_GW
 
         static int grid = 0;
         if (!grid) grid = occ_grid(k_cll_gather<false, 2, 5, kThreads, true, 3, 1, 0>, kThreads);
