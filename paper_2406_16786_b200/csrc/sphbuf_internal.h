@@ -141,7 +141,7 @@ struct Counters {
     int done_app;          // compaction append: finished blocks
     int done_runs;         // update prologue: finished blocks
     int done_upd;          // update: finished blocks (the last one scans the tile counts)
-    int dummy;
+    int ticket_gather;     // cell-list gather: tile tickets (reset by the scatter of the same build)
 };
 
 struct Workspace {

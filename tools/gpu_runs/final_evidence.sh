@@ -1,6 +1,6 @@
 # Round-end evidence on one B200: GPU suite, smoke, default bench, launch list and ncu captures (gpurun_out/).
 set -x
-SPH_WHOLE_RUN=1 python -m pytest tests -m gpu -x -q --durations=12 > gpurun_out/final_gputest.log 2>&1; echo gpu_rc=$? >> gpurun_out/final_gputest.log
+SPH_WHOLE_RUN=${SPH_WHOLE_RUN:-1} python -m pytest tests -m gpu -x -q --durations=12 > gpurun_out/final_gputest.log 2>&1; echo gpu_rc=$? >> gpurun_out/final_gputest.log
 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/final_smoke.log 2>&1
 python bench.py > gpurun_out/final_bench.log 2>&1
 B="python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu --no-sweep"
