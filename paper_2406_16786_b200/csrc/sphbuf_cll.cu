@@ -578,7 +578,10 @@ namespace sphbuf {
 // scatter and the gather more than it saves: measured.)
 // Blocks beyond `nscat` run the update prologue K5 instead (UpdPro): it needs only
 // the cell tables K2 just wrote, so it overlaps the scatter and the gather.
-template <int kScatterItems, int NT>
+// DYN (opt-in, SPHBUF_SCATTER=dyn): warp chunks of 32 x kScatterItems keys handed
+// out by a ticket counter (fetched one chunk ahead; reset by the last block)
+// instead of the static block stride.
+template <int kScatterItems, int NT, int DYN = 0>
 __global__ void __launch_bounds__(NT) k_cll_scatter(Workspace ws, const int *cell_start, int *perm, int nscat,
                                                     const int *cell_end, int pro_runs, int pro_max_ports)
 {
@@ -589,20 +592,20 @@ __global__ void __launch_bounds__(NT) k_cll_scatter(Workspace ws, const int *cel
     }
     const long long n = ws.ctr->n_in;
     if (blockIdx.x == 0 && threadIdx.x == 0) ws.ctr->ticket_gather = 0;   // the gather's tile tickets
-    const long long stride = (long long)nscat * NT * kScatterItems;
-    for (long long base = (long long)blockIdx.x * NT * kScatterItems; base < n; base += stride) {
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = lanemask_lt();
+    // the keys base + it * istride + tid, it < kScatterItems (uniform over the warp)
+    auto chunk = [&](long long base, int istride, int tid) {
         int key[kScatterItems];
 #pragma unroll
         for (int it = 0; it < kScatterItems; ++it) {
-            const long long i = base + it * NT + threadIdx.x;
+            const long long i = base + it * istride + tid;
             key[it] = i < n ? ws.key[i] : -1;
         }
         // lanes with equal keys grouped (match.any: a cell changer between two pieces
         // of a stayer run does not split the run's atomic), one cursor atomic per
         // distinct key of the warp, all items' atomics in flight together; the
         // lanes of a group take consecutive slots in lane order
-        const int lane = threadIdx.x & 31;
-        const unsigned lt = lanemask_lt();
         int b[kScatterItems], hl[kScatterItems], rl[kScatterItems];
 #pragma unroll
         for (int it = 0; it < kScatterItems; ++it) {
@@ -614,7 +617,7 @@ __global__ void __launch_bounds__(NT) k_cll_scatter(Workspace ws, const int *cel
 #pragma unroll
         for (int it = 0; it < kScatterItems; ++it) {
             const int rk = __shfl_sync(0xffffffffu, b[it], hl[it]) + rl[it];
-            const long long i = base + it * NT + threadIdx.x;
+            const long long i = base + it * istride + tid;
             if (i >= n) continue;
             if (key[it] >= 0) {
                 const int slot = __ldg(cell_start + key[it]) + rk;
@@ -624,6 +627,29 @@ __global__ void __launch_bounds__(NT) k_cll_scatter(Workspace ws, const int *cel
                 perm[i] = -1;                                     // tombstone: dropped
             }
         }
+    };
+    if (DYN) {
+        constexpr int WC = 32 * kScatterItems;
+        const int nchunks = (int)((n + WC - 1) / WC);
+        const int nwarps = nscat * (NT / 32);
+        int cur = (int)blockIdx.x * (NT / 32) + (int)(threadIdx.x >> 5);
+        int tk = 0;
+        if (lane == 0) tk = atomicAdd(&ws.ctr->ticket_scatter, 1);
+        while (cur < nchunks) {
+            const int nxt = nwarps + __shfl_sync(0xffffffffu, tk, 0);
+            if (lane == 0) tk = atomicAdd(&ws.ctr->ticket_scatter, 1);   // the chunk after the next one
+            chunk((long long)cur * WC, 32, lane);
+            cur = nxt;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0 && atomicAdd(&ws.ctr->done_scatter, 1) == nscat - 1) {
+            ws.ctr->ticket_scatter = 0;
+            ws.ctr->done_scatter = 0;
+        }
+    } else {
+        const long long stride = (long long)nscat * NT * kScatterItems;
+        for (long long base = (long long)blockIdx.x * NT * kScatterItems; base < n; base += stride)
+            chunk(base, NT, (int)threadIdx.x);
     }
 }
 
@@ -1403,15 +1429,15 @@ __global__ void __launch_bounds__(GtmaCfg<DIM, T, G, S>::NT, 1)
 
 // ------------------------------------------------------------------ launchers
 
-template <int I, int NT>
+template <int I, int NT, int DYN = 0>
 static void scatter_launch(const Workspace &ws, const int *cell_start, const int *cell_end, int *perm, long long cap,
                            const UpdPro &up, cudaStream_t s)
 {
     static int grid = 0;
-    if (!grid) grid = occ_grid(k_cll_scatter<I, NT>, NT);
+    if (!grid) grid = occ_grid(k_cll_scatter<I, NT, DYN>, NT);
     const int nscat = cap_grid(grid, cap, NT * I);
     const int npro = up.n_runs > 0 ? (up.n_runs + NT - 1) / NT : 0;
-    launch_k(k_cll_scatter<I, NT>, dim3(nscat + npro), dim3(NT), 0, s, ws, cell_start, perm, nscat, cell_end,
+    launch_k(k_cll_scatter<I, NT, DYN>, dim3(nscat + npro), dim3(NT), 0, s, ws, cell_start, perm, nscat, cell_end,
              up.n_runs, up.max_ports);
 }
 
@@ -1661,6 +1687,9 @@ cudaError_t launch_cll_finish(const PartDev &in, const PartDev &out, const GridD
         else if (!strcmp(v, "2:256")) scatter_launch<2, 256>(ws, cell_start, cell_end, perm, cap, up, s);
         else if (!strcmp(v, "1:256")) scatter_launch<1, 256>(ws, cell_start, cell_end, perm, cap, up, s);
         else if (!strcmp(v, "2:512")) scatter_launch<2, 512>(ws, cell_start, cell_end, perm, cap, up, s);
+        else if (!strcmp(v, "dyn")) scatter_launch<4, 256, 1>(ws, cell_start, cell_end, perm, cap, up, s);
+        else if (!strcmp(v, "dyn2")) scatter_launch<2, 256, 1>(ws, cell_start, cell_end, perm, cap, up, s);
+        else if (!strcmp(v, "dyn8")) scatter_launch<8, 256, 1>(ws, cell_start, cell_end, perm, cap, up, s);
         else scatter_launch<4, 256>(ws, cell_start, cell_end, perm, cap, up, s);
         L->after(s, KID_CLL_SCATTER);
     }

@@ -142,6 +142,8 @@ struct Counters {
     int done_runs;         // update prologue: finished blocks
     int done_upd;          // update: finished blocks (the last one scans the tile counts)
     int ticket_gather;     // cell-list gather: tile tickets (reset by the scatter of the same build)
+    int ticket_scatter;    // scatter (DYN variant): warp-chunk tickets (reset by its last block)
+    int done_scatter;      // scatter (DYN variant): finished blocks
 };
 
 struct Workspace {
