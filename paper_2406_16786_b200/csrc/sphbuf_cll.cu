@@ -628,7 +628,29 @@ __global__ void __launch_bounds__(NT) k_cll_scatter(Workspace ws, const int *cel
             }
         }
     };
-    if (DYN) {
+    if (DYN == 2) {
+        // block chunks of 4 rounds (4 x NT x kScatterItems keys) per ticket
+        constexpr int R = 4;
+        constexpr long long BC = (long long)NT * kScatterItems * R;
+        const int nch = (int)((n + BC - 1) / BC);
+        __shared__ int s_nx;
+        int cur = (int)blockIdx.x, tk = 0;
+        if (threadIdx.x == 0) tk = atomicAdd(&ws.ctr->ticket_scatter, 1);
+        while (cur < nch) {
+            if (threadIdx.x == 0) s_nx = nscat + tk;
+            __syncthreads();
+            const int nxt = s_nx;
+            if (threadIdx.x == 0) tk = atomicAdd(&ws.ctr->ticket_scatter, 1);   // the chunk after the next one
+#pragma unroll 1
+            for (int r = 0; r < R; ++r) chunk(cur * BC + (long long)r * NT * kScatterItems, NT, (int)threadIdx.x);
+            __syncthreads();
+            cur = nxt;
+        }
+        if (threadIdx.x == 0 && atomicAdd(&ws.ctr->done_scatter, 1) == nscat - 1) {
+            ws.ctr->ticket_scatter = 0;
+            ws.ctr->done_scatter = 0;
+        }
+    } else if (DYN) {
         constexpr int WC = 32 * kScatterItems;
         const int nchunks = (int)((n + WC - 1) / WC);
         const int nwarps = nscat * (NT / 32);
@@ -1688,6 +1710,7 @@ cudaError_t launch_cll_finish(const PartDev &in, const PartDev &out, const GridD
         else if (!strcmp(v, "1:256")) scatter_launch<1, 256>(ws, cell_start, cell_end, perm, cap, up, s);
         else if (!strcmp(v, "2:512")) scatter_launch<2, 512>(ws, cell_start, cell_end, perm, cap, up, s);
         else if (!strcmp(v, "dyn")) scatter_launch<4, 256, 1>(ws, cell_start, cell_end, perm, cap, up, s);
+        else if (!strcmp(v, "dynb")) scatter_launch<4, 256, 2>(ws, cell_start, cell_end, perm, cap, up, s);
         else if (!strcmp(v, "dyn2")) scatter_launch<2, 256, 1>(ws, cell_start, cell_end, perm, cap, up, s);
         else if (!strcmp(v, "dyn8")) scatter_launch<8, 256, 1>(ws, cell_start, cell_end, perm, cap, up, s);
         else scatter_launch<4, 256>(ws, cell_start, cell_end, perm, cap, up, s);
